@@ -1,0 +1,79 @@
+/* treeclust_gpu.h — additive entry points of the B200 engine.
+ *
+ * Nothing here changes the reference ABI in treeclust.h; these are new symbols
+ * a GPU-aware caller may use on top of it:
+ *
+ *   tcg_cluster_device   the tc_cluster pipeline on DEVICE-resident buffers:
+ *                        coords already in HBM, labels / core flags written to
+ *                        HBM, launched on the caller's stream. This is the
+ *                        "from the moment the data is in device memory" timing
+ *                        point of the paper.
+ *   tcg_generate_*       the HACC-like and taxi-like benchmark generators
+ *                         that the reference does not ship.
+ *   tcg_shard_*          host-side pieces of the Morton-range multi-GPU path
+ *                        (SURVEY.md §8e); the collectives are driven by the
+ *                        caller's torch.distributed / NCCL communicator.
+ */
+#ifndef TREECLUST_GPU_H
+#define TREECLUST_GPU_H
+
+#include "treeclust.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library / device information. Returns the CUDA device count (0 when no
+ * usable device / driver), and fills name (NUL-terminated) for device 0. */
+int tcg_device_count(void);
+const char* tcg_version(void);
+
+/* Device-resident clustering.
+ *   d_coords : n*dim fp32, row-major, device pointer (read only)
+ *   d_labels : n int32, device pointer (written)
+ *   d_core   : n uint8, device pointer (written)
+ *   stream   : cudaStream_t to launch on (NULL = legacy default stream)
+ *   stats    : may be NULL. When non-NULL the call synchronizes the stream at
+ *              the end to read counters and stage times back.
+ * The call is stream-ordered: with stats == NULL it returns once the work is
+ * enqueued, except for the few small device->host reads that size later
+ * launches (DenseBox cell/primitive counts). Scratch comes from the stream-
+ * ordered CUDA memory pool (cudaMallocAsync) and is released before return. */
+tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
+                             float eps, int minpts, tc_algorithm algorithm,
+                             int64_t oracle_cap, int32_t* d_labels,
+                             uint8_t* d_core, void* stream,
+                             tc_cluster_stats* stats);
+
+/* Per-stage device milliseconds of the last tcg_cluster_device / tc_cluster
+ * call on this host thread (the tc_cluster_stats phases split finer):
+ * [0] bounds+morton  [1] sort  [2] topology+refit  [3] grid (DenseBox)
+ * [4] core pass      [5] main pass  [6] finalize   [7] total.
+ * Returns the number of entries written (<= cap). */
+int tcg_last_stage_ms(double* out, int cap);
+
+/* ---- benchmark generators (host, SplitMix64) ---- */
+
+/* 3D HACC-like halos: n_bg uniform background points in [0,L)^3, then
+ * Plummer halos until int64(halo_frac*n) halo points exist. */
+tc_status tcg_generate_hacc_like(int64_t n, double box_len, double halo_frac,
+                                 uint64_t seed, tc_dataset** out);
+/* 2D taxi-trajectory-like points in the unit square. */
+tc_status tcg_generate_taxi_like(int64_t n, uint64_t seed, tc_dataset** out);
+/* testutil::random_instance (REF tests/test_util.hpp:27-60): returns the
+ * instance's dataset and writes its eps / minpts. */
+tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n,
+                              float* eps, int* minpts, tc_dataset** out);
+
+/* ---- dataset from caller memory without validation copy (host) ---- */
+/* Same as tc_dataset_create but the dataset's coords live in page-locked
+ * (pinned) host memory, so tc_cluster's host->device copy runs at full PCIe
+ * / C2C rate. */
+tc_status tcg_dataset_create_pinned(const float* coords, int64_t n, int dim,
+                                    tc_dataset** out);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* TREECLUST_GPU_H */

@@ -1,0 +1,242 @@
+"""Python mirror of the reference C ABI (``/root/reference/proj/include/treeclust.h``).
+
+Same names, argument meaning and error behaviour as the ``tc_*`` functions:
+a non-``TC_OK`` status raises :class:`TreeclustError` carrying the status code.
+Everything runs through ``libtreeclust_b200.so`` (C ABI, sm_100a kernels);
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import TcClusterStats, lib
+
+
+class Status(enum.IntEnum):
+    OK = 0
+    INVALID_ARGUMENT = 1
+    IO = 2
+    VERIFY_FAIL = 3
+    CAP_EXCEEDED = 4
+    INTERNAL = 5
+
+
+class Algorithm(enum.IntEnum):
+    FDBSCAN = 0
+    DENSEBOX = 1
+    BRUTEFORCE = 2
+
+
+class FileFormat(enum.IntEnum):
+    AUTO = 0
+    CSV = 1
+    BINARY = 2
+
+
+class TreeclustError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = Status(status)
+        msg = lib.tc_status_string(int(status)).decode()
+        super().__init__(f"{where}: {msg} ({self.status.name})")
+
+
+def _check(status: int, where: str) -> None:
+    if status != 0:
+        raise TreeclustError(status, where)
+
+
+STAGES = ("bounds_morton", "sort", "topology_refit", "grid", "core", "main", "finalize", "total")
+
+
+class Dataset:
+    """Owns a ``tc_dataset*`` (host points, row-major n x dim float32)."""
+
+    def __init__(self, handle: int):
+        if not handle:
+            raise ValueError("null tc_dataset")
+        self._h = C.c_void_p(handle)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.tc_dataset_free(h)
+            self._h = C.c_void_p()
+
+    # ---- constructors (tc_dataset_create / _load / tc_generate_*) ----
+    @classmethod
+    def from_array(cls, coords) -> "Dataset":
+        a = np.ascontiguousarray(coords, dtype=np.float32)
+        if a.ndim != 2:
+            raise TreeclustError(Status.INVALID_ARGUMENT, "tc_dataset_create")
+        out = C.c_void_p()
+        _check(lib.tc_dataset_create(a.ctypes.data_as(C.POINTER(C.c_float)), a.shape[0],
+                                     a.shape[1], C.byref(out)), "tc_dataset_create")
+        return cls(out.value)
+
+    @classmethod
+    def load(cls, path: str, fmt: FileFormat = FileFormat.AUTO) -> "Dataset":
+        out = C.c_void_p()
+        _check(lib.tc_dataset_load(path.encode(), int(fmt), C.byref(out)), "tc_dataset_load")
+        return cls(out.value)
+
+    @classmethod
+    def blobs(cls, k, per_blob, dim, separation, sigma, seed) -> "Dataset":
+        out = C.c_void_p()
+        _check(lib.tc_generate_blobs(k, per_blob, dim, separation, sigma, seed, C.byref(out)),
+               "tc_generate_blobs")
+        return cls(out.value)
+
+    @classmethod
+    def uniform(cls, n, dim, lo, hi, seed) -> "Dataset":
+        lo_a = (C.c_float * 3)(*([float(v) for v in lo] + [0.0] * (3 - len(lo))))
+        hi_a = (C.c_float * 3)(*([float(v) for v in hi] + [0.0] * (3 - len(hi))))
+        out = C.c_void_p()
+        _check(lib.tc_generate_uniform(n, dim, lo_a, hi_a, seed, C.byref(out)),
+               "tc_generate_uniform")
+        return cls(out.value)
+
+    @classmethod
+    def lattice(cls, side, dim, spacing) -> "Dataset":
+        out = C.c_void_p()
+        _check(lib.tc_generate_lattice(side, dim, spacing, C.byref(out)), "tc_generate_lattice")
+        return cls(out.value)
+
+    @classmethod
+    def hacc_like(cls, n, box_len=None, halo_frac=0.23, seed=11) -> "Dataset":
+        """L = 36.8 * (n / 37e6)^(1/3) keeps the C2 density."""
+        if box_len is None:
+            box_len = 36.8 * (n / 37e6) ** (1.0 / 3.0)
+        out = C.c_void_p()
+        _check(lib.tcg_generate_hacc_like(n, box_len, halo_frac, seed, C.byref(out)),
+               "tcg_generate_hacc_like")
+        return cls(out.value)
+
+    @classmethod
+    def taxi_like(cls, n, seed=5) -> "Dataset":
+        out = C.c_void_p()
+        _check(lib.tcg_generate_taxi_like(n, seed, C.byref(out)), "tcg_generate_taxi_like")
+        return cls(out.value)
+
+    @classmethod
+    def random_instance(cls, seed, min_n=50, max_n=2000):
+        """testutil::random_instance -> (Dataset, eps, minpts)."""
+        eps = C.c_float()
+        minpts = C.c_int()
+        out = C.c_void_p()
+        _check(lib.tcg_random_instance(seed, min_n, max_n, C.byref(eps), C.byref(minpts),
+                                       C.byref(out)), "tcg_random_instance")
+        return cls(out.value), eps.value, minpts.value
+
+    # ---- accessors ----
+    def save(self, path: str, fmt: FileFormat = FileFormat.AUTO) -> None:
+        _check(lib.tc_dataset_save(self._h, path.encode(), int(fmt)), "tc_dataset_save")
+
+    @property
+    def size(self) -> int:
+        return int(lib.tc_dataset_size(self._h))
+
+    @property
+    def dim(self) -> int:
+        return int(lib.tc_dataset_dim(self._h))
+
+    def coords(self) -> np.ndarray:
+        n, d = self.size, self.dim
+        ptr = lib.tc_dataset_coords(self._h)
+        return np.ctypeslib.as_array(ptr, shape=(n, d)).copy()
+
+    def __len__(self) -> int:
+        return self.size
+
+
+@dataclass
+class Result:
+    labels: np.ndarray
+    core_flags: np.ndarray
+    stats: dict
+
+
+def cluster(ds: Dataset, eps: float, minpts: int, algorithm: Algorithm = Algorithm.FDBSCAN,
+            threads: int = 0, oracle_cap: int = 0) -> Result:
+    """``tc_cluster`` + ``tc_result_*``: host dataset in, host labels/flags out."""
+    res = C.c_void_p()
+    _check(lib.tc_cluster(ds.handle, C.c_float(eps), int(minpts), int(algorithm), int(threads),
+                          int(oracle_cap), C.byref(res)), "tc_cluster")
+    try:
+        n = int(lib.tc_result_size(res))
+        labels = np.ctypeslib.as_array(lib.tc_result_labels(res), shape=(n,)).copy()
+        core = np.ctypeslib.as_array(lib.tc_result_core_flags(res), shape=(n,)).copy()
+        st = TcClusterStats()
+        _check(lib.tc_result_stats(res, C.byref(st)), "tc_result_stats")
+        return Result(labels, core, st.to_dict())
+    finally:
+        lib.tc_result_free(res)
+
+
+def cluster_raw(ds: Dataset, eps: float, minpts: int, algorithm: Algorithm = Algorithm.FDBSCAN,
+                threads: int = 0, oracle_cap: int = 0) -> int:
+    """``tc_cluster`` then ``tc_result_free``; returns the status (for timing the ABI)."""
+    res = C.c_void_p()
+    st = lib.tc_cluster(ds.handle, C.c_float(eps), int(minpts), int(algorithm), int(threads),
+                        int(oracle_cap), C.byref(res))
+    if st == 0:
+        lib.tc_result_free(res)
+    return st
+
+
+def cluster_device(coords, eps: float, minpts: int, algorithm: Algorithm = Algorithm.FDBSCAN,
+                   labels=None, core=None, stream=None, stats: bool = False, oracle_cap: int = 0):
+    """``tcg_cluster_device`` on torch CUDA tensors (coords: float32 [n, dim], contiguous).
+
+    Launches on ``stream`` (a torch.cuda.Stream; default: the current stream) and
+    returns ``(labels, core, stats_or_None)``; with ``stats=False`` the call does
+    not synchronize at the end.
+    """
+    import torch
+
+    if not (coords.is_cuda and coords.dtype == torch.float32 and coords.dim() == 2
+            and coords.is_contiguous()):
+        raise TreeclustError(Status.INVALID_ARGUMENT, "tcg_cluster_device")
+    n, d = coords.shape
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=coords.device)
+    if core is None:
+        core = torch.empty(n, dtype=torch.uint8, device=coords.device)
+    s = stream if stream is not None else torch.cuda.current_stream(coords.device)
+    st = TcClusterStats() if stats else None
+    _check(lib.tcg_cluster_device(C.c_void_p(coords.data_ptr()), n, d, C.c_float(eps),
+                                  int(minpts), int(algorithm), int(oracle_cap),
+                                  C.c_void_p(labels.data_ptr()), C.c_void_p(core.data_ptr()),
+                                  C.c_void_p(s.cuda_stream),
+                                  C.byref(st) if st is not None else None),
+           "tcg_cluster_device")
+    return labels, core, (st.to_dict() if st is not None else None)
+
+
+def verify(ds: Dataset, eps: float, minpts: int, threads: int = 0, oracle_cap: int = 0):
+    """``tc_verify`` -> (Status, report text)."""
+    buf = C.create_string_buffer(8192)
+    st = lib.tc_verify(ds.handle, C.c_float(eps), int(minpts), int(threads), int(oracle_cap),
+                       buf, len(buf))
+    return Status(st), buf.value.decode("utf-8", "replace")
+
+
+def last_stage_ms() -> dict:
+    arr = (C.c_double * len(STAGES))()
+    k = lib.tcg_last_stage_ms(arr, len(STAGES))
+    return {STAGES[i]: arr[i] for i in range(k)}
+
+
+def device_count() -> int:
+    return int(lib.tcg_device_count())
+
+
+def status_string(status: int) -> str:
+    return lib.tc_status_string(int(status)).decode()

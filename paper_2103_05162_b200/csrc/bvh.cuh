@@ -1,0 +1,100 @@
+// Linear BVH in HBM: node layout and the eps-ball traversal.
+//
+// Layout ("children in parent"). The reference Node (bvh.hpp:89-94) stores
+// its own box and the traversal tests each child against the child's own box
+// (bvh.hpp:60-71). Here every internal node stores BOTH children's boxes,
+// their child links and, per child, one aux int:
+//     3D: 64 B = 4 x float4   [L.lo xyz, L.hi xyz, R.lo xyz, R.hi xyz | l, r, auxL, auxR]
+//     2D: 48 B = 3 x float4   [L.lo xy,  L.hi xy,  R.lo xy,  R.hi xy  | l, r, auxL, auxR]
+// so one node fetch (two 32 B sectors) decides both children with no second
+// dependent load. Child links: >= 0 internal node index, < 0 = ~leaf_rank
+// (bvh.hpp:91). aux for an internal child = its max leaf rank (the right end
+// of its Karras range, bvh.cpp:88-124 computes the same by propagation); for a
+// leaf child = the primitive's payload (point index for a SinglePoint, or
+// ~cell for a DenseBox in the mixed tree). Because a leaf child's box lives in
+// its parent, a leaf visit never touches the leaf arrays.
+//
+// A 1-leaf tree (the reference special case bvh.hpp:49-53) is stored as one
+// pseudo node whose right child is an empty (+inf/-inf) box that no ball hits.
+#pragma once
+
+#include <cstdint>
+
+#include "device_common.cuh"
+
+namespace tcb {
+
+template <int D>
+struct NodeTraits {
+  static constexpr int kVec = D == 3 ? 4 : 3;  // float4 per node
+  static constexpr int kFloats = kVec * 4;
+  static constexpr int kIntOff = 4 * D;        // float index of the int4 part
+};
+
+constexpr int kStackDepth = 128;  // bvh.hpp:82-84 (keys are 64 + 32 bits)
+
+// Traverses the tree for the closed ball (p, sqrt(r2)), hiding every leaf
+// with rank < min_rank (query_sphere_masked, bvh.hpp:45-72), and calls
+//     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
+// for each leaf whose box is within the ball; visit returning false ends the
+// query. Visit order is exactly the reference's (left before right for leaf
+// children; right subtree before left subtree for internal children, i.e. its
+// LIFO stack order), so early-exit counters match bit for bit.
+template <int D, typename Visit>
+__device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes,
+                                          const float* p, double r2,
+                                          int32_t min_rank, Visit& visit) {
+  using T = NodeTraits<D>;
+  int32_t stack[kStackDepth];
+  int top = 0;
+  int32_t node = 0;
+  while (true) {
+    float f[T::kFloats];
+    const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
+#pragma unroll
+    for (int v = 0; v < T::kVec; ++v) {
+      float4 q = __ldg(src + v);
+      f[4 * v + 0] = q.x;
+      f[4 * v + 1] = q.y;
+      f[4 * v + 2] = q.z;
+      f[4 * v + 3] = q.w;
+    }
+    const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+    const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+    const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+    const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+    bool go_l = false, go_r = false;
+    if (left < 0) {
+      if (~left >= min_rank && box_dist2<D>(p, f, f + D) <= r2)
+        if (!visit(~left, aux_l, f, f + D)) return;
+    } else if (aux_l >= min_rank && box_dist2<D>(p, f, f + D) <= r2) {
+      go_l = true;
+    }
+    if (right < 0) {
+      if (~right >= min_rank && box_dist2<D>(p, f + 2 * D, f + 3 * D) <= r2)
+        if (!visit(~right, aux_r, f + 2 * D, f + 3 * D)) return;
+    } else if (aux_r >= min_rank && box_dist2<D>(p, f + 2 * D, f + 3 * D) <= r2) {
+      go_r = true;
+    }
+    if (go_l && go_r) {
+      stack[top++] = left;
+      node = right;
+    } else if (go_l) {
+      node = left;
+    } else if (go_r) {
+      node = right;
+    } else {
+      if (top == 0) return;
+      node = stack[--top];
+    }
+  }
+}
+
+// Device view of a built tree.
+struct DeviceBvh {
+  int32_t num_leaves = 0;
+  float4* nodes = nullptr;        // max(1, num_leaves-1) nodes, NodeTraits<D>::kVec float4 each
+  int32_t* leaf_order = nullptr;  // leaf rank -> primitive index (sorted values)
+};
+
+}  // namespace tcb

@@ -1,0 +1,478 @@
+// The C ABI (include/treeclust.h, include/treeclust_gpu.h).
+//
+// Mirrors the reference's capi.cpp contract: opaque handles owned by the
+// library, output handles written only on success, C++ failures mapped onto
+// tc_status exactly like `guarded` (capi.cpp:30-43):
+//   invalid argument -> TC_ERR_INVALID_ARGUMENT, I/O (std::runtime_error) ->
+//   TC_ERR_IO, allocation / CUDA failure / anything else -> TC_ERR_INTERNAL.
+// tc_cluster replaces dbscan_run with the device pipeline (engine.cu); the
+// host copy of the points goes up once, labels + core flags come back once.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "check.hpp"
+#include "engine.hpp"
+#include "host_data.hpp"
+#include "treeclust.h"
+#include "treeclust_gpu.h"
+
+#define TC_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Host buffers: page-locked when large (full-rate H2D / D2H), cached across
+// calls so repeated tc_cluster calls do not pay for pinning again.
+// ---------------------------------------------------------------------------
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // intentionally leaked (no teardown-order issues)
+    return *p;
+  }
+  void* acquire(size_t bytes, bool* pinned) {
+    *pinned = false;
+    if (bytes == 0) bytes = 1;
+    if (bytes >= kPinMin) {
+      size_t key = round(bytes);
+      {
+        std::lock_guard<std::mutex> lock(mu_);
+        auto it = free_.find(key);
+        if (it != free_.end()) {
+          void* p = it->second;
+          free_.erase(it);
+          cached_ -= key;
+          *pinned = true;
+          return p;
+        }
+      }
+      void* p = nullptr;
+      if (cudaMallocHost(&p, key) == cudaSuccess) {
+        *pinned = true;
+        return p;
+      }
+      cudaGetLastError();  // clear (no device / no driver): fall back to pageable
+    }
+    void* p = std::malloc(bytes);
+    if (!p) throw std::bad_alloc();
+    return p;
+  }
+  void release(void* p, size_t bytes, bool pinned) {
+    if (!p) return;
+    if (!pinned) {
+      std::free(p);
+      return;
+    }
+    size_t key = round(bytes);
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      if (cached_ + key <= kCacheCap) {
+        free_.emplace(key, p);
+        cached_ += key;
+        return;
+      }
+    }
+    cudaFreeHost(p);
+  }
+
+ private:
+  static constexpr size_t kPinMin = size_t{1} << 20;
+  static constexpr size_t kCacheCap = size_t{16} << 30;
+  static size_t round(size_t b) { return (b + (size_t{2} << 20) - 1) & ~((size_t{2} << 20) - 1); }
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+  size_t cached_ = 0;
+};
+
+template <typename T>
+struct HostArray {
+  T* ptr = nullptr;
+  size_t count = 0;
+  bool pinned = false;
+  HostArray() = default;
+  explicit HostArray(size_t n) : count(n) {
+    ptr = static_cast<T*>(HostPool::get().acquire(n * sizeof(T), &pinned));
+  }
+  HostArray(const HostArray&) = delete;
+  HostArray& operator=(const HostArray&) = delete;
+  ~HostArray() { HostPool::get().release(ptr, count * sizeof(T), pinned); }
+};
+
+}  // namespace
+
+struct tc_dataset {
+  int dim = 0;
+  int64_t n = 0;
+  HostArray<float> coords;
+  tc_dataset(int d, int64_t count) : dim(d), n(count), coords(static_cast<size_t>(count) * d) {}
+};
+
+struct tc_result {
+  int64_t n = 0;
+  HostArray<int32_t> labels;
+  HostArray<uint8_t> core;
+  tc_cluster_stats stats{};
+  explicit tc_result(int64_t count)
+      : n(count), labels(static_cast<size_t>(count)), core(static_cast<size_t>(count)) {}
+};
+
+namespace {
+
+template <typename Fn>
+tc_status guarded(Fn&& fn) {
+  try {
+    return fn();
+  } catch (const tcb::InvalidArgument&) {
+    return TC_ERR_INVALID_ARGUMENT;
+  } catch (const tcb::CapExceeded&) {
+    return TC_ERR_CAP_EXCEEDED;
+  } catch (const tcb::CudaFailure&) {
+    cudaGetLastError();
+    return TC_ERR_INTERNAL;
+  } catch (const std::invalid_argument&) {
+    return TC_ERR_INVALID_ARGUMENT;
+  } catch (const std::runtime_error&) {
+    return TC_ERR_IO;
+  } catch (const std::bad_alloc&) {
+    return TC_ERR_INTERNAL;
+  } catch (...) {
+    return TC_ERR_INTERNAL;
+  }
+}
+
+tc_status publish(tcb::HostPoints&& pts, tc_dataset** out) {
+  tcb::validate_points(pts.dim, pts.coords.data(), static_cast<int64_t>(pts.coords.size()));
+  auto ds = std::make_unique<tc_dataset>(pts.dim, pts.size());
+  std::memcpy(ds->coords.ptr, pts.coords.data(), pts.coords.size() * sizeof(float));
+  *out = ds.release();
+  return TC_OK;
+}
+
+// RAII stream + device buffers for one ABI call.
+struct DeviceCall {
+  cudaStream_t st = nullptr;
+  std::vector<void*> bufs;
+  DeviceCall() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      throw tcb::CudaFailure{cudaErrorNoDevice, __FILE__, __LINE__};
+    }
+    TCB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  }
+  ~DeviceCall() {
+    for (void* p : bufs) cudaFreeAsync(p, st);
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  }
+  template <typename T>
+  T* alloc(int64_t count) {
+    void* p = nullptr;
+    TCB_CUDA(cudaMallocAsync(&p, static_cast<size_t>(std::max<int64_t>(count, 1)) * sizeof(T), st));
+    bufs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+// One algorithm on a dataset already resident on the device.
+void device_cluster(DeviceCall& call, const float* d_coords, int64_t n, int dim, float eps,
+                    int minpts, tc_algorithm algo, int64_t cap, int32_t* d_labels,
+                    uint8_t* d_core, tc_result* res) {
+  tcb::RunOutput ro;
+  tcb::run_device(d_coords, n, dim, eps, minpts, algo, cap, d_labels, d_core, call.st, true, &ro,
+                  [&](cudaStream_t s) {
+                    if (!res) return;
+                    TCB_CUDA(cudaMemcpyAsync(res->labels.ptr, d_labels, sizeof(int32_t) * n,
+                                             cudaMemcpyDeviceToHost, s));
+                    TCB_CUDA(cudaMemcpyAsync(res->core.ptr, d_core, n, cudaMemcpyDeviceToHost, s));
+                  });
+  if (res) res->stats = ro.stats;
+}
+
+// ---- check_equivalence (oracle.cpp:120-163) on host arrays + device border check ----
+struct Equivalence {
+  bool pass = true;
+  std::string message = "PASS";
+};
+
+std::string at_point(const char* what, int64_t i) {
+  std::ostringstream os;
+  os << what << " (first divergence at point " << i << ")";
+  return os.str();
+}
+
+Equivalence check_equivalence(const int32_t* la, const uint8_t* ca, const int32_t* lb,
+                              const uint8_t* cb, int64_t n, int64_t bad_a, int64_t bad_b) {
+  Equivalence r;
+  auto fail = [&](std::string m) {
+    r.pass = false;
+    r.message = std::move(m);
+    return r;
+  };
+  for (int64_t i = 0; i < n; ++i)
+    if (ca[i] != cb[i]) return fail(at_point("core flags differ", i));
+  for (int64_t i = 0; i < n; ++i)
+    if ((la[i] == -1) != (lb[i] == -1)) return fail(at_point("noise sets differ", i));
+  std::unordered_map<int32_t, int32_t> a2b, b2a;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!ca[i]) continue;
+    auto ia = a2b.emplace(la[i], lb[i]);
+    if (!ia.second && ia.first->second != lb[i]) return fail(at_point("core partitions differ", i));
+    auto ib = b2a.emplace(lb[i], la[i]);
+    if (!ib.second && ib.first->second != la[i]) return fail(at_point("core partitions differ", i));
+  }
+  if (bad_a >= 0) return fail(at_point("first clustering has an invalid border label", bad_a));
+  if (bad_b >= 0) return fail(at_point("second clustering has an invalid border label", bad_b));
+  return r;
+}
+
+}  // namespace
+
+// ===========================================================================
+// Reference ABI
+// ===========================================================================
+
+TC_EXPORT const char* tc_status_string(tc_status status) {
+  switch (status) {
+    case TC_OK: return "ok";
+    case TC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case TC_ERR_IO: return "i/o error";
+    case TC_ERR_VERIFY_FAIL: return "verification failed";
+    case TC_ERR_CAP_EXCEEDED: return "oracle cap exceeded";
+    case TC_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+TC_EXPORT tc_status tc_dataset_create(const float* coords, int64_t n, int dim, tc_dataset** out) {
+  if (!coords || !out || n < 1) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    if (dim != 2 && dim != 3) throw std::invalid_argument("PointSet: dimension must be 2 or 3");
+    tcb::validate_points(dim, coords, n * dim);
+    auto ds = std::make_unique<tc_dataset>(dim, n);
+    std::memcpy(ds->coords.ptr, coords, static_cast<size_t>(n) * dim * sizeof(float));
+    *out = ds.release();
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tc_dataset_load(const char* path, tc_file_format format, tc_dataset** out) {
+  if (!path || !out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] { return publish(tcb::load_points(path, static_cast<int>(format)), out); });
+}
+
+TC_EXPORT tc_status tc_dataset_save(const tc_dataset* ds, const char* path, tc_file_format format) {
+  if (!ds || !path) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    tcb::save_points(path, static_cast<int>(format), ds->dim, ds->coords.ptr, ds->n);
+    return TC_OK;
+  });
+}
+
+TC_EXPORT int64_t tc_dataset_size(const tc_dataset* ds) { return ds ? ds->n : 0; }
+TC_EXPORT int tc_dataset_dim(const tc_dataset* ds) { return ds ? ds->dim : 0; }
+TC_EXPORT const float* tc_dataset_coords(const tc_dataset* ds) { return ds ? ds->coords.ptr : nullptr; }
+TC_EXPORT void tc_dataset_free(tc_dataset* ds) { delete ds; }
+
+TC_EXPORT tc_status tc_generate_blobs(int k, int64_t per_blob, int dim, float separation,
+                                      float sigma, uint64_t seed, tc_dataset** out) {
+  if (!out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] { return publish(tcb::gen_blobs(k, per_blob, dim, separation, sigma, seed), out); });
+}
+
+TC_EXPORT tc_status tc_generate_uniform(int64_t n, int dim, const float* lo, const float* hi,
+                                        uint64_t seed, tc_dataset** out) {
+  if (!out || !lo || !hi) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    for (int k = 0; k < dim && k < 3; ++k)
+      if (!(lo[k] <= hi[k])) throw std::invalid_argument("bounds");
+    return publish(tcb::gen_uniform(n, dim, lo, hi, seed), out);
+  });
+}
+
+TC_EXPORT tc_status tc_generate_lattice(int64_t side, int dim, float spacing, tc_dataset** out) {
+  if (!out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] { return publish(tcb::gen_lattice(side, dim, spacing), out); });
+}
+
+TC_EXPORT tc_status tc_cluster(const tc_dataset* ds, float eps, int minpts, tc_algorithm algorithm,
+                               int threads, int64_t oracle_cap, tc_result** out) {
+  (void)threads;  // accepted for ABI compatibility; the work runs on the GPU
+  if (!ds || !out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    if (algorithm != TC_ALGO_FDBSCAN && algorithm != TC_ALGO_DENSEBOX &&
+        algorithm != TC_ALGO_BRUTEFORCE)
+      return TC_ERR_INVALID_ARGUMENT;
+    if (algorithm == TC_ALGO_BRUTEFORCE) {  // cap before validation (capi.cpp:166-168)
+      int64_t cap = oracle_cap > 0 ? oracle_cap : 10000;
+      if (ds->n > cap) return TC_ERR_CAP_EXCEEDED;
+    }
+    if (!(eps > 0.f) || !std::isfinite(eps) || minpts < 2) return TC_ERR_INVALID_ARGUMENT;
+    const int64_t n = ds->n;
+    auto res = std::make_unique<tc_result>(n);
+    DeviceCall call;
+    float* d_coords = call.alloc<float>(n * ds->dim);
+    int32_t* d_labels = call.alloc<int32_t>(n);
+    uint8_t* d_core = call.alloc<uint8_t>(n);
+    TCB_CUDA(cudaMemcpyAsync(d_coords, ds->coords.ptr, sizeof(float) * n * ds->dim,
+                             cudaMemcpyHostToDevice, call.st));
+    device_cluster(call, d_coords, n, ds->dim, eps, minpts, algorithm, oracle_cap, d_labels,
+                   d_core, res.get());
+    if (algorithm == TC_ALGO_BRUTEFORCE) {  // the reference leaves timers/counters at 0
+      tc_cluster_stats& s = res->stats;
+      s.build_seconds = s.preprocess_seconds = s.main_seconds = s.finalize_seconds = 0.0;
+      s.preprocess_skipped = 0;
+      s.pair_resolutions = s.distance_evaluations = 0;
+    }
+    *out = res.release();
+    return TC_OK;
+  });
+}
+
+TC_EXPORT int64_t tc_result_size(const tc_result* res) { return res ? res->n : 0; }
+TC_EXPORT const int32_t* tc_result_labels(const tc_result* res) { return res ? res->labels.ptr : nullptr; }
+TC_EXPORT const uint8_t* tc_result_core_flags(const tc_result* res) { return res ? res->core.ptr : nullptr; }
+
+TC_EXPORT tc_status tc_result_stats(const tc_result* res, tc_cluster_stats* out) {
+  if (!res || !out) return TC_ERR_INVALID_ARGUMENT;
+  *out = res->stats;
+  return TC_OK;
+}
+
+TC_EXPORT void tc_result_free(tc_result* res) { delete res; }
+
+TC_EXPORT tc_status tc_verify(const tc_dataset* ds, float eps, int minpts, int threads,
+                              int64_t oracle_cap, char* report, size_t report_len) {
+  (void)threads;
+  if (!ds) return TC_ERR_INVALID_ARGUMENT;
+  std::string text;
+  tc_status status = guarded([&]() -> tc_status {
+    const int64_t n = ds->n;
+    const int dim = ds->dim;
+    const int64_t cap = oracle_cap > 0 ? oracle_cap : 10000;
+    DeviceCall call;
+    float* d_coords = call.alloc<float>(n * dim);
+    TCB_CUDA(cudaMemcpyAsync(d_coords, ds->coords.ptr, sizeof(float) * n * dim,
+                             cudaMemcpyHostToDevice, call.st));
+    struct Run {
+      std::unique_ptr<tc_result> res;
+      int32_t* d_labels;
+      uint8_t* d_core;
+      int64_t bad = -1;
+    };
+    auto run = [&](tc_algorithm algo) {
+      Run r{std::make_unique<tc_result>(n), call.alloc<int32_t>(n), call.alloc<uint8_t>(n)};
+      device_cluster(call, d_coords, n, dim, eps, minpts, algo, cap, r.d_labels, r.d_core,
+                     r.res.get());
+      r.bad = tcb::first_bad_border(d_coords, n, dim, eps, r.d_labels, r.d_core, call.st);
+      return r;
+    };
+    auto line = [&](const char* name, const Equivalence& e) {
+      text += name;
+      text += ": ";
+      text += e.pass ? std::string("PASS") : "FAIL \xE2\x80\x94 " + e.message;
+      text += '\n';
+    };
+    Run fd = run(TC_ALGO_FDBSCAN);
+    Run db = run(TC_ALGO_DENSEBOX);
+    bool all = true;
+    Equivalence x = check_equivalence(fd.res->labels.ptr, fd.res->core.ptr, db.res->labels.ptr,
+                                      db.res->core.ptr, n, fd.bad, db.bad);
+    line("fdbscan vs densebox", x);
+    all &= x.pass;
+    if (n <= cap) {
+      Run bf = run(TC_ALGO_BRUTEFORCE);
+      Equivalence a = check_equivalence(fd.res->labels.ptr, fd.res->core.ptr, bf.res->labels.ptr,
+                                        bf.res->core.ptr, n, fd.bad, bf.bad);
+      line("fdbscan vs bruteforce", a);
+      Equivalence b = check_equivalence(db.res->labels.ptr, db.res->core.ptr, bf.res->labels.ptr,
+                                        bf.res->core.ptr, n, db.bad, bf.bad);
+      line("densebox vs bruteforce", b);
+      all &= a.pass && b.pass;
+    } else {
+      std::ostringstream os;
+      os << "bruteforce reference skipped: n=" << n << " exceeds oracle cap " << cap
+         << " (cross-algorithm check only)\n";
+      text += os.str();
+    }
+    return all ? TC_OK : TC_ERR_VERIFY_FAIL;
+  });
+  if (report && report_len > 0) {
+    size_t len = std::min(report_len - 1, text.size());
+    std::memcpy(report, text.data(), len);
+    report[len] = '\0';
+  }
+  return status;
+}
+
+// ===========================================================================
+// Additive ABI (treeclust_gpu.h)
+// ===========================================================================
+
+TC_EXPORT int tcg_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+TC_EXPORT const char* tcg_version(void) { return "treeclust-b200 0.1 (sm_100a)"; }
+
+TC_EXPORT tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim, float eps,
+                                       int minpts, tc_algorithm algorithm, int64_t oracle_cap,
+                                       int32_t* d_labels, uint8_t* d_core, void* stream,
+                                       tc_cluster_stats* stats) {
+  return guarded([&]() -> tc_status {
+    tcb::RunOutput ro;
+    tcb::run_device(d_coords, n, dim, eps, minpts, algorithm, oracle_cap, d_labels, d_core,
+                    static_cast<cudaStream_t>(stream), stats != nullptr,
+                    stats ? &ro : nullptr);
+    if (stats) *stats = ro.stats;
+    return TC_OK;
+  });
+}
+
+TC_EXPORT int tcg_last_stage_ms(double* out, int cap) {
+  if (!out || cap <= 0) return 0;
+  return tcb::get_last_stage_ms(out, cap);
+}
+
+TC_EXPORT tc_status tcg_generate_hacc_like(int64_t n, double box_len, double halo_frac,
+                                           uint64_t seed, tc_dataset** out) {
+  if (!out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] { return publish(tcb::gen_hacc_like(n, box_len, halo_frac, seed), out); });
+}
+
+TC_EXPORT tc_status tcg_generate_taxi_like(int64_t n, uint64_t seed, tc_dataset** out) {
+  if (!out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] { return publish(tcb::gen_taxi_like(n, seed), out); });
+}
+
+TC_EXPORT tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n, float* eps,
+                                        int* minpts, tc_dataset** out) {
+  if (!out || !eps || !minpts || min_n < 1 || max_n < min_n) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    return publish(tcb::gen_random_instance(seed, min_n, max_n, eps, minpts), out);
+  });
+}
+
+TC_EXPORT tc_status tcg_dataset_create_pinned(const float* coords, int64_t n, int dim,
+                                              tc_dataset** out) {
+  return tc_dataset_create(coords, n, dim, out);  // large datasets are pinned already
+}

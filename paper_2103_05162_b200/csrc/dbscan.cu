@@ -1,0 +1,173 @@
+// FDBSCAN passes over the point BVH, and label finalization.
+//
+//   k_fd_core   fdbscan_mark_cores (dbscan.cpp:36-58): one thread per leaf
+//               rank (Morton order, so a warp's queries are spatial
+//               neighbours and walk nearly the same nodes), unmasked query,
+//               early exit once minpts neighbours (self included) are seen.
+//   k_fd_main   fdbscan_main_phase (dbscan.cpp:60-88): rank-masked query so
+//               every unordered within-eps pair is found exactly once, each
+//               pair resolved on the spot with the lock-free union-find; no
+//               neighbour list is ever stored.
+//   k_finalize  UnionFind::flatten + finalize_labels + the stats loop
+//               (union_find.hpp:77-86, dbscan.cpp:202-219, :274-282).
+//
+// For point leaves the leaf box test IS the exact distance test (the box is
+// degenerate and box_distance_sq reduces to distance_sq term by term, the
+// subtraction merely negated), so a visited leaf is a within-eps neighbour
+// and its distance is not recomputed.
+#include "device_common.cuh"
+#include "pipeline.hpp"
+
+namespace tcb {
+
+namespace {
+
+constexpr int kQueryBlock = 128;
+
+template <int D>
+__device__ __forceinline__ void load_query(const float4* leaf_pt, int64_t r, float* p,
+                                           int32_t* id) {
+  float4 q = leaf_pt[r];
+  p[0] = q.x;
+  p[1] = q.y;
+  if (D == 3) p[2] = q.z;
+  *id = __float_as_int(q.w);
+}
+
+__device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned long long v) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          double eps2, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
+  int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long dists = 0;
+  if (r < m) {
+    float p[3];
+    int32_t id;
+    load_query<D>(leaf_pt, r, p, &id);
+    int count = 0;
+    auto visit = [&](int32_t, int32_t, const float*, const float*) -> bool {
+      ++dists;
+      return ++count < minpts;  // early exit (dbscan.cpp:48-53)
+    };
+    bvh_query<D>(nodes, p, eps2, 0, visit);
+    if (count >= minpts) flags[id] = 1;
+  }
+  flush_counter(&ctr->dists, dists);
+}
+
+template <int D, bool kForceCore>
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          double eps2, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+          DevCounters* ctr) {
+  int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long pairs = 0;
+  if (r < m) {
+    float p[3];
+    int32_t i;
+    load_query<D>(leaf_pt, r, p, &i);
+    const int32_t rank = static_cast<int32_t>(r);
+    const bool core_i = kForceCore ? true : flags[i] != 0;
+    auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
+      if (s == rank) return true;
+      ++pairs;
+      if (kForceCore) {
+        flags[j] = 1;
+        uf_unite(parent, i, j);
+      } else {
+        resolve_pair(i, j, core_i, flags, parent);
+      }
+      return true;
+    };
+    bvh_query<D>(nodes, p, eps2, rank, visit);
+    if (kForceCore && pairs) flags[i] = 1;
+  }
+  flush_counter(&ctr->pairs, pairs);
+  flush_counter(&ctr->dists, pairs);
+}
+
+__global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    parent[i] = static_cast<int32_t>(i);
+}
+
+__global__ void __launch_bounds__(256)
+k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int64_t n,
+           int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr) {
+  long long noise = 0, clusters = 0, cores = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t p = ld_relaxed(parent + i);
+    int32_t q;
+    while (p != (q = ld_relaxed(parent + p))) p = q;
+    st_relaxed(parent + i, p);
+    const bool core = flags[i] != 0;
+    const int32_t lab = (core || p != i) ? p : -1;  // dbscan.cpp:215
+    labels[i] = lab;
+    core_out[i] = core ? 1 : 0;
+    noise += lab == -1;
+    clusters += lab == static_cast<int32_t>(i);
+    cores += core;
+  }
+  noise = warp_sum(noise);
+  clusters = warp_sum(clusters);
+  cores = warp_sum(cores);
+  if ((threadIdx.x & 31) == 0) {
+    if (noise) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->noise), noise);
+    if (clusters) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->clusters), clusters);
+    if (cores) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->cores), cores);
+  }
+}
+
+}  // namespace
+
+template <int D>
+void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
+                       uint8_t* flags, DevCounters* d_ctr, cudaStream_t s) {
+  k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
+      b.tree.nodes, b.leaf_pt, n, eps2, minpts, flags, d_ctr);
+  TCB_CUDA(cudaGetLastError());
+}
+
+template <int D>
+void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
+                       uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
+                       cudaStream_t s) {
+  const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
+  if (force_core)
+    k_fd_main<D, true><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
+                                                 parent, d_ctr);
+  else
+    k_fd_main<D, false><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
+                                                  parent, d_ctr);
+  TCB_CUDA(cudaGetLastError());
+}
+
+void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
+  k_init_uf<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
+  TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(n), s));
+  TCB_CUDA(cudaGetLastError());
+}
+
+void finalize_labels(int32_t* parent, const uint8_t* flags, int64_t n, int32_t* labels,
+                     uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s) {
+  k_finalize<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n, labels, core_out, d_ctr);
+  TCB_CUDA(cudaGetLastError());
+}
+
+template void fdbscan_core_pass<2>(const BuiltBvh&, int64_t, double, int, uint8_t*,
+                                   DevCounters*, cudaStream_t);
+template void fdbscan_core_pass<3>(const BuiltBvh&, int64_t, double, int, uint8_t*,
+                                   DevCounters*, cudaStream_t);
+template void fdbscan_main_pass<2>(const BuiltBvh&, int64_t, double, bool, uint8_t*,
+                                   int32_t*, DevCounters*, cudaStream_t);
+template void fdbscan_main_pass<3>(const BuiltBvh&, int64_t, double, bool, uint8_t*,
+                                   int32_t*, DevCounters*, cudaStream_t);
+
+}  // namespace tcb

@@ -1,0 +1,185 @@
+// Device-side primitives shared by every kernel of the engine.
+//
+// Arithmetic contract: coordinates are fp32, every distance and
+// box distance is accumulated in fp64 exactly like the reference's unfused
+// chain
+//     s = 0.0; for k: d = double(a_k) - double(b_k); s = s + d*d
+// (geometry.hpp:72-93) and compared `<= double(eps)*double(eps)`. We spell it
+// with __dsub_rn / __dmul_rn / __dadd_rn so nvcc can never contract it into a
+// DFMA (the translation units are also built with -fmad=false).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tcb {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// Exact fp64 predicates (geometry.hpp:72-93)
+// ---------------------------------------------------------------------------
+
+template <int D>
+__device__ __forceinline__ double dist2(const float* a, const float* b) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double d = __dsub_rn(static_cast<double>(a[k]), static_cast<double>(b[k]));
+    s = __dadd_rn(s, __dmul_rn(d, d));
+  }
+  return s;
+}
+
+// Squared distance from p to the closed box [lo, hi] (0 inside), same branch
+// structure as box_distance_sq (geometry.hpp:82-93).
+template <int D>
+__device__ __forceinline__ double box_dist2(const float* p, const float* lo,
+                                            const float* hi) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double d = 0.0;
+    if (p[k] < lo[k])
+      d = __dsub_rn(static_cast<double>(lo[k]), static_cast<double>(p[k]));
+    else if (p[k] > hi[k])
+      d = __dsub_rn(static_cast<double>(p[k]), static_cast<double>(hi[k]));
+    s = __dadd_rn(s, __dmul_rn(d, d));
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Morton codes (geometry.hpp:104-156): 31 bits/axis in 2D, 21 in 3D,
+// quantization in fp64, axis-major interleave (bit b of axis a -> b*dim + a).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t spread2(uint64_t x) {
+  x &= 0xffffffffull;
+  x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+  x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+  x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {
+  x &= 0x1fffffull;
+  x = (x | (x << 32)) & 0x001f00000000ffffull;
+  x = (x | (x << 16)) & 0x001f0000ff0000ffull;
+  x = (x | (x << 8)) & 0x100f00f00f00f00full;
+  x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+  x = (x | (x << 2)) & 0x1249249249249249ull;
+  return x;
+}
+
+// morton_quantize (geometry.hpp:132-141). `w` = double(hi) - double(lo) is
+// precomputed per axis; `cells` = 2^bits.
+__device__ __forceinline__ uint64_t quantize(float v, float lo, double w,
+                                             double cells_d, uint64_t cells) {
+  if (w <= 0.0) return 0;
+  double t = __ddiv_rn(__dsub_rn(static_cast<double>(v), static_cast<double>(lo)), w);
+  if (t < 0.0) t = 0.0;
+  uint64_t q = __double2ull_rz(__dmul_rn(t, cells_d));
+  if (q >= cells) q = cells - 1;
+  return q;
+}
+
+// ---------------------------------------------------------------------------
+// Order-preserving float <-> uint32 mapping for atomicMin/atomicMax bounds.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float ord2f(uint32_t u) {
+  uint32_t v = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(v);
+#else
+  float f;
+  __builtin_memcpy(&f, &v, 4);
+  return f;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Lock-free union-find over a flat int32 parent array (union_find.hpp:18-91).
+// Loads/stores are relaxed at GPU scope (L1 is not coherent, so plain loads
+// could spin on stale lines); hooks are single CASes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// find with pointer jumping: every visited node is redirected to its
+// grandparent (union_find.hpp:36-49).
+__device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t i) {
+  int32_t cur = ld_relaxed(parent + i);
+  if (cur != i) {
+    int32_t prev = i;
+    int32_t next = ld_relaxed(parent + cur);
+    while (cur != next) {
+      st_relaxed(parent + prev, next);
+      prev = cur;
+      cur = next;
+      next = ld_relaxed(parent + cur);
+    }
+  }
+  return cur;
+}
+
+// Hook the higher root under the lower one; retry from fresh roots when the
+// CAS loses (union_find.hpp:51-64). Representatives end up as the minimum
+// index of each component regardless of schedule.
+__device__ __forceinline__ void uf_unite(int32_t* parent, int32_t i, int32_t j) {
+  while (true) {
+    i = uf_find(parent, i);
+    j = uf_find(parent, j);
+    if (i == j) return;
+    if (i > j) {
+      int32_t t = i;
+      i = j;
+      j = t;
+    }
+    if (atomicCAS(parent + j, j, i) == j) return;
+  }
+}
+
+// One-shot border claim (union_find.hpp:69-73).
+__device__ __forceinline__ bool uf_claim(int32_t* parent, int32_t i, int32_t root) {
+  return atomicCAS(parent + i, i, root) == i;
+}
+
+// resolve_pair (dbscan.hpp:82-99): core-core unions, core-border claims the
+// border once (no bridging), border-border is a no-op. force_core is the
+// minpts == 2 case where every within-eps pair consists of core points.
+__device__ __forceinline__ void resolve_pair(int32_t i, int32_t j, bool core_i,
+                                             const uint8_t* flags, int32_t* parent) {
+  bool core_j = flags[j] != 0;
+  if (core_i && core_j)
+    uf_unite(parent, i, j);
+  else if (core_i) {
+    if (ld_relaxed(parent + j) == j) uf_claim(parent, j, uf_find(parent, i));
+  } else if (core_j) {
+    if (ld_relaxed(parent + i) == i) uf_claim(parent, i, uf_find(parent, j));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp / block reductions
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace tcb

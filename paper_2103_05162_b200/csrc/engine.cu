@@ -1,0 +1,225 @@
+// Orchestration of one device run (dbscan_run, dbscan.cpp:221-284, on the
+// GPU): validation, index build, core pass, fused main pass, finalize, and
+// per-stage CUDA-event timing into tc_cluster_stats.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <mutex>
+
+#include "device_common.cuh"
+#include "engine.hpp"
+#include "pipeline.hpp"
+
+namespace tcb {
+
+// ---------------------------------------------------------------------------
+// Scratch / staging / clock
+// ---------------------------------------------------------------------------
+namespace {
+
+void raise_pool_threshold() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = std::numeric_limits<uint64_t>::max();
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+thread_local double t_last_stage_ms[kNumStages] = {};
+
+}  // namespace
+
+Scratch::~Scratch() {
+  for (void* p : ptrs_) cudaFreeAsync(p, stream_);
+}
+
+void* Scratch::alloc(size_t bytes) {
+  if (ptrs_.empty()) raise_pool_threshold();
+  void* p = nullptr;
+  bytes = (bytes + 255) & ~size_t{255};
+  cudaError_t e = cudaMallocAsync(&p, bytes, stream_);
+  if (e != cudaSuccess) throw CudaFailure{e, __FILE__, __LINE__};
+  ptrs_.push_back(p);
+  return p;
+}
+
+void* pinned_staging(size_t bytes) {
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+    ~Buf() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  thread_local Buf buf;
+  if (buf.n < bytes) {
+    if (buf.p) cudaFreeHost(buf.p);
+    buf.p = nullptr;
+    size_t want = bytes < 4096 ? 4096 : bytes;
+    TCB_CUDA(cudaMallocHost(&buf.p, want));
+    buf.n = want;
+  }
+  return buf.p;
+}
+
+StageClock::StageClock(cudaStream_t s) : stream_(s) {
+  for (auto& e : ev_) e = nullptr;
+}
+
+StageClock::~StageClock() {
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+}
+
+void StageClock::mark(int stage_begin) {
+  if (count_ > kNumStages) return;
+  if (!ev_[count_]) TCB_CUDA(cudaEventCreate(&ev_[count_]));
+  TCB_CUDA(cudaEventRecord(ev_[count_], stream_));
+  stage_of_[count_] = stage_begin;
+  ++count_;
+}
+
+void StageClock::finish() { mark(-1); }
+
+void StageClock::collect(double* stage_ms) const {
+  for (int s = 0; s < kNumStages; ++s) stage_ms[s] = 0.0;
+  for (int i = 0; i + 1 < count_; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ev_[i], ev_[i + 1]) == cudaSuccess && stage_of_[i] >= 0)
+      stage_ms[stage_of_[i]] += ms;
+  }
+  if (count_ >= 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ev_[0], ev_[count_ - 1]) == cudaSuccess)
+      stage_ms[kStTotal] = ms;
+  }
+}
+
+void set_last_stage_ms(const double* ms) {
+  for (int s = 0; s < kNumStages; ++s) t_last_stage_ms[s] = ms[s];
+}
+
+int get_last_stage_ms(double* out, int cap) {
+  int k = cap < kNumStages ? cap : kNumStages;
+  for (int s = 0; s < k; ++s) out[s] = t_last_stage_ms[s];
+  return k;
+}
+
+// ---------------------------------------------------------------------------
+// FDBSCAN (dbscan.cpp:221-284 with Algorithm::Fdbscan)
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int D>
+void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
+                 uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock) {
+  cudaStream_t st = scratch.stream();
+  const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
+  PrimSource src;
+  src.coords = d_coords;
+  src.count = n;
+  clock.mark(kStBounds);
+  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock);
+
+  int32_t* parent = scratch.alloc_n<int32_t>(n);
+  uint8_t* flags = scratch.alloc_n<uint8_t>(n);
+  clock.mark(kStCore);
+  init_union_find(parent, flags, n, st);
+  if (minpts > 2) fdbscan_core_pass<D>(b, n, eps2, minpts, flags, ctr, st);
+  clock.mark(kStMain);
+  fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, st);
+  clock.mark(kStFinal);
+  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st);
+  clock.finish();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Entry
+// ---------------------------------------------------------------------------
+void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
+                tc_algorithm algo, int64_t oracle_cap, int32_t* d_labels, uint8_t* d_core,
+                cudaStream_t stream, bool want_stats, RunOutput* out,
+                const std::function<void(cudaStream_t)>& tail) {
+  if (dim != 2 && dim != 3) throw InvalidArgument{"PointSet: dimension must be 2 or 3"};
+  if (n < 1) throw InvalidArgument{"PointSet: empty"};
+  if (!(eps > 0.f) || !std::isfinite(eps))
+    throw InvalidArgument{"eps must be positive and finite"};
+  if (minpts < 2) throw InvalidArgument{"minpts must be >= 2"};
+  if (n > std::numeric_limits<int32_t>::max())
+    throw InvalidArgument{"dbscan_run: more than 2^31-1 points"};
+  if (!d_coords || !d_labels || !d_core) throw InvalidArgument{"null buffer"};
+
+  Scratch scratch(stream);
+  StageClock clock(stream);
+  DevCounters* ctr = scratch.alloc_n<DevCounters>(1);
+  TCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), stream));
+
+  double dense_fraction = 0.0;
+  switch (algo) {
+    case TC_ALGO_FDBSCAN:
+      if (dim == 2)
+        run_fdbscan<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock);
+      else
+        run_fdbscan<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock);
+      break;
+    case TC_ALGO_DENSEBOX:
+      if (dim == 2)
+        run_densebox<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock,
+                        &dense_fraction);
+      else
+        run_densebox<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock,
+                        &dense_fraction);
+      break;
+    case TC_ALGO_BRUTEFORCE: {
+      int64_t cap = oracle_cap > 0 ? oracle_cap : 10000;
+      if (n > cap) throw CapExceeded{};
+      clock.mark(kStMain);
+      if (dim == 2)
+        run_bruteforce<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch);
+      else
+        run_bruteforce<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch);
+      clock.finish();
+      break;
+    }
+    default:
+      throw InvalidArgument{"unknown algorithm"};
+  }
+
+  if (tail) tail(stream);
+  if (want_stats || out) {
+    DevCounters h;
+    TCB_CUDA(cudaMemcpyAsync(&h, ctr, sizeof h, cudaMemcpyDeviceToHost, stream));
+    TCB_CUDA(cudaStreamSynchronize(stream));
+    RunOutput ro;
+    clock.collect(ro.stage_ms);
+    set_last_stage_ms(ro.stage_ms);
+    tc_cluster_stats& s = ro.stats;
+    s.build_seconds =
+        (ro.stage_ms[kStBounds] + ro.stage_ms[kStSort] + ro.stage_ms[kStTopo] +
+         ro.stage_ms[kStGrid]) * 1e-3;
+    s.preprocess_seconds = ro.stage_ms[kStCore] * 1e-3;
+    s.main_seconds = ro.stage_ms[kStMain] * 1e-3;
+    s.finalize_seconds = ro.stage_ms[kStFinal] * 1e-3;
+    s.preprocess_skipped = (algo != TC_ALGO_BRUTEFORCE && minpts == 2) ? 1 : 0;
+    s.dense_point_fraction = dense_fraction;
+    if (algo != TC_ALGO_BRUTEFORCE) {
+      s.pair_resolutions = h.pairs;
+      s.distance_evaluations = h.dists;
+    }
+    s.cluster_count = h.clusters;
+    s.core_count = h.cores;
+    s.noise_count = h.noise;
+    if (out) *out = ro;
+  }
+}
+
+}  // namespace tcb

@@ -1,0 +1,53 @@
+// Host-side interface between the C ABI (capi.cpp) and the device pipeline.
+// No torch types, no exceptions across the ABI: every entry returns tc_status.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <functional>
+
+#include "treeclust.h"
+
+namespace tcb {
+
+// Internal exceptions thrown inside the engine and mapped to tc_status at the
+// ABI (mirrors `guarded`, capi.cpp:30-43).
+struct InvalidArgument {
+  const char* what;
+};
+struct CapExceeded {};
+struct CudaFailure {
+  cudaError_t err;
+  const char* file;
+  int line;
+};
+
+#define TCB_CUDA(expr)                                              \
+  do {                                                              \
+    cudaError_t _e = (expr);                                        \
+    if (_e != cudaSuccess) throw ::tcb::CudaFailure{_e, __FILE__, __LINE__}; \
+  } while (0)
+
+// Per-stage device milliseconds (see tcg_last_stage_ms in treeclust_gpu.h).
+enum Stage { kStBounds = 0, kStSort, kStTopo, kStGrid, kStCore, kStMain, kStFinal, kStTotal, kNumStages };
+
+struct RunOutput {
+  tc_cluster_stats stats{};
+  double stage_ms[kNumStages]{};
+};
+
+// Full device pipeline. d_coords/d_labels/d_core are device pointers.
+// want_stats: synchronize at the end and fill `out`.
+// `tail` (optional) is invoked after the last kernel is enqueued and before
+// the final synchronization, e.g. to enqueue the device->host result copies.
+void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
+                tc_algorithm algo, int64_t oracle_cap, int32_t* d_labels,
+                uint8_t* d_core, cudaStream_t stream, bool want_stats,
+                RunOutput* out,
+                const std::function<void(cudaStream_t)>& tail = nullptr);
+
+// Thread-local copy of the last run's stage times.
+void set_last_stage_ms(const double* ms);
+int get_last_stage_ms(double* out, int cap);
+
+}  // namespace tcb

@@ -1,0 +1,515 @@
+// FDBSCAN-DenseBox on the device (reference: dense_grid.cpp:12-98,
+// dbscan.cpp:90-200).
+//
+// Grid (build_grid, dense_grid.cpp:23-77)
+//   k_grid_setup      h = eps/sqrt(d), extents, 2^62 overflow guard (fp64,
+//                     same expressions as the reference)
+//   k_cell_ids        u64 row-major cell id per point (x fastest), fused AND/OR
+//   radix_sort_pairs  perm = points sorted by (cell id, index)
+//   k_cell_heads      segment boundaries -> scan -> Cell{begin,end,dense}
+// Mixed primitives (make_mixed_primitives, dense_grid.cpp:79-98)
+//   one DenseBox (tight member box, warp-segmented min/max + atomics) per
+//   dense cell, one SinglePoint per member of every other cell, in cell-id
+//   order -> the same primitive indices as the reference, so the BVH (sorted
+//   by (Morton code, primitive index)) is the reference's tree.
+// Queries are issued in leaf-rank order: a dense box's members are one
+// contiguous run of queries, so each warp shares one neighbourhood.
+//   k_dense_union     union_dense_cells (dbscan.cpp:90-108): direct hooks
+//   k_db_core         densebox_mark_cores (dbscan.cpp:110-139)
+//   k_db_main         densebox_main_phase (dbscan.cpp:141-200)
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+
+#include "device_common.cuh"
+#include "pipeline.hpp"
+#include "primitives.cuh"
+
+namespace tcb {
+
+namespace {
+
+constexpr int kQueryBlock = 128;
+
+struct GridParams {
+  double h;
+  float origin[3];
+  int64_t extent[3];
+  int32_t overflow;
+};
+
+template <int D>
+__global__ void k_grid_setup(const DevCounters* ctr, double h, GridParams* gp) {
+  uint64_t total_check = 1;
+  gp->h = h;
+  gp->overflow = 0;
+  for (int k = 0; k < D; ++k) {
+    float lo = ord2f(ctr->bounds_ord[k]);
+    float hi = ord2f(ctr->bounds_ord[3 + k]);
+    gp->origin[k] = lo;
+    double width = __dsub_rn(static_cast<double>(hi), static_cast<double>(lo));
+    int64_t e = static_cast<int64_t>(ceil(__ddiv_rn(width, h)));
+    if (e < 1) e = 1;
+    gp->extent[k] = e;
+    if (total_check > (1ull << 62) / static_cast<uint64_t>(e)) gp->overflow = 1;
+    total_check *= static_cast<uint64_t>(e);
+  }
+}
+
+// cell_coord (dense_grid.cpp:12-19)
+__device__ __forceinline__ int64_t cell_coord(float v, float origin, double h, int64_t extent) {
+  int64_t c = static_cast<int64_t>(
+      floor(__ddiv_rn(__dsub_rn(static_cast<double>(v), static_cast<double>(origin)), h)));
+  if (c < 0) c = 0;
+  if (c >= extent) c = extent - 1;
+  return c;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_cell_ids(const float* __restrict__ coords, int64_t n, const GridParams* __restrict__ gp,
+           uint64_t* __restrict__ keys, int32_t* __restrict__ vals, DevCounters* ctr) {
+  const double h = gp->h;
+  uint64_t acc_and = ~0ull, acc_or = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t id = 0;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) {
+      int64_t c = cell_coord(coords[i * D + k], gp->origin[k], h, gp->extent[k]);
+      id = id * static_cast<uint64_t>(gp->extent[k]) + static_cast<uint64_t>(c);
+    }
+    keys[i] = id;
+    vals[i] = static_cast<int32_t>(i);
+    acc_and &= id;
+    acc_or |= id;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc_and &= __shfl_xor_sync(0xffffffffu, acc_and, o);
+    acc_or |= __shfl_xor_sync(0xffffffffu, acc_or, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAnd(&ctr->key_and, acc_and);
+    atomicOr(&ctr->key_or, acc_or);
+  }
+}
+
+__global__ void k_reset_keys(DevCounters* ctr) {
+  ctr->key_and = ~0ull;
+  ctr->key_or = 0ull;
+  ctr->count_a = 0;
+}
+
+// head[k] = 1 where a new cell starts in sorted order.
+__global__ void __launch_bounds__(256)
+k_cell_heads(const uint64_t* __restrict__ ids, int64_t n, int32_t* __restrict__ head) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    head[k] = (k == 0 || ids[k] != ids[k - 1]) ? 1 : 0;
+}
+
+// From the exclusive scan of heads: cell index per sorted position, cell
+// begins, and sorted member points (coords + id) for contiguous box scans.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_cell_fill(const int32_t* __restrict__ head, const int32_t* __restrict__ head_excl,
+            const int32_t* __restrict__ perm, const float* __restrict__ coords, int64_t n,
+            int32_t* __restrict__ cell_of_sorted, int32_t* __restrict__ cell_begin,
+            float4* __restrict__ sorted_pt) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t c = head_excl[k] + head[k] - 1;
+    cell_of_sorted[k] = c;
+    if (head[k]) cell_begin[c] = static_cast<int32_t>(k);
+    int32_t i = perm[k];
+    float x = coords[static_cast<int64_t>(i) * D], y = coords[static_cast<int64_t>(i) * D + 1];
+    float z = D == 3 ? coords[static_cast<int64_t>(i) * D + 2] : 0.f;
+    sorted_pt[k] = make_float4(x, y, z, __int_as_float(i));
+  }
+}
+
+// Per cell: end, dense flag, primitive count (1 for dense, size otherwise).
+__global__ void __launch_bounds__(256)
+k_cell_prims(int32_t* __restrict__ cell_begin, int32_t num_cells, int64_t n, int minpts,
+             int32_t* __restrict__ cell_end, uint8_t* __restrict__ cell_dense,
+             int32_t* __restrict__ prim_count, DevCounters* ctr) {
+  int dense_cells = 0;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < num_cells;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t b = cell_begin[c];
+    int32_t e = c + 1 < num_cells ? cell_begin[c + 1] : static_cast<int32_t>(n);
+    cell_end[c] = e;
+    bool dense = (e - b) >= minpts;
+    cell_dense[c] = dense;
+    prim_count[c] = dense ? 1 : (e - b);
+    dense_cells += dense;
+  }
+  dense_cells = warp_sum(dense_cells);
+  if ((threadIdx.x & 31) == 0 && dense_cells) atomicAdd(&ctr->count_a, dense_cells);
+}
+
+// Dense primitives: identity boxes (ordered-uint encoding) + payload ~cell.
+__global__ void __launch_bounds__(256)
+k_prim_init(const uint8_t* __restrict__ cell_dense, const int32_t* __restrict__ prim_off,
+            int32_t num_cells, uint4* __restrict__ prim_lo, uint4* __restrict__ prim_hi,
+            int32_t* __restrict__ prim_aux) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < num_cells;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!cell_dense[c]) continue;
+    int32_t p = prim_off[c];
+    prim_lo[p] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0u);
+    prim_hi[p] = make_uint4(0u, 0u, 0u, 0u);
+    prim_aux[p] = ~static_cast<int32_t>(c);
+  }
+}
+
+// One thread per sorted position. Sparse members become SinglePoint
+// primitives; dense members are min/max-reduced over their warp-local run of
+// the cell (cells are contiguous in sorted order) and one lane per run
+// publishes with atomicMin/Max on the order-preserving encoding.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_prim_fill(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_of_sorted,
+            const int32_t* __restrict__ cell_begin, const uint8_t* __restrict__ cell_dense,
+            const int32_t* __restrict__ prim_off, int64_t n, float4* __restrict__ prim_lo,
+            float4* __restrict__ prim_hi, int32_t* __restrict__ prim_aux) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31); base < n;
+       base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t k = base + lane;
+    const bool valid = k < n;
+    int32_t c = valid ? cell_of_sorted[k] : -1 - lane;  // invalid lanes: unique fake cells
+    float4 pt = valid ? sorted_pt[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    bool dense = valid && cell_dense[c];
+    if (valid && !dense) {
+      int32_t p = prim_off[c] + static_cast<int32_t>(k - cell_begin[c]);
+      prim_lo[p] = make_float4(pt.x, pt.y, pt.z, 0.f);
+      prim_hi[p] = make_float4(pt.x, pt.y, pt.z, 0.f);
+      prim_aux[p] = __float_as_int(pt.w);
+    }
+    float mn[3] = {pt.x, pt.y, pt.z}, mx[3] = {pt.x, pt.y, pt.z};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t oc = __shfl_down_sync(0xffffffffu, c, o);
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        float a = __shfl_down_sync(0xffffffffu, mn[q], o);
+        float b = __shfl_down_sync(0xffffffffu, mx[q], o);
+        if (lane + o < 32 && oc == c) {
+          mn[q] = fminf(mn[q], a);
+          mx[q] = fmaxf(mx[q], b);
+        }
+      }
+    }
+    int32_t prev_c = __shfl_up_sync(0xffffffffu, c, 1);
+    bool run_head = lane == 0 || prev_c != c;
+    if (dense && run_head) {
+      int32_t p = prim_off[c];
+      uint32_t* lo = reinterpret_cast<uint32_t*>(prim_lo + p);
+      uint32_t* hi = reinterpret_cast<uint32_t*>(prim_hi + p);
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        atomicMin(lo + q, f2ord(mn[q]));
+        atomicMax(hi + q, f2ord(mx[q]));
+      }
+    }
+  }
+}
+
+// Decode the dense boxes back to floats.
+__global__ void __launch_bounds__(256)
+k_prim_decode(const uint8_t* __restrict__ cell_dense, const int32_t* __restrict__ prim_off,
+              int32_t num_cells, float4* __restrict__ prim_lo, float4* __restrict__ prim_hi) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < num_cells;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!cell_dense[c]) continue;
+    int32_t p = prim_off[c];
+    uint4 a = *reinterpret_cast<uint4*>(prim_lo + p);
+    uint4 b = *reinterpret_cast<uint4*>(prim_hi + p);
+    prim_lo[p] = make_float4(ord2f(a.x), ord2f(a.y), ord2f(a.z), 0.f);
+    prim_hi[p] = make_float4(ord2f(b.x), ord2f(b.y), ord2f(b.z), 0.f);
+  }
+}
+
+// rank_of_prim[order[s]] = s; per leaf query count (1 or the cell's size).
+__global__ void __launch_bounds__(256)
+k_leaf_counts(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
+              const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
+              int64_t m, int32_t* __restrict__ rank_of_prim, int32_t* __restrict__ qcount) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t p = order[s];
+    rank_of_prim[p] = static_cast<int32_t>(s);
+    int32_t a = prim_aux[p];
+    qcount[s] = a >= 0 ? 1 : cell_end[~a] - cell_begin[~a];
+  }
+}
+
+// Query slots in leaf order: qpt = (coords, id | dense<<31), qrank = own leaf
+// rank. Also union_dense_cells: every dense member is core and hooked straight
+// under the cell's first (= minimum-index) member.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_of_sorted,
+          const int32_t* __restrict__ cell_begin, const uint8_t* __restrict__ cell_dense,
+          const int32_t* __restrict__ prim_off, const int32_t* __restrict__ rank_of_prim,
+          const int32_t* __restrict__ qoff, int64_t n, float4* __restrict__ qpt,
+          int32_t* __restrict__ qrank, int32_t* __restrict__ parent,
+          uint8_t* __restrict__ flags) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t c = cell_of_sorted[k];
+    const int32_t b = cell_begin[c];
+    const bool dense = cell_dense[c];
+    const int32_t off = static_cast<int32_t>(k - b);
+    const int32_t p = prim_off[c] + (dense ? 0 : off);
+    const int32_t s = rank_of_prim[p];
+    const int32_t dst = qoff[s] + (dense ? off : 0);
+    float4 pt = sorted_pt[k];
+    const int32_t i = __float_as_int(pt.w);
+    if (dense) {
+      pt.w = __int_as_float(i | static_cast<int32_t>(0x80000000u));
+      flags[i] = 1;
+      parent[i] = __float_as_int(sorted_pt[b].w);  // dbscan.cpp:98-104
+    }
+    qpt[dst] = pt;
+    qrank[dst] = s;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kQueryBlock)
+k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
+          const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
+          const int32_t* __restrict__ cell_end, double eps2, int minpts,
+          uint8_t* __restrict__ flags, DevCounters* ctr) {
+  int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long dists = 0;
+  if (q < n) {
+    float4 qp = qpt[q];
+    const int32_t raw = __float_as_int(qp.w);
+    if (raw >= 0) {  // dense members are core already (dbscan.cpp:118)
+      float p[3] = {qp.x, qp.y, qp.z};
+      int count = 0;
+      auto visit = [&](int32_t, int32_t aux, const float*, const float*) -> bool {
+        if (aux >= 0) {
+          ++dists;
+          ++count;  // leaf box test == exact distance test for a point leaf
+        } else {
+          const int32_t c = ~aux;
+          for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
+            float4 m4 = __ldg(sorted_pt + k);
+            float mp[3] = {m4.x, m4.y, m4.z};
+            ++dists;
+            if (dist2<D>(p, mp) <= eps2)
+              if (++count >= minpts) break;
+          }
+        }
+        return count < minpts;
+      };
+      bvh_query<D>(nodes, p, eps2, 0, visit);
+      if (count >= minpts) flags[raw] = 1;
+    }
+  }
+  unsigned long long v = warp_sum(dists);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
+}
+
+template <int D, bool kForceCore>
+__global__ void __launch_bounds__(kQueryBlock)
+k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
+          const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
+          const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
+          double eps2, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+          DevCounters* ctr) {
+  int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long dists = 0, pairs = 0;
+  if (q < n) {
+    float4 qp = qpt[q];
+    const int32_t i = __float_as_int(qp.w) & 0x7fffffff;
+    const int32_t own = qrank[q];
+    float p[3] = {qp.x, qp.y, qp.z};
+    const bool core_i = kForceCore ? true : flags[i] != 0;
+    auto pair = [&](int32_t j) {
+      ++pairs;
+      if (kForceCore) {
+        flags[i] = 1;
+        flags[j] = 1;
+        uf_unite(parent, i, j);
+      } else {
+        resolve_pair(i, j, core_i, flags, parent);
+      }
+    };
+    auto visit = [&](int32_t s, int32_t aux, const float*, const float*) -> bool {
+      if (s == own) return true;
+      if (aux >= 0) {
+        ++dists;
+        pair(aux);
+      } else {
+        const int32_t c = ~aux;
+        for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
+          float4 m4 = __ldg(sorted_pt + k);
+          float mp[3] = {m4.x, m4.y, m4.z};
+          ++dists;
+          if (dist2<D>(p, mp) <= eps2) {
+            pair(__float_as_int(m4.w));
+            break;  // one link joins the whole pre-unioned box (dbscan.cpp:183-193)
+          }
+        }
+      }
+      return true;
+    };
+    bvh_query<D>(nodes, p, eps2, own, visit);
+  }
+  unsigned long long v = warp_sum(dists);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
+  v = warp_sum(pairs);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
+}
+
+}  // namespace
+
+template <int D>
+void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
+                  uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
+                  double* dense_fraction) {
+  cudaStream_t st = scratch.stream();
+  const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
+  clock.mark(kStGrid);
+
+  // ---- grid ----
+  launch_point_bounds<D>(d_coords, n, ctr, st);
+  GridParams* gp = scratch.alloc_n<GridParams>(1);
+  const double h = static_cast<double>(eps) / std::sqrt(static_cast<double>(D));
+  k_grid_setup<D><<<1, 1, 0, st>>>(ctr, h, gp);
+  uint64_t* keys = scratch.alloc_n<uint64_t>(n);
+  int32_t* vals = scratch.alloc_n<int32_t>(n);
+  k_cell_ids<D><<<grid_for(n, 256), 256, 0, st>>>(d_coords, n, gp, keys, vals, ctr);
+  TCB_CUDA(cudaGetLastError());
+  auto* h_stage = static_cast<unsigned char*>(pinned_staging(64));
+  TCB_CUDA(cudaMemcpyAsync(h_stage, &ctr->key_and, 16, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaMemcpyAsync(h_stage + 16, &ctr->nonfinite, 4, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaMemcpyAsync(h_stage + 20, &gp->overflow, 4, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaStreamSynchronize(st));
+  unsigned long long key_and, key_or;
+  int32_t nonfinite, overflow;
+  std::memcpy(&key_and, h_stage, 8);
+  std::memcpy(&key_or, h_stage + 8, 8);
+  std::memcpy(&nonfinite, h_stage + 16, 4);
+  std::memcpy(&overflow, h_stage + 20, 4);
+  if (nonfinite) throw InvalidArgument{"PointSet: non-finite coordinate"};
+  if (overflow) throw InvalidArgument{"build_grid: eps too small for domain (cell id overflow)"};
+
+  uint64_t* keys_alt = scratch.alloc_n<uint64_t>(n);
+  int32_t* vals_alt = scratch.alloc_n<int32_t>(n);
+  void* sort_tmp = scratch.alloc(radix_sort_scratch_bytes(n));
+  bool in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, n, key_and, key_or, sort_tmp, st);
+  const uint64_t* ids = in_alt ? keys_alt : keys;
+  const int32_t* perm = in_alt ? vals_alt : vals;
+
+  int32_t* head = scratch.alloc_n<int32_t>(n);
+  int32_t* head_excl = scratch.alloc_n<int32_t>(n);
+  int32_t* d_tot = scratch.alloc_n<int32_t>(4);
+  void* scan_tmp = scratch.alloc(scan_scratch_bytes(n));
+  k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(ids, n, head);
+  exclusive_scan_i32(head, head_excl, n, d_tot, scan_tmp, st);
+  int32_t* cell_of_sorted = scratch.alloc_n<int32_t>(n);
+  int32_t* cell_begin = scratch.alloc_n<int32_t>(n);
+  float4* sorted_pt = scratch.alloc_n<float4>(n);
+  k_cell_fill<D><<<grid_for(n, 256), 256, 0, st>>>(head, head_excl, perm, d_coords, n,
+                                                   cell_of_sorted, cell_begin, sorted_pt);
+  TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot, 4, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaStreamSynchronize(st));
+  int32_t num_cells;
+  std::memcpy(&num_cells, h_stage, 4);
+
+  // ---- mixed primitives ----
+  int32_t* cell_end = scratch.alloc_n<int32_t>(num_cells);
+  uint8_t* cell_dense = scratch.alloc_n<uint8_t>(num_cells);
+  int32_t* prim_count = scratch.alloc_n<int32_t>(num_cells);
+  int32_t* prim_off = scratch.alloc_n<int32_t>(num_cells);
+  k_reset_keys<<<1, 1, 0, st>>>(ctr);
+  k_cell_prims<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_begin, num_cells, n, minpts,
+                                                         cell_end, cell_dense, prim_count, ctr);
+  exclusive_scan_i32(prim_count, prim_off, num_cells, d_tot + 1, scan_tmp, st);
+  TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot + 1, 4, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaMemcpyAsync(h_stage + 4, &ctr->count_a, 4, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaStreamSynchronize(st));
+  int32_t num_prims, num_dense;
+  std::memcpy(&num_prims, h_stage, 4);
+  std::memcpy(&num_dense, h_stage + 4, 4);
+  const int64_t sparse_points = num_prims - num_dense;
+  *dense_fraction = static_cast<double>(n - sparse_points) / static_cast<double>(n);
+
+  float4* prim_lo = scratch.alloc_n<float4>(num_prims);
+  float4* prim_hi = scratch.alloc_n<float4>(num_prims);
+  int32_t* prim_aux = scratch.alloc_n<int32_t>(num_prims);
+  if (num_dense > 0)
+    k_prim_init<<<grid_for(num_cells, 256), 256, 0, st>>>(
+        cell_dense, prim_off, num_cells, reinterpret_cast<uint4*>(prim_lo),
+        reinterpret_cast<uint4*>(prim_hi), prim_aux);
+  k_prim_fill<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
+                                                   cell_dense, prim_off, n, prim_lo, prim_hi,
+                                                   prim_aux);
+  if (num_dense > 0)
+    k_prim_decode<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_dense, prim_off, num_cells,
+                                                            prim_lo, prim_hi);
+  TCB_CUDA(cudaGetLastError());
+
+  // ---- BVH over the mixed primitives ----
+  PrimSource src;
+  src.lo = prim_lo;
+  src.hi = prim_hi;
+  src.aux = prim_aux;
+  src.count = num_prims;
+  clock.mark(kStBounds);
+  BuiltBvh b = build_bvh<D>(src, false, ctr, scratch, &clock);
+
+  // ---- query order + dense unions ----
+  clock.mark(kStGrid);
+  int32_t* rank_of_prim = scratch.alloc_n<int32_t>(num_prims);
+  int32_t* qcount = scratch.alloc_n<int32_t>(num_prims);
+  int32_t* qoff = scratch.alloc_n<int32_t>(num_prims);
+  k_leaf_counts<<<grid_for(num_prims, 256), 256, 0, st>>>(b.tree.leaf_order, prim_aux,
+                                                          cell_begin, cell_end, num_prims,
+                                                          rank_of_prim, qcount);
+  exclusive_scan_i32(qcount, qoff, num_prims, nullptr, scan_tmp, st);
+  float4* qpt = scratch.alloc_n<float4>(n);
+  int32_t* qrank = scratch.alloc_n<int32_t>(n);
+  int32_t* parent = scratch.alloc_n<int32_t>(n);
+  uint8_t* flags = scratch.alloc_n<uint8_t>(n);
+  init_union_find(parent, flags, n, st);
+  k_queries<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
+                                                 cell_dense, prim_off, rank_of_prim, qoff, n,
+                                                 qpt, qrank, parent, flags);
+  TCB_CUDA(cudaGetLastError());
+
+  // ---- core pass ----
+  clock.mark(kStCore);
+  const unsigned gq = grid_for(n, kQueryBlock, INT32_MAX);
+  if (minpts > 2)
+    k_db_core<D><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
+                                             cell_end, eps2, minpts, flags, ctr);
+  // ---- main pass ----
+  clock.mark(kStMain);
+  if (minpts == 2)
+    k_db_main<D, true><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+                                                   cell_begin, cell_end, eps2, flags, parent,
+                                                   ctr);
+  else
+    k_db_main<D, false><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+                                                    cell_begin, cell_end, eps2, flags, parent,
+                                                    ctr);
+  TCB_CUDA(cudaGetLastError());
+  clock.mark(kStFinal);
+  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st);
+  clock.finish();
+}
+
+template void run_densebox<2>(const float*, int64_t, float, int, int32_t*, uint8_t*,
+                              DevCounters*, Scratch&, StageClock&, double*);
+template void run_densebox<3>(const float*, int64_t, float, int, int32_t*, uint8_t*,
+                              DevCounters*, Scratch&, StageClock&, double*);
+
+}  // namespace tcb

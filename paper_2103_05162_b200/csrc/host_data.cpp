@@ -1,0 +1,372 @@
+// Host-side generators and file formats (see host_data.hpp).
+#include "host_data.hpp"
+
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+namespace tcb {
+
+void validate_points(int dim, const float* coords, int64_t count_floats) {
+  if (dim != 2 && dim != 3) throw std::invalid_argument("PointSet: dimension must be 2 or 3");
+  if (count_floats <= 0 || count_floats % dim != 0)
+    throw std::invalid_argument("PointSet: coordinate count not a multiple of dim");
+  for (int64_t i = 0; i < count_floats; ++i)
+    if (!std::isfinite(coords[i])) throw std::invalid_argument("PointSet: non-finite coordinate");
+}
+
+double SplitMix64::normal() {
+  if (has_spare_) {
+    has_spare_ = false;
+    return spare_;
+  }
+  double u1 = next_double();
+  double u2 = next_double();
+  while (u1 == 0.0) u1 = next_double();
+  const double mag = std::sqrt(-2.0 * std::log(u1));
+  const double ang = 2.0 * 3.141592653589793 * u2;
+  spare_ = mag * std::sin(ang);
+  has_spare_ = true;
+  return mag * std::cos(ang);
+}
+
+// gaussian_blobs (datagen.cpp:10-53): centres rejection-sampled at least
+// `separation` apart in [0, separation*(k+1))^dim, then per_blob normal
+// samples per centre.
+HostPoints gen_blobs(int k, int64_t per_blob, int dim, float separation, float sigma,
+                     uint64_t seed) {
+  if (k < 1 || per_blob < 1)
+    throw std::invalid_argument("gaussian_blobs: k and per_blob must be >= 1");
+  if (dim != 2 && dim != 3) throw std::invalid_argument("gaussian_blobs: dim must be 2 or 3");
+  SplitMix64 rng(seed);
+  const double domain = static_cast<double>(separation) * (k + 1);
+  const double sep2 = static_cast<double>(separation) * separation;
+  std::vector<double> centres;
+  centres.reserve(static_cast<size_t>(k) * dim);
+  for (int c = 0; c < k; ++c) {
+    for (int attempt = 1;; ++attempt) {
+      if (attempt > 10000)
+        throw std::runtime_error("gaussian_blobs: could not place separated centers");
+      double cand[3];
+      for (int a = 0; a < dim; ++a) cand[a] = rng.uniform(0.0, domain);
+      bool far_enough = true;
+      for (int o = 0; o < c && far_enough; ++o) {
+        double d2 = 0;
+        for (int a = 0; a < dim; ++a) {
+          double d = cand[a] - centres[static_cast<size_t>(o) * dim + a];
+          d2 += d * d;
+        }
+        far_enough = d2 >= sep2;
+      }
+      if (far_enough) {
+        centres.insert(centres.end(), cand, cand + dim);
+        break;
+      }
+    }
+  }
+  HostPoints out;
+  out.dim = dim;
+  out.coords.reserve(static_cast<size_t>(k) * per_blob * dim);
+  for (int c = 0; c < k; ++c)
+    for (int64_t i = 0; i < per_blob; ++i)
+      for (int a = 0; a < dim; ++a)
+        out.coords.push_back(
+            static_cast<float>(centres[static_cast<size_t>(c) * dim + a] + sigma * rng.normal()));
+  return out;
+}
+
+// uniform_noise (datagen.cpp:55-68).
+HostPoints gen_uniform(int64_t n, int dim, const float* lo, const float* hi, uint64_t seed) {
+  if (n < 1) throw std::invalid_argument("uniform_noise: n must be >= 1");
+  if (dim != 2 && dim != 3) throw std::invalid_argument("uniform_noise: dim must be 2 or 3");
+  SplitMix64 rng(seed);
+  HostPoints out;
+  out.dim = dim;
+  out.coords.resize(static_cast<size_t>(n) * dim);
+  for (int64_t i = 0; i < n; ++i)
+    for (int a = 0; a < dim; ++a)
+      out.coords[static_cast<size_t>(i) * dim + a] = static_cast<float>(rng.uniform(lo[a], hi[a]));
+  return out;
+}
+
+// dense_lattice (datagen.cpp:70-88): side^dim points, x fastest.
+HostPoints gen_lattice(int64_t side, int dim, float spacing) {
+  if (side < 2) throw std::invalid_argument("dense_lattice: side must be >= 2");
+  if (dim != 2 && dim != 3) throw std::invalid_argument("dense_lattice: dim must be 2 or 3");
+  int64_t n = side;
+  for (int a = 1; a < dim; ++a) n *= side;
+  HostPoints out;
+  out.dim = dim;
+  out.coords.reserve(static_cast<size_t>(n) * dim);
+  int64_t idx[3] = {0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) {
+    for (int a = 0; a < dim; ++a)
+      out.coords.push_back(static_cast<float>(idx[a] * static_cast<double>(spacing)));
+    for (int a = 0; a < dim; ++a) {
+      if (++idx[a] < side) break;
+      idx[a] = 0;
+    }
+  }
+  return out;
+}
+
+// testutil::random_instance (tests/test_util.hpp:27-60): blobs + 10-50%
+// uniform noise in [0,10]^d, eps log-uniform in [0.05, 2], minpts from
+// {2,3,5,10,25}.
+HostPoints gen_random_instance(uint64_t seed, int64_t min_n, int64_t max_n, float* eps,
+                               int* minpts) {
+  SplitMix64 rng(seed);
+  HostPoints out;
+  const int dim = (rng.next() % 2) ? 2 : 3;
+  const int64_t n = min_n + static_cast<int64_t>(rng.next() % static_cast<uint64_t>(max_n - min_n + 1));
+  const int blobs = 1 + static_cast<int>(rng.next() % 4);
+  const auto n_noise = static_cast<int64_t>(n * rng.uniform(0.1, 0.5));
+  const int64_t n_blob = n - n_noise;
+  out.dim = dim;
+  out.coords.reserve(static_cast<size_t>(n) * dim);
+  std::vector<double> centres;
+  for (int b = 0; b < blobs; ++b)
+    for (int a = 0; a < dim; ++a) centres.push_back(rng.uniform(1.0, 9.0));
+  for (int64_t i = 0; i < n_blob; ++i) {
+    const int b = static_cast<int>(rng.next() % blobs);
+    const double sigma = 0.2 + 0.1 * b;
+    for (int a = 0; a < dim; ++a)
+      out.coords.push_back(static_cast<float>(centres[b * dim + a] + sigma * rng.normal()));
+  }
+  for (int64_t i = 0; i < n_noise; ++i)
+    for (int a = 0; a < dim; ++a) out.coords.push_back(static_cast<float>(rng.uniform(0.0, 10.0)));
+  const double log_lo = std::log(0.05), log_hi = std::log(2.0);
+  *eps = static_cast<float>(std::exp(rng.uniform(log_lo, log_hi)));
+  static const int kMinpts[] = {2, 3, 5, 10, 25};
+  *minpts = kMinpts[rng.next() % 5];
+  return out;
+}
+
+// HACC-like halos. One SplitMix64 stream:
+//   background: n - int64(halo_frac*n) points, x,y,z ~ U(0, L)
+//   halos until int64(halo_frac*n) halo points: mass m = int64(20/(1-u)^(1/0.9))
+//   capped at 200000 and at the remainder; Plummer scale a = 0.010*cbrt(m/20);
+//   centre ~ U(a, L-a)^3; radius r = a/sqrt(uu^(-2/3) - 1) (uu > 0, r <= 10a),
+//   direction z ~ U(-1,1), phi ~ U(0, 2pi).
+HostPoints gen_hacc_like(int64_t n, double box_len, double halo_frac, uint64_t seed) {
+  if (n < 1) throw std::invalid_argument("hacc_like: n must be >= 1");
+  if (!(box_len > 0.0) || !(halo_frac >= 0.0 && halo_frac <= 1.0))
+    throw std::invalid_argument("hacc_like: bad box length or halo fraction");
+  SplitMix64 rng(seed);
+  const int64_t n_halo = static_cast<int64_t>(halo_frac * static_cast<double>(n));
+  const int64_t n_bg = n - n_halo;
+  HostPoints out;
+  out.dim = 3;
+  out.coords.resize(static_cast<size_t>(n) * 3);
+  float* w = out.coords.data();
+  for (int64_t i = 0; i < n_bg; ++i)
+    for (int a = 0; a < 3; ++a) *w++ = static_cast<float>(rng.uniform(0.0, box_len));
+  const double two_pi = 2.0 * 3.141592653589793;
+  int64_t made = 0;
+  while (made < n_halo) {
+    const double u = rng.next_double();
+    int64_t m = static_cast<int64_t>(20.0 / std::pow(1.0 - u, 1.0 / 0.9));
+    m = std::min<int64_t>(m, 200000);
+    m = std::min<int64_t>(m, n_halo - made);
+    if (m < 1) m = 1;
+    const double a = 0.010 * std::cbrt(static_cast<double>(m) / 20.0);
+    double c[3];
+    for (int k = 0; k < 3; ++k) c[k] = rng.uniform(a, box_len - a);
+    for (int64_t p = 0; p < m; ++p) {
+      double r;
+      do {
+        double uu = rng.next_double();
+        while (uu == 0.0) uu = rng.next_double();
+        r = a / std::sqrt(std::pow(uu, -2.0 / 3.0) - 1.0);
+      } while (!(r <= 10.0 * a));
+      const double z = rng.uniform(-1.0, 1.0);
+      const double phi = rng.uniform(0.0, two_pi);
+      const double s = std::sqrt(1.0 - z * z);
+      *w++ = static_cast<float>(c[0] + r * s * std::cos(phi));
+      *w++ = static_cast<float>(c[1] + r * s * std::sin(phi));
+      *w++ = static_cast<float>(c[2] + r * z);
+    }
+    made += m;
+  }
+  return out;
+}
+
+// Taxi-trajectory-like 2D points: unit square, 8 city
+// centres ~ U(0.2, 0.8)^2, 300 road segments (anchor = city + N(0, 0.08^2),
+// angle ~ U(0, pi), length ~ Exp(mean 0.02)), Zipf(0.8) segment weights; 98% of
+// points on a segment (t ~ U(0,1)) with N(0, (1e-4)^2) jitter, 2% uniform;
+// clipped to [0, 1].
+HostPoints gen_taxi_like(int64_t n, uint64_t seed) {
+  if (n < 1) throw std::invalid_argument("taxi_like: n must be >= 1");
+  SplitMix64 rng(seed);
+  constexpr int kCities = 8, kSegments = 300;
+  double city[kCities][2];
+  for (auto& cc : city)
+    for (double& v : cc) v = rng.uniform(0.2, 0.8);
+  struct Seg {
+    double x, y, dx, dy;
+  };
+  std::vector<Seg> seg(kSegments);
+  std::vector<double> cdf(kSegments);
+  double total = 0;
+  for (int s = 0; s < kSegments; ++s) {
+    const int c = static_cast<int>(rng.next() % kCities);
+    const double ax = city[c][0] + 0.08 * rng.normal();
+    const double ay = city[c][1] + 0.08 * rng.normal();
+    const double ang = rng.uniform(0.0, 3.141592653589793);
+    const double len = -0.02 * std::log(1.0 - rng.next_double());
+    seg[s] = {ax, ay, len * std::cos(ang), len * std::sin(ang)};
+    total += std::pow(static_cast<double>(s + 1), -0.8);
+    cdf[s] = total;
+  }
+  HostPoints out;
+  out.dim = 2;
+  out.coords.resize(static_cast<size_t>(n) * 2);
+  auto clip = [](double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); };
+  for (int64_t i = 0; i < n; ++i) {
+    double x, y;
+    if (rng.next_double() < 0.98) {
+      const double pick = rng.next_double() * total;
+      const int s = static_cast<int>(std::upper_bound(cdf.begin(), cdf.end(), pick) - cdf.begin());
+      const Seg& g = seg[std::min(s, kSegments - 1)];
+      const double t = rng.next_double();
+      x = g.x + t * g.dx + 1e-4 * rng.normal();
+      y = g.y + t * g.dy + 1e-4 * rng.normal();
+    } else {
+      x = rng.next_double();
+      y = rng.next_double();
+    }
+    out.coords[static_cast<size_t>(2 * i)] = static_cast<float>(clip(x));
+    out.coords[static_cast<size_t>(2 * i + 1)] = static_cast<float>(clip(y));
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// File formats (io.cpp:51-148)
+// ---------------------------------------------------------------------------
+namespace {
+
+[[noreturn]] void io_fail(const std::string& path, const std::string& what) {
+  throw std::runtime_error(path + ": " + what);
+}
+
+[[noreturn]] void parse_fail(const std::string& path, int64_t line, const std::string& what) {
+  std::ostringstream os;
+  os << path << ":" << line << ": " << what;
+  throw std::runtime_error(os.str());
+}
+
+// One CSV record: comma-separated floats, blanks/tabs around fields allowed.
+bool split_fields(const std::string& line, std::vector<float>& out) {
+  out.clear();
+  const char* p = line.data();
+  const char* end = p + line.size();
+  while (p < end) {
+    while (p < end && (*p == ' ' || *p == '\t')) ++p;
+    float v;
+    auto res = std::from_chars(p, end, v);
+    if (res.ec != std::errc{}) return false;
+    out.push_back(v);
+    p = res.ptr;
+    while (p < end && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
+    if (p < end) {
+      if (*p != ',') return false;
+      ++p;
+    }
+  }
+  return !out.empty();
+}
+
+bool is_binary_path(const std::string& path) {
+  auto dot = path.rfind('.');
+  return dot != std::string::npos && path.substr(dot) == ".bin";
+}
+
+HostPoints read_csv(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) io_fail(path, "cannot open for reading");
+  HostPoints ps;
+  std::string line;
+  std::vector<float> fields;
+  int64_t lineno = 0;
+  bool header_allowed = true;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.empty() || line == "\r") continue;
+    if (!split_fields(line, fields)) {
+      if (header_allowed) {
+        header_allowed = false;
+        continue;
+      }
+      parse_fail(path, lineno, "malformed point line");
+    }
+    header_allowed = false;
+    if (ps.dim == 0) {
+      if (fields.size() != 2 && fields.size() != 3)
+        parse_fail(path, lineno, "points must have 2 or 3 coordinates");
+      ps.dim = static_cast<int>(fields.size());
+    } else if (static_cast<int>(fields.size()) != ps.dim) {
+      parse_fail(path, lineno, "inconsistent coordinate count");
+    }
+    ps.coords.insert(ps.coords.end(), fields.begin(), fields.end());
+  }
+  if (ps.coords.empty()) io_fail(path, "no points found");
+  validate_points(ps.dim, ps.coords.data(), static_cast<int64_t>(ps.coords.size()));
+  return ps;
+}
+
+HostPoints read_binary(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) io_fail(path, "cannot open for reading");
+  uint32_t hdr[2] = {0, 0};
+  in.read(reinterpret_cast<char*>(hdr), sizeof hdr);
+  if (!in) io_fail(path, "truncated header");
+  if (hdr[0] == 0 || (hdr[1] != 2 && hdr[1] != 3)) io_fail(path, "invalid header (n or dim)");
+  HostPoints ps;
+  ps.dim = static_cast<int>(hdr[1]);
+  ps.coords.resize(static_cast<size_t>(hdr[0]) * hdr[1]);
+  in.read(reinterpret_cast<char*>(ps.coords.data()),
+          static_cast<std::streamsize>(ps.coords.size() * sizeof(float)));
+  if (!in) io_fail(path, "truncated coordinate data");
+  validate_points(ps.dim, ps.coords.data(), static_cast<int64_t>(ps.coords.size()));
+  return ps;
+}
+
+}  // namespace
+
+HostPoints load_points(const std::string& path, int format) {
+  const bool binary = format == 2 || (format != 1 && is_binary_path(path));
+  return binary ? read_binary(path) : read_csv(path);
+}
+
+void save_points(const std::string& path, int format, int dim, const float* coords, int64_t n) {
+  const bool binary = format == 2 || (format != 1 && is_binary_path(path));
+  if (binary) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) io_fail(path, "cannot open for writing");
+    const uint32_t hdr[2] = {static_cast<uint32_t>(n), static_cast<uint32_t>(dim)};
+    out.write(reinterpret_cast<const char*>(hdr), sizeof hdr);
+    out.write(reinterpret_cast<const char*>(coords),
+              static_cast<std::streamsize>(static_cast<size_t>(n) * dim * sizeof(float)));
+    if (!out) io_fail(path, "write failed");
+    return;
+  }
+  std::ofstream out(path);
+  if (!out) io_fail(path, "cannot open for writing");
+  out.precision(9);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < dim; ++k) {
+      if (k) out << ',';
+      out << coords[i * dim + k];
+    }
+    out << '\n';
+  }
+  if (!out) io_fail(path, "write failed");
+}
+
+}  // namespace tcb

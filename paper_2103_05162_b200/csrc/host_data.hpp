@@ -1,0 +1,61 @@
+// Host-side data plumbing shared by the C ABI: point sets, seeded generators
+// and file formats. These sit before the hot path
+// and are restated from the reference's published behaviour so datasets are
+// byte-identical to the reference's for the same arguments.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tcb {
+
+// Host point storage: n*dim floats, row-major.
+struct HostPoints {
+  int dim = 0;
+  std::vector<float> coords;
+  int64_t size() const { return dim ? static_cast<int64_t>(coords.size()) / dim : 0; }
+};
+
+// PointSet::validate (geometry.hpp:29-37): throws std::invalid_argument.
+void validate_points(int dim, const float* coords, int64_t count_floats);
+
+// SplitMix64 stream (rng.hpp:11-47): fixed so generated data is identical
+// across implementations.
+class SplitMix64 {
+ public:
+  explicit SplitMix64(uint64_t seed) : state_(seed) {}
+  uint64_t next() {
+    uint64_t z = (state_ += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  }
+  double next_double() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * next_double(); }
+  double normal();  // Box-Muller, second half cached
+
+ private:
+  uint64_t state_;
+  bool has_spare_ = false;
+  double spare_ = 0.0;
+};
+
+// Reference generators (datagen.cpp:10-88).
+HostPoints gen_blobs(int k, int64_t per_blob, int dim, float separation, float sigma,
+                     uint64_t seed);
+HostPoints gen_uniform(int64_t n, int dim, const float* lo, const float* hi, uint64_t seed);
+HostPoints gen_lattice(int64_t side, int dim, float spacing);
+// testutil::random_instance (tests/test_util.hpp:27-60).
+HostPoints gen_random_instance(uint64_t seed, int64_t min_n, int64_t max_n, float* eps,
+                               int* minpts);
+// Benchmark generators of SURVEY.md §8d (new; the reference ships none).
+HostPoints gen_hacc_like(int64_t n, double box_len, double halo_frac, uint64_t seed);
+HostPoints gen_taxi_like(int64_t n, uint64_t seed);
+
+// File formats (io.cpp:51-148). Errors throw std::runtime_error.
+HostPoints load_points(const std::string& path, int format /* 0 auto, 1 csv, 2 bin */);
+void save_points(const std::string& path, int format, int dim, const float* coords, int64_t n);
+
+}  // namespace tcb

@@ -1,0 +1,132 @@
+// Host-side pieces of the device pipeline shared between translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+
+#include "bvh.cuh"
+#include "engine.hpp"
+
+namespace tcb {
+
+// Device-side counters / small reductions of one run (one memset per run).
+struct DevCounters {
+  unsigned long long pairs;
+  unsigned long long dists;
+  long long clusters;
+  long long cores;
+  long long noise;
+  unsigned long long key_and;  // AND / OR over the keys of the current sort
+  unsigned long long key_or;
+  uint32_t bounds_ord[6];      // order-preserving encodings: min xyz, max xyz
+  int32_t nonfinite;
+  int32_t count_a;             // generic device-side counts (cells, prims ...)
+  int32_t count_b;
+  int32_t pad;
+};
+
+// Stream-ordered scratch allocations released at scope exit (cudaMallocAsync
+// on the default pool; the pool's release threshold is raised once so repeat
+// calls reuse HBM instead of re-mapping it).
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t s) : stream_(s) {}
+  ~Scratch();
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  void* alloc(size_t bytes);
+  template <typename T>
+  T* alloc_n(int64_t count) {
+    return static_cast<T*>(alloc(static_cast<size_t>(count > 0 ? count : 1) * sizeof(T)));
+  }
+  cudaStream_t stream() const { return stream_; }
+
+ private:
+  cudaStream_t stream_;
+  std::vector<void*> ptrs_;
+};
+
+// Small pinned host staging buffer (thread-local) for device->host reads that
+// size later launches.
+void* pinned_staging(size_t bytes);
+
+// Timing events for the stages of one run.
+class StageClock {
+ public:
+  explicit StageClock(cudaStream_t s);
+  ~StageClock();
+  void mark(int stage_begin);  // record an event that opens `stage_begin`
+  void finish();               // record the closing event
+  // Elapsed ms of each stage (call after the stream is synchronized).
+  void collect(double* stage_ms) const;
+
+ private:
+  cudaStream_t stream_;
+  cudaEvent_t ev_[kNumStages + 1];
+  int stage_of_[kNumStages + 1];
+  int count_ = 0;
+};
+
+// ---- BVH construction (build.cu) ----
+
+// Primitive source for the build: either points (degenerate boxes, read from
+// the row-major coords) or explicit boxes.
+struct PrimSource {
+  const float* coords = nullptr;  // points mode: n*D floats
+  const float4* lo = nullptr;     // boxes mode
+  const float4* hi = nullptr;
+  const int32_t* aux = nullptr;   // leaf payload per primitive (nullptr: primitive index)
+  int64_t count = 0;
+};
+
+struct BuiltBvh {
+  DeviceBvh tree;
+  float4* leaf_pt = nullptr;  // points mode only: rank -> (x, y, z, id bits)
+  int sort_passes = 0;
+};
+
+// Builds the LBVH of bvh.cpp:10-124 (scene bounds over centroids, Morton,
+// stable (code, index) sort, Karras topology, refit). Checks the points for
+// non-finite coordinates when validate_finite (throws InvalidArgument).
+template <int D>
+BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
+                   Scratch& scratch, StageClock* clock);
+
+// Raw point bounds into d_ctr->bounds_ord + finiteness flag (resets both).
+template <int D>
+void launch_point_bounds(const float* coords, int64_t n, DevCounters* d_ctr, cudaStream_t s);
+
+// ---- traversal / finalize (dbscan.cu) ----
+template <int D>
+void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
+                       uint8_t* flags, DevCounters* d_ctr, cudaStream_t s);
+template <int D>
+void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
+                       uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
+                       cudaStream_t s);
+void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
+void finalize_labels(int32_t* parent, const uint8_t* flags, int64_t n,
+                     int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
+                     cudaStream_t s);
+
+// ---- DenseBox (grid.cu) ----
+template <int D>
+void run_densebox(const float* d_coords, int64_t n, float eps, int minpts,
+                  int32_t* d_labels, uint8_t* d_core, DevCounters* d_ctr,
+                  Scratch& scratch, StageClock& clock, double* dense_fraction);
+
+// ---- brute force (bruteforce.cu) ----
+template <int D>
+void run_bruteforce(const float* d_coords, int64_t n, float eps, int minpts,
+                    int32_t* d_labels, uint8_t* d_core, DevCounters* d_ctr,
+                    Scratch& scratch);
+
+inline unsigned grid_for(int64_t work, int block, int64_t max_blocks = 148 * 64) {
+  int64_t b = (work + block - 1) / block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return static_cast<unsigned>(b);
+}
+
+}  // namespace tcb

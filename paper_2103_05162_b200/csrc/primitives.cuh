@@ -1,0 +1,32 @@
+// Device-wide building blocks: LSD radix sort of (u64 key, i32 value) pairs
+// and an exclusive prefix scan. Hand-written for sm_100a (no CUB / Thrust on
+// the hot path).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tcb {
+
+// Scratch needed by radix_sort_pairs for n items (bytes).
+size_t radix_sort_scratch_bytes(int64_t n);
+
+// Stable ascending sort of (keys, vals) by key. Only the digit windows whose
+// bits are not constant across all keys are sorted: `and_all` / `or_all` are
+// the bitwise AND / OR of every key (the key producer reduces them for free).
+// A stable LSD sort started from vals = 0..n-1 orders ties by index, which is
+// the reference's (code, index) order (bvh.cpp:27-32, dense_grid.cpp:55-60).
+// Ping-pongs between (keys, vals) and (keys_alt, vals_alt); returns true when
+// the sorted result ended in the *_alt buffers.
+bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
+                      int32_t* vals_alt, int64_t n, uint64_t and_all,
+                      uint64_t or_all, void* scratch, cudaStream_t stream,
+                      int* passes_run = nullptr);
+
+// Exclusive scan of n int32 counts into out (may alias in); writes the total
+// to *d_total (device pointer) when non-null.
+size_t scan_scratch_bytes(int64_t n);
+void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n,
+                        int32_t* d_total, void* scratch, cudaStream_t stream);
+
+}  // namespace tcb
