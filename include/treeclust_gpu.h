@@ -52,6 +52,10 @@ tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
  * Returns the number of entries written (<= cap). */
 int tcg_last_stage_ms(double* out, int cap);
 
+/* Number of kernels the last tcg_cluster_device / tc_cluster call on this
+ * host thread launched (all of them are this library's own sm_100a kernels). */
+int64_t tcg_last_launch_count(void);
+
 /* ---- benchmark generators (host, SplitMix64) ---- */
 
 /* 3D HACC-like halos: n_bg uniform background points in [0,L)^3, then
@@ -71,6 +75,21 @@ tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n,
  * / C2C rate. */
 tc_status tcg_dataset_create_pinned(const float* coords, int64_t n, int dim,
                                     tc_dataset** out);
+
+/* ---- stage probes for parity tests (each runs one device stage on host
+ *      inputs and copies the result back) ---- */
+
+/* Device LBVH of n points in the reference's node view (bvh.hpp:74-79):
+ * leaf_ids[n] (leaf rank -> point), left/right/max_rank[n-1], boxes[(n-1)*6]
+ * (min xyz, max xyz; unused axes 0). */
+tc_status tcg_debug_point_bvh(const float* coords, int64_t n, int dim, int32_t* leaf_ids,
+                              int32_t* left, int32_t* right, int32_t* max_rank, float* boxes);
+/* Device radix sort of (key, index) pairs: sorted keys and source indices. */
+tc_status tcg_debug_sort_pairs(const uint64_t* keys, int64_t n, uint64_t* keys_out,
+                               int32_t* vals_out);
+/* Concurrent device unite() over m edges (2*m ints) on n elements, then
+ * flatten; parent_out[n] = representative (minimum index of the component). */
+tc_status tcg_debug_union_find(const int32_t* edges, int64_t m, int32_t n, int32_t* parent_out);
 
 #ifdef __cplusplus
 } /* extern "C" */

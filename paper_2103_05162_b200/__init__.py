@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     cluster_device,
     cluster_raw,
     device_count,
+    last_launch_count,
     last_stage_ms,
     status_string,
     verify,

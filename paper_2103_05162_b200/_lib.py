@@ -66,10 +66,19 @@ SIGNATURES = {
     "tcg_cluster_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, C.c_int, C.c_int,
                                      C.c_int64, _P, _P, _P, C.POINTER(TcClusterStats)]),
     "tcg_last_stage_ms": (C.c_int, [C.POINTER(C.c_double), C.c_int]),
+    "tcg_last_launch_count": (C.c_int64, []),
     "tcg_generate_hacc_like": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_uint64, _PP]),
     "tcg_generate_taxi_like": (C.c_int, [C.c_int64, C.c_uint64, _PP]),
     "tcg_random_instance": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_float),
                                       C.POINTER(C.c_int), _PP]),
+    "tcg_debug_point_bvh": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_float)]),
+    "tcg_debug_sort_pairs": (C.c_int, [C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_int32)]),
+    "tcg_debug_union_find": (C.c_int, [C.POINTER(C.c_int32), C.c_int64, C.c_int32,
+                                       C.POINTER(C.c_int32)]),
     "tcg_dataset_create_pinned": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int, _PP]),
 }
 

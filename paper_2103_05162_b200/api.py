@@ -234,9 +234,49 @@ def last_stage_ms() -> dict:
     return {STAGES[i]: arr[i] for i in range(k)}
 
 
+def last_launch_count() -> int:
+    return int(lib.tcg_last_launch_count())
+
+
 def device_count() -> int:
     return int(lib.tcg_device_count())
 
 
 def status_string(status: int) -> str:
     return lib.tc_status_string(int(status)).decode()
+
+
+# ---- stage probes (tcg_debug_*): one device stage, host in / host out ----
+def debug_point_bvh(coords) -> dict:
+    a = np.ascontiguousarray(coords, np.float32)
+    n, d = a.shape
+    m = max(n - 1, 1)
+    leaf = np.empty(n, np.int32)
+    left, right, mr = (np.zeros(m, np.int32) for _ in range(3))
+    boxes = np.zeros((m, 6), np.float32)
+    p = lambda v, t: v.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    _check(lib.tcg_debug_point_bvh(p(a, C.c_float), n, d, p(leaf, C.c_int32), p(left, C.c_int32),
+                                   p(right, C.c_int32), p(mr, C.c_int32), p(boxes, C.c_float)),
+           "tcg_debug_point_bvh")
+    k = n - 1
+    return {"leaf_ids": leaf, "left": left[:k], "right": right[:k], "max_rank": mr[:k],
+            "boxes": boxes[:k]}
+
+
+def debug_sort_pairs(keys):
+    k = np.ascontiguousarray(keys, np.uint64)
+    ko = np.empty_like(k)
+    vo = np.empty(k.shape[0], np.int32)
+    _check(lib.tcg_debug_sort_pairs(k.ctypes.data_as(C.POINTER(C.c_uint64)), k.shape[0],
+                                    ko.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                    vo.ctypes.data_as(C.POINTER(C.c_int32))), "tcg_debug_sort_pairs")
+    return ko, vo
+
+
+def debug_union_find(edges, n: int) -> np.ndarray:
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+    out = np.empty(n, np.int32)
+    _check(lib.tcg_debug_union_find(e.ctypes.data_as(C.POINTER(C.c_int32)), e.shape[0], n,
+                                    out.ctypes.data_as(C.POINTER(C.c_int32))),
+           "tcg_debug_union_find")
+    return out

@@ -146,10 +146,10 @@ void run_bruteforce(const float* d_coords, int64_t n, float eps, int minpts, int
   uint8_t* tmp_flags = scratch.alloc_n<uint8_t>(n);
   init_union_find(parent, tmp_flags, n, st);
   const unsigned g = grid_for(n, kBfBlock, INT32_MAX);
-  k_bf_core<D><<<g, kBfBlock, 0, st>>>(d_coords, n, eps2, minpts, d_core);
-  k_bf_union<D><<<g, kBfBlock, 0, st>>>(d_coords, n, eps2, d_core, parent);
-  k_bf_flatten<<<grid_for(n, 256), 256, 0, st>>>(parent, n);
-  k_bf_label<D><<<g, kBfBlock, 0, st>>>(d_coords, n, eps2, d_core, parent, d_labels, ctr);
+  note_launch(), k_bf_core<D><<<g, kBfBlock, 0, st>>>(d_coords, n, eps2, minpts, d_core);
+  note_launch(), k_bf_union<D><<<g, kBfBlock, 0, st>>>(d_coords, n, eps2, d_core, parent);
+  note_launch(), k_bf_flatten<<<grid_for(n, 256), 256, 0, st>>>(parent, n);
+  note_launch(), k_bf_label<D><<<g, kBfBlock, 0, st>>>(d_coords, n, eps2, d_core, parent, d_labels, ctr);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -293,13 +293,13 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   if (points_mode) out.leaf_pt = scratch.alloc_n<float4>(m);
 
   // Reset the per-build reductions (bounds, key AND/OR, finiteness flag).
-  k_reset_build<<<1, 32, 0, st>>>(d_ctr);
+  note_launch(), k_reset_build<<<1, 32, 0, st>>>(d_ctr);
 
   const unsigned g = grid_for(m, 256);
-  k_centroid_bounds<D><<<g, 256, 0, st>>>(boxes, m, validate_finite, d_ctr);
+  note_launch(), k_centroid_bounds<D><<<g, 256, 0, st>>>(boxes, m, validate_finite, d_ctr);
   uint64_t* keys = scratch.alloc_n<uint64_t>(m);
   int32_t* vals = scratch.alloc_n<int32_t>(m);
-  k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
+  note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
   TCB_CUDA(cudaGetLastError());
 
   // One small read-back: finiteness + key AND/OR decide the sort passes.
@@ -327,15 +327,15 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   if (clock) clock->mark(kStTopo);
   float4* leaf_pt = out.leaf_pt;
   if (m == 1) {
-    k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
+    note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
   } else {
     int32_t* node_parent = scratch.alloc_n<int32_t>(m - 1);
     int32_t* leaf_parent = scratch.alloc_n<int32_t>(m);
     int32_t* arrivals = scratch.alloc_n<int32_t>(m - 1);
     TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * (m - 1), st));
-    k_karras<D><<<grid_for(m - 1, 256, INT32_MAX), 256, 0, st>>>(
+    note_launch(), k_karras<D><<<grid_for(m - 1, 256, INT32_MAX), 256, 0, st>>>(
         codes, order, src.aux, m, out.tree.nodes, node_parent, leaf_parent);
-    k_refit<D><<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
+    note_launch(), k_refit<D><<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
         boxes, order, m, out.tree.nodes, node_parent, leaf_parent, arrivals, leaf_pt);
   }
   TCB_CUDA(cudaGetLastError());
@@ -386,8 +386,8 @@ k_point_bounds(const float* __restrict__ coords, int64_t n, DevCounters* ctr) {
 
 template <int D>
 void launch_point_bounds(const float* coords, int64_t n, DevCounters* ctr, cudaStream_t s) {
-  k_reset_build<<<1, 32, 0, s>>>(ctr);
-  k_point_bounds<D><<<grid_for(n, 256), 256, 0, s>>>(coords, n, ctr);
+  note_launch(), k_reset_build<<<1, 32, 0, s>>>(ctr);
+  note_launch(), k_point_bounds<D><<<grid_for(n, 256), 256, 0, s>>>(coords, n, ctr);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -453,6 +453,8 @@ TC_EXPORT int tcg_last_stage_ms(double* out, int cap) {
   return tcb::get_last_stage_ms(out, cap);
 }
 
+TC_EXPORT int64_t tcg_last_launch_count(void) { return tcb::launch_count(); }
+
 TC_EXPORT tc_status tcg_generate_hacc_like(int64_t n, double box_len, double halo_frac,
                                            uint64_t seed, tc_dataset** out) {
   if (!out) return TC_ERR_INVALID_ARGUMENT;

@@ -51,7 +51,7 @@ int64_t first_bad_border_impl(const float* d_coords, int64_t n, float eps,
   unsigned long long* bad = scratch.alloc_n<unsigned long long>(1);
   TCB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
-  k_border_check<D><<<grid_for(n, 128, INT32_MAX), 128, 0, st>>>(b.tree.nodes, b.leaf_pt, n,
+  note_launch(), k_border_check<D><<<grid_for(n, 128, INT32_MAX), 128, 0, st>>>(b.tree.nodes, b.leaf_pt, n,
                                                                  eps2, d_labels, d_core, bad);
   TCB_CUDA(cudaGetLastError());
   unsigned long long h = 0;

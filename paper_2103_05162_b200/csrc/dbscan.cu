@@ -130,7 +130,7 @@ k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int6
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s) {
-  k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
+  note_launch(), k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
       b.tree.nodes, b.leaf_pt, n, eps2, minpts, flags, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
@@ -141,23 +141,23 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
                        cudaStream_t s) {
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
   if (force_core)
-    k_fd_main<D, true><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
+    note_launch(), k_fd_main<D, true><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
                                                  parent, d_ctr);
   else
-    k_fd_main<D, false><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
+    note_launch(), k_fd_main<D, false><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
                                                   parent, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
-  k_init_uf<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
+  note_launch(), k_init_uf<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
   TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(n), s));
   TCB_CUDA(cudaGetLastError());
 }
 
 void finalize_labels(int32_t* parent, const uint8_t* flags, int64_t n, int32_t* labels,
                      uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s) {
-  k_finalize<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n, labels, core_out, d_ctr);
+  note_launch(), k_finalize<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n, labels, core_out, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -33,6 +33,7 @@ void raise_pool_threshold() {
 }
 
 thread_local double t_last_stage_ms[kNumStages] = {};
+thread_local int64_t t_launches = 0;
 
 }  // namespace
 
@@ -102,6 +103,10 @@ void StageClock::collect(double* stage_ms) const {
   }
 }
 
+void note_launch() { ++t_launches; }
+void reset_launch_count() { t_launches = 0; }
+int64_t launch_count() { return t_launches; }
+
 void set_last_stage_ms(const double* ms) {
   for (int s = 0; s < kNumStages; ++s) t_last_stage_ms[s] = ms[s];
 }
@@ -158,6 +163,7 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
     throw InvalidArgument{"dbscan_run: more than 2^31-1 points"};
   if (!d_coords || !d_labels || !d_core) throw InvalidArgument{"null buffer"};
 
+  reset_launch_count();
   Scratch scratch(stream);
   StageClock clock(stream);
   DevCounters* ctr = scratch.alloc_n<DevCounters>(1);

@@ -46,6 +46,11 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
                 RunOutput* out,
                 const std::function<void(cudaStream_t)>& tail = nullptr);
 
+// Kernel-launch accounting (thread-local; reset at the start of run_device).
+void note_launch();
+void reset_launch_count();
+int64_t launch_count();
+
 // Thread-local copy of the last run's stage times.
 void set_last_stage_ms(const double* ms);
 int get_last_stage_ms(double* out, int cap);

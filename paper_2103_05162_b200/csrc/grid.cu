@@ -382,10 +382,10 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   launch_point_bounds<D>(d_coords, n, ctr, st);
   GridParams* gp = scratch.alloc_n<GridParams>(1);
   const double h = static_cast<double>(eps) / std::sqrt(static_cast<double>(D));
-  k_grid_setup<D><<<1, 1, 0, st>>>(ctr, h, gp);
+  note_launch(), k_grid_setup<D><<<1, 1, 0, st>>>(ctr, h, gp);
   uint64_t* keys = scratch.alloc_n<uint64_t>(n);
   int32_t* vals = scratch.alloc_n<int32_t>(n);
-  k_cell_ids<D><<<grid_for(n, 256), 256, 0, st>>>(d_coords, n, gp, keys, vals, ctr);
+  note_launch(), k_cell_ids<D><<<grid_for(n, 256), 256, 0, st>>>(d_coords, n, gp, keys, vals, ctr);
   TCB_CUDA(cudaGetLastError());
   auto* h_stage = static_cast<unsigned char*>(pinned_staging(64));
   TCB_CUDA(cudaMemcpyAsync(h_stage, &ctr->key_and, 16, cudaMemcpyDeviceToHost, st));
@@ -412,12 +412,12 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   int32_t* head_excl = scratch.alloc_n<int32_t>(n);
   int32_t* d_tot = scratch.alloc_n<int32_t>(4);
   void* scan_tmp = scratch.alloc(scan_scratch_bytes(n));
-  k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(ids, n, head);
+  note_launch(), k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(ids, n, head);
   exclusive_scan_i32(head, head_excl, n, d_tot, scan_tmp, st);
   int32_t* cell_of_sorted = scratch.alloc_n<int32_t>(n);
   int32_t* cell_begin = scratch.alloc_n<int32_t>(n);
   float4* sorted_pt = scratch.alloc_n<float4>(n);
-  k_cell_fill<D><<<grid_for(n, 256), 256, 0, st>>>(head, head_excl, perm, d_coords, n,
+  note_launch(), k_cell_fill<D><<<grid_for(n, 256), 256, 0, st>>>(head, head_excl, perm, d_coords, n,
                                                    cell_of_sorted, cell_begin, sorted_pt);
   TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot, 4, cudaMemcpyDeviceToHost, st));
   TCB_CUDA(cudaStreamSynchronize(st));
@@ -429,8 +429,8 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   uint8_t* cell_dense = scratch.alloc_n<uint8_t>(num_cells);
   int32_t* prim_count = scratch.alloc_n<int32_t>(num_cells);
   int32_t* prim_off = scratch.alloc_n<int32_t>(num_cells);
-  k_reset_keys<<<1, 1, 0, st>>>(ctr);
-  k_cell_prims<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_begin, num_cells, n, minpts,
+  note_launch(), k_reset_keys<<<1, 1, 0, st>>>(ctr);
+  note_launch(), k_cell_prims<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_begin, num_cells, n, minpts,
                                                          cell_end, cell_dense, prim_count, ctr);
   exclusive_scan_i32(prim_count, prim_off, num_cells, d_tot + 1, scan_tmp, st);
   TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot + 1, 4, cudaMemcpyDeviceToHost, st));
@@ -446,14 +446,14 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   float4* prim_hi = scratch.alloc_n<float4>(num_prims);
   int32_t* prim_aux = scratch.alloc_n<int32_t>(num_prims);
   if (num_dense > 0)
-    k_prim_init<<<grid_for(num_cells, 256), 256, 0, st>>>(
+    note_launch(), k_prim_init<<<grid_for(num_cells, 256), 256, 0, st>>>(
         cell_dense, prim_off, num_cells, reinterpret_cast<uint4*>(prim_lo),
         reinterpret_cast<uint4*>(prim_hi), prim_aux);
-  k_prim_fill<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
+  note_launch(), k_prim_fill<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
                                                    cell_dense, prim_off, n, prim_lo, prim_hi,
                                                    prim_aux);
   if (num_dense > 0)
-    k_prim_decode<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_dense, prim_off, num_cells,
+    note_launch(), k_prim_decode<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_dense, prim_off, num_cells,
                                                             prim_lo, prim_hi);
   TCB_CUDA(cudaGetLastError());
 
@@ -471,7 +471,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   int32_t* rank_of_prim = scratch.alloc_n<int32_t>(num_prims);
   int32_t* qcount = scratch.alloc_n<int32_t>(num_prims);
   int32_t* qoff = scratch.alloc_n<int32_t>(num_prims);
-  k_leaf_counts<<<grid_for(num_prims, 256), 256, 0, st>>>(b.tree.leaf_order, prim_aux,
+  note_launch(), k_leaf_counts<<<grid_for(num_prims, 256), 256, 0, st>>>(b.tree.leaf_order, prim_aux,
                                                           cell_begin, cell_end, num_prims,
                                                           rank_of_prim, qcount);
   exclusive_scan_i32(qcount, qoff, num_prims, nullptr, scan_tmp, st);
@@ -480,7 +480,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
   init_union_find(parent, flags, n, st);
-  k_queries<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
+  note_launch(), k_queries<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
                                                  cell_dense, prim_off, rank_of_prim, qoff, n,
                                                  qpt, qrank, parent, flags);
   TCB_CUDA(cudaGetLastError());
@@ -489,16 +489,16 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   clock.mark(kStCore);
   const unsigned gq = grid_for(n, kQueryBlock, INT32_MAX);
   if (minpts > 2)
-    k_db_core<D><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
+    note_launch(), k_db_core<D><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
                                              cell_end, eps2, minpts, flags, ctr);
   // ---- main pass ----
   clock.mark(kStMain);
   if (minpts == 2)
-    k_db_main<D, true><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+    note_launch(), k_db_main<D, true><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
                                                    cell_begin, cell_end, eps2, flags, parent,
                                                    ctr);
   else
-    k_db_main<D, false><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+    note_launch(), k_db_main<D, false><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
                                                     cell_begin, cell_end, eps2, flags, parent,
                                                     ctr);
   TCB_CUDA(cudaGetLastError());

@@ -302,10 +302,10 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
       const int32_t* vin = in_alt ? vals_alt : vals;
       uint64_t* kout = in_alt ? keys : keys_alt;
       int32_t* vout = in_alt ? vals : vals_alt;
-      k_sort_upsweep<<<num_tiles, kSortThreads, 0, stream>>>(kin, n, shift, tile_hist,
+      note_launch(), k_sort_upsweep<<<num_tiles, kSortThreads, 0, stream>>>(kin, n, shift, tile_hist,
                                                              num_tiles);
-      k_sort_scan_rows<<<kRadix, kScanRowThreads, 0, stream>>>(tile_hist, num_tiles, totals);
-      k_sort_downsweep<<<num_tiles, kSortThreads, sizeof(DownsweepSmem), stream>>>(
+      note_launch(), k_sort_scan_rows<<<kRadix, kScanRowThreads, 0, stream>>>(tile_hist, num_tiles, totals);
+      note_launch(), k_sort_downsweep<<<num_tiles, kSortThreads, sizeof(DownsweepSmem), stream>>>(
           kin, vin, kout, vout, n, shift, tile_hist, totals, num_tiles);
       TCB_CUDA(cudaGetLastError());
       in_alt = !in_alt;
@@ -329,9 +329,9 @@ void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, int32_t* d_t
   }
   int blocks = static_cast<int>((n + kScanTile - 1) / kScanTile);
   int32_t* partial = static_cast<int32_t*>(scratch);
-  k_scan_reduce<<<blocks, kScanThreads, 0, stream>>>(in, n, partial);
-  k_scan_partials<<<1, 1024, 0, stream>>>(partial, blocks, d_total);
-  k_scan_downsweep<<<blocks, kScanThreads, 0, stream>>>(in, out, n, partial);
+  note_launch(), k_scan_reduce<<<blocks, kScanThreads, 0, stream>>>(in, n, partial);
+  note_launch(), k_scan_partials<<<1, 1024, 0, stream>>>(partial, blocks, d_total);
+  note_launch(), k_scan_downsweep<<<blocks, kScanThreads, 0, stream>>>(in, out, n, partial);
   TCB_CUDA(cudaGetLastError());
 }
 

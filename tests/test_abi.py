@@ -1,0 +1,200 @@
+"""The drop-in boundary, CPU side: the C-ABI library loads, exports every
+symbol include/*.h declares, and the host half of the ABI (datasets, file
+formats, generators, argument validation, status codes) behaves like the
+reference's (REF tests/test_capi.cpp). No kernel runs here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2103_05162_b200 as tb
+from paper_2103_05162_b200 import Algorithm, Dataset, Status, TreeclustError
+from paper_2103_05162_b200._lib import LIB_PATH, SIGNATURES, lib
+
+from ._util import generators, sha
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in ("treeclust.h", "treeclust_gpu.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(tcg?_[a-z0-9_]+)\s*\(", src))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    # the 18 reference entry points are all there
+    ref18 = {"tc_status_string", "tc_dataset_create", "tc_dataset_load", "tc_dataset_save",
+             "tc_dataset_size", "tc_dataset_dim", "tc_dataset_coords", "tc_dataset_free",
+             "tc_generate_blobs", "tc_generate_uniform", "tc_generate_lattice", "tc_cluster",
+             "tc_result_size", "tc_result_labels", "tc_result_core_flags", "tc_result_stats",
+             "tc_result_free", "tc_verify"}
+    assert ref18 <= names
+    raw = C.CDLL(LIB_PATH)
+    for name in sorted(names):
+        assert hasattr(raw, name), f"{name} declared in include/ but not exported"
+        assert name in SIGNATURES, f"{name} has no ctypes signature"
+
+
+def test_no_torch_or_cpp_symbols_leak():
+    out = os.popen(f"nm -D --defined-only {LIB_PATH}").read()
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    assert all(s.startswith(("tc_", "tcg_")) for s in exported), sorted(exported)[:10]
+
+
+def test_status_strings():
+    assert tb.status_string(0) == "ok"
+    assert tb.status_string(1) == "invalid argument"
+    assert tb.status_string(4) == "oracle cap exceeded"
+    assert tb.status_string(99) == "unknown status"
+
+
+def test_dataset_create_and_accessors():  # REF test_capi.cpp:25-33
+    coords = np.array([[0, 0], [1, 1], [2, 0]], np.float32)
+    ds = Dataset.from_array(coords)
+    assert ds.size == 3 and ds.dim == 2
+    assert np.array_equal(ds.coords(), coords)
+
+
+def test_invalid_dataset_arguments():  # REF test_capi.cpp:35-55
+    out = C.c_void_p()
+    one = (C.c_float * 2)(0.0, 0.0)
+    assert lib.tc_dataset_create(None, 1, 2, C.byref(out)) == Status.INVALID_ARGUMENT
+    assert lib.tc_dataset_create(one, 1, 5, C.byref(out)) == Status.INVALID_ARGUMENT
+    assert lib.tc_dataset_create(one, 0, 2, C.byref(out)) == Status.INVALID_ARGUMENT
+    with pytest.raises(TreeclustError) as e:
+        Dataset.from_array(np.array([[0.0, np.nan]], np.float32))
+    assert e.value.status == Status.INVALID_ARGUMENT
+    with pytest.raises(TreeclustError):
+        Dataset.from_array(np.array([[0.0, np.inf, 1.0]], np.float32))
+
+
+def test_cluster_argument_validation_before_any_device_work():
+    ds = Dataset.from_array(np.zeros((1, 2), np.float32))
+    res = C.c_void_p()
+    assert lib.tc_cluster(ds.handle, C.c_float(-1.0), 2, 0, 1, 0, C.byref(res)) == 1
+    assert lib.tc_cluster(ds.handle, C.c_float(1.0), 1, 0, 1, 0, C.byref(res)) == 1
+    assert lib.tc_cluster(ds.handle, C.c_float(float("nan")), 2, 0, 1, 0, C.byref(res)) == 1
+    assert lib.tc_cluster(ds.handle, C.c_float(float("inf")), 2, 1, 1, 0, C.byref(res)) == 1
+    assert lib.tc_cluster(None, C.c_float(1.0), 2, 0, 1, 0, C.byref(res)) == 1
+    assert lib.tc_cluster(ds.handle, C.c_float(1.0), 2, 0, 1, 0, None) == 1
+    assert lib.tc_cluster(ds.handle, C.c_float(1.0), 2, 7, 1, 0, C.byref(res)) == 1
+    assert not res.value  # *out written only on success
+    big = Dataset.blobs(1, 100, 2, 5.0, 0.3, 2)  # REF test_capi.cpp:131-140
+    assert lib.tc_cluster(big.handle, C.c_float(1.0), 5, 2, 1, 50, C.byref(res)) == 4
+    # cap is checked before eps/minpts, like capi.cpp:166-168
+    assert lib.tc_cluster(big.handle, C.c_float(-1.0), 5, 2, 1, 50, C.byref(res)) == 4
+
+
+@pytest.mark.skipif(tb.device_count() > 0, reason="exercises the no-device error path")
+def test_no_device_is_an_internal_error_not_a_fallback():
+    ds = Dataset.blobs(2, 50, 2, 5.0, 0.3, 7)
+    with pytest.raises(TreeclustError) as e:
+        tb.cluster(ds, 0.5, 5)
+    assert e.value.status == Status.INTERNAL
+
+
+def test_load_save_round_trip(tmp_path):  # REF test_capi.cpp:57-78
+    ds = Dataset.blobs(2, 50, 2, 5.0, 0.3, 7)
+    for name in ("capi_io.csv", "capi_io.bin"):
+        p = str(tmp_path / name)
+        ds.save(p)
+        back = Dataset.load(p)
+        assert back.size == 100 and back.dim == 2
+        assert np.array_equal(back.coords(), ds.coords())
+    with pytest.raises(TreeclustError) as e:
+        Dataset.load("/nonexistent/path.csv")
+    assert e.value.status == Status.IO
+
+
+def test_csv_header_and_errors(tmp_path):  # REF io.cpp:58-104
+    p = tmp_path / "h.csv"
+    p.write_text("x,y\n1,2\n3, 4\n\n5,6\r\n")
+    d = Dataset.load(str(p))
+    assert d.size == 3 and np.array_equal(d.coords(), [[1, 2], [3, 4], [5, 6]])
+    p.write_text("1,2\n3,4,5\n")
+    with pytest.raises(TreeclustError) as e:
+        Dataset.load(str(p))
+    assert e.value.status == Status.IO
+    p.write_text("1,2\nfoo\n")
+    with pytest.raises(TreeclustError):
+        Dataset.load(str(p))
+    b = tmp_path / "t.bin"
+    b.write_bytes(np.array([5, 2], np.uint32).tobytes() + np.zeros(4, np.float32).tobytes())
+    with pytest.raises(TreeclustError) as e:
+        Dataset.load(str(b))
+    assert e.value.status == Status.IO
+
+
+def test_generators_seeded_and_validated():  # REF test_capi.cpp:80-101
+    a = Dataset.blobs(3, 40, 3, 6.0, 0.4, 11)
+    b = Dataset.blobs(3, 40, 3, 6.0, 0.4, 11)
+    assert np.array_equal(a.coords(), b.coords())
+    assert Dataset.uniform(100, 2, [0, 0], [1, 1], 3).size == 100
+    assert Dataset.lattice(5, 2, 0.5).size == 25
+    with pytest.raises(TreeclustError) as e:
+        Dataset.blobs(0, 40, 2, 6.0, 0.4, 1)
+    assert e.value.status == Status.INVALID_ARGUMENT
+    with pytest.raises(TreeclustError):
+        Dataset.uniform(10, 2, [1, 0], [0, 1], 3)
+    with pytest.raises(TreeclustError):
+        Dataset.lattice(1, 2, 0.5)
+
+
+def test_generators_byte_identical_to_reference():
+    """Golden sha256 produced by running the reference generators
+    (tests/golden/make_golden.py)."""
+    g = generators()
+    assert sha(Dataset.blobs(3, 80, 2, 20.0, 0.5, 21).coords()) == g["blobs(3,80,2,20,0.5,21)"]
+    assert sha(Dataset.blobs(3, 40, 3, 6.0, 0.4, 11).coords()) == g["blobs(3,40,3,6,0.4,11)"]
+    assert sha(Dataset.blobs(100, 10000, 2, 0.8333333, 0.08333333, 7).coords()) == \
+        g["blobs(100,10000,2,0.8333333,0.08333333,7)"]
+    assert sha(Dataset.uniform(1000, 3, [0, -1, 2], [1, 1, 5], 3).coords()) == \
+        g["uniform(1000,3,[0,-1,2],[1,1,5],3)"]
+    assert sha(Dataset.lattice(40, 2, 0.1).coords()) == g["lattice(40,2,0.1)"]
+    assert sha(Dataset.lattice(12, 3, 0.1).coords()) == g["lattice(12,3,0.1)"]
+    for s in (1, 7, 24):
+        ds, eps, mp = Dataset.random_instance(s, 50, 1500)
+        want = g[f"random_instance({s},50,1500)"]
+        assert sha(ds.coords()) == want["sha256"] and eps == want["eps"] and mp == want["minpts"]
+
+
+def test_hacc_like_calibration_shape():
+    """The §8d HACC-like generator: 23% of points in Plummer halos, the rest
+    uniform in [0, L)^3 with L scaled to keep the C2 density."""
+    n = 200_000
+    ds = Dataset.hacc_like(n)
+    c = ds.coords()
+    L = 36.8 * (n / 37e6) ** (1 / 3)
+    bg = c[: n - int(0.23 * n)]
+    assert bg.min() >= 0 and bg.max() < L
+    assert ds.size == n and ds.dim == 3
+    assert np.array_equal(c, Dataset.hacc_like(n).coords())  # deterministic
+
+
+def test_taxi_like_in_unit_square():
+    c = Dataset.taxi_like(100_000).coords()
+    assert c.shape == (100_000, 2) and c.min() >= 0 and c.max() <= 1
+
+
+def test_verify_null_dataset():
+    assert lib.tc_verify(None, C.c_float(1.0), 5, 1, 0, None, 0) == Status.INVALID_ARGUMENT
+
+
+def test_product_path_has_no_oracle_dependency():
+    """The shipped package never imports or links the test oracle."""
+    pkg = os.path.join(ROOT, "paper_2103_05162_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".cuh", ".hpp")) or f == "Makefile":
+                txt = open(os.path.join(dirpath, f), errors="replace").read()
+                assert "oracle/" not in txt and "import oracle" not in txt and \
+                    "from oracle" not in txt and "liboracle" not in txt, f
+    libs = os.popen(f"ldd {LIB_PATH}").read()
+    assert "oracle" not in libs and "treeclust_ref" not in libs

@@ -1,0 +1,270 @@
+"""Parity of the sm_100a path against the oracle / the reference (the gates of
+SURVEY.md §8): core flags bit-exact, noise set exact, core labels EQUAL (the
+minimum core index of the cluster), every border valid, pair_resolutions and
+distance_evaluations exact. Everything goes through the C ABI."""
+import numpy as np
+import pytest
+
+import paper_2103_05162_b200 as tb
+from oracle import oracle, ref
+from paper_2103_05162_b200 import Algorithm, Dataset, Status, TreeclustError
+
+from ._util import SEEDS, assert_parity, brute_pair_count, golden_run, instance, npz
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert tb.device_count() > 0, "GPU tests need a CUDA device (no CPU fallback exists)"
+
+
+def run(coords, eps, minpts, algo, cap=0):
+    return tb.cluster(Dataset.from_array(coords), eps, minpts, Algorithm(algo), oracle_cap=cap)
+
+
+def check_against_oracle(coords, eps, minpts, algo, tag=""):
+    got = run(coords, eps, minpts, algo)
+    want = oracle.dbscan(coords, eps, minpts, algo)
+    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], tag)
+    ok, msg = oracle.check_equivalence(coords, eps, got.labels, got.core_flags, want["labels"],
+                                       want["core"])
+    assert ok, f"{tag}: {msg}"
+    if algo < 2:
+        for k in ("pair_resolutions", "distance_evaluations", "cluster_count", "core_count",
+                  "noise_count", "preprocess_skipped"):
+            assert got.stats[k] == want["stats"][k], (tag, k, got.stats[k], want["stats"][k])
+    if algo == 1:
+        assert got.stats["dense_point_fraction"] == want["stats"]["dense_point_fraction"]
+    return got, want
+
+
+# ---------------- golden instances (reference outputs, committed) ----------------
+@pytest.mark.parametrize("seed", SEEDS)
+def test_golden_instances(seed):
+    _, coords, eps, mp = instance(seed)
+    db = npz("dbscan.npz")
+    for algo in (0, 1, 2):
+        want = golden_run(db, seed, algo)
+        got = run(coords, eps, mp, algo)
+        assert_parity(got.labels, got.core_flags, want["labels"], want["core"], f"{seed}/{algo}")
+        ok, msg = oracle.check_equivalence(coords, eps, got.labels, got.core_flags,
+                                           want["labels"], want["core"])
+        assert ok, msg
+        if algo == 2:  # brute force is deterministic end to end
+            assert np.array_equal(got.labels, want["labels"])
+        else:
+            for k, v in want["counters"].items():
+                assert got.stats[k] == v, (seed, algo, k)
+        if algo == 1:
+            assert got.stats["dense_point_fraction"] == want["dense_fraction"]
+
+
+@pytest.mark.parametrize("seed", range(100, 140))
+def test_more_random_instances_against_oracle(seed):
+    import paper_2103_05162_b200 as t
+
+    ds, eps, mp = t.Dataset.random_instance(seed, 50, 2500)
+    for algo in (0, 1, 2):
+        check_against_oracle(ds.coords(), eps, mp, algo, f"seed {seed} algo {algo}")
+
+
+# ---------------- stage probes vs the reference's own accessors ----------------
+def test_device_bvh_is_the_reference_tree():
+    g = npz("bvh.npz")
+    for name in ("two", "dups", "rand2", "rand3", "clump3"):
+        t = tb.api.debug_point_bvh(g[f"{name}_pts"])
+        for k in ("leaf_ids", "left", "right", "max_rank", "boxes"):
+            assert np.array_equal(t[k], g[f"{name}_{k}"]), (name, k)
+    rng = np.random.default_rng(5)
+    for d in (2, 3):
+        pts = np.concatenate([rng.normal(0, 1, (30000, d)), rng.uniform(-5, 5, (20000, d)),
+                              np.repeat(rng.normal(0, 1, (10, d)), 50, axis=0)]).astype(np.float32)
+        t = tb.api.debug_point_bvh(pts)
+        w = oracle.point_bvh(pts)
+        for k in ("leaf_ids", "left", "right", "max_rank", "boxes"):
+            assert np.array_equal(t[k], w[k]), (d, k)
+
+
+def test_radix_sort_is_stable_and_exact():
+    rng = np.random.default_rng(7)
+    cases = [
+        rng.integers(0, 2 ** 63, 1_000_003, dtype=np.uint64),
+        rng.integers(0, 50, 300_000).astype(np.uint64) << np.uint64(40),  # heavy duplicates
+        np.full(5000, 12345, np.uint64),  # all digits constant
+        np.array([7], np.uint64),
+        rng.integers(0, 2 ** 64 - 1, 100_000, dtype=np.uint64, endpoint=True),
+    ]
+    for keys in cases:
+        ko, vo = tb.api.debug_sort_pairs(keys)
+        order = np.argsort(keys, kind="stable")
+        assert np.array_equal(vo, order)
+        assert np.array_equal(ko, keys[order])
+
+
+def test_device_union_find_matches_sequential_replay():  # REF acceptance criterion 5
+    rng = np.random.default_rng(99)
+    for trial in range(10):
+        n = 10000
+        edges = rng.integers(0, n, (100_000, 2)).astype(np.int32)
+        got = tb.api.debug_union_find(edges, n)
+        parent = np.arange(n)
+
+        def find(i):
+            while parent[i] != i:
+                parent[i] = parent[parent[i]]
+                i = parent[i]
+            return i
+
+        for a, b in edges:
+            ra, rb = find(a), find(b)
+            if ra != rb:
+                parent[max(ra, rb)] = min(ra, rb)
+        want = np.array([find(i) for i in range(n)])
+        assert np.array_equal(got, want), trial
+        assert np.array_equal(got, got[got])  # flattened
+
+
+# ---------------- edge cases the reference tests ----------------
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_single_and_pair(algo):
+    one = run(np.array([[1, 1]], np.float32), 1.0, 2, algo)
+    assert one.labels[0] == -1 and one.core_flags[0] == 0
+    pair = run(np.array([[0, 0], [0.5, 0]], np.float32), 1.0, 2, algo)
+    assert list(pair.labels) == [0, 0] and list(pair.core_flags) == [1, 1]
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_degenerate_inputs(algo):
+    cases = [
+        (np.ones((3, 2), np.float32), 0.5, 3),                      # coincident points
+        (np.ones((500, 3), np.float32), 0.5, 10),                   # one dense cell / 1-leaf tree
+        (np.array([[5.0, y] for y in np.linspace(0, 1, 200)], np.float32), 0.01, 2),  # zero-width x
+        (np.array([[0.9 * i, 0] for i in range(50)], np.float32), 1.0, 2),  # chain
+        (np.array([[0, 0], [.1, 0], [0, .1], [5, 5], [5.1, 5], [5, 5.1]], np.float32), 0.2, 3),
+        (np.random.default_rng(3).normal(0, 1e30, (400, 2)).astype(np.float32), 3e29, 3),
+        (np.random.default_rng(4).uniform(-1e-30, 1e-30, (300, 3)).astype(np.float32), 1e-31, 4),
+    ]
+    for i, (c, eps, mp) in enumerate(cases):
+        check_against_oracle(c, eps, mp, algo, f"case {i} algo {algo}")
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2])
+def test_eps_boundary_is_the_exact_fp64_predicate(algo):
+    """Pairs at, one ulp inside and one ulp outside eps: fp32 arithmetic would
+    get some of these wrong; the fp64 chain of geometry.hpp:72-79 decides."""
+    eps = np.float32(0.1)
+    pts = [[0.0, 0.0]]
+    x = np.float32(0.1)
+    for dx in (x, np.nextafter(x, np.float32(0)), np.nextafter(x, np.float32(1))):
+        base = np.float32(len(pts) * 10.0)
+        pts += [[base, 0.0], [base + dx, 0.0]]
+    # diagonal pairs whose squared distance is within 1e-7 relative of eps^2
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        a = rng.uniform(100, 200, 2).astype(np.float32)
+        ang = rng.uniform(0, 2 * np.pi)
+        b = (a + np.array([np.cos(ang), np.sin(ang)]) * float(eps) * (1 + rng.normal(0, 1e-7))).astype(np.float32)
+        pts += [a.tolist(), b.tolist()]
+    c = np.array(pts, np.float32)
+    got, want = check_against_oracle(c, float(eps), 2, algo, f"boundary algo {algo}")
+    if algo == 0:
+        assert got.stats["pair_resolutions"] == brute_pair_count(c, float(eps))
+
+
+def test_invalid_inputs_return_status_codes():
+    c = np.random.default_rng(0).uniform(0, 1000, (1000, 3)).astype(np.float32)
+    with pytest.raises(TreeclustError) as e:  # grid would exceed 2^62 cells
+        tb.cluster(Dataset.from_array(c), 1e-12, 5, Algorithm.DENSEBOX)
+    assert e.value.status == Status.INVALID_ARGUMENT
+    import torch
+
+    x = torch.tensor([[0.0, 0.0], [float("nan"), 1.0]], device="cuda")
+    for algo in (0, 1, 2):
+        with pytest.raises(TreeclustError) as e:
+            tb.cluster_device(x, 1.0, 2, Algorithm(algo), stats=True)
+        assert e.value.status == Status.INVALID_ARGUMENT
+    with pytest.raises(TreeclustError) as e:
+        tb.cluster(Dataset.from_array(c), 1.0, 5, Algorithm.BRUTEFORCE, oracle_cap=500)
+    assert e.value.status == Status.CAP_EXCEEDED
+    # a library error leaves the device usable
+    ok = tb.cluster(Dataset.from_array(c[:100]), 50.0, 3)
+    assert ok.labels.shape == (100,)
+
+
+def test_verify_passes():  # REF test_capi.cpp:142-150
+    ds = Dataset.blobs(3, 100, 2, 10.0, 0.6, 31)
+    st, report = tb.verify(ds, 1.2, 5)
+    assert st == Status.OK, report
+    assert "PASS" in report and "FAIL" not in report
+    big = Dataset.blobs(5, 4000, 3, 10.0, 0.6, 3)
+    st, report = tb.verify(big, 0.3, 5)
+    assert st == Status.OK and "skipped" in report, report
+
+
+def test_device_api_matches_host_api():
+    import torch
+
+    ds = Dataset.blobs(10, 5000, 3, 3.0, 0.5, 9)
+    c = ds.coords()
+    for algo, mp in ((0, 5), (1, 5), (0, 2), (1, 2)):
+        host = tb.cluster(ds, 0.2, mp, Algorithm(algo))
+        lab, core, st = tb.cluster_device(torch.from_numpy(c).cuda(), 0.2, mp, Algorithm(algo),
+                                          stats=True)
+        assert_parity(lab.cpu().numpy(), core.cpu().numpy(), host.labels, host.core_flags)
+        assert st["pair_resolutions"] == host.stats["pair_resolutions"]
+
+
+# ---------------- medium / full size against the compiled reference ----------------
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("algo", [0, 1])
+def test_c1_blobs_1m_against_reference(algo):
+    """C1: 2D Gaussian blobs, 1M points, eps 0.01, minpts 5 (BASELINE configs[0])."""
+    ds = Dataset.blobs(100, 10000, 2, 0.8333333, 0.08333333, 7)
+    c = ds.coords()
+    got = tb.cluster(ds, 0.01, 5, Algorithm(algo))
+    want = ref.dbscan(c, 0.01, 5, algo, threads=0)
+    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], "C1")
+    ok, msg = ref.check_equivalence(c, 0.01, 5, got.labels, got.core_flags, want["labels"],
+                                    want["core"])
+    assert ok, msg
+    for k in ("pair_resolutions", "distance_evaluations", "cluster_count", "core_count",
+              "noise_count"):
+        assert got.stats[k] == want["stats"][k], k
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_c2_hacc_37m_against_reference():
+    """C2 at full size: 37M HACC-like points, eps 0.042, minpts 2, FDBSCAN — the
+    bench workload — against the reference run on the host cores."""
+    ds = Dataset.hacc_like(37_000_000)
+    c = ds.coords()
+    got = tb.cluster(ds, 0.042, 2, Algorithm.FDBSCAN)
+    want = ref.dbscan(c, 0.042, 2, 0, threads=0)
+    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], "C2")
+    assert got.stats["pair_resolutions"] == want["stats"]["pair_resolutions"] == 898_475_393
+    assert got.stats["cluster_count"] == want["stats"]["cluster_count"]
+    # minpts == 2: no borders, so labels are fully determined
+    assert np.array_equal(got.labels, want["labels"])
+
+
+@pytest.mark.slow
+def test_c3_full_size_properties():
+    """C3 at full size on the device only: FDBSCAN and DenseBox agree exactly
+    on cores / noise / core labels, the GPU border checker passes, and the
+    result is identical run to run."""
+    import torch
+
+    ds = Dataset.hacc_like(37_000_000)
+    x = torch.from_numpy(ds.coords()).cuda()
+    l0, c0, s0 = tb.cluster_device(x, 0.042, 100, Algorithm.FDBSCAN, stats=True)
+    l1, c1, s1 = tb.cluster_device(x, 0.042, 100, Algorithm.DENSEBOX, stats=True)
+    l2, c2, _ = tb.cluster_device(x, 0.042, 100, Algorithm.FDBSCAN, stats=True)
+    assert torch.equal(c0, c1) and torch.equal(c0, c2)
+    assert torch.equal(l0 == -1, l1 == -1)
+    m = c0.bool()
+    assert torch.equal(l0[m], l1[m]) and torch.equal(l0[m], l2[m])
+    assert s0["pair_resolutions"] == 898_475_393
+    assert s0["core_count"] == s1["core_count"] == 4_243_007
+    assert s0["cluster_count"] == s1["cluster_count"] == 5000
