@@ -88,23 +88,7 @@ k_centroid_bounds(Src src, int64_t m, bool check_finite, DevCounters* ctr) {
       mx[k] = fmaxf(mx[k], c[k]);
     }
   }
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
-      mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
-    }
-  }
-  bad = __any_sync(0xffffffffu, bad);
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      atomicMin(&ctr->bounds_ord[k], f2ord(mn[k]));
-      atomicMax(&ctr->bounds_ord[3 + k], f2ord(mx[k]));
-    }
-    if (bad) atomicOr(&ctr->nonfinite, 1);
-  }
+  publish_bounds<D>(mn, mx, bad, ctr);
 }
 
 template <int D, class Src>
@@ -145,15 +129,7 @@ k_morton(Src src, int64_t m, DevCounters* ctr, uint64_t* __restrict__ keys,
     acc_and &= code;
     acc_or |= code;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    acc_and &= __shfl_xor_sync(0xffffffffu, acc_and, o);
-    acc_or |= __shfl_xor_sync(0xffffffffu, acc_or, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAnd(&ctr->key_and, acc_and);
-    atomicOr(&ctr->key_or, acc_or);
-  }
+  publish_and_or(acc_and, acc_or, ctr);
 }
 
 // Bvh::delta (bvh.cpp:49-56): common prefix of (code, index) keys.
@@ -165,11 +141,11 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
   return 64 + __clz(static_cast<int>(static_cast<uint32_t>(i) ^ static_cast<uint32_t>(j)));
 }
 
-template <int D>
+template <int D, class Src>
 __global__ void __launch_bounds__(256)
-k_karras(const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
+k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
          const int32_t* __restrict__ prim_aux, int64_t m, float4* __restrict__ nodes,
-         int32_t* __restrict__ node_parent, int32_t* __restrict__ leaf_parent) {
+         int32_t* __restrict__ node_parent, float4* __restrict__ leaf_pt) {
   using T = NodeTraits<D>;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= m - 1) return;
@@ -190,73 +166,94 @@ k_karras(const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
   const int64_t gamma = i + s * d + (d < 0 ? d : 0);
   const int64_t lo = i < j ? i : j, hi = i < j ? j : i;
 
+  float* f = reinterpret_cast<float*>(nodes + i * T::kVec);
+  // A leaf child's box goes straight into its slot here (bvh.cpp:34-39's
+  // gather fused in), so the refit only ever waits on internal children.
+  auto leaf_child = [&](int64_t rank, int slot, int32_t& link, int32_t& aux) {
+    link = ~static_cast<int32_t>(rank);
+    const int32_t prim = order[rank];
+    aux = prim_aux ? prim_aux[prim] : prim;
+    float blo[3], bhi[3];
+    src.box(prim, blo, bhi);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      f[slot * 2 * D + k] = blo[k];
+      f[slot * 2 * D + D + k] = bhi[k];
+    }
+  };
   int32_t left, right, aux_l, aux_r;
   if (lo == gamma) {
-    left = ~static_cast<int32_t>(gamma);
-    int32_t prim = order[gamma];
-    aux_l = prim_aux ? prim_aux[prim] : prim;
-    leaf_parent[gamma] = static_cast<int32_t>(i);
+    leaf_child(gamma, 0, left, aux_l);
   } else {
     left = static_cast<int32_t>(gamma);
     aux_l = static_cast<int32_t>(gamma);  // max leaf rank of [lo, gamma]
     node_parent[gamma] = static_cast<int32_t>(i);
   }
   if (hi == gamma + 1) {
-    right = ~static_cast<int32_t>(gamma + 1);
-    int32_t prim = order[gamma + 1];
-    aux_r = prim_aux ? prim_aux[prim] : prim;
-    leaf_parent[gamma + 1] = static_cast<int32_t>(i);
+    leaf_child(gamma + 1, 1, right, aux_r);
   } else {
     right = static_cast<int32_t>(gamma + 1);
     aux_r = static_cast<int32_t>(hi);  // max leaf rank of [gamma+1, hi]
     node_parent[gamma + 1] = static_cast<int32_t>(i);
   }
-  int4* ip = reinterpret_cast<int4*>(reinterpret_cast<float*>(nodes + i * T::kVec) + T::kIntOff);
-  *ip = make_int4(left, right, aux_l, aux_r);
+  *reinterpret_cast<int4*>(f + T::kIntOff) = make_int4(left, right, aux_l, aux_r);
   if (i == 0) node_parent[0] = -1;
+  if (leaf_pt) {  // Morton-ordered query points (x, y, z, id)
+    auto emit = [&](int64_t rank) {
+      const int32_t prim = order[rank];
+      float blo[3], bhi[3];
+      src.box(prim, blo, bhi);
+      leaf_pt[rank] = make_float4(blo[0], blo[1], D == 3 ? blo[2] : 0.f, __int_as_float(prim));
+    };
+    emit(i);
+    if (i == m - 2) emit(m - 1);
+  }
 }
 
-// Bottom-up refit. Each leaf thread writes its box into its slot of the parent
-// node, then climbs: the second arrival at a node owns it, unions the two
-// child slots (read through L2: the sibling was written by another SM) and
-// writes the union into the node's slot of its own parent.
-template <int D, class Src>
+// Bottom-up refit (bvh.cpp:88-124). Climbers start at the nodes whose two
+// children are leaves (their slots are already filled). A finished node
+// writes its box (union of its two slots) into its slot of the parent; if the
+// sibling is a leaf the climber continues at once, otherwise the two climbers
+// meet with an arrival counter (the only place a fence is needed) and the
+// second one continues. Slots written by another SM are read through L2.
+template <int D>
 __global__ void __launch_bounds__(256)
-k_refit(Src src, const int32_t* __restrict__ order, int64_t m, float4* nodes,
-        const int32_t* __restrict__ node_parent, const int32_t* __restrict__ leaf_parent,
-        int32_t* __restrict__ arrivals, float4* __restrict__ leaf_pt) {
+k_refit(int64_t m, float4* nodes, const int32_t* __restrict__ node_parent,
+        int32_t* __restrict__ arrivals) {
   using T = NodeTraits<D>;
-  int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (s >= m) return;
-  const int32_t prim = order[s];
-  float lo[3], hi[3];
-  src.box(prim, lo, hi);
-  if (leaf_pt) leaf_pt[s] = make_float4(lo[0], lo[1], D == 3 ? lo[2] : 0.f, __int_as_float(prim));
-
-  int32_t child = ~static_cast<int32_t>(s);
-  int32_t p = leaf_parent[s];
-  while (true) {
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= m - 1) return;
+  {
+    const int4 links = *reinterpret_cast<const int4*>(
+        reinterpret_cast<const float*>(nodes + i * T::kVec) + T::kIntOff);
+    if (links.x >= 0 || links.y >= 0) return;
+  }
+  int32_t c = static_cast<int32_t>(i);
+  while (c != 0) {  // the root's own box is never tested (bvh.hpp:55-58)
+    const float* cf = reinterpret_cast<const float*>(nodes + static_cast<int64_t>(c) * T::kVec);
+    float lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      lo[k] = fminf(__ldcg(cf + k), __ldcg(cf + 2 * D + k));
+      hi[k] = fmaxf(__ldcg(cf + D + k), __ldcg(cf + 3 * D + k));
+    }
+    const int32_t p = node_parent[c];
     float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
-    const int32_t pleft = reinterpret_cast<const int32_t*>(pf + T::kIntOff)[0];
-    float* slot = pf + (pleft == child ? 0 : 2 * D);
+    const int2 pl = *reinterpret_cast<const int2*>(pf + T::kIntOff);
+    const bool is_left = pl.x == c;
+    float* slot = pf + (is_left ? 0 : 2 * D);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       slot[k] = lo[k];
       slot[D + k] = hi[k];
     }
-    __threadfence();
-    if (atomicAdd(arrivals + p, 1) == 0) return;
-    __threadfence();
-    if (p == 0) return;  // the root's own box is never tested (bvh.hpp:55-58)
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      float a0 = __ldcg(pf + k), a1 = __ldcg(pf + D + k);
-      float b0 = __ldcg(pf + 2 * D + k), b1 = __ldcg(pf + 3 * D + k);
-      lo[k] = fminf(a0, b0);
-      hi[k] = fmaxf(a1, b1);
+    const int32_t sibling = is_left ? pl.y : pl.x;
+    if (sibling >= 0) {
+      __threadfence();
+      if (atomicAdd(arrivals + p, 1) == 0) return;
+      __threadfence();
     }
-    child = p;
-    p = node_parent[p];
+    c = p;
   }
 }
 
@@ -295,7 +292,7 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   // Reset the per-build reductions (bounds, key AND/OR, finiteness flag).
   note_launch(), k_reset_build<<<1, 32, 0, st>>>(d_ctr);
 
-  const unsigned g = grid_for(m, 256);
+  const unsigned g = grid_for(m, 256, 148 * 8);
   note_launch(), k_centroid_bounds<D><<<g, 256, 0, st>>>(boxes, m, validate_finite, d_ctr);
   uint64_t* keys = scratch.alloc_n<uint64_t>(m);
   int32_t* vals = scratch.alloc_n<int32_t>(m);
@@ -330,13 +327,12 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
   } else {
     int32_t* node_parent = scratch.alloc_n<int32_t>(m - 1);
-    int32_t* leaf_parent = scratch.alloc_n<int32_t>(m);
     int32_t* arrivals = scratch.alloc_n<int32_t>(m - 1);
     TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * (m - 1), st));
-    note_launch(), k_karras<D><<<grid_for(m - 1, 256, INT32_MAX), 256, 0, st>>>(
-        codes, order, src.aux, m, out.tree.nodes, node_parent, leaf_parent);
-    note_launch(), k_refit<D><<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
-        boxes, order, m, out.tree.nodes, node_parent, leaf_parent, arrivals, leaf_pt);
+    const unsigned gn = grid_for(m - 1, 256, INT32_MAX);
+    note_launch(), k_karras<D><<<gn, 256, 0, st>>>(boxes, codes, order, src.aux, m,
+                                                   out.tree.nodes, node_parent, leaf_pt);
+    note_launch(), k_refit<D><<<gn, 256, 0, st>>>(m, out.tree.nodes, node_parent, arrivals);
   }
   TCB_CUDA(cudaGetLastError());
   return out;
@@ -363,23 +359,7 @@ k_point_bounds(const float* __restrict__ coords, int64_t n, DevCounters* ctr) {
       mx[k] = fmaxf(mx[k], v);
     }
   }
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
-      mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
-    }
-  }
-  bad = __any_sync(0xffffffffu, bad);
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      atomicMin(&ctr->bounds_ord[k], f2ord(mn[k]));
-      atomicMax(&ctr->bounds_ord[3 + k], f2ord(mx[k]));
-    }
-    if (bad) atomicOr(&ctr->nonfinite, 1);
-  }
+  publish_bounds<D>(mn, mx, bad, ctr);
 }
 
 }  // namespace
@@ -387,7 +367,7 @@ k_point_bounds(const float* __restrict__ coords, int64_t n, DevCounters* ctr) {
 template <int D>
 void launch_point_bounds(const float* coords, int64_t n, DevCounters* ctr, cudaStream_t s) {
   note_launch(), k_reset_build<<<1, 32, 0, s>>>(ctr);
-  note_launch(), k_point_bounds<D><<<grid_for(n, 256), 256, 0, s>>>(coords, n, ctr);
+  note_launch(), k_point_bounds<D><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(coords, n, ctr);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -33,6 +33,44 @@ struct NodeTraits {
 
 constexpr int kStackDepth = 128;  // bvh.hpp:82-84 (keys are 64 + 32 bits)
 
+// The ball-vs-box predicate of the traversal: exactly box_distance_sq <= r2
+// in fp64 (geometry.hpp:82-93), answered by an fp32 estimate whenever the
+// estimate is outside a relative guard band of 2^-17 around r2. The fp32 sum
+// of three rounded squared differences is within ~6 * 2^-24 (relative) of the
+// real value and the fp64 chain within ~6 * 2^-53, so a decision outside the
+// band is the fp64 decision; inside it the fp64 chain runs. The fast path is
+// enabled only when r2 is a normal fp32 number far from under/overflow
+// (1e-20 <= r2 <= 1e30), so the relative bound holds.
+struct BallTest {
+  double r2;
+  float lo_f, hi_f;  // r2 * (1 -+ 2^-17) in fp32
+  bool fast;
+  __host__ static BallTest make(double eps2) {
+    BallTest b;
+    b.r2 = eps2;
+    b.fast = eps2 >= 1e-20 && eps2 <= 1e30;
+    b.lo_f = static_cast<float>(eps2 * (1.0 - 0x1.0p-17));
+    b.hi_f = static_cast<float>(eps2 * (1.0 + 0x1.0p-17));
+    return b;
+  }
+};
+
+template <int D>
+__device__ __forceinline__ bool ball_hits(const float* p, const float* lo, const float* hi,
+                                          const BallTest& bt) {
+  if (bt.fast) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float d = fmaxf(fmaxf(__fsub_rn(lo[k], p[k]), __fsub_rn(p[k], hi[k])), 0.f);
+      s = __fadd_rn(s, __fmul_rn(d, d));
+    }
+    if (s < bt.lo_f) return true;
+    if (s > bt.hi_f) return false;
+  }
+  return box_dist2<D>(p, lo, hi) <= bt.r2;
+}
+
 // Traverses the tree for the closed ball (p, sqrt(r2)), hiding every leaf
 // with rank < min_rank (query_sphere_masked, bvh.hpp:45-72), and calls
 //     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
@@ -42,7 +80,7 @@ constexpr int kStackDepth = 128;  // bvh.hpp:82-84 (keys are 64 + 32 bits)
 // LIFO stack order), so early-exit counters match bit for bit.
 template <int D, typename Visit>
 __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes,
-                                          const float* p, double r2,
+                                          const float* p, const BallTest& bt,
                                           int32_t min_rank, Visit& visit) {
   using T = NodeTraits<D>;
   int32_t stack[kStackDepth];
@@ -65,15 +103,15 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes,
     const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
     bool go_l = false, go_r = false;
     if (left < 0) {
-      if (~left >= min_rank && box_dist2<D>(p, f, f + D) <= r2)
+      if (~left >= min_rank && ball_hits<D>(p, f, f + D, bt))
         if (!visit(~left, aux_l, f, f + D)) return;
-    } else if (aux_l >= min_rank && box_dist2<D>(p, f, f + D) <= r2) {
+    } else if (aux_l >= min_rank && ball_hits<D>(p, f, f + D, bt)) {
       go_l = true;
     }
     if (right < 0) {
-      if (~right >= min_rank && box_dist2<D>(p, f + 2 * D, f + 3 * D) <= r2)
+      if (~right >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt))
         if (!visit(~right, aux_r, f + 2 * D, f + 3 * D)) return;
-    } else if (aux_r >= min_rank && box_dist2<D>(p, f + 2 * D, f + 3 * D) <= r2) {
+    } else if (aux_r >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
       go_r = true;
     }
     if (go_l && go_r) {

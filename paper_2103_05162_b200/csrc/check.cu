@@ -17,7 +17,7 @@ namespace {
 template <int D>
 __global__ void __launch_bounds__(128)
 k_border_check(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-               double eps2, const int32_t* __restrict__ labels, const uint8_t* __restrict__ core,
+               BallTest bt, const int32_t* __restrict__ labels, const uint8_t* __restrict__ core,
                unsigned long long* __restrict__ bad) {
   int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (r >= m) return;
@@ -34,7 +34,7 @@ k_border_check(const float4* __restrict__ nodes, const float4* __restrict__ leaf
     }
     return true;
   };
-  bvh_query<D>(nodes, p, eps2, 0, visit);
+  bvh_query<D>(nodes, p, bt, 0, visit);
   if (!ok) atomicMin(bad, static_cast<unsigned long long>(i));
 }
 
@@ -52,7 +52,7 @@ int64_t first_bad_border_impl(const float* d_coords, int64_t n, float eps,
   TCB_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
   note_launch(), k_border_check<D><<<grid_for(n, 128, INT32_MAX), 128, 0, st>>>(b.tree.nodes, b.leaf_pt, n,
-                                                                 eps2, d_labels, d_core, bad);
+                                                                 BallTest::make(eps2), d_labels, d_core, bad);
   TCB_CUDA(cudaGetLastError());
   unsigned long long h = 0;
   TCB_CUDA(cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, st));

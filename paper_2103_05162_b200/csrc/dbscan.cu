@@ -42,7 +42,7 @@ __device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned 
 template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          double eps2, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
+          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
   int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   unsigned long long dists = 0;
   if (r < m) {
@@ -54,7 +54,7 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
       ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
-    bvh_query<D>(nodes, p, eps2, 0, visit);
+    bvh_query<D>(nodes, p, bt, 0, visit);
     if (count >= minpts) flags[id] = 1;
   }
   flush_counter(&ctr->dists, dists);
@@ -63,7 +63,7 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
 template <int D, bool kForceCore>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          double eps2, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
           DevCounters* ctr) {
   int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   unsigned long long pairs = 0;
@@ -73,19 +73,18 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
     load_query<D>(leaf_pt, r, p, &i);
     const int32_t rank = static_cast<int32_t>(r);
     const bool core_i = kForceCore ? true : flags[i] != 0;
+    int32_t hint = i;
+    bool settled = false;
     auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
       if (s == rank) return true;
       ++pairs;
-      if (kForceCore) {
-        flags[j] = 1;
-        uf_unite(parent, i, j);
-      } else {
-        resolve_pair(i, j, core_i, flags, parent);
-      }
+      if (kForceCore)
+        uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
+      else
+        resolve_pair(i, j, core_i, flags, parent, hint, settled);
       return true;
     };
-    bvh_query<D>(nodes, p, eps2, rank, visit);
-    if (kForceCore && pairs) flags[i] = 1;
+    bvh_query<D>(nodes, p, bt, rank, visit);
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
@@ -95,6 +94,24 @@ __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     parent[i] = static_cast<int32_t>(i);
+}
+
+// minpts == 2: a point is core iff some other point lies within eps, i.e.
+// iff it shares a union-find set with another point. Flatten, and mark every
+// non-root point and the root it hangs under (the reference sets both flags
+// per pair instead, dbscan.hpp:85-88; the final flags are the same).
+__global__ void __launch_bounds__(256)
+k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t p = ld_relaxed(parent + i);
+    if (p == static_cast<int32_t>(i)) continue;
+    int32_t q;
+    while (p != (q = ld_relaxed(parent + p))) p = q;
+    st_relaxed(parent + i, p);
+    flags[i] = 1;
+    if (!flags[p]) flags[p] = 1;
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -131,7 +148,7 @@ template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s) {
   note_launch(), k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-      b.tree.nodes, b.leaf_pt, n, eps2, minpts, flags, d_ctr);
+      b.tree.nodes, b.leaf_pt, n, BallTest::make(eps2), minpts, flags, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -140,12 +157,13 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s) {
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
+  const BallTest bt = BallTest::make(eps2);
   if (force_core)
-    note_launch(), k_fd_main<D, true><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
-                                                 parent, d_ctr);
+    note_launch(), k_fd_main<D, true><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
+                                                                flags, parent, d_ctr);
   else
-    note_launch(), k_fd_main<D, false><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, eps2, flags,
-                                                  parent, d_ctr);
+    note_launch(), k_fd_main<D, false><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
+                                                                 flags, parent, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -155,8 +173,9 @@ void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s)
   TCB_CUDA(cudaGetLastError());
 }
 
-void finalize_labels(int32_t* parent, const uint8_t* flags, int64_t n, int32_t* labels,
-                     uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s) {
+void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n, int32_t* labels,
+                     uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s, bool force_core) {
+  if (force_core) note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
   note_launch(), k_finalize<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n, labels, core_out, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }

@@ -137,19 +137,32 @@ __device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t i) {
 
 // Hook the higher root under the lower one; retry from fresh roots when the
 // CAS loses (union_find.hpp:51-64). Representatives end up as the minimum
-// index of each component regardless of schedule.
-__device__ __forceinline__ void uf_unite(int32_t* parent, int32_t i, int32_t j) {
+// index of each component regardless of schedule. Returns the root the two
+// sets were joined under (an ancestor of both from then on).
+__device__ __forceinline__ int32_t uf_unite(int32_t* parent, int32_t i, int32_t j) {
   while (true) {
     i = uf_find(parent, i);
     j = uf_find(parent, j);
-    if (i == j) return;
+    if (i == j) return i;
     if (i > j) {
       int32_t t = i;
       i = j;
       j = t;
     }
-    if (atomicCAS(parent + j, j, i) == j) return;
+    if (atomicCAS(parent + j, j, i) == j) return i;
   }
+}
+
+// Query-side union with a root hint. `hint` is some ancestor of i (i itself,
+// or a root i's set had at some point; sets only ever merge, so it stays in
+// i's set). When j's parent already IS the hint, i and j are in one set and
+// the pair is a no-op with a single load — the common case inside a halo,
+// where a query meets hundreds of neighbours that joined its set long ago.
+__device__ __forceinline__ void uf_unite_hinted(int32_t* parent, int32_t i, int32_t j,
+                                                int32_t& hint) {
+  const int32_t pj = ld_relaxed(parent + j);
+  if (pj == hint || j == hint) return;
+  hint = uf_unite(parent, i, j);
 }
 
 // One-shot border claim (union_find.hpp:69-73).
@@ -157,24 +170,52 @@ __device__ __forceinline__ bool uf_claim(int32_t* parent, int32_t i, int32_t roo
   return atomicCAS(parent + i, i, root) == i;
 }
 
-// resolve_pair (dbscan.hpp:82-99): core-core unions, core-border claims the
-// border once (no bridging), border-border is a no-op. force_core is the
-// minpts == 2 case where every within-eps pair consists of core points.
+// resolve_pair (dbscan.hpp:82-99) for core flags that are final (minpts > 2):
+// core-core unions, core-border claims the border once (no bridging),
+// border-border is a no-op. Per-query state:
+//   hint       root hint of i (see uf_unite_hinted); a core i claims borders
+//              under it: the reference claims under find(i), and any ancestor
+//              of i flattens to the same representative
+//   i_settled  a border i that has been claimed (by anyone) can take no
+//              further action, so its remaining pairs are skipped
+// force_core (minpts == 2) never comes here: every pair is a core-core union
+// and the core flags are derived at finalize (dbscan.hpp:85-89).
 __device__ __forceinline__ void resolve_pair(int32_t i, int32_t j, bool core_i,
-                                             const uint8_t* flags, int32_t* parent) {
-  bool core_j = flags[j] != 0;
-  if (core_i && core_j)
-    uf_unite(parent, i, j);
-  else if (core_i) {
-    if (ld_relaxed(parent + j) == j) uf_claim(parent, j, uf_find(parent, i));
-  } else if (core_j) {
+                                             const uint8_t* flags, int32_t* parent,
+                                             int32_t& hint, bool& i_settled) {
+  if (core_i) {
+    if (flags[j]) {
+      uf_unite_hinted(parent, i, j, hint);
+    } else if (ld_relaxed(parent + j) == j) {
+      uf_claim(parent, j, hint);
+    }
+  } else if (!i_settled && flags[j]) {
     if (ld_relaxed(parent + i) == i) uf_claim(parent, i, uf_find(parent, j));
+    i_settled = true;  // claimed now, or by someone else before
   }
 }
 
 // ---------------------------------------------------------------------------
 // Warp / block reductions
 // ---------------------------------------------------------------------------
+// Block-wide reduction (any blockDim multiple of 32, <= 1024); the result is
+// valid in thread 0. `scratch` holds >= 32 T.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T identity, T* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < static_cast<int>(blockDim.x >> 5) ? scratch[lane] : identity;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

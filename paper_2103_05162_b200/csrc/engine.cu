@@ -141,7 +141,7 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   clock.mark(kStMain);
   fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, st);
   clock.mark(kStFinal);
-  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st);
+  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st, minpts == 2);
   clock.finish();
 }
 

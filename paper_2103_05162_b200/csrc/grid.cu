@@ -84,15 +84,7 @@ k_cell_ids(const float* __restrict__ coords, int64_t n, const GridParams* __rest
     acc_and &= id;
     acc_or |= id;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    acc_and &= __shfl_xor_sync(0xffffffffu, acc_and, o);
-    acc_or |= __shfl_xor_sync(0xffffffffu, acc_or, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAnd(&ctr->key_and, acc_and);
-    atomicOr(&ctr->key_or, acc_or);
-  }
+  publish_and_or(acc_and, acc_or, ctr);
 }
 
 __global__ void k_reset_keys(DevCounters* ctr) {
@@ -282,7 +274,7 @@ template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
-          const int32_t* __restrict__ cell_end, double eps2, int minpts,
+          const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
           uint8_t* __restrict__ flags, DevCounters* ctr) {
   int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   unsigned long long dists = 0;
@@ -302,13 +294,13 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
             float4 m4 = __ldg(sorted_pt + k);
             float mp[3] = {m4.x, m4.y, m4.z};
             ++dists;
-            if (dist2<D>(p, mp) <= eps2)
+            if (ball_hits<D>(p, mp, mp, bt))
               if (++count >= minpts) break;
           }
         }
         return count < minpts;
       };
-      bvh_query<D>(nodes, p, eps2, 0, visit);
+      bvh_query<D>(nodes, p, bt, 0, visit);
       if (count >= minpts) flags[raw] = 1;
     }
   }
@@ -321,7 +313,7 @@ __global__ void __launch_bounds__(kQueryBlock)
 k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
           const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
           const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
-          double eps2, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
           DevCounters* ctr) {
   int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   unsigned long long dists = 0, pairs = 0;
@@ -331,15 +323,14 @@ k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
     const int32_t own = qrank[q];
     float p[3] = {qp.x, qp.y, qp.z};
     const bool core_i = kForceCore ? true : flags[i] != 0;
+    int32_t hint = i;
+    bool settled = false;
     auto pair = [&](int32_t j) {
       ++pairs;
-      if (kForceCore) {
-        flags[i] = 1;
-        flags[j] = 1;
-        uf_unite(parent, i, j);
-      } else {
-        resolve_pair(i, j, core_i, flags, parent);
-      }
+      if (kForceCore)
+        uf_unite_hinted(parent, i, j, hint);  // core flags derived at finalize
+      else
+        resolve_pair(i, j, core_i, flags, parent, hint, settled);
     };
     auto visit = [&](int32_t s, int32_t aux, const float*, const float*) -> bool {
       if (s == own) return true;
@@ -352,7 +343,7 @@ k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
           float4 m4 = __ldg(sorted_pt + k);
           float mp[3] = {m4.x, m4.y, m4.z};
           ++dists;
-          if (dist2<D>(p, mp) <= eps2) {
+          if (ball_hits<D>(p, mp, mp, bt)) {
             pair(__float_as_int(m4.w));
             break;  // one link joins the whole pre-unioned box (dbscan.cpp:183-193)
           }
@@ -360,7 +351,7 @@ k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
       }
       return true;
     };
-    bvh_query<D>(nodes, p, eps2, own, visit);
+    bvh_query<D>(nodes, p, bt, own, visit);
   }
   unsigned long long v = warp_sum(dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
@@ -375,7 +366,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
                   uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
                   double* dense_fraction) {
   cudaStream_t st = scratch.stream();
-  const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
+  const BallTest bt = BallTest::make(static_cast<double>(eps) * static_cast<double>(eps));
   clock.mark(kStGrid);
 
   // ---- grid ----
@@ -385,7 +376,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   note_launch(), k_grid_setup<D><<<1, 1, 0, st>>>(ctr, h, gp);
   uint64_t* keys = scratch.alloc_n<uint64_t>(n);
   int32_t* vals = scratch.alloc_n<int32_t>(n);
-  note_launch(), k_cell_ids<D><<<grid_for(n, 256), 256, 0, st>>>(d_coords, n, gp, keys, vals, ctr);
+  note_launch(), k_cell_ids<D><<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(d_coords, n, gp, keys, vals, ctr);
   TCB_CUDA(cudaGetLastError());
   auto* h_stage = static_cast<unsigned char*>(pinned_staging(64));
   TCB_CUDA(cudaMemcpyAsync(h_stage, &ctr->key_and, 16, cudaMemcpyDeviceToHost, st));
@@ -490,20 +481,20 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   const unsigned gq = grid_for(n, kQueryBlock, INT32_MAX);
   if (minpts > 2)
     note_launch(), k_db_core<D><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
-                                             cell_end, eps2, minpts, flags, ctr);
+                                             cell_end, bt, minpts, flags, ctr);
   // ---- main pass ----
   clock.mark(kStMain);
   if (minpts == 2)
     note_launch(), k_db_main<D, true><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
-                                                   cell_begin, cell_end, eps2, flags, parent,
+                                                   cell_begin, cell_end, bt, flags, parent,
                                                    ctr);
   else
     note_launch(), k_db_main<D, false><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
-                                                    cell_begin, cell_end, eps2, flags, parent,
+                                                    cell_begin, cell_end, bt, flags, parent,
                                                     ctr);
   TCB_CUDA(cudaGetLastError());
   clock.mark(kStFinal);
-  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st);
+  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st, minpts == 2);
   clock.finish();
 }
 

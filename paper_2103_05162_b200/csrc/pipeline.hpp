@@ -1,6 +1,7 @@
 // Host-side pieces of the device pipeline shared between translation units.
 #pragma once
 
+#include <cfloat>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <vector>
@@ -106,9 +107,11 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s);
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
-void finalize_labels(int32_t* parent, const uint8_t* flags, int64_t n,
+// force_core (minpts == 2): core flags are derived here from the union-find
+// structure instead of being stored per pair in the main pass.
+void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,
                      int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
-                     cudaStream_t s);
+                     cudaStream_t s, bool force_core);
 
 // ---- DenseBox (grid.cu) ----
 template <int D>
@@ -121,6 +124,36 @@ template <int D>
 void run_bruteforce(const float* d_coords, int64_t n, float eps, int minpts,
                     int32_t* d_labels, uint8_t* d_core, DevCounters* d_ctr,
                     Scratch& scratch);
+
+#ifdef __CUDACC__
+// One atomic per block (not per warp): ~1k same-address atomics instead of
+// ~1e5 serialized ones at the L2 slice.
+template <int D>
+__device__ __forceinline__ void publish_bounds(float* mn, float* mx, bool bad, DevCounters* ctr) {
+  __shared__ float red[32];
+  auto fmin_op = [](float a, float b) { return fminf(a, b); };
+  auto fmax_op = [](float a, float b) { return fmaxf(a, b); };
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    float lo = block_reduce(mn[k], fmin_op, FLT_MAX, red);
+    if (threadIdx.x == 0) atomicMin(&ctr->bounds_ord[k], f2ord(lo));
+    float hi = block_reduce(mx[k], fmax_op, -FLT_MAX, red);
+    if (threadIdx.x == 0) atomicMax(&ctr->bounds_ord[3 + k], f2ord(hi));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ctr->nonfinite, 1);
+}
+
+__device__ __forceinline__ void publish_and_or(uint64_t a, uint64_t o, DevCounters* ctr) {
+  __shared__ unsigned long long red64[32];
+  auto and_op = [](unsigned long long x, unsigned long long y) { return x & y; };
+  auto or_op = [](unsigned long long x, unsigned long long y) { return x | y; };
+  unsigned long long ra = block_reduce<unsigned long long>(a, and_op, ~0ull, red64);
+  if (threadIdx.x == 0) atomicAnd(&ctr->key_and, ra);
+  unsigned long long ro = block_reduce<unsigned long long>(o, or_op, 0ull, red64);
+  if (threadIdx.x == 0) atomicOr(&ctr->key_or, ro);
+}
+
+#endif
 
 inline unsigned grid_for(int64_t work, int block, int64_t max_blocks = 148 * 64) {
   int64_t b = (work + block - 1) / block;
