@@ -71,59 +71,143 @@ __device__ __forceinline__ bool ball_hits(const float* p, const float* lo, const
   return box_dist2<D>(p, lo, hi) <= bt.r2;
 }
 
-// Traverses the tree for the closed ball (p, sqrt(r2)), hiding every leaf
-// with rank < min_rank (query_sphere_masked, bvh.hpp:45-72), and calls
+// One traversal step of the closed-ball query (p, sqrt(r2)) that hides every
+// leaf with rank < min_rank (query_sphere_masked, bvh.hpp:45-72): processes
+// ONE node, calling
 //     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
-// for each leaf whose box is within the ball; visit returning false ends the
-// query. Visit order is exactly the reference's (left before right for leaf
-// children; right subtree before left subtree for internal children, i.e. its
-// LIFO stack order), so early-exit counters match bit for bit.
+// for each leaf child whose box is within the ball (false = stop the query),
+// and advances `node` / the stack. Returns false when the query is finished.
+// The visit order is exactly the reference's (left before right for leaf
+// children; right subtree before left subtree for internal children — its LIFO
+// stack order), so early-exit counters match bit for bit.
 template <int D, typename Visit>
-__device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes,
-                                          const float* p, const BallTest& bt,
-                                          int32_t min_rank, Visit& visit) {
+__device__ __forceinline__ bool bvh_step(const float4* __restrict__ nodes, const float* p,
+                                         const BallTest& bt, int32_t min_rank, int32_t& node,
+                                         int& top, int32_t* stack, Visit& visit) {
   using T = NodeTraits<D>;
+  float f[T::kFloats];
+  const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
+#pragma unroll
+  for (int v = 0; v < T::kVec; ++v) {
+    float4 q = __ldg(src + v);
+    f[4 * v + 0] = q.x;
+    f[4 * v + 1] = q.y;
+    f[4 * v + 2] = q.z;
+    f[4 * v + 3] = q.w;
+  }
+  const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+  const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+  const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+  const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+  bool go_l = false, go_r = false;
+  if (left < 0) {
+    if (~left >= min_rank && ball_hits<D>(p, f, f + D, bt))
+      if (!visit(~left, aux_l, f, f + D)) return false;
+  } else if (aux_l >= min_rank && ball_hits<D>(p, f, f + D, bt)) {
+    go_l = true;
+  }
+  if (right < 0) {
+    if (~right >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt))
+      if (!visit(~right, aux_r, f + 2 * D, f + 3 * D)) return false;
+  } else if (aux_r >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
+    go_r = true;
+  }
+  if (go_l && go_r) {
+    stack[top++] = left;
+    node = right;
+  } else if (go_l) {
+    node = left;
+  } else if (go_r) {
+    node = right;
+  } else {
+    if (top == 0) return false;
+    node = stack[--top];
+  }
+  return true;
+}
+
+// The whole query on one thread.
+template <int D, typename Visit>
+__device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, const float* p,
+                                          const BallTest& bt, int32_t min_rank, Visit& visit) {
   int32_t stack[kStackDepth];
   int top = 0;
   int32_t node = 0;
+  while (bvh_step<D>(nodes, p, bt, min_rank, node, top, stack, visit)) {
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent, warp-refilled query driver.
+//
+// Per-query work varies by orders of magnitude (a point in a halo core has
+// thousands of neighbours, a background point none), so one-query-per-thread
+// launches leave most lanes of a warp idle while the longest query runs
+// (ncu, round 1: 5.6 active threads / warp). Instead each warp owns a chunk of
+// kQueryChunk Morton-consecutive queries (grabbed with one atomic) and refills
+// every lane the moment its query finishes; all lanes advance one node per
+// iteration. Chunks are handed out in rank order, so the queries in flight
+// stay a narrow, L2-resident window of the tree.
+//
+// Q provides:  bool begin(int64_t q)  start query q (false: nothing to do)
+//              bool step()            one node; false when the query is done
+//              void end()             finish the current query
+// ---------------------------------------------------------------------------
+constexpr int kQueryChunk = 256;
+
+// One query per thread, grid covers all queries (the plain launch).
+template <class Q>
+__device__ __forceinline__ void run_query_direct(int64_t m, Q& qp) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (q < m && qp.begin(q)) {
+    while (qp.step()) {
+    }
+    qp.end();
+  }
+}
+
+// Query scheduling mode of the traversal kernels: 0 = one query per thread,
+// 1 = persistent warp-refilled queue. Chosen once per process (TCB_QUERY_MODE).
+int query_mode();
+
+__device__ __forceinline__ uint32_t lanemask_lt_u32() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <class Q>
+__device__ __forceinline__ void run_query_queue(int64_t m, unsigned long long* next_chunk, Q& qp) {
+  const int lane = threadIdx.x & 31;
+  long long cur = 0, end = 0;  // warp-uniform chunk [cur, end)
+  bool exhausted = false;      // warp-uniform
+  bool busy = false;
   while (true) {
-    float f[T::kFloats];
-    const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
-#pragma unroll
-    for (int v = 0; v < T::kVec; ++v) {
-      float4 q = __ldg(src + v);
-      f[4 * v + 0] = q.x;
-      f[4 * v + 1] = q.y;
-      f[4 * v + 2] = q.z;
-      f[4 * v + 3] = q.w;
+    const uint32_t idle = __ballot_sync(0xffffffffu, !busy);
+    if (idle) {
+      if (cur >= end && !exhausted) {
+        long long base = 0;
+        if (lane == 0) base = static_cast<long long>(atomicAdd(next_chunk, kQueryChunk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= m) {
+          exhausted = true;
+        } else {
+          cur = base;
+          end = base + kQueryChunk < m ? base + kQueryChunk : m;
+        }
+      }
+      if (cur >= end) {
+        if (idle == 0xffffffffu && exhausted) break;
+      } else {
+        const long long q = cur + __popc(idle & lanemask_lt_u32());
+        if (!busy && q < end) busy = qp.begin(q);
+        cur += __popc(idle);
+        if (cur > end) cur = end;
+      }
     }
-    const int32_t left = __float_as_int(f[T::kIntOff + 0]);
-    const int32_t right = __float_as_int(f[T::kIntOff + 1]);
-    const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
-    const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
-    bool go_l = false, go_r = false;
-    if (left < 0) {
-      if (~left >= min_rank && ball_hits<D>(p, f, f + D, bt))
-        if (!visit(~left, aux_l, f, f + D)) return;
-    } else if (aux_l >= min_rank && ball_hits<D>(p, f, f + D, bt)) {
-      go_l = true;
-    }
-    if (right < 0) {
-      if (~right >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt))
-        if (!visit(~right, aux_r, f + 2 * D, f + 3 * D)) return;
-    } else if (aux_r >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
-      go_r = true;
-    }
-    if (go_l && go_r) {
-      stack[top++] = left;
-      node = right;
-    } else if (go_l) {
-      node = left;
-    } else if (go_r) {
-      node = right;
-    } else {
-      if (top == 0) return;
-      node = stack[--top];
+    if (busy && !qp.step()) {
+      qp.end();
+      busy = false;
     }
   }
 }

@@ -39,42 +39,66 @@ __device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned 
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
 }
 
+// fdbscan_mark_cores query (dbscan.cpp:36-58): unmasked, early exit once
+// minpts neighbours (self included) are seen.
 template <int D>
-__global__ void __launch_bounds__(kQueryBlock)
-k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
-  int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+struct CoreQuery {
+  const float4* __restrict__ nodes;
+  const float4* __restrict__ leaf_pt;
+  BallTest bt;
+  int minpts;
+  uint8_t* __restrict__ flags;
+  int32_t* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long dists = 0;
-  if (r < m) {
-    float p[3];
-    int32_t id;
+  float p[3];
+  int32_t id, node;
+  int count, top;
+  __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &id);
-    int count = 0;
+    count = 0;
+    node = 0;
+    top = 0;
+    return true;
+  }
+  __device__ bool step() {
     auto visit = [&](int32_t, int32_t, const float*, const float*) -> bool {
       ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
-    bvh_query<D>(nodes, p, bt, 0, visit);
+    return bvh_step<D>(nodes, p, bt, 0, node, top, stack, visit);
+  }
+  __device__ void end() {
     if (count >= minpts) flags[id] = 1;
   }
-  flush_counter(&ctr->dists, dists);
-}
+};
 
+// fdbscan_main_phase query (dbscan.cpp:60-88): masked at the query's own rank
+// so each unordered pair is met exactly once; each pair is resolved on the
+// spot, no neighbour list is stored.
 template <int D, bool kForceCore>
-__global__ void __launch_bounds__(kQueryBlock)
-k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-          DevCounters* ctr) {
-  int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+struct MainQuery {
+  const float4* __restrict__ nodes;
+  const float4* __restrict__ leaf_pt;
+  BallTest bt;
+  const uint8_t* __restrict__ flags;
+  int32_t* __restrict__ parent;
+  int32_t* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long pairs = 0;
-  if (r < m) {
-    float p[3];
-    int32_t i;
+  float p[3];
+  int32_t i, rank, hint, node;
+  int top;
+  bool core_i, settled;
+  __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &i);
-    const int32_t rank = static_cast<int32_t>(r);
-    const bool core_i = kForceCore ? true : flags[i] != 0;
-    int32_t hint = i;
-    bool settled = false;
+    rank = static_cast<int32_t>(r);
+    core_i = kForceCore ? true : flags[i] != 0;
+    hint = i;
+    settled = false;
+    node = 0;
+    top = 0;
+    return true;
+  }
+  __device__ bool step() {
     auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
       if (s == rank) return true;
       ++pairs;
@@ -84,10 +108,37 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
         resolve_pair(i, j, core_i, flags, parent, hint, settled);
       return true;
     };
-    bvh_query<D>(nodes, p, bt, rank, visit);
+    return bvh_step<D>(nodes, p, bt, rank, node, top, stack, visit);
   }
-  flush_counter(&ctr->pairs, pairs);
-  flush_counter(&ctr->dists, pairs);
+  __device__ void end() {}
+};
+
+template <int D>
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent) {
+  int32_t stack[kStackDepth];
+  CoreQuery<D> q{nodes, leaf_pt, bt, minpts, flags, stack};
+  if (persistent)
+    run_query_queue(m, &ctr->queue[0], q);
+  else
+    run_query_direct(m, q);
+  flush_counter(&ctr->dists, q.dists);
+}
+
+template <int D, bool kForceCore>
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+          DevCounters* ctr, bool persistent) {
+  int32_t stack[kStackDepth];
+  MainQuery<D, kForceCore> q{nodes, leaf_pt, bt, flags, parent, stack};
+  if (persistent)
+    run_query_queue(m, &ctr->queue[1], q);
+  else
+    run_query_direct(m, q);
+  flush_counter(&ctr->pairs, q.pairs);
+  flush_counter(&ctr->dists, q.pairs);
 }
 
 __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
@@ -147,8 +198,8 @@ k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int6
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s) {
-  note_launch(), k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-      b.tree.nodes, b.leaf_pt, n, BallTest::make(eps2), minpts, flags, d_ctr);
+  note_launch(), k_fd_core<D><<<query_grid(k_fd_core<D>, n), kQueryBlock, 0, s>>>(
+      b.tree.nodes, b.leaf_pt, n, BallTest::make(eps2), minpts, flags, d_ctr, query_mode() == 1);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -156,14 +207,13 @@ template <int D>
 void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s) {
-  const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
   const BallTest bt = BallTest::make(eps2);
   if (force_core)
-    note_launch(), k_fd_main<D, true><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
-                                                                flags, parent, d_ctr);
+    note_launch(), k_fd_main<D, true><<<query_grid(k_fd_main<D, true>, n), kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
+                                                                flags, parent, d_ctr, query_mode() == 1);
   else
-    note_launch(), k_fd_main<D, false><<<g, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
-                                                                 flags, parent, d_ctr);
+    note_launch(), k_fd_main<D, false><<<query_grid(k_fd_main<D, false>, n), kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
+                                                                 flags, parent, d_ctr, query_mode() == 1);
   TCB_CUDA(cudaGetLastError());
 }
 

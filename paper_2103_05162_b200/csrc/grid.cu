@@ -270,41 +270,140 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
   }
 }
 
+// densebox_mark_cores query (dbscan.cpp:110-139): unmasked; a SinglePoint
+// leaf is one neighbour, a DenseBox leaf is scanned member by member until
+// minpts is reached. Dense members are core already and skip (dbscan.cpp:118).
+template <int D>
+struct DbCoreQuery {
+  const float4* __restrict__ nodes;
+  const float4* __restrict__ qpt;
+  const float4* __restrict__ sorted_pt;
+  const int32_t* __restrict__ cell_begin;
+  const int32_t* __restrict__ cell_end;
+  BallTest bt;
+  int minpts;
+  uint8_t* __restrict__ flags;
+  int32_t* stack;  // per-thread traversal stack, kept outside the struct
+  unsigned long long dists = 0;
+  float p[3];
+  int32_t id, node;
+  int count, top;
+  __device__ bool begin(int64_t q) {
+    const float4 qp = qpt[q];
+    id = __float_as_int(qp.w);
+    if (id < 0) return false;  // member of a dense cell
+    p[0] = qp.x;
+    p[1] = qp.y;
+    p[2] = qp.z;
+    count = 0;
+    node = 0;
+    top = 0;
+    return true;
+  }
+  __device__ bool step() {
+    auto visit = [&](int32_t, int32_t aux, const float*, const float*) -> bool {
+      if (aux >= 0) {
+        ++dists;
+        ++count;  // leaf box test == exact distance test for a point leaf
+      } else {
+        const int32_t c = ~aux;
+        for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
+          const float4 m4 = __ldg(sorted_pt + k);
+          const float mp[3] = {m4.x, m4.y, m4.z};
+          ++dists;
+          if (ball_hits<D>(p, mp, mp, bt))
+            if (++count >= minpts) break;
+        }
+      }
+      return count < minpts;
+    };
+    return bvh_step<D>(nodes, p, bt, 0, node, top, stack, visit);
+  }
+  __device__ void end() {
+    if (count >= minpts) flags[id] = 1;
+  }
+};
+
+// densebox_main_phase query (dbscan.cpp:141-200): masked at the rank of the
+// query's own primitive (its own leaf skipped); a SinglePoint leaf is one
+// pair, a DenseBox leaf contributes the first member within eps only — every
+// member is a core of one pre-unioned cluster, so one link joins them all.
+template <int D, bool kForceCore>
+struct DbMainQuery {
+  const float4* __restrict__ nodes;
+  const float4* __restrict__ qpt;
+  const int32_t* __restrict__ qrank;
+  const float4* __restrict__ sorted_pt;
+  const int32_t* __restrict__ cell_begin;
+  const int32_t* __restrict__ cell_end;
+  BallTest bt;
+  const uint8_t* __restrict__ flags;
+  int32_t* __restrict__ parent;
+  int32_t* stack;  // per-thread traversal stack, kept outside the struct
+  unsigned long long dists = 0, pairs = 0;
+  float p[3];
+  int32_t i, own, hint, node;
+  int top;
+  bool core_i, settled;
+  __device__ bool begin(int64_t q) {
+    const float4 qp = qpt[q];
+    i = __float_as_int(qp.w) & 0x7fffffff;
+    own = qrank[q];
+    p[0] = qp.x;
+    p[1] = qp.y;
+    p[2] = qp.z;
+    core_i = kForceCore ? true : flags[i] != 0;
+    hint = i;
+    settled = false;
+    node = 0;
+    top = 0;
+    return true;
+  }
+  __device__ void pair(int32_t j) {
+    ++pairs;
+    if (kForceCore)
+      uf_unite_hinted(parent, i, j, hint);  // core flags derived at finalize
+    else
+      resolve_pair(i, j, core_i, flags, parent, hint, settled);
+  }
+  __device__ bool step() {
+    auto visit = [&](int32_t s, int32_t aux, const float*, const float*) -> bool {
+      if (s == own) return true;
+      if (aux >= 0) {
+        ++dists;
+        pair(aux);
+      } else {
+        const int32_t c = ~aux;
+        for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
+          const float4 m4 = __ldg(sorted_pt + k);
+          const float mp[3] = {m4.x, m4.y, m4.z};
+          ++dists;
+          if (ball_hits<D>(p, mp, mp, bt)) {
+            pair(__float_as_int(m4.w));
+            break;  // dbscan.cpp:183-193
+          }
+        }
+      }
+      return true;
+    };
+    return bvh_step<D>(nodes, p, bt, own, node, top, stack, visit);
+  }
+  __device__ void end() {}
+};
+
 template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
-          uint8_t* __restrict__ flags, DevCounters* ctr) {
-  int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  unsigned long long dists = 0;
-  if (q < n) {
-    float4 qp = qpt[q];
-    const int32_t raw = __float_as_int(qp.w);
-    if (raw >= 0) {  // dense members are core already (dbscan.cpp:118)
-      float p[3] = {qp.x, qp.y, qp.z};
-      int count = 0;
-      auto visit = [&](int32_t, int32_t aux, const float*, const float*) -> bool {
-        if (aux >= 0) {
-          ++dists;
-          ++count;  // leaf box test == exact distance test for a point leaf
-        } else {
-          const int32_t c = ~aux;
-          for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
-            float4 m4 = __ldg(sorted_pt + k);
-            float mp[3] = {m4.x, m4.y, m4.z};
-            ++dists;
-            if (ball_hits<D>(p, mp, mp, bt))
-              if (++count >= minpts) break;
-          }
-        }
-        return count < minpts;
-      };
-      bvh_query<D>(nodes, p, bt, 0, visit);
-      if (count >= minpts) flags[raw] = 1;
-    }
-  }
-  unsigned long long v = warp_sum(dists);
+          uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent) {
+  int32_t stack[kStackDepth];
+  DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, stack};
+  if (persistent)
+    run_query_queue(n, &ctr->queue[2], q);
+  else
+    run_query_direct(n, q);
+  unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
 }
 
@@ -314,48 +413,17 @@ k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
           const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
           const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-          DevCounters* ctr) {
-  int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  unsigned long long dists = 0, pairs = 0;
-  if (q < n) {
-    float4 qp = qpt[q];
-    const int32_t i = __float_as_int(qp.w) & 0x7fffffff;
-    const int32_t own = qrank[q];
-    float p[3] = {qp.x, qp.y, qp.z};
-    const bool core_i = kForceCore ? true : flags[i] != 0;
-    int32_t hint = i;
-    bool settled = false;
-    auto pair = [&](int32_t j) {
-      ++pairs;
-      if (kForceCore)
-        uf_unite_hinted(parent, i, j, hint);  // core flags derived at finalize
-      else
-        resolve_pair(i, j, core_i, flags, parent, hint, settled);
-    };
-    auto visit = [&](int32_t s, int32_t aux, const float*, const float*) -> bool {
-      if (s == own) return true;
-      if (aux >= 0) {
-        ++dists;
-        pair(aux);
-      } else {
-        const int32_t c = ~aux;
-        for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
-          float4 m4 = __ldg(sorted_pt + k);
-          float mp[3] = {m4.x, m4.y, m4.z};
-          ++dists;
-          if (ball_hits<D>(p, mp, mp, bt)) {
-            pair(__float_as_int(m4.w));
-            break;  // one link joins the whole pre-unioned box (dbscan.cpp:183-193)
-          }
-        }
-      }
-      return true;
-    };
-    bvh_query<D>(nodes, p, bt, own, visit);
-  }
-  unsigned long long v = warp_sum(dists);
+          DevCounters* ctr, bool persistent) {
+  int32_t stack[kStackDepth];
+  DbMainQuery<D, kForceCore> q{nodes, qpt, qrank, sorted_pt, cell_begin, cell_end, bt, flags,
+                               parent, stack};
+  if (persistent)
+    run_query_queue(n, &ctr->queue[3], q);
+  else
+    run_query_direct(n, q);
+  unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
-  v = warp_sum(pairs);
+  v = warp_sum(q.pairs);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
 }
 
@@ -478,20 +546,19 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
 
   // ---- core pass ----
   clock.mark(kStCore);
-  const unsigned gq = grid_for(n, kQueryBlock, INT32_MAX);
   if (minpts > 2)
-    note_launch(), k_db_core<D><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
-                                             cell_end, bt, minpts, flags, ctr);
+    note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
+                                             cell_end, bt, minpts, flags, ctr, query_mode() == 1);
   // ---- main pass ----
   clock.mark(kStMain);
   if (minpts == 2)
-    note_launch(), k_db_main<D, true><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+    note_launch(), k_db_main<D, true><<<query_grid(k_db_main<D, true>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
                                                    cell_begin, cell_end, bt, flags, parent,
-                                                   ctr);
+                                                   ctr, query_mode() == 1);
   else
-    note_launch(), k_db_main<D, false><<<gq, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+    note_launch(), k_db_main<D, false><<<query_grid(k_db_main<D, false>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
                                                     cell_begin, cell_end, bt, flags, parent,
-                                                    ctr);
+                                                    ctr, query_mode() == 1);
   TCB_CUDA(cudaGetLastError());
   clock.mark(kStFinal);
   finalize_labels(parent, flags, n, d_labels, d_core, ctr, st, minpts == 2);
