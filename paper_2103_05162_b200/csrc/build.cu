@@ -145,7 +145,8 @@ template <int D, class Src>
 __global__ void __launch_bounds__(256)
 k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
          const int32_t* __restrict__ prim_aux, int64_t m, float4* __restrict__ nodes,
-         int32_t* __restrict__ node_parent, float4* __restrict__ leaf_pt) {
+         int32_t* __restrict__ node_parent, int32_t* __restrict__ node_delta,
+         int32_t* __restrict__ leaf_parent, float4* __restrict__ leaf_pt) {
   using T = NodeTraits<D>;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= m - 1) return;
@@ -182,8 +183,10 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
     }
   };
   int32_t left, right, aux_l, aux_r;
+  node_delta[i] = delta_node;  // prefix length shared by the whole range
   if (lo == gamma) {
     leaf_child(gamma, 0, left, aux_l);
+    leaf_parent[gamma] = static_cast<int32_t>(i);
   } else {
     left = static_cast<int32_t>(gamma);
     aux_l = static_cast<int32_t>(gamma);  // max leaf rank of [lo, gamma]
@@ -191,6 +194,7 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
   }
   if (hi == gamma + 1) {
     leaf_child(gamma + 1, 1, right, aux_r);
+    leaf_parent[gamma + 1] = static_cast<int32_t>(i);
   } else {
     right = static_cast<int32_t>(gamma + 1);
     aux_r = static_cast<int32_t>(hi);  // max leaf rank of [gamma+1, hi]
@@ -259,8 +263,12 @@ k_refit(int64_t m, float4* nodes, const int32_t* __restrict__ node_parent,
 
 // 1-leaf tree: pseudo root with the leaf on the left and an empty box right.
 template <int D, class Src>
-__global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux,
-                              float4* nodes, float4* leaf_pt) {
+__global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, float4* nodes,
+                              float4* leaf_pt, int32_t* node_parent, int32_t* node_delta,
+                              int32_t* leaf_parent) {
+  node_parent[0] = -1;
+  node_delta[0] = 0;
+  leaf_parent[0] = 0;
   using T = NodeTraits<D>;
   float lo[3], hi[3];
   src.box(0, lo, hi);
@@ -323,15 +331,26 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
 
   if (clock) clock->mark(kStTopo);
   float4* leaf_pt = out.leaf_pt;
+  out.codes = codes;
+  out.node_parent = scratch.alloc_n<int32_t>(std::max<int64_t>(1, m - 1));
+  out.node_delta = scratch.alloc_n<int32_t>(std::max<int64_t>(1, m - 1));
+  out.leaf_parent = scratch.alloc_n<int32_t>(m);
+  uint32_t* scene = scratch.alloc_n<uint32_t>(8);
+  TCB_CUDA(cudaMemcpyAsync(scene, &d_ctr->bounds_ord[0], 6 * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, st));
+  out.scene_ord = scene;
   if (m == 1) {
-    note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
+    note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt,
+                                                     out.node_parent, out.node_delta,
+                                                     out.leaf_parent);
   } else {
-    int32_t* node_parent = scratch.alloc_n<int32_t>(m - 1);
+    int32_t* node_parent = out.node_parent;
     int32_t* arrivals = scratch.alloc_n<int32_t>(m - 1);
     TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * (m - 1), st));
     const unsigned gn = grid_for(m - 1, 256, INT32_MAX);
     note_launch(), k_karras<D><<<gn, 256, 0, st>>>(boxes, codes, order, src.aux, m,
-                                                   out.tree.nodes, node_parent, leaf_pt);
+                                                   out.tree.nodes, node_parent, out.node_delta,
+                                                   out.leaf_parent, leaf_pt);
     note_launch(), k_refit<D><<<gn, 256, 0, st>>>(m, out.tree.nodes, node_parent, arrivals);
   }
   TCB_CUDA(cudaGetLastError());

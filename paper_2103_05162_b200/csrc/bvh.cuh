@@ -138,6 +138,119 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
 }
 
 // ---------------------------------------------------------------------------
+// Bottom-up masked traversal with Morton-cell early termination (main pass).
+//
+// The masked query of leaf r must find every leaf of rank > r within the
+// ball. Those leaves are exactly the right siblings of r's ancestors (where
+// r's path turns left), so instead of descending from the root (~35 levels for
+// 37M leaves, before any neighbour is met) the query climbs from its own leaf
+// and explores only right siblings whose box meets the ball.
+//
+// It stops climbing at the first ancestor A whose Morton cell contains the
+// ball: a Karras node is a binary radix-tree node, so its subtree holds
+// exactly the primitives whose codes share its prefix (node_delta bits), i.e.
+// whose centroid quantizes into A's cell. A primitive outside A therefore has
+// its centroid outside the cell, hence farther than `reach` from p when the
+// reach-ball lies inside the cell (reach = eps + the largest primitive
+// half-diagonal: eps for points). The cell test runs in the integer
+// quantized space with the same monotone quantize() as the codes, on a ball
+// widened by relative margins, so it is conservative under rounding.
+//
+// The visit order differs from the reference's DFS; the main pass has no
+// early exit, so its pair set and counters are order independent.
+// ---------------------------------------------------------------------------
+
+// Largest 64-bit common-prefix length at which an ancestor's Morton cell is
+// known to contain the ball (p, reach); anchor = a point of the query's own
+// leaf (its centroid), which lies in every ancestor's cell.
+template <int D>
+__device__ __forceinline__ int morton_stop_delta(const float* p, double reach,
+                                                 const float* anchor,
+                                                 const uint32_t* __restrict__ scene_ord) {
+  constexpr int B = D == 2 ? 31 : 21;
+  constexpr uint64_t cells = 1ull << B;
+  const double cells_d = static_cast<double>(cells);
+  const double e = reach * (1.0 + 0x1.0p-20);
+  int agree[3];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float lo = ord2f(__ldg(scene_ord + k));
+    const float hi = ord2f(__ldg(scene_ord + 3 + k));
+    const double w = __dsub_rn(static_cast<double>(hi), static_cast<double>(lo));
+    if (w <= 0.0) {
+      agree[k] = B;
+      continue;
+    }
+    const double pk = static_cast<double>(p[k]);
+    const double slack = (fabs(pk) + e) * 0x1.0p-50;
+    const uint64_t qa = quantize(anchor[k], lo, w, cells_d, cells);
+    const uint64_t ql = quantize_d(pk - e - slack, lo, w, cells_d, cells);
+    const uint64_t qh = quantize_d(pk + e + slack, lo, w, cells_d, cells);
+    const uint32_t x = static_cast<uint32_t>((ql ^ qa) | (qh ^ qa));
+    agree[k] = x == 0 ? B : __clz(static_cast<int>(x)) - (32 - B);
+  }
+  int dmax;  // meaningful prefix bits (MSB = highest bit of the last axis)
+  if (D == 3)
+    dmax = min(min(3 * agree[2], 3 * agree[1] + 1), min(3 * agree[0] + 2, 63));
+  else
+    dmax = min(min(2 * agree[1], 2 * agree[0] + 1), 62);
+  return dmax + (64 - D * B);
+}
+
+struct UpState {
+  int32_t c;     // link of the child we climbed from (~rank for a leaf)
+  int32_t P;     // current ancestor (-1: climb finished)
+  int32_t node;  // exploration cursor inside a right sibling
+  int top;
+  bool exploring;
+};
+
+template <int D, typename Visit>
+__device__ __forceinline__ bool bvh_up_step(const float4* __restrict__ nodes,
+                                            const int32_t* __restrict__ node_parent,
+                                            const int32_t* __restrict__ node_delta,
+                                            const float* p, const BallTest& bt, int stop_delta,
+                                            UpState& s, int32_t* stack, Visit& visit) {
+  using T = NodeTraits<D>;
+  if (s.exploring) {
+    if (!bvh_step<D>(nodes, p, bt, 0, s.node, s.top, stack, visit)) s.exploring = false;
+    return true;
+  }
+  if (s.P < 0) return false;
+  const float4* src = nodes + static_cast<int64_t>(s.P) * T::kVec;
+  const int32_t dP = __ldg(node_delta + s.P);
+  const int32_t pP = __ldg(node_parent + s.P);
+  float f[T::kFloats];
+#pragma unroll
+  for (int v = 0; v < T::kVec; ++v) {
+    float4 q = __ldg(src + v);
+    f[4 * v + 0] = q.x;
+    f[4 * v + 1] = q.y;
+    f[4 * v + 2] = q.z;
+    f[4 * v + 3] = q.w;
+  }
+  const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+  const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+  const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+  if (left == s.c && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
+    if (right < 0) {
+      visit(~right, aux_r, f + 2 * D, f + 3 * D);
+    } else {
+      s.exploring = true;
+      s.node = right;
+      s.top = 0;
+    }
+  }
+  if (dP <= stop_delta) {
+    s.P = -1;
+  } else {
+    s.c = s.P;
+    s.P = pP;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // Persistent, warp-refilled query driver.
 //
 // Per-query work varies by orders of magnitude (a point in a halo core has

@@ -15,6 +15,8 @@
 // degenerate and box_distance_sq reduces to distance_sq term by term, the
 // subtraction merely negated), so a visited leaf is a within-eps neighbour
 // and its distance is not recomputed.
+#include <cmath>
+
 #include "device_common.cuh"
 #include "pipeline.hpp"
 
@@ -72,35 +74,53 @@ struct CoreQuery {
   }
 };
 
-// fdbscan_main_phase query (dbscan.cpp:60-88): masked at the query's own rank
-// so each unordered pair is met exactly once; each pair is resolved on the
-// spot, no neighbour list is stored.
-template <int D, bool kForceCore>
+// fdbscan_main_phase query (dbscan.cpp:60-88): every leaf of rank > r
+// within eps, i.e. each unordered pair exactly once, found by the bottom-up
+// masked traversal (bvh_up_step) from the query's own leaf; each pair is
+// resolved on the spot, no neighbour list is stored.
+template <int D, bool kForceCore, bool kUp>
 struct MainQuery {
   const float4* __restrict__ nodes;
   const float4* __restrict__ leaf_pt;
+  const int32_t* __restrict__ node_parent;
+  const int32_t* __restrict__ node_delta;
+  const int32_t* __restrict__ leaf_parent;
+  const uint32_t* __restrict__ scene_ord;
   BallTest bt;
+  double eps;
   const uint8_t* __restrict__ flags;
   int32_t* __restrict__ parent;
   int32_t* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long pairs = 0;
   float p[3];
-  int32_t i, rank, hint, node;
-  int top;
+  int32_t i, hint;
+  int stop_delta;
+  int32_t rank;
   bool core_i, settled;
+  UpState us;
+
   __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &i);
     rank = static_cast<int32_t>(r);
+    if (kUp) {
+      float anchor[3];
+#pragma unroll
+      for (int k = 0; k < D; ++k) anchor[k] = __fmul_rn(0.5f, __fadd_rn(p[k], p[k]));
+      stop_delta = morton_stop_delta<D>(p, eps, anchor, scene_ord);
+    }
     core_i = kForceCore ? true : flags[i] != 0;
     hint = i;
     settled = false;
-    node = 0;
-    top = 0;
+    us.c = ~static_cast<int32_t>(r);
+    us.P = kUp ? __ldg(leaf_parent + r) : 0;
+    us.node = 0;
+    us.top = 0;
+    us.exploring = false;
     return true;
   }
   __device__ bool step() {
     auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
-      if (s == rank) return true;
+      if (!kUp && s == rank) return true;
       ++pairs;
       if (kForceCore)
         uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
@@ -108,7 +128,12 @@ struct MainQuery {
         resolve_pair(i, j, core_i, flags, parent, hint, settled);
       return true;
     };
-    return bvh_step<D>(nodes, p, bt, rank, node, top, stack, visit);
+    if (kUp)
+      return bvh_up_step<D>(nodes, node_parent, node_delta, p, bt, stop_delta, us, stack, visit);
+    // top-down masked traversal (the reference's order)
+    if (us.P < 0) return false;
+    if (!bvh_step<D>(nodes, p, bt, rank, us.node, us.top, stack, visit)) us.P = -1;
+    return us.P >= 0;
   }
   __device__ void end() {}
 };
@@ -126,13 +151,16 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
   flush_counter(&ctr->dists, q.dists);
 }
 
-template <int D, bool kForceCore>
+template <int D, bool kForceCore, bool kUp>
 __global__ void __launch_bounds__(kQueryBlock)
-k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-          DevCounters* ctr, bool persistent) {
+k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt,
+          const int32_t* __restrict__ node_parent, const int32_t* __restrict__ node_delta,
+          const int32_t* __restrict__ leaf_parent, const uint32_t* __restrict__ scene_ord,
+          int64_t m, BallTest bt, double eps, const uint8_t* __restrict__ flags,
+          int32_t* __restrict__ parent, DevCounters* ctr, bool persistent) {
   int32_t stack[kStackDepth];
-  MainQuery<D, kForceCore> q{nodes, leaf_pt, bt, flags, parent, stack};
+  MainQuery<D, kForceCore, kUp> q{nodes,    leaf_pt, node_parent, node_delta, leaf_parent, scene_ord,
+                             bt,       eps,     flags,       parent,     stack};
   if (persistent)
     run_query_queue(m, &ctr->queue[1], q);
   else
@@ -208,12 +236,17 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s) {
   const BallTest bt = BallTest::make(eps2);
+  const double eps = std::sqrt(eps2);  // exact: eps2 is the square of an fp32 value
+  auto launch = [&](auto kernel) {
+    note_launch(), kernel<<<query_grid(kernel, n), kQueryBlock, 0, s>>>(
+        b.tree.nodes, b.leaf_pt, b.node_parent, b.node_delta, b.leaf_parent, b.scene_ord, n, bt,
+        eps, flags, parent, d_ctr, query_mode() == 1);
+  };
+  const bool up = main_traversal_up();
   if (force_core)
-    note_launch(), k_fd_main<D, true><<<query_grid(k_fd_main<D, true>, n), kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
-                                                                flags, parent, d_ctr, query_mode() == 1);
+    up ? launch(k_fd_main<D, true, true>) : launch(k_fd_main<D, true, false>);
   else
-    note_launch(), k_fd_main<D, false><<<query_grid(k_fd_main<D, false>, n), kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt,
-                                                                 flags, parent, d_ctr, query_mode() == 1);
+    up ? launch(k_fd_main<D, false, true>) : launch(k_fd_main<D, false, false>);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -76,14 +76,21 @@ __device__ __forceinline__ uint64_t spread3(uint64_t x) {
 
 // morton_quantize (geometry.hpp:132-141). `w` = double(hi) - double(lo) is
 // precomputed per axis; `cells` = 2^bits.
-__device__ __forceinline__ uint64_t quantize(float v, float lo, double w,
-                                             double cells_d, uint64_t cells) {
+// Monotone non-decreasing in v (every step is a correctly rounded, monotone
+// operation), which the Morton-cell early termination relies on.
+__device__ __forceinline__ uint64_t quantize_d(double v, float lo, double w, double cells_d,
+                                               uint64_t cells) {
   if (w <= 0.0) return 0;
-  double t = __ddiv_rn(__dsub_rn(static_cast<double>(v), static_cast<double>(lo)), w);
+  double t = __ddiv_rn(__dsub_rn(v, static_cast<double>(lo)), w);
   if (t < 0.0) t = 0.0;
   uint64_t q = __double2ull_rz(__dmul_rn(t, cells_d));
   if (q >= cells) q = cells - 1;
   return q;
+}
+
+__device__ __forceinline__ uint64_t quantize(float v, float lo, double w, double cells_d,
+                                             uint64_t cells) {
+  return quantize_d(static_cast<double>(v), lo, w, cells_d, cells);
 }
 
 // ---------------------------------------------------------------------------

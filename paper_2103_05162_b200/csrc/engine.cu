@@ -6,6 +6,7 @@
 #include <cstring>
 #include <limits>
 #include <mutex>
+#include <string>
 
 #include "device_common.cuh"
 #include "engine.hpp"
@@ -114,6 +115,14 @@ int query_mode() {
     return v ? std::atoi(v) : 0;
   }();
   return mode;
+}
+
+bool main_traversal_up() {
+  static const bool up = [] {
+    const char* v = std::getenv("TCB_MAIN_TRAVERSAL");
+    return v ? std::string(v) != "down" : true;
+  }();
+  return up;
 }
 
 void set_last_stage_ms(const double* ms) {

@@ -84,7 +84,12 @@ struct PrimSource {
 
 struct BuiltBvh {
   DeviceBvh tree;
-  float4* leaf_pt = nullptr;  // points mode only: rank -> (x, y, z, id bits)
+  float4* leaf_pt = nullptr;          // points mode only: rank -> (x, y, z, id bits)
+  const uint64_t* codes = nullptr;    // sorted Morton codes (leaf rank order)
+  int32_t* node_parent = nullptr;     // internal node -> parent (-1 at the root)
+  int32_t* node_delta = nullptr;      // internal node -> common prefix length of its range
+  int32_t* leaf_parent = nullptr;     // leaf rank -> parent node
+  const uint32_t* scene_ord = nullptr;  // Morton scene box (order-preserving bits, 6)
   int sort_passes = 0;
 };
 
@@ -168,6 +173,9 @@ inline unsigned persistent_grid(Kernel kernel, int block) {
 }
 
 int query_mode();
+// Main-pass traversal: bottom-up with Morton-cell termination (default) or the
+// reference's top-down DFS (TCB_MAIN_TRAVERSAL=down).
+bool main_traversal_up();
 
 inline unsigned grid_for(int64_t work, int block, int64_t max_blocks = 148 * 64);
 
