@@ -145,8 +145,8 @@ template <int D, class Src>
 __global__ void __launch_bounds__(256)
 k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
          const int32_t* __restrict__ prim_aux, int64_t m, float4* __restrict__ nodes,
-         int32_t* __restrict__ node_parent, int32_t* __restrict__ node_delta,
-         int32_t* __restrict__ leaf_parent, float4* __restrict__ leaf_pt) {
+         int4* __restrict__ node_info, int32_t* __restrict__ leaf_up,
+         float4* __restrict__ leaf_pt) {
   using T = NodeTraits<D>;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= m - 1) return;
@@ -183,25 +183,31 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
     }
   };
   int32_t left, right, aux_l, aux_r;
-  node_delta[i] = delta_node;  // prefix length shared by the whole range
+  // Own info (delta = prefix length shared by the whole range, the range);
+  // the parent link of each child is written here, by its parent.
+  node_info[i].y = delta_node;
+  node_info[i].z = static_cast<int32_t>(lo);
+  node_info[i].w = static_cast<int32_t>(hi);
+  const int32_t up_left = static_cast<int32_t>(i) | kUpLeftBit;
+  const int32_t up_right = static_cast<int32_t>(i);
   if (lo == gamma) {
     leaf_child(gamma, 0, left, aux_l);
-    leaf_parent[gamma] = static_cast<int32_t>(i);
+    leaf_up[gamma] = up_left;
   } else {
     left = static_cast<int32_t>(gamma);
     aux_l = static_cast<int32_t>(gamma);  // max leaf rank of [lo, gamma]
-    node_parent[gamma] = static_cast<int32_t>(i);
+    node_info[gamma].x = up_left;
   }
   if (hi == gamma + 1) {
     leaf_child(gamma + 1, 1, right, aux_r);
-    leaf_parent[gamma + 1] = static_cast<int32_t>(i);
+    leaf_up[gamma + 1] = up_right;
   } else {
     right = static_cast<int32_t>(gamma + 1);
     aux_r = static_cast<int32_t>(hi);  // max leaf rank of [gamma+1, hi]
-    node_parent[gamma + 1] = static_cast<int32_t>(i);
+    node_info[gamma + 1].x = up_right;
   }
   *reinterpret_cast<int4*>(f + T::kIntOff) = make_int4(left, right, aux_l, aux_r);
-  if (i == 0) node_parent[0] = -1;
+  if (i == 0) node_info[0].x = kNoParent;
   if (leaf_pt) {  // Morton-ordered query points (x, y, z, id)
     auto emit = [&](int64_t rank) {
       const int32_t prim = order[rank];
@@ -222,7 +228,7 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
 // second one continues. Slots written by another SM are read through L2.
 template <int D>
 __global__ void __launch_bounds__(256)
-k_refit(int64_t m, float4* nodes, const int32_t* __restrict__ node_parent,
+k_refit(int64_t m, float4* nodes, const int4* __restrict__ node_info,
         int32_t* __restrict__ arrivals) {
   using T = NodeTraits<D>;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -241,7 +247,7 @@ k_refit(int64_t m, float4* nodes, const int32_t* __restrict__ node_parent,
       lo[k] = fminf(__ldcg(cf + k), __ldcg(cf + 2 * D + k));
       hi[k] = fmaxf(__ldcg(cf + D + k), __ldcg(cf + 3 * D + k));
     }
-    const int32_t p = node_parent[c];
+    const int32_t p = up_parent(node_info[c].x);
     float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
     const int2 pl = *reinterpret_cast<const int2*>(pf + T::kIntOff);
     const bool is_left = pl.x == c;
@@ -261,14 +267,32 @@ k_refit(int64_t m, float4* nodes, const int32_t* __restrict__ node_parent,
   }
 }
 
+// Per leaf: the highest ancestor whose leaf range holds <= k leaves (its
+// "bucket"; ~rank when even the parent is larger). Buckets partition the
+// Morton order into runs that the main pass scans linearly instead of
+// descending into.
+__global__ void __launch_bounds__(256)
+k_buckets(const int4* __restrict__ node_info, const int32_t* __restrict__ leaf_up, int64_t m,
+          int k, int32_t* __restrict__ bucket) {
+  int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= m) return;
+  int32_t c = ~static_cast<int32_t>(r);
+  int32_t P = up_parent(leaf_up[r]);
+  while (P != kNoParent) {
+    const int4 info = node_info[P];
+    if (info.w - info.z + 1 > k) break;
+    c = P;
+    P = up_parent(info.x);
+  }
+  bucket[r] = c;
+}
+
 // 1-leaf tree: pseudo root with the leaf on the left and an empty box right.
 template <int D, class Src>
 __global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, float4* nodes,
-                              float4* leaf_pt, int32_t* node_parent, int32_t* node_delta,
-                              int32_t* leaf_parent) {
-  node_parent[0] = -1;
-  node_delta[0] = 0;
-  leaf_parent[0] = 0;
+                              float4* leaf_pt, int4* node_info, int32_t* leaf_up) {
+  node_info[0] = make_int4(kNoParent, 0, 0, 0);
+  leaf_up[0] = kUpLeftBit;
   using T = NodeTraits<D>;
   float lo[3], hi[3];
   src.box(0, lo, hi);
@@ -288,7 +312,7 @@ __global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, flo
 template <int D, class Src>
 BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finite,
                     bool points_mode, DevCounters* d_ctr, Scratch& scratch,
-                    StageClock* clock) {
+                    StageClock* clock, int bucket_k) {
   cudaStream_t st = scratch.stream();
   const int64_t m = src.count;
   BuiltBvh out;
@@ -332,26 +356,28 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   if (clock) clock->mark(kStTopo);
   float4* leaf_pt = out.leaf_pt;
   out.codes = codes;
-  out.node_parent = scratch.alloc_n<int32_t>(std::max<int64_t>(1, m - 1));
-  out.node_delta = scratch.alloc_n<int32_t>(std::max<int64_t>(1, m - 1));
-  out.leaf_parent = scratch.alloc_n<int32_t>(m);
+  out.node_info = scratch.alloc_n<int4>(std::max<int64_t>(1, m - 1));
+  out.leaf_up = scratch.alloc_n<int32_t>(m);
   uint32_t* scene = scratch.alloc_n<uint32_t>(8);
   TCB_CUDA(cudaMemcpyAsync(scene, &d_ctr->bounds_ord[0], 6 * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, st));
   out.scene_ord = scene;
   if (m == 1) {
     note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt,
-                                                     out.node_parent, out.node_delta,
-                                                     out.leaf_parent);
+                                                     out.node_info, out.leaf_up);
   } else {
-    int32_t* node_parent = out.node_parent;
     int32_t* arrivals = scratch.alloc_n<int32_t>(m - 1);
     TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * (m - 1), st));
     const unsigned gn = grid_for(m - 1, 256, INT32_MAX);
     note_launch(), k_karras<D><<<gn, 256, 0, st>>>(boxes, codes, order, src.aux, m,
-                                                   out.tree.nodes, node_parent, out.node_delta,
-                                                   out.leaf_parent, leaf_pt);
-    note_launch(), k_refit<D><<<gn, 256, 0, st>>>(m, out.tree.nodes, node_parent, arrivals);
+                                                   out.tree.nodes, out.node_info, out.leaf_up,
+                                                   leaf_pt);
+    note_launch(), k_refit<D><<<gn, 256, 0, st>>>(m, out.tree.nodes, out.node_info, arrivals);
+  }
+  if (bucket_k > 0) {
+    out.bucket = scratch.alloc_n<int32_t>(m);
+    note_launch(), k_buckets<<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
+        out.node_info, out.leaf_up, m, bucket_k, out.bucket);
   }
   TCB_CUDA(cudaGetLastError());
   return out;
@@ -395,16 +421,16 @@ template void launch_point_bounds<3>(const float*, int64_t, DevCounters*, cudaSt
 
 template <int D>
 BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
-                   Scratch& scratch, StageClock* clock) {
+                   Scratch& scratch, StageClock* clock, int bucket_k) {
   if (src.coords) {
     PointBoxes<D> b{src.coords};
-    return build_impl<D>(b, src, validate_finite, true, d_ctr, scratch, clock);
+    return build_impl<D>(b, src, validate_finite, true, d_ctr, scratch, clock, bucket_k);
   }
   ExplicitBoxes<D> b{src.lo, src.hi};
-  return build_impl<D>(b, src, validate_finite, false, d_ctr, scratch, clock);
+  return build_impl<D>(b, src, validate_finite, false, d_ctr, scratch, clock, bucket_k);
 }
 
-template BuiltBvh build_bvh<2>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*);
-template BuiltBvh build_bvh<3>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*);
+template BuiltBvh build_bvh<2>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*, int);
+template BuiltBvh build_bvh<3>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*, int);
 
 }  // namespace tcb

@@ -33,6 +33,13 @@ struct NodeTraits {
 
 constexpr int kStackDepth = 128;  // bvh.hpp:82-84 (keys are 64 + 32 bits)
 
+// Parent links: parent node index, bit 31 set when the child is the parent's
+// LEFT child; kNoParent at the root.
+constexpr int32_t kUpLeftBit = static_cast<int32_t>(0x80000000u);
+constexpr int32_t kNoParent = 0x7fffffff;
+__host__ __device__ __forceinline__ int32_t up_parent(int32_t x) { return x & 0x7fffffff; }
+__host__ __device__ __forceinline__ bool up_is_left(int32_t x) { return x < 0; }
+
 // The ball-vs-box predicate of the traversal: exactly box_distance_sq <= r2
 // in fp64 (geometry.hpp:82-93), answered by an fp32 estimate whenever the
 // estimate is outside a relative guard band of 2^-17 around r2. The fp32 sum
@@ -148,7 +155,7 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
 //
 // It stops climbing at the first ancestor A whose Morton cell contains the
 // ball: a Karras node is a binary radix-tree node, so its subtree holds
-// exactly the primitives whose codes share its prefix (node_delta bits), i.e.
+// exactly the primitives whose codes share its prefix (node_info delta), i.e.
 // whose centroid quantizes into A's cell. A primitive outside A therefore has
 // its centroid outside the cell, hence farther than `reach` from p when the
 // reach-ball lies inside the cell (reach = eps + the largest primitive
@@ -156,6 +163,8 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
 // quantized space with the same monotone quantize() as the codes, on a ball
 // widened by relative margins, so it is conservative under rounding.
 //
+// Below `bucket` size the subtree is not descended at all: its leaves are a
+// contiguous run of the Morton-ordered leaf array and are scanned linearly.
 // The visit order differs from the reference's DFS; the main pass has no
 // early exit, so its pair set and counters are order independent.
 // ---------------------------------------------------------------------------
@@ -195,59 +204,6 @@ __device__ __forceinline__ int morton_stop_delta(const float* p, double reach,
   else
     dmax = min(min(2 * agree[1], 2 * agree[0] + 1), 62);
   return dmax + (64 - D * B);
-}
-
-struct UpState {
-  int32_t c;     // link of the child we climbed from (~rank for a leaf)
-  int32_t P;     // current ancestor (-1: climb finished)
-  int32_t node;  // exploration cursor inside a right sibling
-  int top;
-  bool exploring;
-};
-
-template <int D, typename Visit>
-__device__ __forceinline__ bool bvh_up_step(const float4* __restrict__ nodes,
-                                            const int32_t* __restrict__ node_parent,
-                                            const int32_t* __restrict__ node_delta,
-                                            const float* p, const BallTest& bt, int stop_delta,
-                                            UpState& s, int32_t* stack, Visit& visit) {
-  using T = NodeTraits<D>;
-  if (s.exploring) {
-    if (!bvh_step<D>(nodes, p, bt, 0, s.node, s.top, stack, visit)) s.exploring = false;
-    return true;
-  }
-  if (s.P < 0) return false;
-  const float4* src = nodes + static_cast<int64_t>(s.P) * T::kVec;
-  const int32_t dP = __ldg(node_delta + s.P);
-  const int32_t pP = __ldg(node_parent + s.P);
-  float f[T::kFloats];
-#pragma unroll
-  for (int v = 0; v < T::kVec; ++v) {
-    float4 q = __ldg(src + v);
-    f[4 * v + 0] = q.x;
-    f[4 * v + 1] = q.y;
-    f[4 * v + 2] = q.z;
-    f[4 * v + 3] = q.w;
-  }
-  const int32_t left = __float_as_int(f[T::kIntOff + 0]);
-  const int32_t right = __float_as_int(f[T::kIntOff + 1]);
-  const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
-  if (left == s.c && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
-    if (right < 0) {
-      visit(~right, aux_r, f + 2 * D, f + 3 * D);
-    } else {
-      s.exploring = true;
-      s.node = right;
-      s.top = 0;
-    }
-  }
-  if (dP <= stop_delta) {
-    s.P = -1;
-  } else {
-    s.c = s.P;
-    s.P = pP;
-  }
-  return true;
 }
 
 // ---------------------------------------------------------------------------

@@ -75,65 +75,147 @@ struct CoreQuery {
 };
 
 // fdbscan_main_phase query (dbscan.cpp:60-88): every leaf of rank > r
-// within eps, i.e. each unordered pair exactly once, found by the bottom-up
-// masked traversal (bvh_up_step) from the query's own leaf; each pair is
-// resolved on the spot, no neighbour list is stored.
-template <int D, bool kForceCore, bool kUp>
+// within eps — each unordered pair exactly once — resolved on the spot (no
+// neighbour list is stored). Bottom-up (see bvh.cuh): scan the rest of the
+// query's own bucket, then climb; at each ancestor reached from its left side
+// explore the right sibling (all of its ranks are > r), descending only into
+// subtrees of more than kBucket leaves and scanning smaller ones linearly;
+// stop at the first ancestor whose Morton cell holds the eps-ball.
+constexpr int kBucket = kMainBucket;
+
+template <int D, bool kForceCore>
 struct MainQuery {
   const float4* __restrict__ nodes;
   const float4* __restrict__ leaf_pt;
-  const int32_t* __restrict__ node_parent;
-  const int32_t* __restrict__ node_delta;
-  const int32_t* __restrict__ leaf_parent;
+  const int4* __restrict__ node_info;
+  const int32_t* __restrict__ leaf_up;
+  const int32_t* __restrict__ bucket;
   const uint32_t* __restrict__ scene_ord;
   BallTest bt;
   double eps;
   const uint8_t* __restrict__ flags;
   int32_t* __restrict__ parent;
-  int32_t* stack;  // per-thread traversal stack, kept outside the struct
+  int2* stack;  // {node, other end of its leaf range}; kept outside the struct
   unsigned long long pairs = 0;
   float p[3];
-  int32_t i, hint;
-  int stop_delta;
-  int32_t rank;
-  bool core_i, settled;
-  UpState us;
+  int32_t i, hint, P, scan_k, scan_end;
+  int stop_delta, top;
+  bool came_left, core_i, settled;
 
+  __device__ void pair(int32_t j) {
+    ++pairs;
+    if (kForceCore)
+      uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
+    else
+      resolve_pair(i, j, core_i, flags, parent, hint, settled);
+  }
+  __device__ void climb_from(int32_t up) {
+    came_left = up_is_left(up);
+    P = up_parent(up);
+  }
   __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &i);
-    rank = static_cast<int32_t>(r);
-    if (kUp) {
-      float anchor[3];
+    float anchor[3];
 #pragma unroll
-      for (int k = 0; k < D; ++k) anchor[k] = __fmul_rn(0.5f, __fadd_rn(p[k], p[k]));
-      stop_delta = morton_stop_delta<D>(p, eps, anchor, scene_ord);
-    }
+    for (int k = 0; k < D; ++k) anchor[k] = __fmul_rn(0.5f, __fadd_rn(p[k], p[k]));
+    stop_delta = morton_stop_delta<D>(p, eps, anchor, scene_ord);
     core_i = kForceCore ? true : flags[i] != 0;
     hint = i;
     settled = false;
-    us.c = ~static_cast<int32_t>(r);
-    us.P = kUp ? __ldg(leaf_parent + r) : 0;
-    us.node = 0;
-    us.top = 0;
-    us.exploring = false;
+    top = 0;
+    const int32_t b = __ldg(bucket + r);
+    if (b < 0) {  // the leaf is its own bucket
+      scan_k = 1;
+      scan_end = 0;
+      climb_from(__ldg(leaf_up + r));
+    } else {
+      const int4 info = __ldg(node_info + b);
+      scan_k = static_cast<int32_t>(r) + 1;  // ranks > r of the own bucket
+      scan_end = info.w;
+      if (info.y <= stop_delta)
+        P = kNoParent;
+      else
+        climb_from(info.x);
+    }
     return true;
   }
-  __device__ bool step() {
-    auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
-      if (!kUp && s == rank) return true;
-      ++pairs;
-      if (kForceCore)
-        uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
+  // Node X (leaf range [lo, hi], more than kBucket leaves) meets the ball:
+  // test both children; leaves pair directly, subtrees go on the stack.
+  __device__ void expand(int32_t X, int32_t lo, int32_t hi) {
+    using T = NodeTraits<D>;
+    float f[T::kFloats];
+    const float4* src = nodes + static_cast<int64_t>(X) * T::kVec;
+#pragma unroll
+    for (int v = 0; v < T::kVec; ++v) {
+      const float4 q = __ldg(src + v);
+      f[4 * v + 0] = q.x;
+      f[4 * v + 1] = q.y;
+      f[4 * v + 2] = q.z;
+      f[4 * v + 3] = q.w;
+    }
+    const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+    const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+    if (ball_hits<D>(p, f, f + D, bt)) {
+      if (left < 0)
+        pair(__float_as_int(f[T::kIntOff + 2]));
       else
-        resolve_pair(i, j, core_i, flags, parent, hint, settled);
+        stack[top++] = make_int2(left, lo);  // left child: range [lo, left]
+    }
+    if (ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
+      if (right < 0)
+        pair(__float_as_int(f[T::kIntOff + 3]));
+      else
+        stack[top++] = make_int2(right, hi);  // right child: range [right, hi]
+    }
+  }
+  __device__ bool step() {
+    if (scan_k <= scan_end) {  // linear scan of a bucket-sized run
+#pragma unroll 1
+      for (int t = 0; t < 4 && scan_k <= scan_end; ++t, ++scan_k) {
+        const float4 q = __ldg(leaf_pt + scan_k);
+        const float qp[3] = {q.x, q.y, q.z};
+        if (ball_hits<D>(p, qp, qp, bt)) pair(__float_as_int(q.w));
+      }
       return true;
-    };
-    if (kUp)
-      return bvh_up_step<D>(nodes, node_parent, node_delta, p, bt, stop_delta, us, stack, visit);
-    // top-down masked traversal (the reference's order)
-    if (us.P < 0) return false;
-    if (!bvh_step<D>(nodes, p, bt, rank, us.node, us.top, stack, visit)) us.P = -1;
-    return us.P >= 0;
+    }
+    if (top > 0) {
+      const int2 e = stack[--top];
+      const int32_t lo = min(e.x, e.y), hi = max(e.x, e.y);
+      if (hi - lo + 1 <= kBucket) {
+        scan_k = lo;
+        scan_end = hi;
+      } else {
+        expand(e.x, lo, hi);
+      }
+      return true;
+    }
+    if (P == kNoParent) return false;
+    const int4 info = __ldg(node_info + P);
+    if (came_left) {  // the right sibling holds only ranks > r
+      using T = NodeTraits<D>;
+      const float4* src = nodes + static_cast<int64_t>(P) * T::kVec;
+      float f[T::kFloats];
+#pragma unroll
+      for (int v = 0; v < T::kVec; ++v) {
+        const float4 q = __ldg(src + v);
+        f[4 * v + 0] = q.x;
+        f[4 * v + 1] = q.y;
+        f[4 * v + 2] = q.z;
+        f[4 * v + 3] = q.w;
+      }
+      if (ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
+        const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+        if (right < 0)
+          pair(__float_as_int(f[T::kIntOff + 3]));
+        else
+          stack[top++] = make_int2(right, info.w);
+      }
+    }
+    if (info.y <= stop_delta)
+      P = kNoParent;
+    else
+      climb_from(info.x);
+    return true;
   }
   __device__ void end() {}
 };
@@ -151,16 +233,16 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
   flush_counter(&ctr->dists, q.dists);
 }
 
-template <int D, bool kForceCore, bool kUp>
+template <int D, bool kForceCore>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt,
-          const int32_t* __restrict__ node_parent, const int32_t* __restrict__ node_delta,
-          const int32_t* __restrict__ leaf_parent, const uint32_t* __restrict__ scene_ord,
-          int64_t m, BallTest bt, double eps, const uint8_t* __restrict__ flags,
+          const int4* __restrict__ node_info, const int32_t* __restrict__ leaf_up,
+          const int32_t* __restrict__ bucket, const uint32_t* __restrict__ scene_ord, int64_t m,
+          BallTest bt, double eps, const uint8_t* __restrict__ flags,
           int32_t* __restrict__ parent, DevCounters* ctr, bool persistent) {
-  int32_t stack[kStackDepth];
-  MainQuery<D, kForceCore, kUp> q{nodes,    leaf_pt, node_parent, node_delta, leaf_parent, scene_ord,
-                             bt,       eps,     flags,       parent,     stack};
+  int2 stack[kStackDepth];
+  MainQuery<D, kForceCore> q{nodes, leaf_pt, node_info, leaf_up, bucket, scene_ord,
+                             bt,    eps,     flags,     parent,  stack};
   if (persistent)
     run_query_queue(m, &ctr->queue[1], q);
   else
@@ -239,14 +321,13 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
   const double eps = std::sqrt(eps2);  // exact: eps2 is the square of an fp32 value
   auto launch = [&](auto kernel) {
     note_launch(), kernel<<<query_grid(kernel, n), kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, b.node_parent, b.node_delta, b.leaf_parent, b.scene_ord, n, bt,
-        eps, flags, parent, d_ctr, query_mode() == 1);
+        b.tree.nodes, b.leaf_pt, b.node_info, b.leaf_up, b.bucket, b.scene_ord, n, bt, eps, flags,
+        parent, d_ctr, query_mode() == 1);
   };
-  const bool up = main_traversal_up();
   if (force_core)
-    up ? launch(k_fd_main<D, true, true>) : launch(k_fd_main<D, true, false>);
+    launch(k_fd_main<D, true>);
   else
-    up ? launch(k_fd_main<D, false, true>) : launch(k_fd_main<D, false, false>);
+    launch(k_fd_main<D, false>);
   TCB_CUDA(cudaGetLastError());
 }
 

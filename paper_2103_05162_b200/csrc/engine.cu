@@ -149,7 +149,7 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   src.coords = d_coords;
   src.count = n;
   clock.mark(kStBounds);
-  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock);
+  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock, kMainBucket);
 
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);

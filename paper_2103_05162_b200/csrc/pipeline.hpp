@@ -86,9 +86,11 @@ struct BuiltBvh {
   DeviceBvh tree;
   float4* leaf_pt = nullptr;          // points mode only: rank -> (x, y, z, id bits)
   const uint64_t* codes = nullptr;    // sorted Morton codes (leaf rank order)
-  int32_t* node_parent = nullptr;     // internal node -> parent (-1 at the root)
-  int32_t* node_delta = nullptr;      // internal node -> common prefix length of its range
-  int32_t* leaf_parent = nullptr;     // leaf rank -> parent node
+  // internal node -> {parent | kUpLeftBit if it is its parent's left child
+  // (kNoParent at the root), common prefix length of its codes, lo, hi rank}
+  int4* node_info = nullptr;
+  int32_t* leaf_up = nullptr;         // leaf rank -> parent | kUpLeftBit
+  int32_t* bucket = nullptr;          // leaf rank -> its bucket (see k_buckets) or null
   const uint32_t* scene_ord = nullptr;  // Morton scene box (order-preserving bits, 6)
   int sort_passes = 0;
 };
@@ -96,15 +98,17 @@ struct BuiltBvh {
 // Builds the LBVH of bvh.cpp:10-124 (scene bounds over centroids, Morton,
 // stable (code, index) sort, Karras topology, refit). Checks the points for
 // non-finite coordinates when validate_finite (throws InvalidArgument).
+// bucket_k > 0 also computes the per-leaf buckets of <= bucket_k leaves.
 template <int D>
 BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
-                   Scratch& scratch, StageClock* clock);
+                   Scratch& scratch, StageClock* clock, int bucket_k = 0);
 
 // Raw point bounds into d_ctr->bounds_ord + finiteness flag (resets both).
 template <int D>
 void launch_point_bounds(const float* coords, int64_t n, DevCounters* d_ctr, cudaStream_t s);
 
 // ---- traversal / finalize (dbscan.cu) ----
+constexpr int kMainBucket = 16;  // leaves per linearly scanned run in the main pass
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s);
