@@ -169,43 +169,6 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
 // early exit, so its pair set and counters are order independent.
 // ---------------------------------------------------------------------------
 
-// Largest 64-bit common-prefix length at which an ancestor's Morton cell is
-// known to contain the ball (p, reach); anchor = a point of the query's own
-// leaf (its centroid), which lies in every ancestor's cell.
-template <int D>
-__device__ __forceinline__ int morton_stop_delta(const float* p, double reach,
-                                                 const float* anchor,
-                                                 const uint32_t* __restrict__ scene_ord) {
-  constexpr int B = D == 2 ? 31 : 21;
-  constexpr uint64_t cells = 1ull << B;
-  const double cells_d = static_cast<double>(cells);
-  const double e = reach * (1.0 + 0x1.0p-20);
-  int agree[3];
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const float lo = ord2f(__ldg(scene_ord + k));
-    const float hi = ord2f(__ldg(scene_ord + 3 + k));
-    const double w = __dsub_rn(static_cast<double>(hi), static_cast<double>(lo));
-    if (w <= 0.0) {
-      agree[k] = B;
-      continue;
-    }
-    const double pk = static_cast<double>(p[k]);
-    const double slack = (fabs(pk) + e) * 0x1.0p-50;
-    const uint64_t qa = quantize(anchor[k], lo, w, cells_d, cells);
-    const uint64_t ql = quantize_d(pk - e - slack, lo, w, cells_d, cells);
-    const uint64_t qh = quantize_d(pk + e + slack, lo, w, cells_d, cells);
-    const uint32_t x = static_cast<uint32_t>((ql ^ qa) | (qh ^ qa));
-    agree[k] = x == 0 ? B : __clz(static_cast<int>(x)) - (32 - B);
-  }
-  int dmax;  // meaningful prefix bits (MSB = highest bit of the last axis)
-  if (D == 3)
-    dmax = min(min(3 * agree[2], 3 * agree[1] + 1), min(3 * agree[0] + 2, 63));
-  else
-    dmax = min(min(2 * agree[1], 2 * agree[0] + 1), 62);
-  return dmax + (64 - D * B);
-}
-
 // ---------------------------------------------------------------------------
 // Persistent, warp-refilled query driver.
 //

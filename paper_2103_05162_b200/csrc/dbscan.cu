@@ -74,152 +74,6 @@ struct CoreQuery {
   }
 };
 
-// fdbscan_main_phase query (dbscan.cpp:60-88): every leaf of rank > r
-// within eps — each unordered pair exactly once — resolved on the spot (no
-// neighbour list is stored). Bottom-up (see bvh.cuh): scan the rest of the
-// query's own bucket, then climb; at each ancestor reached from its left side
-// explore the right sibling (all of its ranks are > r), descending only into
-// subtrees of more than kBucket leaves and scanning smaller ones linearly;
-// stop at the first ancestor whose Morton cell holds the eps-ball.
-constexpr int kBucket = kMainBucket;
-
-template <int D, bool kForceCore>
-struct MainQuery {
-  const float4* __restrict__ nodes;
-  const float4* __restrict__ leaf_pt;
-  const int4* __restrict__ node_info;
-  const int32_t* __restrict__ leaf_up;
-  const int32_t* __restrict__ bucket;
-  const uint32_t* __restrict__ scene_ord;
-  BallTest bt;
-  double eps;
-  const uint8_t* __restrict__ flags;
-  int32_t* __restrict__ parent;
-  int2* stack;  // {node, other end of its leaf range}; kept outside the struct
-  unsigned long long pairs = 0;
-  float p[3];
-  int32_t i, hint, P, scan_k, scan_end;
-  int stop_delta, top;
-  bool came_left, core_i, settled;
-
-  __device__ void pair(int32_t j) {
-    ++pairs;
-    if (kForceCore)
-      uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
-    else
-      resolve_pair(i, j, core_i, flags, parent, hint, settled);
-  }
-  __device__ void climb_from(int32_t up) {
-    came_left = up_is_left(up);
-    P = up_parent(up);
-  }
-  __device__ bool begin(int64_t r) {
-    load_query<D>(leaf_pt, r, p, &i);
-    float anchor[3];
-#pragma unroll
-    for (int k = 0; k < D; ++k) anchor[k] = __fmul_rn(0.5f, __fadd_rn(p[k], p[k]));
-    stop_delta = morton_stop_delta<D>(p, eps, anchor, scene_ord);
-    core_i = kForceCore ? true : flags[i] != 0;
-    hint = i;
-    settled = false;
-    top = 0;
-    const int32_t b = __ldg(bucket + r);
-    if (b < 0) {  // the leaf is its own bucket
-      scan_k = 1;
-      scan_end = 0;
-      climb_from(__ldg(leaf_up + r));
-    } else {
-      const int4 info = __ldg(node_info + b);
-      scan_k = static_cast<int32_t>(r) + 1;  // ranks > r of the own bucket
-      scan_end = info.w;
-      if (info.y <= stop_delta)
-        P = kNoParent;
-      else
-        climb_from(info.x);
-    }
-    return true;
-  }
-  // Node X (leaf range [lo, hi], more than kBucket leaves) meets the ball:
-  // test both children; leaves pair directly, subtrees go on the stack.
-  __device__ void expand(int32_t X, int32_t lo, int32_t hi) {
-    using T = NodeTraits<D>;
-    float f[T::kFloats];
-    const float4* src = nodes + static_cast<int64_t>(X) * T::kVec;
-#pragma unroll
-    for (int v = 0; v < T::kVec; ++v) {
-      const float4 q = __ldg(src + v);
-      f[4 * v + 0] = q.x;
-      f[4 * v + 1] = q.y;
-      f[4 * v + 2] = q.z;
-      f[4 * v + 3] = q.w;
-    }
-    const int32_t left = __float_as_int(f[T::kIntOff + 0]);
-    const int32_t right = __float_as_int(f[T::kIntOff + 1]);
-    if (ball_hits<D>(p, f, f + D, bt)) {
-      if (left < 0)
-        pair(__float_as_int(f[T::kIntOff + 2]));
-      else
-        stack[top++] = make_int2(left, lo);  // left child: range [lo, left]
-    }
-    if (ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
-      if (right < 0)
-        pair(__float_as_int(f[T::kIntOff + 3]));
-      else
-        stack[top++] = make_int2(right, hi);  // right child: range [right, hi]
-    }
-  }
-  __device__ bool step() {
-    if (scan_k <= scan_end) {  // linear scan of a bucket-sized run
-#pragma unroll 1
-      for (int t = 0; t < 4 && scan_k <= scan_end; ++t, ++scan_k) {
-        const float4 q = __ldg(leaf_pt + scan_k);
-        const float qp[3] = {q.x, q.y, q.z};
-        if (ball_hits<D>(p, qp, qp, bt)) pair(__float_as_int(q.w));
-      }
-      return true;
-    }
-    if (top > 0) {
-      const int2 e = stack[--top];
-      const int32_t lo = min(e.x, e.y), hi = max(e.x, e.y);
-      if (hi - lo + 1 <= kBucket) {
-        scan_k = lo;
-        scan_end = hi;
-      } else {
-        expand(e.x, lo, hi);
-      }
-      return true;
-    }
-    if (P == kNoParent) return false;
-    const int4 info = __ldg(node_info + P);
-    if (came_left) {  // the right sibling holds only ranks > r
-      using T = NodeTraits<D>;
-      const float4* src = nodes + static_cast<int64_t>(P) * T::kVec;
-      float f[T::kFloats];
-#pragma unroll
-      for (int v = 0; v < T::kVec; ++v) {
-        const float4 q = __ldg(src + v);
-        f[4 * v + 0] = q.x;
-        f[4 * v + 1] = q.y;
-        f[4 * v + 2] = q.z;
-        f[4 * v + 3] = q.w;
-      }
-      if (ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
-        const int32_t right = __float_as_int(f[T::kIntOff + 1]);
-        if (right < 0)
-          pair(__float_as_int(f[T::kIntOff + 3]));
-        else
-          stack[top++] = make_int2(right, info.w);
-      }
-    }
-    if (info.y <= stop_delta)
-      P = kNoParent;
-    else
-      climb_from(info.x);
-    return true;
-  }
-  __device__ void end() {}
-};
-
 template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
@@ -233,22 +87,38 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
   flush_counter(&ctr->dists, q.dists);
 }
 
+// fdbscan_main_phase (dbscan.cpp:60-88): one thread per leaf rank r (Morton
+// order, so a warp's queries are spatial neighbours walking nearly the same
+// nodes), top-down query masked at r so each unordered within-eps pair is met
+// exactly once, and resolved on the spot — no neighbour list is stored.
 template <int D, bool kForceCore>
 __global__ void __launch_bounds__(kQueryBlock)
-k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt,
-          const int4* __restrict__ node_info, const int32_t* __restrict__ leaf_up,
-          const int32_t* __restrict__ bucket, const uint32_t* __restrict__ scene_ord, int64_t m,
-          BallTest bt, double eps, const uint8_t* __restrict__ flags,
-          int32_t* __restrict__ parent, DevCounters* ctr, bool persistent) {
-  int2 stack[kStackDepth];
-  MainQuery<D, kForceCore> q{nodes, leaf_pt, node_info, leaf_up, bucket, scene_ord,
-                             bt,    eps,     flags,     parent,  stack};
-  if (persistent)
-    run_query_queue(m, &ctr->queue[1], q);
-  else
-    run_query_direct(m, q);
-  flush_counter(&ctr->pairs, q.pairs);
-  flush_counter(&ctr->dists, q.pairs);
+k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+          DevCounters* ctr) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long pairs = 0;
+  if (r < m) {
+    float p[3];
+    int32_t i;
+    load_query<D>(leaf_pt, r, p, &i);
+    const int32_t rank = static_cast<int32_t>(r);
+    const bool core_i = kForceCore ? true : flags[i] != 0;
+    int32_t hint = i;
+    bool settled = false;
+    auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
+      if (s == rank) return true;
+      ++pairs;
+      if (kForceCore)
+        uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
+      else
+        resolve_pair(i, j, core_i, flags, parent, hint, settled);
+      return true;
+    };
+    bvh_query<D>(nodes, p, bt, rank, visit);
+  }
+  flush_counter(&ctr->pairs, pairs);
+  flush_counter(&ctr->dists, pairs);
 }
 
 __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
@@ -318,11 +188,9 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s) {
   const BallTest bt = BallTest::make(eps2);
-  const double eps = std::sqrt(eps2);  // exact: eps2 is the square of an fp32 value
   auto launch = [&](auto kernel) {
-    note_launch(), kernel<<<query_grid(kernel, n), kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, b.node_info, b.leaf_up, b.bucket, b.scene_ord, n, bt, eps, flags,
-        parent, d_ctr, query_mode() == 1);
+    note_launch(), kernel<<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
+        b.tree.nodes, b.leaf_pt, n, bt, flags, parent, d_ctr);
   };
   if (force_core)
     launch(k_fd_main<D, true>);

@@ -108,7 +108,7 @@ template <int D>
 void launch_point_bounds(const float* coords, int64_t n, DevCounters* d_ctr, cudaStream_t s);
 
 // ---- traversal / finalize (dbscan.cu) ----
-constexpr int kMainBucket = 16;  // leaves per linearly scanned run in the main pass
+constexpr int kMainBucket = 32;  // leaves per bucket (a warp's worth) in the main pass
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s);
@@ -116,6 +116,13 @@ template <int D>
 void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s);
+// Warp-per-bucket main pass (main_warp.cu); needs the build's buckets.
+template <int D>
+void fdbscan_main_pass_warp(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
+                            uint8_t* flags, int32_t* parent, DevCounters* d_ctr, Scratch& scratch);
+// Main-pass variant: 0 = thread per point, top-down (default), 1 = warp per
+// bucket (experimental, TCB_MAIN_KERNEL=warp).
+int main_kernel_variant();
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
 // force_core (minpts == 2): core flags are derived here from the union-find
 // structure instead of being stored per pair in the main pass.
@@ -177,9 +184,6 @@ inline unsigned persistent_grid(Kernel kernel, int block) {
 }
 
 int query_mode();
-// Main-pass traversal: bottom-up with Morton-cell termination (default) or the
-// reference's top-down DFS (TCB_MAIN_TRAVERSAL=down).
-bool main_traversal_up();
 
 inline unsigned grid_for(int64_t work, int block, int64_t max_blocks = 148 * 64);
 
