@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(256)
 k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
          const int32_t* __restrict__ prim_aux, int64_t m, float4* __restrict__ nodes,
          int4* __restrict__ node_info, int32_t* __restrict__ leaf_up,
-         float4* __restrict__ leaf_pt) {
+         float4* __restrict__ leaf_pt, int32_t* __restrict__ starts,
+         int32_t* __restrict__ num_starts) {
   using T = NodeTraits<D>;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= m - 1) return;
@@ -208,6 +209,16 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
   }
   *reinterpret_cast<int4*>(f + T::kIntOff) = make_int4(left, right, aux_l, aux_r);
   if (i == 0) node_info[0].x = kNoParent;
+  // refit climbers start at the nodes with two leaf children
+  const bool start = left < 0 && right < 0;
+  const uint32_t mask = __ballot_sync(__activemask(), start);
+  if (mask) {
+    const int leader = __ffs(mask) - 1;
+    int32_t base = 0;
+    if ((threadIdx.x & 31) == leader) base = atomicAdd(num_starts, __popc(mask));
+    base = __shfl_sync(__activemask(), base, leader);
+    if (start) starts[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = static_cast<int32_t>(i);
+  }
   if (leaf_pt) {  // Morton-ordered query points (x, y, z, id)
     auto emit = [&](int64_t rank) {
       const int32_t prim = order[rank];
@@ -221,49 +232,62 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
 }
 
 // Bottom-up refit (bvh.cpp:88-124). Climbers start at the nodes whose two
-// children are leaves (their slots are already filled). A finished node
-// writes its box (union of its two slots) into its slot of the parent; if the
-// sibling is a leaf the climber continues at once, otherwise the two climbers
-// meet with an arrival counter (the only place a fence is needed) and the
-// second one continues. Slots written by another SM are read through L2.
+// children are leaves (their slots were filled by k_karras, which also listed
+// them). A finished node writes its box (union of its two slots) into its slot
+// of the parent; if the sibling is a leaf the climber continues at once,
+// otherwise the two climbers meet at an arrival counter and the second one
+// continues. Only that meeting needs ordering: the writer's slot store must be
+// visible before its arrival (release fence, issued once per warp step for all
+// lanes that need it); the second arriver reads the sibling slot through L2
+// (ld.cg), after the atomic that observed the sibling's arrival.
 template <int D>
 __global__ void __launch_bounds__(256)
-k_refit(int64_t m, float4* nodes, const int4* __restrict__ node_info,
-        int32_t* __restrict__ arrivals) {
+k_refit(const int32_t* __restrict__ starts, const int32_t* __restrict__ num_starts,
+        float4* nodes, const int4* __restrict__ node_info, int32_t* __restrict__ arrivals) {
   using T = NodeTraits<D>;
-  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= m - 1) return;
-  {
-    const int4 links = *reinterpret_cast<const int4*>(
-        reinterpret_cast<const float*>(nodes + i * T::kVec) + T::kIntOff);
-    if (links.x >= 0 || links.y >= 0) return;
-  }
-  int32_t c = static_cast<int32_t>(i);
-  while (c != 0) {  // the root's own box is never tested (bvh.hpp:55-58)
-    const float* cf = reinterpret_cast<const float*>(nodes + static_cast<int64_t>(c) * T::kVec);
-    float lo[3], hi[3];
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int32_t count = *num_starts;
+  if (blockIdx.x * static_cast<int64_t>(blockDim.x) >= count) return;  // whole block idle
+  bool active = t < count;
+  int32_t c = active ? starts[t] : 0;
+  while (__any_sync(0xffffffffu, active)) {
+    bool fence = false;
+    int32_t p = 0;
+    if (active) {
+      if (c == 0) {  // the root's own box is never tested (bvh.hpp:55-58)
+        active = false;
+      } else {
+        const float* cf = reinterpret_cast<const float*>(nodes + static_cast<int64_t>(c) * T::kVec);
+        float lo[3], hi[3];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      lo[k] = fminf(__ldcg(cf + k), __ldcg(cf + 2 * D + k));
-      hi[k] = fmaxf(__ldcg(cf + D + k), __ldcg(cf + 3 * D + k));
-    }
-    const int32_t p = up_parent(node_info[c].x);
-    float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
-    const int2 pl = *reinterpret_cast<const int2*>(pf + T::kIntOff);
-    const bool is_left = pl.x == c;
-    float* slot = pf + (is_left ? 0 : 2 * D);
+        for (int k = 0; k < D; ++k) {
+          lo[k] = fminf(__ldcg(cf + k), __ldcg(cf + 2 * D + k));
+          hi[k] = fmaxf(__ldcg(cf + D + k), __ldcg(cf + 3 * D + k));
+        }
+        p = up_parent(node_info[c].x);
+        float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
+        const int2 pl = *reinterpret_cast<const int2*>(pf + T::kIntOff);
+        const bool is_left = pl.x == c;
+        float* slot = pf + (is_left ? 0 : 2 * D);
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      slot[k] = lo[k];
-      slot[D + k] = hi[k];
+        for (int k = 0; k < D; ++k) {
+          __stcg(slot + k, lo[k]);
+          __stcg(slot + D + k, hi[k]);
+        }
+        const int32_t sibling = is_left ? pl.y : pl.x;
+        if (sibling >= 0)
+          fence = true;  // meet the sibling's climber
+        else
+          c = p;  // sibling is a leaf: its slot is already in place
+      }
     }
-    const int32_t sibling = is_left ? pl.y : pl.x;
-    if (sibling >= 0) {
-      __threadfence();
-      if (atomicAdd(arrivals + p, 1) == 0) return;
-      __threadfence();
+    if (__any_sync(0xffffffffu, fence)) __threadfence();
+    if (fence) {
+      if (atomicAdd(arrivals + p, 1) == 0)
+        active = false;
+      else
+        c = p;
     }
-    c = p;
   }
 }
 
@@ -366,13 +390,15 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt,
                                                      out.node_info, out.leaf_up);
   } else {
-    int32_t* arrivals = scratch.alloc_n<int32_t>(m - 1);
-    TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * (m - 1), st));
+    int32_t* arrivals = scratch.alloc_n<int32_t>(m);  // [m-1] = start count
+    int32_t* starts = scratch.alloc_n<int32_t>(m / 2 + 1);
+    TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * m, st));
     const unsigned gn = grid_for(m - 1, 256, INT32_MAX);
     note_launch(), k_karras<D><<<gn, 256, 0, st>>>(boxes, codes, order, src.aux, m,
                                                    out.tree.nodes, out.node_info, out.leaf_up,
-                                                   leaf_pt);
-    note_launch(), k_refit<D><<<gn, 256, 0, st>>>(m, out.tree.nodes, out.node_info, arrivals);
+                                                   leaf_pt, starts, arrivals + (m - 1));
+    note_launch(), k_refit<D><<<grid_for(m / 2 + 1, 256, INT32_MAX), 256, 0, st>>>(
+        starts, arrivals + (m - 1), out.tree.nodes, out.node_info, arrivals);
   }
   if (bucket_k > 0) {
     out.bucket = scratch.alloc_n<int32_t>(m);
