@@ -181,6 +181,64 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+def run_sharded(args, rank, world, dev, n):
+    """N>1: one global HACC-like cloud of world*n points (rank r generates the
+    slab x in [r*L, (r+1)*L) with its own seed, same density as C2), clustered
+    by the Morton-range sharded path (shard.py): redistribution, eps halo,
+    local passes, cross-shard merge. Weak scaling: n points per GPU."""
+    import torch
+    import torch.distributed as dist
+    import paper_2103_05162_b200 as tb
+    from paper_2103_05162_b200.shard import DeviceEngine, cluster_sharded
+
+    L = 36.8 * (n / 37e6) ** (1.0 / 3.0)
+    c = torch.from_numpy(tb.Dataset.hacc_like(n, box_len=L, seed=11 + rank).coords())
+    c[:, 0] += rank * L
+    x = c.to(dev)
+    gid = (torch.arange(n, dtype=torch.int64) + rank * n).to(dev)
+    engine = DeviceEngine(dev)
+    for _ in range(args.warmup):
+        cluster_sharded(x, gid, EPS, MINPTS, engine)
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(dev.index or 0)
+    sampler.start()
+    time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        own_gid, labels, core = cluster_sharded(x, gid, EPS, MINPTS, engine)
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    value = n * world / (ms * 1e-3) / 1e6
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 coords / f64 distances (exact reference predicate)",
+            "data": "synthetic (HACC-like halo slabs, SURVEY.md §8d)",
+            "config": {"workload": f"C5-shaped: 3D HACC-like, {n} points per GPU x {world} GPUs, "
+                                   "eps=0.042, minpts=2, FDBSCAN, Morton-range sharded",
+                       "points_per_rank": n, "parallelism": f"morton-range shards x{world}",
+                       "l2": "inputs exceed the 126 MB L2"},
+            "clocks": clocks, "gpu_launches": None, "e2e": None, "cpu_baseline": None,
+            "roofline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -189,6 +247,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=N_POINTS, help="points per rank (default: 37M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of the Morton-range sharded path")
     args = ap.parse_args()
 
     rank = env_int("RANK", 0)
@@ -210,6 +270,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     n = args.n
+    if world > 1 and not args.replicas:
+        return run_sharded(args, rank, world, dev, n)
     # Synthetic HACC-like halos; each rank its own cloud.
     ds = tb.Dataset.hacc_like(n, seed=11 + rank)
     host = torch.from_numpy(ds.coords())

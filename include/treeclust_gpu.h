@@ -76,6 +76,38 @@ tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n,
 tc_status tcg_dataset_create_pinned(const float* coords, int64_t n, int dim,
                                     tc_dataset** out);
 
+/* ---- device stages of the Morton-range multi-GPU path ----
+ * The collectives between them are issued by the caller's communicator
+ * (paper_2103_05162_b200/shard.py uses torch.distributed / NCCL). All
+ * pointers named d_* are device pointers; calls are ordered on `stream`. */
+
+/* Morton codes of n points against the GLOBAL scene box lo/hi (host arrays of
+ * dim floats), the tree build's fp64 quantization (geometry.hpp:132-156). */
+tc_status tcg_morton_codes_device(const float* d_coords, int64_t n, int dim, const float* lo,
+                                  const float* hi, uint64_t* d_codes, void* stream);
+/* d_mask[i] = 1 iff point i lies within eps of one of the num_boxes boxes
+ * (d_box_lo / d_box_hi: num_boxes*dim floats): the eps-halo a peer needs. */
+tc_status tcg_near_boxes_device(const float* d_coords, int64_t n, int dim, float eps,
+                                const float* d_box_lo, const float* d_box_hi, int64_t num_boxes,
+                                uint8_t* d_mask, void* stream);
+/* Exact core flags (|N_eps(i)| >= minpts, i itself included) of n points. */
+tc_status tcg_core_flags_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
+                                uint8_t* d_core, void* stream);
+/* Main pass + finalize with caller-supplied core flags (the FDBSCAN main
+ * phase, dbscan.cpp:60-88, never the minpts == 2 shortcut): labels are the
+ * minimum LOCAL index of each cluster's cores, -1 for noise. stats may be NULL
+ * (no synchronization then). */
+tc_status tcg_cluster_given_core_device(const float* d_coords, int64_t n, int dim, float eps,
+                                        const uint8_t* d_core_in, int32_t* d_labels,
+                                        uint8_t* d_core_out, void* stream,
+                                        tc_cluster_stats* stats);
+
+/* Connected components of m edges (2*m int32 endpoints in [0, n)): d_root[i]
+ * = the minimum index of i's component (min-index hooking + flatten). Used
+ * for the cross-shard merge of (ghost, local root) edges. */
+tc_status tcg_union_edges_device(const int32_t* d_edges, int64_t m, int32_t n, int32_t* d_root,
+                                 void* stream);
+
 /* ---- stage probes for parity tests (each runs one device stage on host
  *      inputs and copies the result back) ---- */
 

@@ -71,6 +71,14 @@ SIGNATURES = {
     "tcg_generate_taxi_like": (C.c_int, [C.c_int64, C.c_uint64, _PP]),
     "tcg_random_instance": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_float),
                                       C.POINTER(C.c_int), _PP]),
+    "tcg_morton_codes_device": (C.c_int, [_P, C.c_int64, C.c_int, C.POINTER(C.c_float),
+                                          C.POINTER(C.c_float), _P, _P]),
+    "tcg_near_boxes_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, C.c_int64,
+                                        _P, _P]),
+    "tcg_core_flags_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, C.c_int, _P, _P]),
+    "tcg_cluster_given_core_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P,
+                                                _P, C.POINTER(TcClusterStats)]),
+    "tcg_union_edges_device": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P]),
     "tcg_debug_point_bvh": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int,
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -1,0 +1,264 @@
+// Device stages of the Morton-range multi-GPU path, exposed
+// through the additive C ABI (treeclust_gpu.h). The collectives between them
+// (bounds all-reduce, splitter all-gather, point / halo / flag all-to-all,
+// cross-shard edge all-gather) are issued by the caller's communicator
+// (paper_2103_05162_b200/shard.py drives them through torch.distributed).
+//
+//   tcg_morton_codes_device   Morton codes of a shard's points against the
+//                             GLOBAL scene box (same fp64 quantization as the
+//                             tree build, geometry.hpp:132-156)
+//   tcg_near_boxes_device     which points lie within eps of any box of a
+//                             peer's region (halo selection): an LBVH over
+//                             the peer's boxes + an early-exit ball query
+//   tcg_core_flags_device     exact core flags (|N_eps| >= minpts, self
+//                             included) of every point of own + ghost set
+//   tcg_cluster_given_core_device
+//                             main pass + finalize with core flags supplied
+//                             by the caller (owners' exact flags for ghosts)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <limits>
+
+#include "device_common.cuh"
+#include "engine.hpp"
+#include "pipeline.hpp"
+#include "treeclust_gpu.h"
+
+#define TC_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace tcb {
+namespace {
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_codes(const float* __restrict__ coords, int64_t n, float3 lo, float3 hi,
+        unsigned long long* __restrict__ codes) {
+  constexpr int bits = D == 2 ? 31 : 21;
+  constexpr uint64_t cells = 1ull << bits;
+  const double cells_d = static_cast<double>(cells);
+  const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+  double w[3];
+#pragma unroll
+  for (int k = 0; k < D; ++k) w[k] = __dsub_rn(static_cast<double>(h[k]), static_cast<double>(l[k]));
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t q[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = quantize(coords[i * D + k], l[k], w[k], cells_d, cells);
+    codes[i] = D == 2 ? (spread2(q[0]) | (spread2(q[1]) << 1))
+                      : (spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2));
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_pack_boxes(const float* __restrict__ lo, const float* __restrict__ hi, int64_t nb,
+             float4* __restrict__ lo4, float4* __restrict__ hi4) {
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nb;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    lo4[b] = make_float4(lo[b * D], lo[b * D + 1], D == 3 ? lo[b * D + 2] : 0.f, 0.f);
+    hi4[b] = make_float4(hi[b * D], hi[b * D + 1], D == 3 ? hi[b * D + 2] : 0.f, 0.f);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128)
+k_near(const float4* __restrict__ nodes, const float* __restrict__ coords, int64_t n, BallTest bt,
+       uint8_t* __restrict__ mask) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  float p[3] = {coords[i * D], coords[i * D + 1], D == 3 ? coords[i * D + 2] : 0.f};
+  bool hit = false;
+  auto visit = [&](int32_t, int32_t, const float*, const float*) -> bool {
+    hit = true;
+    return false;
+  };
+  bvh_query<D>(nodes, p, bt, 0, visit);
+  mask[i] = hit ? 1 : 0;
+}
+
+template <int D>
+void near_boxes(const float* d_coords, int64_t n, float eps, const float* d_lo, const float* d_hi,
+                int64_t nb, uint8_t* d_mask, cudaStream_t st) {
+  Scratch scratch(st);
+  if (nb == 0) {
+    TCB_CUDA(cudaMemsetAsync(d_mask, 0, static_cast<size_t>(n), st));
+    return;
+  }
+  DevCounters* ctr = scratch.alloc_n<DevCounters>(1);
+  TCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), st));
+  float4* lo4 = scratch.alloc_n<float4>(nb);
+  float4* hi4 = scratch.alloc_n<float4>(nb);
+  note_launch(), k_pack_boxes<D><<<grid_for(nb, 256), 256, 0, st>>>(d_lo, d_hi, nb, lo4, hi4);
+  PrimSource src;
+  src.lo = lo4;
+  src.hi = hi4;
+  src.count = nb;
+  BuiltBvh b = build_bvh<D>(src, false, ctr, scratch, nullptr);
+  const BallTest bt = BallTest::make(static_cast<double>(eps) * static_cast<double>(eps));
+  note_launch(), k_near<D><<<grid_for(n, 128, INT32_MAX), 128, 0, st>>>(b.tree.nodes, d_coords, n, bt,
+                                                                        d_mask);
+  TCB_CUDA(cudaGetLastError());
+}
+
+template <int D>
+void core_flags(const float* d_coords, int64_t n, float eps, int minpts, uint8_t* d_core,
+                cudaStream_t st) {
+  Scratch scratch(st);
+  DevCounters* ctr = scratch.alloc_n<DevCounters>(1);
+  TCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), st));
+  PrimSource src;
+  src.coords = d_coords;
+  src.count = n;
+  BuiltBvh b = build_bvh<D>(src, true, ctr, scratch, nullptr);
+  TCB_CUDA(cudaMemsetAsync(d_core, 0, static_cast<size_t>(n), st));
+  const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
+  fdbscan_core_pass<D>(b, n, eps2, minpts, d_core, ctr, st);
+}
+
+template <int D>
+void given_core(const float* d_coords, int64_t n, float eps, const uint8_t* d_core_in,
+                int32_t* d_labels, uint8_t* d_core_out, cudaStream_t st, tc_cluster_stats* stats) {
+  Scratch scratch(st);
+  DevCounters* ctr = scratch.alloc_n<DevCounters>(1);
+  TCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), st));
+  PrimSource src;
+  src.coords = d_coords;
+  src.count = n;
+  BuiltBvh b = build_bvh<D>(src, true, ctr, scratch, nullptr);
+  int32_t* parent = scratch.alloc_n<int32_t>(n);
+  uint8_t* flags = scratch.alloc_n<uint8_t>(n);
+  init_union_find(parent, flags, n, st);
+  TCB_CUDA(cudaMemcpyAsync(flags, d_core_in, static_cast<size_t>(n), cudaMemcpyDeviceToDevice, st));
+  const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
+  fdbscan_main_pass<D>(b, n, eps2, /*force_core=*/false, flags, parent, ctr, st);
+  finalize_labels(parent, flags, n, d_labels, d_core_out, ctr, st, /*force_core=*/false);
+  if (stats) {
+    DevCounters h;
+    TCB_CUDA(cudaMemcpyAsync(&h, ctr, sizeof h, cudaMemcpyDeviceToHost, st));
+    TCB_CUDA(cudaStreamSynchronize(st));
+    *stats = tc_cluster_stats{};
+    stats->pair_resolutions = h.pairs;
+    stats->distance_evaluations = h.dists;
+    stats->cluster_count = h.clusters;
+    stats->core_count = h.cores;
+    stats->noise_count = h.noise;
+  }
+}
+
+__global__ void k_unite_pairs(const int32_t* __restrict__ edges, int64_t m, int32_t* parent) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    uf_unite(parent, edges[2 * e], edges[2 * e + 1]);
+}
+
+__global__ void k_flatten_all(int32_t* parent, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t p = ld_relaxed(parent + i), q;
+    while (p != (q = ld_relaxed(parent + p))) p = q;
+    st_relaxed(parent + i, p);
+  }
+}
+
+template <typename Fn>
+tc_status run_guarded(Fn&& fn) {
+  try {
+    fn();
+    return TC_OK;
+  } catch (const InvalidArgument&) {
+    return TC_ERR_INVALID_ARGUMENT;
+  } catch (...) {
+    cudaGetLastError();
+    return TC_ERR_INTERNAL;
+  }
+}
+
+bool bad_shape(const void* p, int64_t n, int dim) {
+  return !p || n < 0 || n > std::numeric_limits<int32_t>::max() || (dim != 2 && dim != 3);
+}
+
+}  // namespace
+}  // namespace tcb
+
+using namespace tcb;
+
+TC_EXPORT tc_status tcg_morton_codes_device(const float* d_coords, int64_t n, int dim,
+                                            const float* lo, const float* hi, uint64_t* d_codes,
+                                            void* stream) {
+  if (bad_shape(d_coords, n, dim) || !lo || !hi || !d_codes) return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    const float3 l = make_float3(lo[0], lo[1], dim == 3 ? lo[2] : 0.f);
+    const float3 h = make_float3(hi[0], hi[1], dim == 3 ? hi[2] : 0.f);
+    auto st = static_cast<cudaStream_t>(stream);
+    auto* out = reinterpret_cast<unsigned long long*>(d_codes);
+    if (n == 0) return;
+    if (dim == 2)
+      note_launch(), k_codes<2><<<grid_for(n, 256), 256, 0, st>>>(d_coords, n, l, h, out);
+    else
+      note_launch(), k_codes<3><<<grid_for(n, 256), 256, 0, st>>>(d_coords, n, l, h, out);
+    TCB_CUDA(cudaGetLastError());
+  });
+}
+
+TC_EXPORT tc_status tcg_near_boxes_device(const float* d_coords, int64_t n, int dim, float eps,
+                                          const float* d_box_lo, const float* d_box_hi,
+                                          int64_t num_boxes, uint8_t* d_mask, void* stream) {
+  if (bad_shape(d_coords, n, dim) || !d_mask || num_boxes < 0 || !(eps > 0.f))
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    if (n == 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (dim == 2)
+      near_boxes<2>(d_coords, n, eps, d_box_lo, d_box_hi, num_boxes, d_mask, st);
+    else
+      near_boxes<3>(d_coords, n, eps, d_box_lo, d_box_hi, num_boxes, d_mask, st);
+  });
+}
+
+TC_EXPORT tc_status tcg_core_flags_device(const float* d_coords, int64_t n, int dim, float eps,
+                                          int minpts, uint8_t* d_core, void* stream) {
+  if (bad_shape(d_coords, n, dim) || n < 1 || !d_core || !(eps > 0.f) || !std::isfinite(eps) ||
+      minpts < 2)
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    reset_launch_count();
+    if (dim == 2)
+      core_flags<2>(d_coords, n, eps, minpts, d_core, st);
+    else
+      core_flags<3>(d_coords, n, eps, minpts, d_core, st);
+  });
+}
+
+TC_EXPORT tc_status tcg_cluster_given_core_device(const float* d_coords, int64_t n, int dim,
+                                                  float eps, const uint8_t* d_core_in,
+                                                  int32_t* d_labels, uint8_t* d_core_out,
+                                                  void* stream, tc_cluster_stats* stats) {
+  if (bad_shape(d_coords, n, dim) || n < 1 || !d_core_in || !d_labels || !d_core_out ||
+      !(eps > 0.f) || !std::isfinite(eps))
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    reset_launch_count();
+    if (dim == 2)
+      given_core<2>(d_coords, n, eps, d_core_in, d_labels, d_core_out, st, stats);
+    else
+      given_core<3>(d_coords, n, eps, d_core_in, d_labels, d_core_out, st, stats);
+  });
+}
+
+TC_EXPORT tc_status tcg_union_edges_device(const int32_t* d_edges, int64_t m, int32_t n,
+                                           int32_t* d_root, void* stream) {
+  if ((!d_edges && m > 0) || m < 0 || n < 1 || !d_root) return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    Scratch scratch(st);
+    uint8_t* tmp = scratch.alloc_n<uint8_t>(n);
+    init_union_find(d_root, tmp, n, st);
+    if (m > 0) note_launch(), k_unite_pairs<<<grid_for(m, 256), 256, 0, st>>>(d_edges, m, d_root);
+    note_launch(), k_flatten_all<<<grid_for(n, 256), 256, 0, st>>>(d_root, n);
+    TCB_CUDA(cudaGetLastError());
+  });
+}

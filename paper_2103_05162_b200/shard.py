@@ -1,0 +1,288 @@
+"""Morton-range sharded DBSCAN across GPUs.
+
+One process per GPU; the collectives go through torch.distributed (NCCL on
+GPUs, gloo in the CPU tests); every data-path stage runs in the C-ABI library
+(`DeviceEngine`, tcg_*_device). Protocol, for eps and minpts:
+
+1. global scene box: all-reduce MIN / MAX of the local bounds;
+2. Morton codes against the global box; every rank all-gathers a sorted
+   sample of its codes, the world picks world-1 splitters;
+3. all-to-all: each point (coords + global id) moves to the rank owning its
+   Morton range;
+4. each rank describes its region by the boxes of runs of `block`
+   consecutive own points in Morton order and all-gathers them; every rank
+   sends each peer the own points within eps of one of that peer's boxes
+   (all-to-all). Every point within eps of a peer-owned point is within eps of
+   a box holding it, so the ghosts a rank receives contain every neighbour of
+   its own points;
+5. local set = own + ghosts, ordered by global id (so local minimum index ==
+   global minimum id). Core flags of own points are exact (complete
+   neighbourhoods); ghosts take their owner's flags (all-to-all of the flags of
+   the points sent in step 4, same order);
+6. local main pass with those flags (tcg_cluster_given_core_device);
+7. every core point that is a ghost here or was exported as a ghost yields an
+   edge (global id, global id of its local root); the edges are all-gathered
+   and merged by a device union-find (min-index hooking, so representatives
+   are global minimum ids) — the cluster representative is then the global
+   minimum core id, exactly the 1-GPU label; own points are relabelled.
+
+Result per rank: (global ids, labels, core flags) of the points it owns.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from ._lib import TcClusterStats, lib
+from .api import Status, TreeclustError
+
+
+def _check(st, where):
+    if st != 0:
+        raise TreeclustError(st, where)
+
+
+class DeviceEngine:
+    """The product engine: device stages of the C ABI on CUDA tensors."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+
+    def _s(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def morton(self, x, lo, hi):
+        n, d = x.shape
+        out = torch.empty(n, dtype=torch.int64, device=x.device)
+        lo_h = (C.c_float * 3)(*[float(v) for v in lo.tolist()] + [0.0] * (3 - d))
+        hi_h = (C.c_float * 3)(*[float(v) for v in hi.tolist()] + [0.0] * (3 - d))
+        _check(lib.tcg_morton_codes_device(C.c_void_p(x.data_ptr()), n, d, lo_h, hi_h,
+                                           C.c_void_p(out.data_ptr()), self._s()),
+               "tcg_morton_codes_device")
+        return out
+
+    def near_boxes(self, x, eps, blo, bhi):
+        n, d = x.shape
+        mask = torch.empty(n, dtype=torch.uint8, device=x.device)
+        if n == 0:
+            return mask
+        blo = blo.contiguous()
+        bhi = bhi.contiguous()
+        _check(lib.tcg_near_boxes_device(C.c_void_p(x.data_ptr()), n, d, C.c_float(eps),
+                                         C.c_void_p(blo.data_ptr()), C.c_void_p(bhi.data_ptr()),
+                                         blo.shape[0], C.c_void_p(mask.data_ptr()), self._s()),
+               "tcg_near_boxes_device")
+        return mask
+
+    def core_flags(self, x, eps, minpts):
+        n, d = x.shape
+        core = torch.empty(n, dtype=torch.uint8, device=x.device)
+        _check(lib.tcg_core_flags_device(C.c_void_p(x.data_ptr()), n, d, C.c_float(eps),
+                                         int(minpts), C.c_void_p(core.data_ptr()), self._s()),
+               "tcg_core_flags_device")
+        return core
+
+    def cluster_given_core(self, x, eps, core):
+        n, d = x.shape
+        labels = torch.empty(n, dtype=torch.int32, device=x.device)
+        core_out = torch.empty(n, dtype=torch.uint8, device=x.device)
+        core = core.contiguous()
+        _check(lib.tcg_cluster_given_core_device(C.c_void_p(x.data_ptr()), n, d, C.c_float(eps),
+                                                 C.c_void_p(core.data_ptr()),
+                                                 C.c_void_p(labels.data_ptr()),
+                                                 C.c_void_p(core_out.data_ptr()), self._s(),
+                                                 None),
+               "tcg_cluster_given_core_device")
+        return labels
+
+    def union_edges(self, edges, n):
+        root = torch.empty(n, dtype=torch.int32, device=self.device)
+        edges = edges.to(device=self.device, dtype=torch.int32).contiguous()
+        _check(lib.tcg_union_edges_device(C.c_void_p(edges.data_ptr()), edges.shape[0], int(n),
+                                          C.c_void_p(root.data_ptr()), self._s()),
+               "tcg_union_edges_device")
+        return root
+
+
+# ---------------------------------------------------------------------------
+# collectives (moved through host memory when the backend is gloo)
+# ---------------------------------------------------------------------------
+def _host_collectives(group):
+    return dist.get_backend(group) == "gloo"
+
+
+def _to_comm(t, group):
+    return t.cpu() if _host_collectives(group) else t
+
+
+def _all_reduce(t, op, group):
+    c = _to_comm(t, group)
+    dist.all_reduce(c, op=op, group=group)
+    return c.to(t.device)
+
+
+def _all_gather_var(t, group):
+    """All-gather tensors whose first dimension differs per rank."""
+    world = dist.get_world_size(group)
+    dev = t.device
+    c = _to_comm(t.contiguous(), group)
+    n = torch.tensor([c.shape[0]], dtype=torch.int64, device=c.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes) if sizes else 0
+    pad = torch.zeros((mx,) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)
+    pad[: c.shape[0]] = c
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return [o[:s].to(dev) for o, s in zip(outs, sizes)]
+
+
+def _all_to_all(t, send_counts, group):
+    """Variable all-to-all along dim 0; send_counts[j] rows go to rank j."""
+    world = dist.get_world_size(group)
+    dev = t.device
+    sc = torch.tensor(send_counts, dtype=torch.int64)
+    rc = torch.empty(world, dtype=torch.int64)
+    if _host_collectives(group):
+        dist.all_to_all_single(rc, sc, group=group)
+    else:
+        rcd = torch.empty(world, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(rcd, sc.to(dev), group=group)
+        rc = rcd.cpu()
+    recv = [int(v) for v in rc.tolist()]
+    c = _to_comm(t.contiguous(), group)
+    out = torch.empty((sum(recv),) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)
+    dist.all_to_all_single(out, c, recv, list(send_counts), group=group)
+    return out.to(dev), recv
+
+
+# ---------------------------------------------------------------------------
+def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples=4096):
+    """Clusters the union of every rank's (x, gid) points.
+
+    x: (n_local, dim) float32 tensor on the engine's device; gid: (n_local,)
+    int64 global ids (unique across ranks). Returns (own_gid, labels, core)
+    for the points this rank owns after the Morton-range redistribution;
+    labels are global ids of the cluster representative (minimum core id), -1
+    for noise. Identical to the single-GPU result on the concatenated input.
+    """
+    if not (eps > 0) or minpts < 2:
+        raise TreeclustError(Status.INVALID_ARGUMENT, "cluster_sharded")
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = x.device
+    n, dim = x.shape
+
+    # 1. global scene box
+    if n:
+        lo = x.min(0).values
+        hi = x.max(0).values
+    else:
+        lo = torch.full((dim,), float("inf"), device=dev)
+        hi = torch.full((dim,), float("-inf"), device=dev)
+    lo = _all_reduce(lo.clone(), dist.ReduceOp.MIN, group)
+    hi = _all_reduce(hi.clone(), dist.ReduceOp.MAX, group)
+
+    # 2. codes and splitters
+    codes = engine.morton(x, lo, hi) if n else torch.empty(0, dtype=torch.int64, device=dev)
+    scodes = torch.sort(codes).values
+    k = min(n, samples)
+    if k:
+        pos = torch.div(torch.arange(k, device=dev) * n + n // 2, k, rounding_mode="floor")
+        sample = scodes[pos.clamp(max=n - 1)]
+    else:
+        sample = scodes[:0]
+    allsamp = torch.sort(torch.cat(_all_gather_var(sample, group))).values
+    m = allsamp.shape[0]
+    if world > 1 and m:
+        q = torch.tensor([(j * m) // world for j in range(1, world)], device=dev)
+        splitters = allsamp[q.clamp(max=m - 1)]
+    else:
+        splitters = torch.empty(0, dtype=torch.int64, device=dev)
+    owner = torch.bucketize(codes, splitters, right=True)
+
+    # 3. redistribution by Morton range
+    order = torch.argsort(owner, stable=True)
+    counts = torch.bincount(owner, minlength=world).tolist() if n else [0] * world
+    payload = torch.cat([x[order].view(torch.int32), gid[order].view(torch.int32).view(-1, 2)], 1)
+    recv, _ = _all_to_all(payload, counts, group)
+    own_x = recv[:, :dim].contiguous().view(torch.float32)
+    own_gid = recv[:, dim:].contiguous().view(torch.int64).view(-1)
+    n_own = own_x.shape[0]
+
+    # 4. region boxes and the eps halo
+    if n_own:
+        oc = engine.morton(own_x, lo, hi)
+        perm = torch.argsort(oc)
+        xs = own_x[perm]
+        nb = (n_own + block - 1) // block
+        padn = nb * block - n_own
+        big = torch.full((padn, dim), float("inf"), device=dev)
+        blo = torch.cat([xs, big]).view(nb, block, dim).min(1).values
+        bhi = torch.cat([xs, -big]).view(nb, block, dim).max(1).values
+        boxes = torch.cat([blo, bhi], 1)
+    else:
+        boxes = torch.empty((0, 2 * dim), dtype=torch.float32, device=dev)
+    peer_boxes = _all_gather_var(boxes, group)
+    send_idx, send_counts = [], []
+    for j in range(world):
+        if j == rank or n_own == 0 or peer_boxes[j].shape[0] == 0:
+            send_counts.append(0)
+            continue
+        pb = peer_boxes[j]
+        mask = engine.near_boxes(own_x, eps, pb[:, :dim], pb[:, dim:])
+        idx = torch.nonzero(mask, as_tuple=False).view(-1)
+        send_idx.append(idx)
+        send_counts.append(int(idx.shape[0]))
+    send_idx = torch.cat(send_idx) if send_idx else torch.empty(0, dtype=torch.int64, device=dev)
+    halo_payload = torch.cat([own_x[send_idx].view(torch.int32),
+                              own_gid[send_idx].view(torch.int32).view(-1, 2)], 1)
+    ghost, _ = _all_to_all(halo_payload, send_counts, group)
+    ghost_x = ghost[:, :dim].contiguous().view(torch.float32)
+    ghost_gid = ghost[:, dim:].contiguous().view(torch.int64).view(-1)
+
+    # 5. local set ordered by global id; exact own flags; owners' ghost flags
+    lx = torch.cat([own_x, ghost_x])
+    lgid = torch.cat([own_gid, ghost_gid])
+    lorder = torch.argsort(lgid)
+    lx = lx[lorder].contiguous()
+    lgid = lgid[lorder]
+    inv = torch.empty_like(lorder)
+    inv[lorder] = torch.arange(lorder.shape[0], device=dev)
+    own_pos = inv[:n_own]
+    ghost_pos = inv[n_own:]
+    nl = lx.shape[0]
+    if nl == 0:
+        e = torch.empty(0, dtype=torch.int64, device=dev)
+        _all_gather_var(torch.empty((0, 2), dtype=torch.int64, device=dev), group)
+        return e, e.to(torch.int32), e.to(torch.uint8)
+    local_core = engine.core_flags(lx, eps, minpts)
+    own_core = local_core[own_pos]
+    ghost_core, _ = _all_to_all(own_core[send_idx].view(-1, 1), send_counts, group)
+    core = local_core.clone()
+    core[ghost_pos] = ghost_core.view(-1)
+
+    # 6. local main pass with the true flags
+    lab = engine.cluster_given_core(lx, eps, core).to(torch.int64)
+
+    # 7. cross-shard edges (global ids) and the global merge
+    exported = torch.zeros(nl, dtype=torch.bool, device=dev)
+    exported[own_pos[send_idx]] = True
+    is_ghost = torch.zeros(nl, dtype=torch.bool, device=dev)
+    is_ghost[ghost_pos] = True
+    sel = (core.bool() & (is_ghost | exported)).nonzero(as_tuple=False).view(-1)
+    edges = torch.stack([lgid[sel], lgid[lab[sel]]], 1)
+    all_edges = torch.cat(_all_gather_var(edges, group))
+    own_lab = lab[own_pos]
+    root_gid = torch.where(own_lab >= 0, lgid[own_lab.clamp(min=0)], torch.full_like(own_lab, -1))
+    if all_edges.shape[0]:
+        uniq, comp = torch.unique(all_edges.view(-1), return_inverse=True)
+        root = engine.union_edges(comp.view(-1, 2), uniq.shape[0]).to(torch.int64)
+        rep = uniq[root]  # compact ids are ordered like global ids: min id wins
+        pos = torch.searchsorted(uniq, root_gid.clamp(min=0))
+        hit = (root_gid >= 0) & (pos < uniq.shape[0]) & (uniq[pos.clamp(max=uniq.shape[0] - 1)] == root_gid)
+        root_gid = torch.where(hit, rep[pos.clamp(max=uniq.shape[0] - 1)], root_gid)
+    return own_gid, root_gid, own_core

@@ -1,0 +1,194 @@
+"""The Morton-range sharded path (paper_2103_05162_b200/shard.py)
+with world size 2 over gloo.
+
+CPU tests run the distributed protocol with the oracle as the local engine
+(test infrastructure: O(n^2) numpy neighbourhoods, the C restatement's
+Morton codes); the gpu-marked tests run the same protocol with the product
+DeviceEngine (C-ABI device stages), two processes sharing cuda:0. In both,
+the union of the shards' results must equal the single-process reference
+result: core flags and noise exact, core labels equal (global minimum core
+id), every border label valid."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle
+
+
+class OracleEngine:
+    """Test-only local engine on CPU tensors (exact fp64 predicates)."""
+
+    def morton(self, x, lo, hi):
+        c = oracle.morton_codes(x.numpy(), lo.numpy(), hi.numpy())
+        return torch.from_numpy(c.astype(np.int64))
+
+    @staticmethod
+    def _d2(a, b):
+        a = a.astype(np.float64)
+        b = b.astype(np.float64)
+        d = a[:, None, 0] - b[None, :, 0]
+        s = d * d
+        for k in range(1, a.shape[1]):
+            d = a[:, None, k] - b[None, :, k]
+            s = s + d * d
+        return s
+
+    def near_boxes(self, x, eps, blo, bhi):
+        p = x.numpy().astype(np.float64)
+        lo = blo.numpy().astype(np.float64)
+        hi = bhi.numpy().astype(np.float64)
+        s = np.zeros((p.shape[0], lo.shape[0]))
+        for k in range(p.shape[1]):
+            d = np.maximum(np.maximum(lo[None, :, k] - p[:, None, k], p[:, None, k] - hi[None, :, k]), 0)
+            s = s + d * d
+        e2 = np.float64(np.float32(eps)) ** 2
+        return torch.from_numpy((s <= e2).any(1).astype(np.uint8))
+
+    def core_flags(self, x, eps, minpts):
+        e2 = np.float64(np.float32(eps)) ** 2
+        cnt = (self._d2(x.numpy(), x.numpy()) <= e2).sum(1)
+        return torch.from_numpy((cnt >= minpts).astype(np.uint8))
+
+    def cluster_given_core(self, x, eps, core):
+        e2 = np.float64(np.float32(eps)) ** 2
+        adj = self._d2(x.numpy(), x.numpy()) <= e2
+        c = core.numpy().astype(bool)
+        n = len(c)
+        parent = np.arange(n)
+
+        def find(i):
+            while parent[i] != i:
+                parent[i] = parent[parent[i]]
+                i = parent[i]
+            return i
+
+        for i, j in zip(*np.nonzero(np.triu(adj & c[:, None] & c[None, :], 1))):
+            a, b = find(i), find(j)
+            if a != b:
+                parent[max(a, b)] = min(a, b)
+        lab = np.full(n, -1, np.int64)
+        for i in range(n):
+            if c[i]:
+                lab[i] = find(i)
+        for i in range(n):
+            if not c[i]:
+                nb = np.nonzero(adj[i] & c)[0]
+                if len(nb):
+                    lab[i] = lab[nb].min()
+        return torch.from_numpy(lab.astype(np.int32))
+
+    def union_edges(self, edges, n):
+        parent = np.arange(n)
+
+        def find(i):
+            while parent[i] != i:
+                parent[i] = parent[parent[i]]
+                i = parent[i]
+            return i
+
+        for a, b in edges.numpy():
+            ra, rb = find(a), find(b)
+            if ra != rb:
+                parent[max(ra, rb)] = min(ra, rb)
+        return torch.from_numpy(np.array([find(i) for i in range(n)], np.int32))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, coords, eps, minpts, use_gpu, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2103_05162_b200.shard import DeviceEngine, cluster_sharded
+
+    n = coords.shape[0]
+    # input partition: interleaved slices (deliberately not spatial)
+    idx = np.arange(rank, n, world)
+    x = torch.from_numpy(coords[idx])
+    gid = torch.from_numpy(idx.astype(np.int64))
+    if use_gpu:
+        engine = DeviceEngine("cuda:0")
+        x = x.cuda()
+        gid = gid.cuda()
+    else:
+        engine = OracleEngine()
+    g, lab, core = cluster_sharded(x, gid, eps, minpts, engine, block=64, samples=256)
+    out_q.put((rank, g.cpu().numpy(), lab.cpu().numpy(), core.cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def run_sharded(coords, eps, minpts, world=2, use_gpu=False):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, coords, eps, minpts, use_gpu, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = coords.shape[0]
+    labels = np.full(n, -2, np.int64)
+    core = np.zeros(n, np.uint8)
+    owned = 0
+    for _, g, lab, c in res:
+        labels[g] = lab
+        core[g] = c
+        owned += len(g)
+    assert owned == n and (labels != -2).all(), "every point owned exactly once"
+    return labels, core
+
+
+def check_against_oracle(coords, eps, minpts, labels, core):
+    want = oracle.dbscan(coords, eps, minpts, 0)
+    assert np.array_equal(core, want["core"]), "core flags differ"
+    assert np.array_equal(labels == -1, want["labels"] == -1), "noise differs"
+    cm = want["core"] == 1
+    assert np.array_equal(labels[cm], want["labels"][cm]), "core labels differ"
+    ok, msg = oracle.check_equivalence(coords, eps, labels.astype(np.int32), core,
+                                       want["labels"], want["core"])
+    assert ok, msg
+
+
+def blob_mix(seed, n, dim):
+    rng = np.random.default_rng(seed)
+    k = 6
+    centers = rng.uniform(0, 10, (k, dim))
+    pts = [rng.normal(centers[rng.integers(k)], 0.35, (n // (2 * k), dim)) for _ in range(2 * k)]
+    pts.append(rng.uniform(0, 10, (n // 4, dim)))
+    return np.concatenate(pts).astype(np.float32)
+
+
+@pytest.mark.parametrize("dim,eps,minpts", [(3, 0.3, 2), (3, 0.45, 5), (2, 0.2, 4), (2, 0.15, 2)])
+def test_sharded_world2_matches_single_process(dim, eps, minpts):
+    coords = blob_mix(10 + dim + minpts, 1800, dim)
+    labels, core = run_sharded(coords, eps, minpts, world=2)
+    check_against_oracle(coords, eps, minpts, labels, core)
+
+
+def test_sharded_world3_uneven():
+    coords = blob_mix(5, 1500, 3)[:1237]
+    labels, core = run_sharded(coords, 0.4, 4, world=3)
+    check_against_oracle(coords, 0.4, 4, labels, core)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,eps,minpts", [(3, 0.3, 2), (2, 0.2, 5)])
+def test_sharded_device_engine_world2(dim, eps, minpts):
+    coords = blob_mix(40 + dim, 6000, dim)
+    labels, core = run_sharded(coords, eps, minpts, world=2, use_gpu=True)
+    check_against_oracle(coords, eps, minpts, labels, core)
