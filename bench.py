@@ -14,8 +14,12 @@ copy of labels + core flags are inside its timed region.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank clusters its own 37M-point cloud (different
-seed) — weak scaling of independent replicas; timed as the max over ranks.
+N > 1 (torchrun): one global HACC-like cloud of N x 37M points (a slab per
+rank) clustered by the Morton-range sharded path (paper_2103_05162_b200/
+shard.py: redistribution, eps halo, local passes, cross-shard merge) — weak
+scaling; `--replicas` instead runs N independent 37M clouds. Timed as the max
+over ranks. (TCB_BENCH_BACKEND=gloo TCB_BENCH_SAME_DEVICE=1 lets a 1-GPU box
+smoke-test the N>1 protocol with every rank on cuda:0.)
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref = /root/reference/proj compiled unmodified, via its C ABI) on the
 host cores, on a bounded sample of the same workload (same density).
@@ -245,7 +249,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_POINTS, help="points per rank (default: 37M)")
+    ap.add_argument("--points", type=int, default=N_POINTS, help="points per rank (default: 37M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the Morton-range sharded path")
@@ -264,12 +268,18 @@ def main():
 
     if args.warmup < 3:
         args.warmup = 3
+    if os.environ.get("TCB_BENCH_SAME_DEVICE") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("TCB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
-    n = args.n
+    n = args.points
     if world > 1 and not args.replicas:
         return run_sharded(args, rank, world, dev, n)
     # Synthetic HACC-like halos; each rank its own cloud.

@@ -21,8 +21,9 @@ def launches(path):
     ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
     agg = collections.OrderedDict()
     for r in data:
-        name = r[ik].split("(")[0].replace("void ", "").replace("tcb::<unnamed>::", "")
-        name = name.replace("tcb::", "")
+        name = r[ik].split("(")[0].replace("void ", "")
+        if "::k_" in name:
+            name = "k_" + name.split("::k_", 1)[1]
         v = float(r[iv].replace(",", ""))
         agg.setdefault(name, [0, 0.0])
         agg[name][0] += 1
