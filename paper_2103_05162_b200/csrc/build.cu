@@ -291,26 +291,6 @@ k_refit(const int32_t* __restrict__ starts, const int32_t* __restrict__ num_star
   }
 }
 
-// Per leaf: the highest ancestor whose leaf range holds <= k leaves (its
-// "bucket"; ~rank when even the parent is larger). Buckets partition the
-// Morton order into runs that the main pass scans linearly instead of
-// descending into.
-__global__ void __launch_bounds__(256)
-k_buckets(const int4* __restrict__ node_info, const int32_t* __restrict__ leaf_up, int64_t m,
-          int k, int32_t* __restrict__ bucket) {
-  int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (r >= m) return;
-  int32_t c = ~static_cast<int32_t>(r);
-  int32_t P = up_parent(leaf_up[r]);
-  while (P != kNoParent) {
-    const int4 info = node_info[P];
-    if (info.w - info.z + 1 > k) break;
-    c = P;
-    P = up_parent(info.x);
-  }
-  bucket[r] = c;
-}
-
 // 1-leaf tree: pseudo root with the leaf on the left and an empty box right.
 template <int D, class Src>
 __global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, float4* nodes,
@@ -336,7 +316,7 @@ __global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, flo
 template <int D, class Src>
 BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finite,
                     bool points_mode, DevCounters* d_ctr, Scratch& scratch,
-                    StageClock* clock, int bucket_k) {
+                    StageClock* clock) {
   cudaStream_t st = scratch.stream();
   const int64_t m = src.count;
   BuiltBvh out;
@@ -400,11 +380,6 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     note_launch(), k_refit<D><<<grid_for(m / 2 + 1, 256, INT32_MAX), 256, 0, st>>>(
         starts, arrivals + (m - 1), out.tree.nodes, out.node_info, arrivals);
   }
-  if (bucket_k > 0) {
-    out.bucket = scratch.alloc_n<int32_t>(m);
-    note_launch(), k_buckets<<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
-        out.node_info, out.leaf_up, m, bucket_k, out.bucket);
-  }
   TCB_CUDA(cudaGetLastError());
   return out;
 }
@@ -447,16 +422,16 @@ template void launch_point_bounds<3>(const float*, int64_t, DevCounters*, cudaSt
 
 template <int D>
 BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
-                   Scratch& scratch, StageClock* clock, int bucket_k) {
+                   Scratch& scratch, StageClock* clock) {
   if (src.coords) {
     PointBoxes<D> b{src.coords};
-    return build_impl<D>(b, src, validate_finite, true, d_ctr, scratch, clock, bucket_k);
+    return build_impl<D>(b, src, validate_finite, true, d_ctr, scratch, clock);
   }
   ExplicitBoxes<D> b{src.lo, src.hi};
-  return build_impl<D>(b, src, validate_finite, false, d_ctr, scratch, clock, bucket_k);
+  return build_impl<D>(b, src, validate_finite, false, d_ctr, scratch, clock);
 }
 
-template BuiltBvh build_bvh<2>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*, int);
-template BuiltBvh build_bvh<3>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*, int);
+template BuiltBvh build_bvh<2>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*);
+template BuiltBvh build_bvh<3>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*);
 
 }  // namespace tcb

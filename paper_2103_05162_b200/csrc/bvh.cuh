@@ -145,31 +145,6 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
 }
 
 // ---------------------------------------------------------------------------
-// Bottom-up masked traversal with Morton-cell early termination (main pass).
-//
-// The masked query of leaf r must find every leaf of rank > r within the
-// ball. Those leaves are exactly the right siblings of r's ancestors (where
-// r's path turns left), so instead of descending from the root (~35 levels for
-// 37M leaves, before any neighbour is met) the query climbs from its own leaf
-// and explores only right siblings whose box meets the ball.
-//
-// It stops climbing at the first ancestor A whose Morton cell contains the
-// ball: a Karras node is a binary radix-tree node, so its subtree holds
-// exactly the primitives whose codes share its prefix (node_info delta), i.e.
-// whose centroid quantizes into A's cell. A primitive outside A therefore has
-// its centroid outside the cell, hence farther than `reach` from p when the
-// reach-ball lies inside the cell (reach = eps + the largest primitive
-// half-diagonal: eps for points). The cell test runs in the integer
-// quantized space with the same monotone quantize() as the codes, on a ball
-// widened by relative margins, so it is conservative under rounding.
-//
-// Below `bucket` size the subtree is not descended at all: its leaves are a
-// contiguous run of the Morton-ordered leaf array and are scanned linearly.
-// The visit order differs from the reference's DFS; the main pass has no
-// early exit, so its pair set and counters are order independent.
-// ---------------------------------------------------------------------------
-
-// ---------------------------------------------------------------------------
 // Persistent, warp-refilled query driver.
 //
 // Per-query work varies by orders of magnitude (a point in a halo core has

@@ -57,6 +57,7 @@ struct CoreQuery {
   int count, top;
   __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &id);
+    id = static_cast<int32_t>(r);  // flags are kept in rank space
     count = 0;
     node = 0;
     top = 0;
@@ -95,30 +96,41 @@ template <int D, bool kForceCore>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-          DevCounters* ctr) {
+          const int32_t* __restrict__ key, DevCounters* ctr) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   unsigned long long pairs = 0;
   if (r < m) {
     float p[3];
-    int32_t i;
-    load_query<D>(leaf_pt, r, p, &i);
+    int32_t id;
+    load_query<D>(leaf_pt, r, p, &id);
     const int32_t rank = static_cast<int32_t>(r);
-    const bool core_i = kForceCore ? true : flags[i] != 0;
-    int32_t hint = i;
+    const bool core_r = kForceCore ? true : flags[rank] != 0;
+    int32_t hint = rank;
     bool settled = false;
-    auto visit = [&](int32_t s, int32_t j, const float*, const float*) -> bool {
+    auto visit = [&](int32_t s, int32_t, const float*, const float*) -> bool {
       if (s == rank) return true;
       ++pairs;
       if (kForceCore)
-        uf_unite_hinted(parent, i, j, hint);  // every pair is core-core (dbscan.hpp:85-89)
+        uf_unite_hinted_keyed(parent, key, rank, s, hint);  // all pairs core-core (dbscan.hpp:85-89)
       else
-        resolve_pair(i, j, core_i, flags, parent, hint, settled);
+        resolve_pair_keyed(rank, s, core_r, flags, parent, key, hint, settled);
       return true;
     };
     bvh_query<D>(nodes, p, bt, rank, visit);
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
+}
+
+__global__ void k_permute(const uint8_t* __restrict__ src, const int32_t* __restrict__ order,
+                          int64_t n, uint8_t* __restrict__ dst, bool to_rank) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (to_rank)
+      dst[r] = src[order[r]];
+    else
+      dst[order[r]] = src[r];
+  }
 }
 
 __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
@@ -142,6 +154,39 @@ k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_
     st_relaxed(parent + i, p);
     flags[i] = 1;
     if (!flags[p]) flags[p] = 1;
+  }
+}
+
+// Rank-space finalize (FDBSCAN): flatten over ranks; outputs scattered back
+// to input order through key[rank] = original index. The representative of a
+// set is its minimum-key rank, so label = key[root] = minimum original index.
+__global__ void __launch_bounds__(256)
+k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
+                 const int32_t* __restrict__ key, int64_t n, int32_t* __restrict__ labels,
+                 uint8_t* __restrict__ core_out, DevCounters* ctr) {
+  long long noise = 0, clusters = 0, cores = 0;
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t p = ld_relaxed(parent + s);
+    int32_t q;
+    while (p != (q = ld_relaxed(parent + p))) p = q;
+    st_relaxed(parent + s, p);
+    const bool core = flags[s] != 0;
+    const int32_t i = key[s];
+    const int32_t lab = (core || p != s) ? key[p] : -1;  // dbscan.cpp:215
+    labels[i] = lab;
+    core_out[i] = core ? 1 : 0;
+    noise += lab == -1;
+    clusters += lab == i;
+    cores += core;
+  }
+  noise = warp_sum(noise);
+  clusters = warp_sum(clusters);
+  cores = warp_sum(cores);
+  if ((threadIdx.x & 31) == 0) {
+    if (noise) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->noise), noise);
+    if (clusters) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->clusters), clusters);
+    if (cores) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->cores), cores);
   }
 }
 
@@ -190,7 +235,7 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
   const BallTest bt = BallTest::make(eps2);
   auto launch = [&](auto kernel) {
     note_launch(), kernel<<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, n, bt, flags, parent, d_ctr);
+        b.tree.nodes, b.leaf_pt, n, bt, flags, parent, b.tree.leaf_order, d_ctr);
   };
   if (force_core)
     launch(k_fd_main<D, true>);
@@ -199,9 +244,24 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
   TCB_CUDA(cudaGetLastError());
 }
 
+void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t* dst, bool to_rank,
+                   cudaStream_t s) {
+  note_launch(), k_permute<<<grid_for(n, 256), 256, 0, s>>>(src, order, n, dst, to_rank);
+  TCB_CUDA(cudaGetLastError());
+}
+
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
   note_launch(), k_init_uf<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
   TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(n), s));
+  TCB_CUDA(cudaGetLastError());
+}
+
+void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key, int64_t n,
+                           int32_t* labels, uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
+                           bool force_core) {
+  if (force_core) note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
+  note_launch(), k_finalize_ranks<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, key, n, labels,
+                                                                   core_out, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 

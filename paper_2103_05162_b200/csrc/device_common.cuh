@@ -172,6 +172,36 @@ __device__ __forceinline__ void uf_unite_hinted(int32_t* parent, int32_t i, int3
   hint = uf_unite(parent, i, j);
 }
 
+// ---- rank-space variant ---------------------------------------------------
+// FDBSCAN runs its union-find over LEAF RANKS (Morton order), so a query's
+// neighbours — ranks close to its own — have their parent entries in the same
+// or nearby cache lines (L1 hits instead of scattered L2 traffic on an array
+// indexed by input order). Roots are still chosen by the ORIGINAL index:
+// key[rank] = original index, and the higher-key root is hooked under the
+// lower-key one, so every representative is the minimum original index of its
+// set — the reference's labels (union_find.hpp:51-64).
+__device__ __forceinline__ int32_t uf_unite_keyed(int32_t* parent, const int32_t* __restrict__ key,
+                                                  int32_t a, int32_t b) {
+  while (true) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return a;
+    if (__ldg(key + a) > __ldg(key + b)) {
+      int32_t t = a;
+      a = b;
+      b = t;
+    }
+    if (atomicCAS(parent + b, b, a) == b) return a;
+  }
+}
+
+__device__ __forceinline__ void uf_unite_hinted_keyed(int32_t* parent, const int32_t* key,
+                                                      int32_t a, int32_t b, int32_t& hint) {
+  const int32_t pb = ld_relaxed(parent + b);
+  if (pb == hint || b == hint) return;
+  hint = uf_unite_keyed(parent, key, a, b);
+}
+
 // One-shot border claim (union_find.hpp:69-73).
 __device__ __forceinline__ bool uf_claim(int32_t* parent, int32_t i, int32_t root) {
   return atomicCAS(parent + i, i, root) == i;
@@ -199,6 +229,23 @@ __device__ __forceinline__ void resolve_pair(int32_t i, int32_t j, bool core_i,
   } else if (!i_settled && flags[j]) {
     if (ld_relaxed(parent + i) == i) uf_claim(parent, i, uf_find(parent, j));
     i_settled = true;  // claimed now, or by someone else before
+  }
+}
+
+// resolve_pair in rank space (see uf_unite_keyed); a, b and flags are ranks.
+__device__ __forceinline__ void resolve_pair_keyed(int32_t a, int32_t b, bool core_a,
+                                                   const uint8_t* flags, int32_t* parent,
+                                                   const int32_t* key, int32_t& hint,
+                                                   bool& a_settled) {
+  if (core_a) {
+    if (flags[b]) {
+      uf_unite_hinted_keyed(parent, key, a, b, hint);
+    } else if (ld_relaxed(parent + b) == b) {
+      uf_claim(parent, b, hint);
+    }
+  } else if (!a_settled && flags[b]) {
+    if (ld_relaxed(parent + a) == a) uf_claim(parent, a, uf_find(parent, b));
+    a_settled = true;
   }
 }
 

@@ -117,14 +117,6 @@ int query_mode() {
   return mode;
 }
 
-int main_kernel_variant() {
-  static const int v = [] {
-    const char* s = std::getenv("TCB_MAIN_KERNEL");
-    return (s && std::string(s) == "warp") ? 1 : 0;
-  }();
-  return v;
-}
-
 void set_last_stage_ms(const double* ms) {
   for (int s = 0; s < kNumStages; ++s) t_last_stage_ms[s] = ms[s];
 }
@@ -149,8 +141,7 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   src.coords = d_coords;
   src.count = n;
   clock.mark(kStBounds);
-  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock,
-                            main_kernel_variant() == 1 ? kMainBucket : 0);
+  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock);
 
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
@@ -158,12 +149,10 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   init_union_find(parent, flags, n, st);
   if (minpts > 2) fdbscan_core_pass<D>(b, n, eps2, minpts, flags, ctr, st);
   clock.mark(kStMain);
-  if (main_kernel_variant() == 1)
-    fdbscan_main_pass_warp<D>(b, n, eps2, minpts == 2, flags, parent, ctr, scratch);
-  else
-    fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, st);
+  fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, st);
   clock.mark(kStFinal);
-  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st, minpts == 2);
+  finalize_labels_ranks(parent, flags, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
+                        minpts == 2);
   clock.finish();
 }
 

@@ -90,7 +90,6 @@ struct BuiltBvh {
   // (kNoParent at the root), common prefix length of its codes, lo, hi rank}
   int4* node_info = nullptr;
   int32_t* leaf_up = nullptr;         // leaf rank -> parent | kUpLeftBit
-  int32_t* bucket = nullptr;          // leaf rank -> its bucket (see k_buckets) or null
   const uint32_t* scene_ord = nullptr;  // Morton scene box (order-preserving bits, 6)
   int sort_passes = 0;
 };
@@ -98,17 +97,16 @@ struct BuiltBvh {
 // Builds the LBVH of bvh.cpp:10-124 (scene bounds over centroids, Morton,
 // stable (code, index) sort, Karras topology, refit). Checks the points for
 // non-finite coordinates when validate_finite (throws InvalidArgument).
-// bucket_k > 0 also computes the per-leaf buckets of <= bucket_k leaves.
 template <int D>
 BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
-                   Scratch& scratch, StageClock* clock, int bucket_k = 0);
+                   Scratch& scratch, StageClock* clock);
 
 // Raw point bounds into d_ctr->bounds_ord + finiteness flag (resets both).
 template <int D>
 void launch_point_bounds(const float* coords, int64_t n, DevCounters* d_ctr, cudaStream_t s);
 
 // ---- traversal / finalize (dbscan.cu) ----
-constexpr int kMainBucket = 32;  // leaves per bucket (a warp's worth) in the main pass
+// FDBSCAN core pass / main pass: flags and parent are indexed by LEAF RANK.
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s);
@@ -116,14 +114,15 @@ template <int D>
 void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        cudaStream_t s);
-// Warp-per-bucket main pass (main_warp.cu); needs the build's buckets.
-template <int D>
-void fdbscan_main_pass_warp(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
-                            uint8_t* flags, int32_t* parent, DevCounters* d_ctr, Scratch& scratch);
-// Main-pass variant: 0 = thread per point, top-down (default), 1 = warp per
-// bucket (experimental, TCB_MAIN_KERNEL=warp).
-int main_kernel_variant();
+// Moves per-point bytes between input order and leaf-rank order:
+// to_rank: dst[r] = src[order[r]]; else dst[order[r]] = src[r].
+void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t* dst,
+                   bool to_rank, cudaStream_t s);
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
+// FDBSCAN: parent / flags indexed by leaf rank, key[rank] = original index.
+void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key, int64_t n,
+                           int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
+                           cudaStream_t s, bool force_core);
 // force_core (minpts == 2): core flags are derived here from the union-find
 // structure instead of being stored per pair in the main pass.
 void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,

@@ -112,9 +112,11 @@ void core_flags(const float* d_coords, int64_t n, float eps, int minpts, uint8_t
   src.coords = d_coords;
   src.count = n;
   BuiltBvh b = build_bvh<D>(src, true, ctr, scratch, nullptr);
-  TCB_CUDA(cudaMemsetAsync(d_core, 0, static_cast<size_t>(n), st));
+  uint8_t* flags = scratch.alloc_n<uint8_t>(n);  // rank space
+  TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(n), st));
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
-  fdbscan_core_pass<D>(b, n, eps2, minpts, d_core, ctr, st);
+  fdbscan_core_pass<D>(b, n, eps2, minpts, flags, ctr, st);
+  permute_flags(flags, b.tree.leaf_order, n, d_core, /*to_rank=*/false, st);
 }
 
 template <int D>
@@ -130,10 +132,11 @@ void given_core(const float* d_coords, int64_t n, float eps, const uint8_t* d_co
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
   init_union_find(parent, flags, n, st);
-  TCB_CUDA(cudaMemcpyAsync(flags, d_core_in, static_cast<size_t>(n), cudaMemcpyDeviceToDevice, st));
+  permute_flags(d_core_in, b.tree.leaf_order, n, flags, /*to_rank=*/true, st);
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
   fdbscan_main_pass<D>(b, n, eps2, /*force_core=*/false, flags, parent, ctr, st);
-  finalize_labels(parent, flags, n, d_labels, d_core_out, ctr, st, /*force_core=*/false);
+  finalize_labels_ranks(parent, flags, b.tree.leaf_order, n, d_labels, d_core_out, ctr, st,
+                        /*force_core=*/false);
   if (stats) {
     DevCounters h;
     TCB_CUDA(cudaMemcpyAsync(&h, ctr, sizeof h, cudaMemcpyDeviceToHost, st));
