@@ -1,21 +1,13 @@
-// LSD radix sort (8-bit digits, reduce-then-scan) and exclusive scan.
-//
-// Per sorted digit window:
-//   k_sort_upsweep    per-tile digit histogram, warp-aggregated with
-//                     __match_any_sync (Morton digits are heavily skewed in
-//                     clustered data, so plain shared atomics would serialize)
-//   k_sort_scan_rows  one CTA per digit scans that digit's row of tile counts
-//                     (digit-major layout -> global offsets) and its total
-//   k_sort_downsweep  stable in-tile ranking (match_any + per-warp counters),
-//                     staging through shared memory so the global writes are
-//                     contiguous runs per digit
-// Constant digit windows (AND == OR over all keys) are skipped entirely.
+// LSD radix sort (8-bit digits, Onesweep-style single pass per digit window
+// with decoupled look-back) and a device-wide exclusive scan. Constant digit
+// windows (AND == OR over all keys) are skipped entirely.
 #include "primitives.cuh"
 
 #include <algorithm>
 
 #include "device_common.cuh"
 #include "engine.hpp"
+#include "pipeline.hpp"
 
 namespace tcb {
 
@@ -25,7 +17,8 @@ constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / kWarp;
 constexpr int kIPT = 16;
 constexpr int kTile = kSortThreads * kIPT;  // 4096 keys per tile
-constexpr int kRadix = 256;
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -63,112 +56,114 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* smem_w
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Onesweep LSD radix sort (one kernel per digit window, decoupled look-back).
+//
+//   k_sort_hist      ONE read of the keys: the global histogram of every
+//                    digit window that will be sorted (block-private shared
+//                    histograms, one global atomic per bin per block)
+//   k_sort_onesweep  per digit window: a tile grabs its id from a counter (so
+//                    look-back only ever waits on tiles already running),
+//                    ranks its keys stably (__match_any_sync + per-warp
+//                    counters), publishes its digit counts, looks back over
+//                    the predecessors' published counts (flag + 30-bit count
+//                    in one word: no fence needed) for its exclusive offsets,
+//                    and scatters through shared memory so the global writes
+//                    are contiguous runs per digit.
+// Per key and window: 12 B read + 12 B written (the reduce-then-scan scheme
+// it replaces also re-read the keys for a separate histogram pass).
+// ---------------------------------------------------------------------------
+constexpr int kMaxPasses = 8;
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kCountMask = (1u << 30) - 1;
+
+struct PassShifts {
+  int shift[kMaxPasses];
+  int count;
+};
+
 __global__ void __launch_bounds__(kSortThreads)
-k_sort_upsweep(const uint64_t* __restrict__ keys, int64_t n, int shift,
-               uint32_t* __restrict__ tile_hist, int num_tiles) {
-  __shared__ uint32_t h[kRadix];
-  for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
+k_sort_hist(const uint64_t* __restrict__ keys, int64_t n, PassShifts ps,
+            uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kSortThreads) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + w * (kIPT * 32);
-  uint64_t k[kIPT];
-#pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
-    int64_t idx = base + j * 32 + lane;
-    k[j] = idx < n ? __ldcs(keys + idx) : 0;
-  }
-#pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
-    int64_t idx = base + j * 32 + lane;
-    uint32_t mask = __ballot_sync(0xffffffffu, idx < n);
-    if (idx < n) {
-      uint32_t d = static_cast<uint32_t>(k[j] >> shift) & (kRadix - 1);
-      uint32_t peers = __match_any_sync(mask, d);
-      if ((peers & lanemask_lt()) == 0) atomicAdd(&h[d], __popc(peers));
-    }
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = __ldcs(keys + i);
+    for (int p = 0; p < ps.count; ++p)
+      atomicAdd(&h[p][static_cast<uint32_t>(k >> ps.shift[p]) & (kRadix - 1)], 1u);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRadix; d += kSortThreads)
-    tile_hist[static_cast<int64_t>(d) * num_tiles + blockIdx.x] = h[d];
-}
-
-constexpr int kScanRowThreads = 1024;
-
-// One CTA per digit: exclusive scan of tile counts along the row, row total
-// into totals[d].
-__global__ void __launch_bounds__(kScanRowThreads)
-k_sort_scan_rows(uint32_t* __restrict__ tile_hist, int num_tiles,
-                 uint32_t* __restrict__ totals) {
-  __shared__ uint32_t warp_tot[32];
-  uint32_t* row = tile_hist + static_cast<int64_t>(blockIdx.x) * num_tiles;
-  uint32_t running = 0;
-  for (int base = 0; base < num_tiles; base += kScanRowThreads * 4) {
-    uint32_t v[4];
-    uint32_t s = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int i = base + threadIdx.x * 4 + q;
-      v[q] = i < num_tiles ? row[i] : 0;
-      s += v[q];
-    }
-    uint32_t tot;
-    uint32_t pre = block_excl_scan<kScanRowThreads>(s, warp_tot, &tot);
-    pre += running;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int i = base + threadIdx.x * 4 + q;
-      if (i < num_tiles) row[i] = pre;
-      pre += v[q];
-    }
-    running += tot;
+  for (int i = threadIdx.x; i < ps.count * kRadix; i += kSortThreads) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(ghist + i, v);
   }
-  if (threadIdx.x == 0) totals[blockIdx.x] = running;
 }
 
-struct DownsweepSmem {
+struct OnesweepSmem {
   uint64_t keys[kTile];
   int32_t vals[kTile];
   uint32_t wcnt[kSortWarps][kRadix];
   uint32_t tile_start[kRadix];
   uint32_t global_start[kRadix];
   uint32_t warp_tot[32];
+  int tile;
 };
 
-__global__ void __launch_bounds__(kSortThreads)
-k_sort_downsweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
-                 uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out,
-                 int64_t n, int shift, const uint32_t* __restrict__ tile_hist,
-                 const uint32_t* __restrict__ totals, int num_tiles) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  DownsweepSmem& S = *reinterpret_cast<DownsweepSmem*>(smem_raw);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads)
-    (&S.wcnt[0][0])[i] = 0;
+__device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
-  const int64_t tile_base = static_cast<int64_t>(blockIdx.x) * kTile;
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
+                uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, int64_t n,
+                int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
+                uint32_t* __restrict__ tile_counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) S.tile = static_cast<int>(atomicAdd(tile_counter, 1u));
+  for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const int tile = S.tile;
+
+  const int64_t tile_base = static_cast<int64_t>(tile) * kTile;
   const int64_t base = tile_base + w * (kIPT * 32);
   uint64_t k[kIPT];
   int32_t v[kIPT];
 #pragma unroll
   for (int j = 0; j < kIPT; ++j) {
-    int64_t idx = base + j * 32 + lane;
+    const int64_t idx = base + j * 32 + lane;
     if (idx < n) {
       k[j] = __ldcs(keys_in + idx);
       v[j] = __ldcs(vals_in + idx);
     }
   }
-  __syncthreads();
 
   uint32_t rank[kIPT];
 #pragma unroll
   for (int j = 0; j < kIPT; ++j) {
-    int64_t idx = base + j * 32 + lane;
-    uint32_t mask = __ballot_sync(0xffffffffu, idx < n);
+    const int64_t idx = base + j * 32 + lane;
+    const uint32_t mask = __ballot_sync(0xffffffffu, idx < n);
     rank[j] = 0;
+    const uint32_t d = static_cast<uint32_t>(k[j] >> shift) & (kRadix - 1);
+    // peers = lanes with the same digit: 8 ballots (one per digit bit)
+    // instead of __match_any_sync, which is the slow part of the ranking
+    uint32_t peers = mask;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+      const uint32_t bit = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bit : ~bit;
+    }
     if (idx < n) {
-      uint32_t d = static_cast<uint32_t>(k[j] >> shift) & (kRadix - 1);
-      uint32_t peers = __match_any_sync(mask, d);
-      uint32_t before = S.wcnt[w][d];
+      const uint32_t before = S.wcnt[w][d];
       rank[j] = before + __popc(peers & lanemask_lt());
       __syncwarp(mask);
       if ((peers & lanemask_lt()) == 0) S.wcnt[w][d] = before + __popc(peers);
@@ -177,30 +172,38 @@ k_sort_downsweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict
   }
   __syncthreads();
 
-  // Per digit (thread d): exclusive prefix over warps, tile count.
+  // thread d owns digit d: warp prefix, tile count, publish, look back
+  const int d = threadIdx.x;  // kSortThreads == kRadix
   uint32_t tile_count = 0;
-  {
-    const int d = threadIdx.x;  // kSortThreads == kRadix
 #pragma unroll
-    for (int ww = 0; ww < kSortWarps; ++ww) {
-      uint32_t c = S.wcnt[ww][d];
-      S.wcnt[ww][d] = tile_count;
-      tile_count += c;
-    }
+  for (int ww = 0; ww < kSortWarps; ++ww) {
+    const uint32_t c = S.wcnt[ww][d];
+    S.wcnt[ww][d] = tile_count;
+    tile_count += c;
   }
-  uint32_t tstart = block_excl_scan<kSortThreads>(tile_count, S.warp_tot, nullptr);
-  uint32_t dstart = block_excl_scan<kSortThreads>(totals[threadIdx.x], S.warp_tot, nullptr);
-  S.tile_start[threadIdx.x] = tstart;
-  S.global_start[threadIdx.x] =
-      dstart + tile_hist[static_cast<int64_t>(threadIdx.x) * num_tiles + blockIdx.x];
+  uint32_t* my = status + static_cast<int64_t>(tile) * kRadix + d;
+  st_status(my, (tile == 0 ? kFlagInc : kFlagAgg) | tile_count);
+  uint32_t excl = 0;
+  for (int t = tile - 1; t >= 0;) {
+    const uint32_t s = ld_status(status + static_cast<int64_t>(t) * kRadix + d);
+    if ((s & ~kCountMask) == 0) continue;  // predecessor not published yet
+    excl += s & kCountMask;
+    if (s & kFlagInc) break;
+    --t;
+  }
+  if (tile > 0) st_status(my, kFlagInc | (excl + tile_count));
+  const uint32_t tstart = block_excl_scan<kSortThreads>(tile_count, S.warp_tot, nullptr);
+  const uint32_t dbase = block_excl_scan<kSortThreads>(ghist[d], S.warp_tot, nullptr);
+  S.tile_start[d] = tstart;
+  S.global_start[d] = dbase + excl;
   __syncthreads();
 
 #pragma unroll
   for (int j = 0; j < kIPT; ++j) {
-    int64_t idx = base + j * 32 + lane;
+    const int64_t idx = base + j * 32 + lane;
     if (idx < n) {
-      uint32_t d = static_cast<uint32_t>(k[j] >> shift) & (kRadix - 1);
-      uint32_t pos = S.tile_start[d] + S.wcnt[w][d] + rank[j];
+      const uint32_t dd = static_cast<uint32_t>(k[j] >> shift) & (kRadix - 1);
+      const uint32_t pos = S.tile_start[dd] + S.wcnt[w][dd] + rank[j];
       S.keys[pos] = k[j];
       S.vals[pos] = v[j];
     }
@@ -209,9 +212,9 @@ k_sort_downsweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict
 
   const int tile_n = static_cast<int>(n - tile_base < kTile ? n - tile_base : kTile);
   for (int p = threadIdx.x; p < tile_n; p += kSortThreads) {
-    uint64_t key = S.keys[p];
-    uint32_t d = static_cast<uint32_t>(key >> shift) & (kRadix - 1);
-    uint32_t out = S.global_start[d] + (p - S.tile_start[d]);
+    const uint64_t key = S.keys[p];
+    const uint32_t dd = static_cast<uint32_t>(key >> shift) & (kRadix - 1);
+    const uint32_t out = S.global_start[dd] + (p - S.tile_start[dd]);
     keys_out[out] = key;
     vals_out[out] = S.vals[p];
   }
@@ -278,41 +281,45 @@ int64_t num_sort_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 }  // namespace
 
 size_t radix_sort_scratch_bytes(int64_t n) {
-  int64_t t = num_sort_tiles(std::max<int64_t>(n, 1));
-  return static_cast<size_t>(t) * kRadix * sizeof(uint32_t) + kRadix * sizeof(uint32_t) + 256;
+  const int64_t t = num_sort_tiles(std::max<int64_t>(n, 1));
+  // status words (tiles x radix) + per-pass tile counters + global histograms
+  return static_cast<size_t>(t) * kRadix * sizeof(uint32_t) + 64 * sizeof(uint32_t) +
+         kMaxPasses * kRadix * sizeof(uint32_t) + 256;
 }
 
 bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
                       int32_t* vals_alt, int64_t n, uint64_t and_all,
                       uint64_t or_all, void* scratch, cudaStream_t stream,
                       int* passes_run) {
-  int passes = 0;
+  PassShifts ps{};
+  const uint64_t varying = and_all ^ or_all;
+  for (int shift = 0; shift < 64; shift += kRadixBits)
+    if ((varying >> shift) & (kRadix - 1)) ps.shift[ps.count++] = shift;  // skip constant windows
   bool in_alt = false;
-  if (n > 1) {
-    const int num_tiles = static_cast<int>(num_sort_tiles(n));
-    uint32_t* tile_hist = static_cast<uint32_t*>(scratch);
-    uint32_t* totals = tile_hist + static_cast<int64_t>(num_tiles) * kRadix;
-    TCB_CUDA(cudaFuncSetAttribute(k_sort_downsweep,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(DownsweepSmem))));
-    const uint64_t varying = and_all ^ or_all;
-    for (int shift = 0; shift < 64; shift += 8) {
-      if (((varying >> shift) & 0xffull) == 0) continue;  // constant digit window
+  if (n > 1 && ps.count > 0) {
+    const int64_t num_tiles = num_sort_tiles(n);
+    uint32_t* status = static_cast<uint32_t*>(scratch);
+    uint32_t* counters = status + num_tiles * kRadix;
+    uint32_t* ghist = counters + 64;
+    TCB_CUDA(cudaMemsetAsync(counters, 0, (64 + kMaxPasses * kRadix) * sizeof(uint32_t), stream));
+    note_launch(), k_sort_hist<<<grid_for(n, kSortThreads, 148 * 4), kSortThreads, 0, stream>>>(
+        keys, n, ps, ghist);
+    TCB_CUDA(cudaFuncSetAttribute(k_sort_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(OnesweepSmem))));
+    for (int p = 0; p < ps.count; ++p) {
       const uint64_t* kin = in_alt ? keys_alt : keys;
       const int32_t* vin = in_alt ? vals_alt : vals;
       uint64_t* kout = in_alt ? keys : keys_alt;
       int32_t* vout = in_alt ? vals : vals_alt;
-      note_launch(), k_sort_upsweep<<<num_tiles, kSortThreads, 0, stream>>>(kin, n, shift, tile_hist,
-                                                             num_tiles);
-      note_launch(), k_sort_scan_rows<<<kRadix, kScanRowThreads, 0, stream>>>(tile_hist, num_tiles, totals);
-      note_launch(), k_sort_downsweep<<<num_tiles, kSortThreads, sizeof(DownsweepSmem), stream>>>(
-          kin, vin, kout, vout, n, shift, tile_hist, totals, num_tiles);
+      TCB_CUDA(cudaMemsetAsync(status, 0, num_tiles * kRadix * sizeof(uint32_t), stream));
+      note_launch(), k_sort_onesweep<<<static_cast<unsigned>(num_tiles), kSortThreads,
+                                       sizeof(OnesweepSmem), stream>>>(
+          kin, vin, kout, vout, n, ps.shift[p], ghist + p * kRadix, status, counters + p);
       TCB_CUDA(cudaGetLastError());
       in_alt = !in_alt;
-      ++passes;
     }
   }
-  if (passes_run) *passes_run = passes;
+  if (passes_run) *passes_run = n > 1 ? ps.count : 0;
   return in_alt;
 }
 
