@@ -141,13 +141,34 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
   return 64 + __clz(static_cast<int>(static_cast<uint32_t>(i) ^ static_cast<uint32_t>(j)));
 }
 
+// Leaves in Morton rank order (bvh.cpp:34-39): leaf_lo[s] / leaf_hi[s] =
+// box of primitive order[s]; in points mode both alias one array whose w
+// component carries the point id (the query points of the traversals).
 template <int D, class Src>
 __global__ void __launch_bounds__(256)
-k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
+k_gather_leaves(Src src, const int32_t* __restrict__ order, int64_t m, float4* __restrict__ leaf_lo,
+                float4* __restrict__ leaf_hi) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t prim = order[s];
+    float lo[3], hi[3];
+    src.box(prim, lo, hi);
+    leaf_lo[s] = make_float4(lo[0], lo[1], D == 3 ? lo[2] : 0.f, __int_as_float(prim));
+    if (leaf_hi != leaf_lo) leaf_hi[s] = make_float4(hi[0], hi[1], D == 3 ? hi[2] : 0.f, 0.f);
+  }
+}
+
+// Subtrees of at most kDirectRange leaves get their boxes straight from the
+// contiguous leaf run (k_small_boxes); only larger nodes are refit bottom-up.
+constexpr int kDirectRange = 32;
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_karras(const float4* __restrict__ leaf_lo, const float4* __restrict__ leaf_hi,
+         const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
          const int32_t* __restrict__ prim_aux, int64_t m, float4* __restrict__ nodes,
          int4* __restrict__ node_info, int32_t* __restrict__ leaf_up,
-         float4* __restrict__ leaf_pt, int32_t* __restrict__ starts,
-         int32_t* __restrict__ num_starts) {
+         int32_t* __restrict__ starts, int32_t* __restrict__ num_starts) {
   using T = NodeTraits<D>;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= m - 1) return;
@@ -175,8 +196,8 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
     link = ~static_cast<int32_t>(rank);
     const int32_t prim = order[rank];
     aux = prim_aux ? prim_aux[prim] : prim;
-    float blo[3], bhi[3];
-    src.box(prim, blo, bhi);
+    const float4 a = leaf_lo[rank], c = leaf_hi[rank];
+    const float blo[3] = {a.x, a.y, a.z}, bhi[3] = {c.x, c.y, c.z};
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       f[slot * 2 * D + k] = blo[k];
@@ -209,8 +230,10 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
   }
   *reinterpret_cast<int4*>(f + T::kIntOff) = make_int4(left, right, aux_l, aux_r);
   if (i == 0) node_info[0].x = kNoParent;
-  // refit climbers start at the nodes with two leaf children
-  const bool start = left < 0 && right < 0;
+  // refit climbers start at the large nodes whose two children are leaves or
+  // small subtrees (both slots are complete before k_refit runs)
+  const bool start = (hi - lo + 1 > kDirectRange) && (gamma - lo + 1 <= kDirectRange) &&
+                     (hi - gamma <= kDirectRange);
   const uint32_t mask = __ballot_sync(__activemask(), start);
   if (mask) {
     const int leader = __ffs(mask) - 1;
@@ -219,22 +242,44 @@ k_karras(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict_
     base = __shfl_sync(__activemask(), base, leader);
     if (start) starts[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = static_cast<int32_t>(i);
   }
-  if (leaf_pt) {  // Morton-ordered query points (x, y, z, id)
-    auto emit = [&](int64_t rank) {
-      const int32_t prim = order[rank];
-      float blo[3], bhi[3];
-      src.box(prim, blo, bhi);
-      leaf_pt[rank] = make_float4(blo[0], blo[1], D == 3 ? blo[2] : 0.f, __int_as_float(prim));
-    };
-    emit(i);
-    if (i == m - 2) emit(m - 1);
+}
+
+// Box of every non-root internal node with <= kDirectRange leaves, reduced
+// directly over its contiguous leaf run, into its slot of the parent.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_small_boxes(const float4* __restrict__ leaf_lo, const float4* __restrict__ leaf_hi,
+              const int4* __restrict__ node_info, int64_t m, float4* __restrict__ nodes) {
+  using T = NodeTraits<D>;
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x + 1; c < m - 1;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int4 info = node_info[c];
+    if (info.w - info.z + 1 > kDirectRange) continue;
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int32_t s = info.z; s <= info.w; ++s) {
+      const float4 a = __ldg(leaf_lo + s), b = __ldg(leaf_hi + s);
+      lo[0] = fminf(lo[0], a.x);
+      lo[1] = fminf(lo[1], a.y);
+      lo[2] = fminf(lo[2], a.z);
+      hi[0] = fmaxf(hi[0], b.x);
+      hi[1] = fmaxf(hi[1], b.y);
+      hi[2] = fmaxf(hi[2], b.z);
+    }
+    float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(up_parent(info.x)) * T::kVec);
+    float* slot = pf + (up_is_left(info.x) ? 0 : 2 * D);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      slot[k] = lo[k];
+      slot[D + k] = hi[k];
+    }
   }
 }
 
-// Bottom-up refit (bvh.cpp:88-124). Climbers start at the nodes whose two
-// children are leaves (their slots were filled by k_karras, which also listed
-// them). A finished node writes its box (union of its two slots) into its slot
-// of the parent; if the sibling is a leaf the climber continues at once,
+// Bottom-up refit (bvh.cpp:88-124) of the nodes above kDirectRange leaves.
+// Climbers start at the large nodes whose children are leaves or small
+// subtrees (slots filled by k_karras / k_small_boxes, which run first; k_karras
+// lists them). A finished node writes its box (union of its two slots) into its
+// slot of the parent; if the sibling is a leaf or small the climber continues,
 // otherwise the two climbers meet at an arrival counter and the second one
 // continues. Only that meeting needs ordering: the writer's slot store must be
 // visible before its arrival (release fence, issued once per warp step for all
@@ -275,10 +320,15 @@ k_refit(const int32_t* __restrict__ starts, const int32_t* __restrict__ num_star
           __stcg(slot + D + k, hi[k]);
         }
         const int32_t sibling = is_left ? pl.y : pl.x;
-        if (sibling >= 0)
-          fence = true;  // meet the sibling's climber
+        bool ready = sibling < 0;  // a leaf: its slot is already in place
+        if (!ready) {
+          const int4 si = node_info[sibling];
+          ready = si.w - si.z + 1 <= kDirectRange;  // filled by k_small_boxes
+        }
+        if (ready)
+          c = p;
         else
-          c = p;  // sibling is a leaf: its slot is already in place
+          fence = true;  // meet the sibling's climber
       }
     }
     if (__any_sync(0xffffffffu, fence)) __threadfence();
@@ -374,9 +424,17 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     int32_t* starts = scratch.alloc_n<int32_t>(m / 2 + 1);
     TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * m, st));
     const unsigned gn = grid_for(m - 1, 256, INT32_MAX);
-    note_launch(), k_karras<D><<<gn, 256, 0, st>>>(boxes, codes, order, src.aux, m,
+    // sorted leaf boxes (points mode: the query points themselves)
+    float4* leaf_lo = points_mode ? leaf_pt : scratch.alloc_n<float4>(m);
+    float4* leaf_hi = points_mode ? leaf_pt : scratch.alloc_n<float4>(m);
+    note_launch(), k_gather_leaves<D><<<grid_for(m, 256), 256, 0, st>>>(boxes, order, m, leaf_lo,
+                                                                         leaf_hi);
+    note_launch(), k_karras<D><<<gn, 256, 0, st>>>(leaf_lo, leaf_hi, codes, order, src.aux, m,
                                                    out.tree.nodes, out.node_info, out.leaf_up,
-                                                   leaf_pt, starts, arrivals + (m - 1));
+                                                   starts, arrivals + (m - 1));
+    note_launch(), k_small_boxes<D><<<grid_for(m, 256), 256, 0, st>>>(leaf_lo, leaf_hi,
+                                                                       out.node_info, m,
+                                                                       out.tree.nodes);
     note_launch(), k_refit<D><<<grid_for(m / 2 + 1, 256, INT32_MAX), 256, 0, st>>>(
         starts, arrivals + (m - 1), out.tree.nodes, out.node_info, arrivals);
   }
