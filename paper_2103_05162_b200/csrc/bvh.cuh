@@ -78,6 +78,34 @@ __device__ __forceinline__ bool ball_hits(const float* p, const float* lo, const
   return box_dist2<D>(p, lo, hi) <= bt.r2;
 }
 
+// True when EVERY point of the closed box [lo, hi] is within the ball, by the
+// same exact fp64 predicate: per axis the farthest box coordinate is at least
+// as far as any member (rounding is monotone), so fl(maxdist^2) <= r2 implies
+// fl(dist^2) <= r2 for every member. fp32 guard-band fast path as ball_hits.
+template <int D>
+__device__ __forceinline__ bool box_inside_ball(const float* p, const float* lo, const float* hi,
+                                                const BallTest& bt) {
+  if (bt.fast) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float d = fmaxf(fabsf(__fsub_rn(p[k], lo[k])), fabsf(__fsub_rn(hi[k], p[k])));
+      s = __fadd_rn(s, __fmul_rn(d, d));
+    }
+    if (s < bt.lo_f) return true;
+    if (s > bt.hi_f) return false;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double a = fabs(__dsub_rn(static_cast<double>(p[k]), static_cast<double>(lo[k])));
+    double b = fabs(__dsub_rn(static_cast<double>(hi[k]), static_cast<double>(p[k])));
+    double d = a > b ? a : b;
+    s = __dadd_rn(s, __dmul_rn(d, d));
+  }
+  return s <= bt.r2;
+}
+
 // One traversal step of the closed-ball query (p, sqrt(r2)) that hides every
 // leaf with rank < min_rank (query_sphere_masked, bvh.hpp:45-72): processes
 // ONE node, calling

@@ -301,18 +301,27 @@ struct DbCoreQuery {
     return true;
   }
   __device__ bool step() {
-    auto visit = [&](int32_t, int32_t aux, const float*, const float*) -> bool {
+    auto visit = [&](int32_t, int32_t aux, const float* lo, const float* hi) -> bool {
       if (aux >= 0) {
         ++dists;
         ++count;  // leaf box test == exact distance test for a point leaf
       } else {
         const int32_t c = ~aux;
-        for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
-          const float4 m4 = __ldg(sorted_pt + k);
-          const float mp[3] = {m4.x, m4.y, m4.z};
-          ++dists;
-          if (ball_hits<D>(p, mp, mp, bt))
-            if (++count >= minpts) break;
+        const int32_t kb = cell_begin[c], ke = cell_end[c];
+        if (box_inside_ball<D>(p, lo, hi, bt)) {
+          // every member is within eps: the member-by-member loop would count
+          // and test exactly min(size, minpts - count) members
+          const int take = min(ke - kb, minpts - count);
+          dists += take;
+          count += take;
+        } else {
+          for (int32_t k = kb; k < ke; ++k) {
+            const float4 m4 = __ldg(sorted_pt + k);
+            const float mp[3] = {m4.x, m4.y, m4.z};
+            ++dists;
+            if (ball_hits<D>(p, mp, mp, bt))
+              if (++count >= minpts) break;
+          }
         }
       }
       return count < minpts;
@@ -367,20 +376,27 @@ struct DbMainQuery {
       resolve_pair(i, j, core_i, flags, parent, hint, settled);
   }
   __device__ bool step() {
-    auto visit = [&](int32_t s, int32_t aux, const float*, const float*) -> bool {
+    auto visit = [&](int32_t s, int32_t aux, const float* lo, const float* hi) -> bool {
       if (s == own) return true;
       if (aux >= 0) {
         ++dists;
         pair(aux);
       } else {
         const int32_t c = ~aux;
-        for (int32_t k = cell_begin[c], e = cell_end[c]; k < e; ++k) {
-          const float4 m4 = __ldg(sorted_pt + k);
-          const float mp[3] = {m4.x, m4.y, m4.z};
+        const int32_t kb = cell_begin[c], ke = cell_end[c];
+        if (box_inside_ball<D>(p, lo, hi, bt)) {
+          // every member is within eps: the scan stops at the first one
           ++dists;
-          if (ball_hits<D>(p, mp, mp, bt)) {
-            pair(__float_as_int(m4.w));
-            break;  // dbscan.cpp:183-193
+          pair(__float_as_int(__ldg(sorted_pt + kb).w));
+        } else {
+          for (int32_t k = kb; k < ke; ++k) {
+            const float4 m4 = __ldg(sorted_pt + k);
+            const float mp[3] = {m4.x, m4.y, m4.z};
+            ++dists;
+            if (ball_hits<D>(p, mp, mp, bt)) {
+              pair(__float_as_int(m4.w));
+              break;  // dbscan.cpp:183-193
+            }
           }
         }
       }
