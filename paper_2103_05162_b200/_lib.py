@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtreeclust_b200.so")
+LIB_PATH = os.environ.get("TCB_LIB_PATH") or os.path.join(_HERE, "libtreeclust_b200.so")
 
 
 class TcClusterStats(C.Structure):

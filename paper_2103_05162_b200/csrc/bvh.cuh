@@ -18,6 +18,7 @@
 // pseudo node whose right child is an empty (+inf/-inf) box that no ball hits.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -50,11 +51,14 @@ __host__ __device__ __forceinline__ bool up_is_left(int32_t x) { return x < 0; }
 // (1e-20 <= r2 <= 1e30), so the relative bound holds.
 struct BallTest {
   double r2;
+  double reach;      // per-axis bound on |q_k - p_k| of any q the predicate accepts
   float lo_f, hi_f;  // r2 * (1 -+ 2^-17) in fp32
   bool fast;
   __host__ static BallTest make(double eps2) {
     BallTest b;
     b.r2 = eps2;
+    // fl(sum of squares) <= r2 implies every |d_k| <= sqrt(r2) (1 + ~2^-52)
+    b.reach = std::sqrt(eps2) * (1.0 + 0x1.0p-30);
     b.fast = eps2 >= 1e-20 && eps2 <= 1e30;
     b.lo_f = static_cast<float>(eps2 * (1.0 - 0x1.0p-17));
     b.hi_f = static_cast<float>(eps2 * (1.0 + 0x1.0p-17));
@@ -159,6 +163,167 @@ __device__ __forceinline__ bool bvh_step(const float4* __restrict__ nodes, const
     node = stack[--top];
   }
   return true;
+}
+
+// Ball vs a child's box, with containment: 0 = miss, 1 = hit, 2 = the whole
+// box lies inside the ball, so every leaf of the subtree is within eps by the
+// exact predicate (see box_inside_ball). Hit / miss is exact (fp64 chain
+// inside the guard band); containment is only ever reported from the fp32
+// estimate outside the band, and conservatively answered "hit" inside it
+// (descending is always correct), so it needs no fp64 chain. For a leaf's
+// degenerate box any answer > 0 means "within eps". The fp32 estimates use
+// fused multiply-adds: one rounding per term instead of two, inside the same
+// error bound as the unfused chain the band was sized for.
+template <int D>
+__device__ __forceinline__ int ball_classify(const float* p, const float* lo, const float* hi,
+                                             const BallTest& bt) {
+  if (!bt.fast) return ball_hits<D>(p, lo, hi, bt) ? 1 : 0;
+  float sn = 0.f, sf = 0.f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float a = __fsub_rn(lo[k], p[k]);  // > 0: p below the box
+    const float b = __fsub_rn(p[k], hi[k]);  // > 0: p above the box
+    const float dn = fmaxf(fmaxf(a, b), 0.f);
+    const float df = fminf(a, b);            // -(farthest face distance)
+    sn = __fmaf_rn(dn, dn, sn);
+    sf = __fmaf_rn(df, df, sf);
+  }
+  if (sf < bt.lo_f) return 2;
+  if (sn < bt.lo_f) return 1;
+  if (sn > bt.hi_f) return 0;
+  return box_dist2<D>(p, lo, hi) <= bt.r2 ? 1 : 0;
+}
+
+// Traversal step with subtree containment. Also tracks `nlo`, the first leaf
+// rank of the current node (Karras ranges: a node's left child covers
+// [lo, split], its right child [split + 1, hi]; the root covers [0, n-1]), so
+// that a contained internal child is reported as its unmasked leaf-rank range
+// instead of being walked:
+//     bool visit(int32_t rank, int32_t aux)      leaf `rank` is within eps
+//     bool inside(int32_t first, int32_t last)   every rank in [first, last]
+//                                                  (first >= min_rank) is a hit
+// (false = stop the query). Both children are classified with the same
+// straight-line code (leaf or internal, masked or not) so the lanes of a warp
+// only diverge on the rare visit / inside actions. Children are masked at
+// min_rank like query_sphere_masked (bvh.hpp:45-72); the order in which
+// leaves are reported is not the reference's DFS order (callers only depend
+// on the set, or, for early exit, on the count — see CoreQuery).
+
+template <int D, typename Visit, typename Inside>
+__device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes, const float* p,
+                                                const BallTest& bt, int32_t min_rank,
+                                                int32_t& node, int32_t& nlo, int& top,
+                                                int2* stack, Visit& visit, Inside& inside) {
+  using T = NodeTraits<D>;
+  float f[T::kFloats];
+  const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
+#pragma unroll
+  for (int v = 0; v < T::kVec; ++v) {
+    float4 q = __ldg(src + v);
+    f[4 * v + 0] = q.x;
+    f[4 * v + 1] = q.y;
+    f[4 * v + 2] = q.z;
+    f[4 * v + 3] = q.w;
+  }
+  const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+  const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+  const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+  const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+  const bool leaf_l = left < 0, leaf_r = right < 0;
+  const int32_t split = leaf_l ? ~left : aux_l;  // last rank of the left child
+  const int32_t max_r = leaf_r ? ~right : aux_r;
+  const int32_t lo_l = nlo > min_rank ? nlo : min_rank;
+  const int32_t lo_r = split + 1 > min_rank ? split + 1 : min_rank;
+  int cl = ball_classify<D>(p, f, f + D, bt);
+  int cr = ball_classify<D>(p, f + 2 * D, f + 3 * D, bt);
+  if (split < min_rank) cl = 0;
+  if (max_r < min_rank) cr = 0;
+  if (cl > 0 && (leaf_l || cl == 2)) {
+    if (!(leaf_l ? visit(~left, aux_l) : inside(lo_l, aux_l))) return false;
+  }
+  if (cr > 0 && (leaf_r || cr == 2)) {
+    if (!(leaf_r ? visit(~right, aux_r) : inside(lo_r, aux_r))) return false;
+  }
+  const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
+  if (go_l && go_r) {
+    stack[top++] = make_int2(left, nlo);
+    node = right;
+    nlo = split + 1;
+  } else if (go_l) {
+    node = left;
+  } else if (go_r) {
+    node = right;
+    nlo = split + 1;
+  } else {
+    if (top == 0) return false;
+    const int2 e = stack[--top];
+    node = e.x;
+    nlo = e.y;
+  }
+  return true;
+}
+
+// Warp-shared descent to a common start node. The 32 queries of a warp are
+// Morton-consecutive leaves, so their top-down walks share a long prefix:
+// the path from the root to the smallest subtree that can hold a neighbour
+// of ANY of them. The warp walks that prefix once, uniformly: U = the box of
+// the lanes' query points grown by `reach` on every axis (directed rounding,
+// so U contains every point the exact predicate accepts for any lane); from
+// the root, while exactly one child of the node can matter (its box meets U
+// and its max rank >= the warp's min_rank) and that child is internal, step
+// into it. Nothing outside the stop node can be a hit for any lane, so each
+// lane's own traversal starts there (node, nlo) instead of at the root.
+// Every lane must call it (valid = false for lanes without a query).
+template <int D>
+__device__ __forceinline__ void warp_start_node(const float4* __restrict__ nodes, const float* p,
+                                                bool valid, const BallTest& bt,
+                                                int32_t min_rank, int32_t& node, int32_t& nlo) {
+  node = 0;
+  nlo = 0;
+  float ulo[3], uhi[3];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const uint32_t mn = __reduce_min_sync(0xffffffffu, valid ? f2ord(p[k]) : 0xffffffffu);
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, valid ? f2ord(p[k]) : 0u);
+    if (mn > mx) return;  // no lane has a query
+    ulo[k] = __double2float_rd(static_cast<double>(ord2f(mn)) - bt.reach);
+    uhi[k] = __double2float_ru(static_cast<double>(ord2f(mx)) + bt.reach);
+  }
+  min_rank = __reduce_min_sync(0xffffffffu, valid ? min_rank : INT32_MAX);
+  using T = NodeTraits<D>;
+  while (true) {
+    float f[T::kFloats];
+    const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
+#pragma unroll
+    for (int v = 0; v < T::kVec; ++v) {
+      float4 q = __ldg(src + v);
+      f[4 * v + 0] = q.x;
+      f[4 * v + 1] = q.y;
+      f[4 * v + 2] = q.z;
+      f[4 * v + 3] = q.w;
+    }
+    const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+    const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+    const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+    const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+    auto meets = [&](const float* lo, const float* hi) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < D; ++k) ok = ok && lo[k] <= uhi[k] && hi[k] >= ulo[k];
+      return ok;
+    };
+    const int32_t max_l = left < 0 ? ~left : aux_l, max_r = right < 0 ? ~right : aux_r;
+    const bool live_l = max_l >= min_rank && meets(f, f + D);
+    const bool live_r = max_r >= min_rank && meets(f + 2 * D, f + 3 * D);
+    if (live_l && !live_r && left >= 0) {
+      node = left;
+    } else if (live_r && !live_l && right >= 0) {
+      nlo = max_l + 1;
+      node = right;
+    } else {
+      return;
+    }
+  }
 }
 
 // The whole query on one thread.

@@ -42,7 +42,11 @@ __device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned 
 }
 
 // fdbscan_mark_cores query (dbscan.cpp:36-58): unmasked, early exit once
-// minpts neighbours (self included) are seen.
+// minpts neighbours (self included) are seen. A subtree whose box lies inside
+// the ball adds its leaf count at once; when that crosses minpts the
+// reference would have stopped inside it after exactly minpts - count more
+// leaf hits, so the distance counter (one per hit, dists == count) is still
+// the reference's.
 template <int D>
 struct CoreQuery {
   const float4* __restrict__ nodes;
@@ -50,25 +54,37 @@ struct CoreQuery {
   BallTest bt;
   int minpts;
   uint8_t* __restrict__ flags;
-  int32_t* stack;  // per-thread traversal stack, kept outside the struct
+  int2* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long dists = 0;
   float p[3];
-  int32_t id, node;
+  int32_t id, node, nlo;
   int count, top;
   __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &id);
     id = static_cast<int32_t>(r);  // flags are kept in rank space
     count = 0;
     node = 0;
+    nlo = 0;
     top = 0;
     return true;
   }
   __device__ bool step() {
-    auto visit = [&](int32_t, int32_t, const float*, const float*) -> bool {
+    auto visit = [&](int32_t, int32_t) -> bool {
       ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
-    return bvh_step<D>(nodes, p, bt, 0, node, top, stack, visit);
+    auto inside = [&](int32_t first, int32_t last) -> bool {
+      const int64_t k = static_cast<int64_t>(last) - first + 1;
+      if (count + k >= minpts) {
+        dists += static_cast<unsigned long long>(minpts - count);
+        count = minpts;
+        return false;
+      }
+      dists += static_cast<unsigned long long>(k);
+      count += static_cast<int>(k);
+      return true;
+    };
+    return bvh_step_ranged<D>(nodes, p, bt, 0, node, nlo, top, stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[id] = 1;
@@ -79,20 +95,32 @@ template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent) {
-  int32_t stack[kStackDepth];
+  int2 stack[kStackDepth];
   CoreQuery<D> q{nodes, leaf_pt, bt, minpts, flags, stack};
-  if (persistent)
+  if (persistent) {
     run_query_queue(m, &ctr->queue[0], q);
-  else
-    run_query_direct(m, q);
+  } else {
+    // one query per thread, started at the warp's common start node
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const bool valid = r < m;
+    if (valid) q.begin(r);
+    warp_start_node<D>(nodes, q.p, valid, bt, 0, q.node, q.nlo);
+    if (valid) {
+      while (q.step()) {
+      }
+      q.end();
+    }
+  }
   flush_counter(&ctr->dists, q.dists);
 }
 
 // fdbscan_main_phase (dbscan.cpp:60-88): one thread per leaf rank r (Morton
 // order, so a warp's queries are spatial neighbours walking nearly the same
-// nodes), top-down query masked at r so each unordered within-eps pair is met
+// nodes), top-down query masked at r + 1 (the reference masks at r and skips
+// the self leaf: the same pairs) so each unordered within-eps pair is met
 // exactly once, and resolved on the spot — no neighbour list is stored.
-template <int D, bool kForceCore>
+// minpts > 2 path: core flags are final, pairs resolve per dbscan.hpp:82-99.
+template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
@@ -104,22 +132,171 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
     int32_t id;
     load_query<D>(leaf_pt, r, p, &id);
     const int32_t rank = static_cast<int32_t>(r);
-    const bool core_r = kForceCore ? true : flags[rank] != 0;
+    const bool core_r = flags[rank] != 0;
     int32_t hint = rank;
     bool settled = false;
     auto visit = [&](int32_t s, int32_t, const float*, const float*) -> bool {
-      if (s == rank) return true;
       ++pairs;
-      if (kForceCore)
-        uf_unite_hinted_keyed(parent, key, rank, s, hint);  // all pairs core-core (dbscan.hpp:85-89)
-      else
-        resolve_pair_keyed(rank, s, core_r, flags, parent, key, hint, settled);
+      resolve_pair_keyed(rank, s, core_r, flags, parent, key, hint, settled);
       return true;
     };
-    bvh_query<D>(nodes, p, bt, rank, visit);
+    bvh_query<D>(nodes, p, bt, rank + 1, visit);
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
+}
+
+// minpts == 2 (friends-of-friends) main pass. Every within-eps pair is a
+// core-core union (dbscan.hpp:85-89), so a subtree whose whole box lies inside
+// the eps-ball needs no walk: all of its unmasked leaves [first, last] are
+// neighbours of r. The query unites r with `first` and records that the run
+// [first, last] must be connected (reach[first] = max(reach[first], last));
+// k_cover_* later unite every covered rank with its predecessor. Same final
+// partition as uniting r with each leaf (each leaf is joined to r through the
+// run); pairs counted per leaf, so pair_resolutions / distance_evaluations
+// stay exact.
+template <int D>
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+              BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
+              int32_t* __restrict__ reach, DevCounters* ctr) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  unsigned long long pairs = 0;
+  TCB_PROBE_ONLY(unsigned long long pr[7] = {};)
+  if (r < m) {
+    float p[3];
+    int32_t id;
+    load_query<D>(leaf_pt, r, p, &id);
+    const int32_t rank = static_cast<int32_t>(r);
+    int32_t hint = rank;
+    auto visit = [&](int32_t s, int32_t) -> bool {
+      ++pairs;
+      TCB_PROBE_ONLY(++pr[2];)
+      uf_unite_hinted_keyed(parent, key, rank, s, hint);
+      return true;
+    };
+    auto inside = [&](int32_t first, int32_t last) -> bool {
+      pairs += static_cast<unsigned long long>(last - first + 1);
+      TCB_PROBE_ONLY(++pr[1]; pr[4] += last - first + 1;)
+      uf_unite_hinted_keyed(parent, key, rank, first, hint);
+      if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
+      return true;
+    };
+    int2 stack[kStackDepth];
+    int top = 0;
+    int32_t node, nlo;
+    warp_start_node<D>(nodes, p, true, bt, rank + 1, node, nlo);
+    while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, top, stack, visit, inside)) {
+      TCB_PROBE_ONLY(++pr[0];)
+    }
+    TCB_PROBE_ONLY(++pr[0]; pr[5] += pairs == 0; pr[6] = pr[0]; if (pairs == 0) pr[3] = pr[0];)
+  } else {
+    float p[3] = {0.f, 0.f, 0.f};
+    int32_t node, nlo;
+    warp_start_node<D>(nodes, p, false, bt, 0, node, nlo);
+  }
+  flush_counter(&ctr->pairs, pairs);
+  flush_counter(&ctr->dists, pairs);
+  TCB_PROBE_ONLY(for (int k = 0; k < 6; ++k) flush_counter(&ctr->probe[k], pr[k]);
+                 const unsigned wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(pr[6]));
+                 if ((threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[6], wmax);
+                 const bool allz = __all_sync(0xffffffffu, pairs == 0);
+                 if (allz && (threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[7], wmax);)
+}
+
+// ---- covered runs: rank l joins l - 1 iff some recorded run [f, t] has
+// f < l <= t, i.e. iff max(reach[0 .. l-1]) >= l. A max-scan in three
+// kernels over tiles of kCoverTile ranks: tile maxima, a one-block scan of
+// those, then the tile-local scan that performs the unions.
+constexpr int kCoverThreads = 256;
+constexpr int kCoverItems = 8;
+constexpr int kCoverTile = kCoverThreads * kCoverItems;
+
+__device__ __forceinline__ void load_tile(const int32_t* __restrict__ reach, int64_t n,
+                                          int64_t base, int32_t* v) {
+  const int64_t i0 = base + threadIdx.x * kCoverItems;
+  if (i0 + kCoverItems <= n) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(reach + i0));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(reach + i0) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kCoverItems; ++k) v[k] = i0 + k < n ? reach[i0 + k] : -1;
+  }
+}
+
+__global__ void __launch_bounds__(kCoverThreads)
+k_cover_tiles(const int32_t* __restrict__ reach, int64_t n, int32_t* __restrict__ tile_max) {
+  __shared__ int32_t red[32];
+  int32_t v[kCoverItems];
+  load_tile(reach, n, blockIdx.x * static_cast<int64_t>(kCoverTile), v);
+  int32_t mx = v[0];
+#pragma unroll
+  for (int k = 1; k < kCoverItems; ++k) mx = max(mx, v[k]);
+  mx = block_reduce(mx, [](int32_t a, int32_t b) { return max(a, b); }, -1, red);
+  if (threadIdx.x == 0) tile_max[blockIdx.x] = mx;
+}
+
+// Exclusive max-scan of the tile maxima, one block (each thread a contiguous
+// chunk).
+__global__ void __launch_bounds__(1024)
+k_cover_carry(int32_t* __restrict__ tile_max, int64_t tiles) {
+  __shared__ int32_t part[1024];
+  const int64_t per = (tiles + blockDim.x - 1) / blockDim.x;
+  const int64_t b = threadIdx.x * per, e = min(b + per, tiles);
+  int32_t mx = -1;
+  for (int64_t t = b; t < e; ++t) mx = max(mx, tile_max[t]);
+  part[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
+    int32_t x = threadIdx.x >= static_cast<unsigned>(o) ? part[threadIdx.x - o] : -1;
+    __syncthreads();
+    part[threadIdx.x] = max(part[threadIdx.x], x);
+    __syncthreads();
+  }
+  int32_t run = threadIdx.x > 0 ? part[threadIdx.x - 1] : -1;
+  for (int64_t t = b; t < e; ++t) {
+    const int32_t x = tile_max[t];
+    tile_max[t] = run;
+    run = max(run, x);
+  }
+}
+
+__global__ void __launch_bounds__(kCoverThreads)
+k_cover_unite(const int32_t* __restrict__ reach, int64_t n, const int32_t* __restrict__ carry,
+              int32_t* __restrict__ parent, const int32_t* __restrict__ key) {
+  __shared__ int32_t warp_max[kCoverThreads / 32];
+  const int64_t base = blockIdx.x * static_cast<int64_t>(kCoverTile);
+  int32_t v[kCoverItems];
+  load_tile(reach, n, base, v);
+  int32_t mine = v[0];
+#pragma unroll
+  for (int k = 1; k < kCoverItems; ++k) mine = max(mine, v[k]);
+  // exclusive max over the threads before this one (warp scan + warp totals)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc = max(inc, x);
+  }
+  if (lane == 31) warp_max[w] = inc;
+  __syncthreads();
+  int32_t run = max(carry[blockIdx.x], __shfl_up_sync(0xffffffffu, inc, 1));
+  if (lane == 0) run = carry[blockIdx.x];
+  for (int k = 0; k < w; ++k) run = max(run, warp_max[k]);
+  const int64_t i0 = base + threadIdx.x * kCoverItems;
+#pragma unroll
+  for (int k = 0; k < kCoverItems; ++k) {
+    const int64_t l = i0 + k;
+    if (l < n && run >= l && l > 0) {
+      const int32_t a = static_cast<int32_t>(l);
+      const int32_t pa = ld_relaxed(parent + a), pb = ld_relaxed(parent + a - 1);
+      if (pa != pb && pa != a - 1 && pb != a) uf_unite_keyed(parent, key, a, a - 1);
+    }
+    run = max(run, v[k]);
+  }
 }
 
 __global__ void k_permute(const uint8_t* __restrict__ src, const int32_t* __restrict__ order,
@@ -231,16 +408,27 @@ void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
 template <int D>
 void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
-                       cudaStream_t s) {
+                       Scratch& scratch) {
+  cudaStream_t s = scratch.stream();
   const BallTest bt = BallTest::make(eps2);
-  auto launch = [&](auto kernel) {
-    note_launch(), kernel<<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, n, bt, flags, parent, b.tree.leaf_order, d_ctr);
-  };
-  if (force_core)
-    launch(k_fd_main<D, true>);
-  else
-    launch(k_fd_main<D, false>);
+  const unsigned grid = grid_for(n, kQueryBlock, INT32_MAX);
+  if (!force_core) {
+    note_launch(), k_fd_main<D><<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags,
+                                                             parent, b.tree.leaf_order, d_ctr);
+    TCB_CUDA(cudaGetLastError());
+    return;
+  }
+  int32_t* reach = scratch.alloc_n<int32_t>(n + kCoverItems);
+  const int64_t tiles = (n + kCoverTile - 1) / kCoverTile;
+  int32_t* tile_max = scratch.alloc_n<int32_t>(tiles);
+  TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
+  note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
+      b.tree.nodes, b.leaf_pt, n, bt, parent, b.tree.leaf_order, reach, d_ctr);
+  note_launch(), k_cover_tiles<<<static_cast<unsigned>(tiles), kCoverThreads, 0, s>>>(reach, n,
+                                                                                       tile_max);
+  note_launch(), k_cover_carry<<<1, 1024, 0, s>>>(tile_max, tiles);
+  note_launch(), k_cover_unite<<<static_cast<unsigned>(tiles), kCoverThreads, 0, s>>>(
+      reach, n, tile_max, parent, b.tree.leaf_order);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -277,8 +465,8 @@ template void fdbscan_core_pass<2>(const BuiltBvh&, int64_t, double, int, uint8_
 template void fdbscan_core_pass<3>(const BuiltBvh&, int64_t, double, int, uint8_t*,
                                    DevCounters*, cudaStream_t);
 template void fdbscan_main_pass<2>(const BuiltBvh&, int64_t, double, bool, uint8_t*,
-                                   int32_t*, DevCounters*, cudaStream_t);
+                                   int32_t*, DevCounters*, Scratch&);
 template void fdbscan_main_pass<3>(const BuiltBvh&, int64_t, double, bool, uint8_t*,
-                                   int32_t*, DevCounters*, cudaStream_t);
+                                   int32_t*, DevCounters*, Scratch&);
 
 }  // namespace tcb

@@ -121,6 +121,16 @@ __device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// CTA-scope relaxed load: may be served by this SM's L1, so it can return an
+// older value of the word. Only used where any value the word EVER held is
+// good enough (a union-find parent that equals a hint proves set membership
+// forever, because sets only merge; a stale coverage bound only costs an
+// extra atomic).
+__device__ __forceinline__ int32_t ld_cached(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.cta.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -197,7 +207,7 @@ __device__ __forceinline__ int32_t uf_unite_keyed(int32_t* parent, const int32_t
 
 __device__ __forceinline__ void uf_unite_hinted_keyed(int32_t* parent, const int32_t* key,
                                                       int32_t a, int32_t b, int32_t& hint) {
-  const int32_t pb = ld_relaxed(parent + b);
+  const int32_t pb = ld_cached(parent + b);  // any past parent of b is proof enough
   if (pb == hint || b == hint) return;
   hint = uf_unite_keyed(parent, key, a, b);
 }

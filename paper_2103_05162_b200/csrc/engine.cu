@@ -3,6 +3,7 @@
 // per-stage CUDA-event timing into tc_cluster_stats.
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -149,7 +150,7 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   init_union_find(parent, flags, n, st);
   if (minpts > 2) fdbscan_core_pass<D>(b, n, eps2, minpts, flags, ctr, st);
   clock.mark(kStMain);
-  fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, st);
+  fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, scratch);
   clock.mark(kStFinal);
   finalize_labels_ranks(parent, flags, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
                         minpts == 2);
@@ -235,6 +236,9 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
     s.cluster_count = h.clusters;
     s.core_count = h.cores;
     s.noise_count = h.noise;
+    TCB_PROBE_ONLY(std::fprintf(stderr, "[probe] %llu %llu %llu %llu %llu %llu %llu %llu\n",
+                                h.probe[0], h.probe[1], h.probe[2], h.probe[3], h.probe[4],
+                                h.probe[5], h.probe[6], h.probe[7]);)
     if (out) *out = ro;
   }
 }

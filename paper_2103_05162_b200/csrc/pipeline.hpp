@@ -26,7 +26,14 @@ struct DevCounters {
   int32_t count_b;
   int32_t pad;
   unsigned long long queue[4];  // chunk counters of the persistent query kernels
+  unsigned long long probe[8];  // -DTCB_PROBE builds only (make probe): work counters
 };
+
+#ifdef TCB_PROBE
+#define TCB_PROBE_ONLY(...) __VA_ARGS__
+#else
+#define TCB_PROBE_ONLY(...)
+#endif
 
 // Stream-ordered scratch allocations released at scope exit (cudaMallocAsync
 // on the default pool; the pool's release threshold is raised once so repeat
@@ -110,10 +117,12 @@ void launch_point_bounds(const float* coords, int64_t n, DevCounters* d_ctr, cud
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s);
+// force_core (minpts == 2) uses the contained-subtree pass (k_fd_main_fof) and
+// allocates its run-coverage scratch from `scratch`.
 template <int D>
 void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
                        uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
-                       cudaStream_t s);
+                       Scratch& scratch);
 // Moves per-point bytes between input order and leaf-rank order:
 // to_rank: dst[r] = src[order[r]]; else dst[order[r]] = src[r].
 void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t* dst,
