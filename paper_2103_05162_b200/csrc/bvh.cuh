@@ -32,7 +32,36 @@ struct NodeTraits {
   static constexpr int kIntOff = 4 * D;        // float index of the int4 part
 };
 
-constexpr int kStackDepth = 128;  // bvh.hpp:82-84 (keys are 64 + 32 bits)
+constexpr int kStackDepth = 128;
+
+// One node record into registers. 3D records (64 B, 32-byte aligned) take two
+// 256-bit loads (sm_100 LDG.256): half the load requests of float4 loads on
+// the L1 pipe that bounds the traversal. 2D records (48 B) are only 16-byte
+// aligned and keep three 128-bit loads.
+__device__ __forceinline__ void ld_nc_v8(const float* src, float* f) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]), "=f"(f[4]), "=f"(f[5]), "=f"(f[6]),
+        "=f"(f[7])
+      : "l"(src));
+}
+
+template <int D>
+__device__ __forceinline__ void load_node(const float4* __restrict__ src, float* f) {
+  if (D == 3) {
+    const float* s = reinterpret_cast<const float*>(src);
+    ld_nc_v8(s, f);
+    ld_nc_v8(s + 8, f + 8);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+      const float4 q = __ldg(src + v);
+      f[4 * v + 0] = q.x;
+      f[4 * v + 1] = q.y;
+      f[4 * v + 2] = q.z;
+      f[4 * v + 3] = q.w;
+    }
+  }
+}  // bvh.hpp:82-84 (keys are 64 + 32 bits)
 
 // Parent links: parent node index, bit 31 set when the child is the parent's
 // LEFT child; kNoParent at the root.
@@ -125,15 +154,7 @@ __device__ __forceinline__ bool bvh_step(const float4* __restrict__ nodes, const
                                          int& top, int32_t* stack, Visit& visit) {
   using T = NodeTraits<D>;
   float f[T::kFloats];
-  const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
-#pragma unroll
-  for (int v = 0; v < T::kVec; ++v) {
-    float4 q = __ldg(src + v);
-    f[4 * v + 0] = q.x;
-    f[4 * v + 1] = q.y;
-    f[4 * v + 2] = q.z;
-    f[4 * v + 3] = q.w;
-  }
+  load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
   const int32_t left = __float_as_int(f[T::kIntOff + 0]);
   const int32_t right = __float_as_int(f[T::kIntOff + 1]);
   const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
@@ -202,29 +223,22 @@ __device__ __forceinline__ int ball_classify(const float* p, const float* lo, co
 //     bool visit(int32_t rank, int32_t aux)      leaf `rank` is within eps
 //     bool inside(int32_t first, int32_t last)   every rank in [first, last]
 //                                                  (first >= min_rank) is a hit
-// (false = stop the query). Both children are classified with the same
+// (false = stop the query). Pending subtrees go on `stack` (LocalStack
+// below; a shared-memory ring measured slower: it costs occupancy). Both children are classified with the same
 // straight-line code (leaf or internal, masked or not) so the lanes of a warp
 // only diverge on the rare visit / inside actions. Children are masked at
 // min_rank like query_sphere_masked (bvh.hpp:45-72); the order in which
 // leaves are reported is not the reference's DFS order (callers only depend
 // on the set, or, for early exit, on the count — see CoreQuery).
 
-template <int D, typename Visit, typename Inside>
+template <int D, typename Stack, typename Visit, typename Inside>
 __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes, const float* p,
                                                 const BallTest& bt, int32_t min_rank,
-                                                int32_t& node, int32_t& nlo, int& top,
-                                                int2* stack, Visit& visit, Inside& inside) {
+                                                int32_t& node, int32_t& nlo, Stack& stack,
+                                                Visit& visit, Inside& inside) {
   using T = NodeTraits<D>;
   float f[T::kFloats];
-  const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
-#pragma unroll
-  for (int v = 0; v < T::kVec; ++v) {
-    float4 q = __ldg(src + v);
-    f[4 * v + 0] = q.x;
-    f[4 * v + 1] = q.y;
-    f[4 * v + 2] = q.z;
-    f[4 * v + 3] = q.w;
-  }
+  load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
   const int32_t left = __float_as_int(f[T::kIntOff + 0]);
   const int32_t right = __float_as_int(f[T::kIntOff + 1]);
   const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
@@ -246,7 +260,7 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   }
   const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
   if (go_l && go_r) {
-    stack[top++] = make_int2(left, nlo);
+    stack.push(make_int2(left, nlo));
     node = right;
     nlo = split + 1;
   } else if (go_l) {
@@ -255,13 +269,26 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
     node = right;
     nlo = split + 1;
   } else {
-    if (top == 0) return false;
-    const int2 e = stack[--top];
+    int2 e;
+    if (!stack.pop(e)) return false;
     node = e.x;
     nlo = e.y;
   }
   return true;
 }
+
+// Traversal stacks of (node, first leaf rank) entries for bvh_step_ranged.
+struct LocalStack {  // per-thread local memory
+  int2 e[kStackDepth];
+  int top = 0;
+  __device__ __forceinline__ void push(int2 v) { e[top++] = v; }
+  __device__ __forceinline__ bool pop(int2& v) {
+    if (top == 0) return false;
+    v = e[--top];
+    return true;
+  }
+};
+
 
 // Warp-shared descent to a common start node. The 32 queries of a warp are
 // Morton-consecutive leaves, so their top-down walks share a long prefix:
@@ -293,15 +320,7 @@ __device__ __forceinline__ void warp_start_node(const float4* __restrict__ nodes
   using T = NodeTraits<D>;
   while (true) {
     float f[T::kFloats];
-    const float4* src = nodes + static_cast<int64_t>(node) * T::kVec;
-#pragma unroll
-    for (int v = 0; v < T::kVec; ++v) {
-      float4 q = __ldg(src + v);
-      f[4 * v + 0] = q.x;
-      f[4 * v + 1] = q.y;
-      f[4 * v + 2] = q.z;
-      f[4 * v + 3] = q.w;
-    }
+    load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
     const int32_t left = __float_as_int(f[T::kIntOff + 0]);
     const int32_t right = __float_as_int(f[T::kIntOff + 1]);
     const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);

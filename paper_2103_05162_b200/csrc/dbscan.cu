@@ -54,18 +54,18 @@ struct CoreQuery {
   BallTest bt;
   int minpts;
   uint8_t* __restrict__ flags;
-  int2* stack;  // per-thread traversal stack, kept outside the struct
+  LocalStack* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long dists = 0;
   float p[3];
   int32_t id, node, nlo;
-  int count, top;
+  int count;
   __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &id);
     id = static_cast<int32_t>(r);  // flags are kept in rank space
     count = 0;
     node = 0;
     nlo = 0;
-    top = 0;
+    stack->top = 0;
     return true;
   }
   __device__ bool step() {
@@ -84,7 +84,7 @@ struct CoreQuery {
       count += static_cast<int>(k);
       return true;
     };
-    return bvh_step_ranged<D>(nodes, p, bt, 0, node, nlo, top, stack, visit, inside);
+    return bvh_step_ranged<D>(nodes, p, bt, 0, node, nlo, *stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[id] = 1;
@@ -95,8 +95,8 @@ template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent) {
-  int2 stack[kStackDepth];
-  CoreQuery<D> q{nodes, leaf_pt, bt, minpts, flags, stack};
+  LocalStack stack;
+  CoreQuery<D> q{nodes, leaf_pt, bt, minpts, flags, &stack};
   if (persistent) {
     run_query_queue(m, &ctr->queue[0], q);
   } else {
@@ -161,13 +161,19 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
               BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
               int32_t* __restrict__ reach, DevCounters* ctr) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
   unsigned long long pairs = 0;
   TCB_PROBE_ONLY(unsigned long long pr[7] = {};)
-  if (r < m) {
-    float p[3];
+  float p[3] = {0.f, 0.f, 0.f};
+  int32_t rank = 0;
+  if (valid) {
     int32_t id;
     load_query<D>(leaf_pt, r, p, &id);
-    const int32_t rank = static_cast<int32_t>(r);
+    rank = static_cast<int32_t>(r);
+  }
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
+  if (valid) {
     int32_t hint = rank;
     auto visit = [&](int32_t s, int32_t) -> bool {
       ++pairs;
@@ -182,26 +188,17 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
       if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
       return true;
     };
-    int2 stack[kStackDepth];
-    int top = 0;
-    int32_t node, nlo;
-    warp_start_node<D>(nodes, p, true, bt, rank + 1, node, nlo);
-    while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, top, stack, visit, inside)) {
+    LocalStack stack;
+    while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
       TCB_PROBE_ONLY(++pr[0];)
     }
     TCB_PROBE_ONLY(++pr[0]; pr[5] += pairs == 0; pr[6] = pr[0]; if (pairs == 0) pr[3] = pr[0];)
-  } else {
-    float p[3] = {0.f, 0.f, 0.f};
-    int32_t node, nlo;
-    warp_start_node<D>(nodes, p, false, bt, 0, node, nlo);
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
   TCB_PROBE_ONLY(for (int k = 0; k < 6; ++k) flush_counter(&ctr->probe[k], pr[k]);
                  const unsigned wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(pr[6]));
-                 if ((threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[6], wmax);
-                 const bool allz = __all_sync(0xffffffffu, pairs == 0);
-                 if (allz && (threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[7], wmax);)
+                 if ((threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[6], wmax);)
 }
 
 // ---- covered runs: rank l joins l - 1 iff some recorded run [f, t] has
