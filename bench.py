@@ -212,17 +212,44 @@ def run_sharded(args, rank, world, dev, n):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    engine.launches = 0
     ev0.record()
     for _ in range(args.steps):
         own_gid, labels, core = cluster_sharded(x, gid, EPS, MINPTS, engine)
     ev1.record()
     torch.cuda.synchronize()
+    launches = engine.launches
     dist.barrier()
     clocks = sampler.stop()
     t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item()) / args.steps
     value = n * world / (ms * 1e-3) / 1e6
+
+    # e2e: the rank's points from pinned host memory -> sharded clustering ->
+    # labels + core flags of its own points back to the host, every step.
+    host_x = c.pin_memory()
+    host_gid = (torch.arange(n, dtype=torch.int64) + rank * n).pin_memory()
+    e2e_ms, h2d, d2h = [], 0, 0
+    for it in range(1 + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        xd = host_x.to(dev, non_blocking=True)
+        gd = host_gid.to(dev, non_blocking=True)
+        og, lab, cor = cluster_sharded(xd, gd, EPS, MINPTS, engine)
+        out = (og.cpu(), lab.cpu(), cor.cpu())
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 1:
+            e2e_ms.append(e0.elapsed_time(e1))
+        h2d = host_x.numel() * 4 + host_gid.numel() * 8
+        d2h = sum(o.numel() * o.element_size() for o in out)
+    te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n * world / (float(te.item()) * 1e-3) / 1e6
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
@@ -234,8 +261,11 @@ def run_sharded(args, rank, world, dev, n):
                                    "eps=0.042, minpts=2, FDBSCAN, Morton-range sharded",
                        "points_per_rank": n, "parallelism": f"morton-range shards x{world}",
                        "l2": "inputs exceed the 126 MB L2"},
-            "clocks": clocks, "gpu_launches": None, "e2e": None, "cpu_baseline": None,
-            "roofline": None,
+            "clocks": clocks, "gpu_launches": launches,
+            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(float(te.item()), 3),
+                    "api": "paper_2103_05162_b200.shard.cluster_sharded (host tensors in/out)"},
+            "cpu_baseline": None, "roofline": None,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -345,6 +345,22 @@ __device__ __forceinline__ void warp_start_node(const float4* __restrict__ nodes
   }
 }
 
+template <int D, class Q>
+__device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp,
+                                                    const float4* __restrict__ nodes,
+                                                    const BallTest& bt) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = q < m && qp.begin(q);
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, qp.p, valid, bt, valid ? qp.mask_rank : 0, node, nlo);
+  if (valid) {
+    qp.node = node;
+    while (qp.step()) {
+    }
+    qp.end();
+  }
+}
+
 // The whole query on one thread.
 template <int D, typename Visit>
 __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, const float* p,
@@ -384,6 +400,16 @@ __device__ __forceinline__ void run_query_direct(int64_t m, Q& qp) {
     qp.end();
   }
 }
+
+// One query per thread started at the warp's common start node
+// (warp_start_node, defined below). Q also exposes p[3], node and
+// mask_rank (the query's min_rank). Starting below the root skips only nodes
+// with a single live child, so the order of the query's visit calls is the
+// same as from the root (the DenseBox core pass depends on that order).
+template <int D, class Q>
+__device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp,
+                                                    const float4* __restrict__ nodes,
+                                                    const BallTest& bt);
 
 // Query scheduling mode of the traversal kernels: 0 = one query per thread,
 // 1 = persistent warp-refilled queue. Chosen once per process (TCB_QUERY_MODE).

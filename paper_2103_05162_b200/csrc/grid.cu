@@ -286,7 +286,7 @@ struct DbCoreQuery {
   int32_t* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long dists = 0;
   float p[3];
-  int32_t id, node;
+  int32_t id, node, mask_rank = 0;
   int count, top;
   __device__ bool begin(int64_t q) {
     const float4 qp = qpt[q];
@@ -351,13 +351,14 @@ struct DbMainQuery {
   int32_t* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long dists = 0, pairs = 0;
   float p[3];
-  int32_t i, own, hint, node;
+  int32_t i, own, hint, node, mask_rank;
   int top;
   bool core_i, settled;
   __device__ bool begin(int64_t q) {
     const float4 qp = qpt[q];
     i = __float_as_int(qp.w) & 0x7fffffff;
     own = qrank[q];
+    mask_rank = own;
     p[0] = qp.x;
     p[1] = qp.y;
     p[2] = qp.z;
@@ -418,7 +419,7 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
   if (persistent)
     run_query_queue(n, &ctr->queue[2], q);
   else
-    run_query_direct(n, q);
+    run_query_warpstart<D>(n, q, nodes, bt);
   unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
 }
@@ -436,7 +437,7 @@ k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
   if (persistent)
     run_query_queue(n, &ctr->queue[3], q);
   else
-    run_query_direct(n, q);
+    run_query_warpstart<D>(n, q, nodes, bt);
   unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
   v = warp_sum(q.pairs);

@@ -192,6 +192,7 @@ TC_EXPORT tc_status tcg_morton_codes_device(const float* d_coords, int64_t n, in
                                             void* stream) {
   if (bad_shape(d_coords, n, dim) || !lo || !hi || !d_codes) return TC_ERR_INVALID_ARGUMENT;
   return run_guarded([&] {
+    reset_launch_count();
     const float3 l = make_float3(lo[0], lo[1], dim == 3 ? lo[2] : 0.f);
     const float3 h = make_float3(hi[0], hi[1], dim == 3 ? hi[2] : 0.f);
     auto st = static_cast<cudaStream_t>(stream);
@@ -211,6 +212,7 @@ TC_EXPORT tc_status tcg_near_boxes_device(const float* d_coords, int64_t n, int 
   if (bad_shape(d_coords, n, dim) || !d_mask || num_boxes < 0 || !(eps > 0.f))
     return TC_ERR_INVALID_ARGUMENT;
   return run_guarded([&] {
+    reset_launch_count();
     if (n == 0) return;
     auto st = static_cast<cudaStream_t>(stream);
     if (dim == 2)
@@ -256,6 +258,7 @@ TC_EXPORT tc_status tcg_union_edges_device(const int32_t* d_edges, int64_t m, in
                                            int32_t* d_root, void* stream) {
   if ((!d_edges && m > 0) || m < 0 || n < 1 || !d_root) return TC_ERR_INVALID_ARGUMENT;
   return run_guarded([&] {
+    reset_launch_count();
     auto st = static_cast<cudaStream_t>(stream);
     Scratch scratch(st);
     uint8_t* tmp = scratch.alloc_n<uint8_t>(n);

@@ -49,9 +49,13 @@ class DeviceEngine:
 
     def __init__(self, device):
         self.device = torch.device(device)
+        self.launches = 0  # kernels of this library launched through the engine
 
     def _s(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _count(self):
+        self.launches += int(lib.tcg_last_launch_count())
 
     def morton(self, x, lo, hi):
         n, d = x.shape
@@ -61,6 +65,7 @@ class DeviceEngine:
         _check(lib.tcg_morton_codes_device(C.c_void_p(x.data_ptr()), n, d, lo_h, hi_h,
                                            C.c_void_p(out.data_ptr()), self._s()),
                "tcg_morton_codes_device")
+        self._count()
         return out
 
     def near_boxes(self, x, eps, blo, bhi):
@@ -74,6 +79,7 @@ class DeviceEngine:
                                          C.c_void_p(blo.data_ptr()), C.c_void_p(bhi.data_ptr()),
                                          blo.shape[0], C.c_void_p(mask.data_ptr()), self._s()),
                "tcg_near_boxes_device")
+        self._count()
         return mask
 
     def core_flags(self, x, eps, minpts):
@@ -82,6 +88,7 @@ class DeviceEngine:
         _check(lib.tcg_core_flags_device(C.c_void_p(x.data_ptr()), n, d, C.c_float(eps),
                                          int(minpts), C.c_void_p(core.data_ptr()), self._s()),
                "tcg_core_flags_device")
+        self._count()
         return core
 
     def cluster_given_core(self, x, eps, core):
@@ -95,6 +102,7 @@ class DeviceEngine:
                                                  C.c_void_p(core_out.data_ptr()), self._s(),
                                                  None),
                "tcg_cluster_given_core_device")
+        self._count()
         return labels
 
     def union_edges(self, edges, n):
@@ -103,6 +111,7 @@ class DeviceEngine:
         _check(lib.tcg_union_edges_device(C.c_void_p(edges.data_ptr()), edges.shape[0], int(n),
                                           C.c_void_p(root.data_ptr()), self._s()),
                "tcg_union_edges_device")
+        self._count()
         return root
 
 
