@@ -131,8 +131,6 @@ int get_last_stage_ms(double* out, int cap) {
 // ---------------------------------------------------------------------------
 // FDBSCAN (dbscan.cpp:221-284 with Algorithm::Fdbscan)
 // ---------------------------------------------------------------------------
-namespace {
-
 template <int D>
 void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
                  uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock) {
@@ -157,7 +155,10 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   clock.finish();
 }
 
-}  // namespace
+template void run_fdbscan<2>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
+                             Scratch&, StageClock&);
+template void run_fdbscan<3>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
+                             Scratch&, StageClock&);
 
 // ---------------------------------------------------------------------------
 // Entry

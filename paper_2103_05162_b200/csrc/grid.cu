@@ -517,6 +517,17 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   std::memcpy(&num_dense, h_stage + 4, 4);
   const int64_t sparse_points = num_prims - num_dense;
   *dense_fraction = static_cast<double>(n - sparse_points) / static_cast<double>(n);
+  if (num_dense == 0) {
+    // No dense cell: every primitive is a SinglePoint, so the mixed BVH is the
+    // point BVH (make_mixed_primitives, dense_grid.cpp:79-98) and the DenseBox
+    // passes are the FDBSCAN passes: densebox_mark_cores / densebox_main_phase
+    // (dbscan.cpp:110-200) reduce to fdbscan_mark_cores / fdbscan_main_phase
+    // with the same pairs and the same per-hit distance counts
+    // (dbscan.cpp:36-88). Run the point pipeline (rank-space union-find,
+    // contained subtrees) instead of the mixed-tree kernels.
+    run_fdbscan<D>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock);
+    return;
+  }
 
   float4* prim_lo = scratch.alloc_n<float4>(num_prims);
   float4* prim_hi = scratch.alloc_n<float4>(num_prims);

@@ -138,6 +138,11 @@ void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,
                      int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
                      cudaStream_t s, bool force_core);
 
+// ---- whole FDBSCAN pipeline over the point BVH (engine.cu) ----
+template <int D>
+void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
+                 uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock);
+
 // ---- DenseBox (grid.cu) ----
 template <int D>
 void run_densebox(const float* d_coords, int64_t n, float eps, int minpts,
