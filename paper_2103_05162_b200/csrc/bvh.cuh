@@ -215,18 +215,24 @@ __device__ __forceinline__ int ball_classify(const float* p, const float* lo, co
   return box_dist2<D>(p, lo, hi) <= bt.r2 ? 1 : 0;
 }
 
+// Answers of an `inside` callback (bvh_step_ranged).
+constexpr int kStop = 0, kTaken = 1, kWalk = 2;
+
 // Traversal step with subtree containment. Also tracks `nlo`, the first leaf
 // rank of the current node (Karras ranges: a node's left child covers
 // [lo, split], its right child [split + 1, hi]; the root covers [0, n-1]), so
 // that a contained internal child is reported as its unmasked leaf-rank range
 // instead of being walked:
-//     bool visit(int32_t rank, int32_t aux)      leaf `rank` is within eps
-//     bool inside(int32_t first, int32_t last)   every rank in [first, last]
-//                                                  (first >= min_rank) is a hit
-// (false = stop the query). Pending subtrees go on `stack` (LocalStack
-// below; a shared-memory ring measured slower: it costs occupancy). Both children are classified with the same
-// straight-line code (leaf or internal, masked or not) so the lanes of a warp
-// only diverge on the rare visit / inside actions. Children are masked at
+//     bool visit(int32_t rank, int32_t aux)     leaf `rank` is within eps
+//                                               (false = stop the query)
+//     int inside(int32_t first, int32_t last)   every rank in [first, last]
+//                                               (first >= min_rank) is a hit:
+//                                               kStop, kTaken, or kWalk (not
+//                                               taken as a run: descend)
+// Pending subtrees go on `stack` (LocalStack below; a shared-memory ring
+// measured slower: it costs occupancy). Both children are classified with the
+// same straight-line code (leaf or internal, masked or not) so the lanes of a
+// warp only diverge on the rare visit / inside actions. Children are masked at
 // min_rank like query_sphere_masked (bvh.hpp:45-72); the order in which
 // leaves are reported is not the reference's DFS order (callers only depend
 // on the set, or, for early exit, on the count — see CoreQuery).
@@ -253,10 +259,22 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   if (split < min_rank) cl = 0;
   if (max_r < min_rank) cr = 0;
   if (cl > 0 && (leaf_l || cl == 2)) {
-    if (!(leaf_l ? visit(~left, aux_l) : inside(lo_l, aux_l))) return false;
+    if (leaf_l) {
+      if (!visit(~left, aux_l)) return false;
+    } else {
+      const int a = inside(lo_l, aux_l);
+      if (a == kStop) return false;
+      if (a == kWalk) cl = 1;
+    }
   }
   if (cr > 0 && (leaf_r || cr == 2)) {
-    if (!(leaf_r ? visit(~right, aux_r) : inside(lo_r, aux_r))) return false;
+    if (leaf_r) {
+      if (!visit(~right, aux_r)) return false;
+    } else {
+      const int a = inside(lo_r, aux_r);
+      if (a == kStop) return false;
+      if (a == kWalk) cr = 1;
+    }
   }
   const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
   if (go_l && go_r) {

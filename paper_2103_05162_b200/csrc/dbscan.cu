@@ -19,6 +19,7 @@
 
 #include "device_common.cuh"
 #include "pipeline.hpp"
+#include "primitives.cuh"
 
 namespace tcb {
 
@@ -73,16 +74,16 @@ struct CoreQuery {
       ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
-    auto inside = [&](int32_t first, int32_t last) -> bool {
+    auto inside = [&](int32_t first, int32_t last) -> int {
       const int64_t k = static_cast<int64_t>(last) - first + 1;
       if (count + k >= minpts) {
         dists += static_cast<unsigned long long>(minpts - count);
         count = minpts;
-        return false;
+        return kStop;
       }
       dists += static_cast<unsigned long long>(k);
       count += static_cast<int>(k);
-      return true;
+      return kTaken;
     };
     return bvh_step_ranged<D>(nodes, p, bt, 0, node, nlo, *stack, visit, inside);
   }
@@ -120,30 +121,69 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
 // the self leaf: the same pairs) so each unordered within-eps pair is met
 // exactly once, and resolved on the spot — no neighbour list is stored.
 // minpts > 2 path: core flags are final, pairs resolve per dbscan.hpp:82-99.
+// Contained subtrees (every leaf of [first, last] within eps), with
+// noncore_before[] prefix counts telling how many of them are borders/noise:
+//   core query,   all leaves core: a run like in k_fd_main_fof (unite with
+//                 `first`, record the run; the cover pass joins neighbouring
+//                 ranks inside it — all cores within eps of the query);
+//   border query, no core leaf or already settled (claimed): every pair is a
+//                 no-op, counted only; all leaves core: claimed by the run;
+//   otherwise the subtree is walked leaf by leaf (per-pair rule).
 template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-          const int32_t* __restrict__ key, DevCounters* ctr) {
+          const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
+          int32_t* __restrict__ reach, DevCounters* ctr) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
   unsigned long long pairs = 0;
-  if (r < m) {
-    float p[3];
+  float p[3] = {0.f, 0.f, 0.f};
+  int32_t rank = 0;
+  if (valid) {
     int32_t id;
     load_query<D>(leaf_pt, r, p, &id);
-    const int32_t rank = static_cast<int32_t>(r);
+    rank = static_cast<int32_t>(r);
+  }
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
+  if (valid) {
     const bool core_r = flags[rank] != 0;
     int32_t hint = rank;
     bool settled = false;
-    auto visit = [&](int32_t s, int32_t, const float*, const float*) -> bool {
+    auto visit = [&](int32_t s, int32_t) -> bool {
       ++pairs;
       resolve_pair_keyed(rank, s, core_r, flags, parent, key, hint, settled);
       return true;
     };
-    bvh_query<D>(nodes, p, bt, rank + 1, visit);
+    auto inside = [&](int32_t first, int32_t last) -> int {
+      const int32_t size = last - first + 1;
+      const int32_t noncore = __ldg(noncore_before + last + 1) - __ldg(noncore_before + first);
+      if (core_r) {
+        if (noncore != 0) return kWalk;
+        uf_unite_hinted_keyed(parent, key, rank, first, hint);
+        if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
+      } else if (!settled && noncore != size) {
+        if (noncore != 0) return kWalk;
+        if (ld_relaxed(parent + rank) == rank) uf_claim(parent, rank, uf_find(parent, first));
+        settled = true;
+      }
+      pairs += static_cast<unsigned long long>(size);
+      return kTaken;
+    };
+    LocalStack stack;
+    while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
+    }
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
+}
+
+__global__ void k_noncore_ind(const uint8_t* __restrict__ flags, int64_t n,
+                              int32_t* __restrict__ ind) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i <= n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    ind[i] = i < n ? (flags[i] == 0) : 0;
 }
 
 // minpts == 2 (friends-of-friends) main pass. Every within-eps pair is a
@@ -181,12 +221,12 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
       uf_unite_hinted_keyed(parent, key, rank, s, hint);
       return true;
     };
-    auto inside = [&](int32_t first, int32_t last) -> bool {
+    auto inside = [&](int32_t first, int32_t last) -> int {
       pairs += static_cast<unsigned long long>(last - first + 1);
       TCB_PROBE_ONLY(++pr[1]; pr[4] += last - first + 1;)
       uf_unite_hinted_keyed(parent, key, rank, first, hint);
       if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
-      return true;
+      return kTaken;
     };
     LocalStack stack;
     while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
@@ -409,23 +449,29 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
   cudaStream_t s = scratch.stream();
   const BallTest bt = BallTest::make(eps2);
   const unsigned grid = grid_for(n, kQueryBlock, INT32_MAX);
-  if (!force_core) {
-    note_launch(), k_fd_main<D><<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags,
-                                                             parent, b.tree.leaf_order, d_ctr);
-    TCB_CUDA(cudaGetLastError());
-    return;
-  }
-  int32_t* reach = scratch.alloc_n<int32_t>(n + kCoverItems);
   const int64_t tiles = (n + kCoverTile - 1) / kCoverTile;
+  const unsigned tgrid = static_cast<unsigned>(tiles);
+  int32_t* reach = scratch.alloc_n<int32_t>(n + kCoverItems);
   int32_t* tile_max = scratch.alloc_n<int32_t>(tiles);
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
-  note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
-      b.tree.nodes, b.leaf_pt, n, bt, parent, b.tree.leaf_order, reach, d_ctr);
-  note_launch(), k_cover_tiles<<<static_cast<unsigned>(tiles), kCoverThreads, 0, s>>>(reach, n,
-                                                                                       tile_max);
+  if (force_core) {
+    note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
+        b.tree.nodes, b.leaf_pt, n, bt, parent, b.tree.leaf_order, reach, d_ctr);
+  } else {
+    int32_t* ind = scratch.alloc_n<int32_t>(n + 1);
+    int32_t* noncore_before = scratch.alloc_n<int32_t>(n + 1);
+    void* scan_tmp = scratch.alloc(scan_scratch_bytes(n + 1));
+    note_launch(), k_noncore_ind<<<grid_for(n + 1, 256), 256, 0, s>>>(flags, n, ind);
+    exclusive_scan_i32(ind, noncore_before, n + 1, nullptr, scan_tmp, s);
+    note_launch(), k_fd_main<D><<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags,
+                                                             parent, b.tree.leaf_order,
+                                                             noncore_before, reach, d_ctr);
+  }
+  // covered runs (all-core): join each covered rank to its predecessor
+  note_launch(), k_cover_tiles<<<tgrid, kCoverThreads, 0, s>>>(reach, n, tile_max);
   note_launch(), k_cover_carry<<<1, 1024, 0, s>>>(tile_max, tiles);
-  note_launch(), k_cover_unite<<<static_cast<unsigned>(tiles), kCoverThreads, 0, s>>>(
-      reach, n, tile_max, parent, b.tree.leaf_order);
+  note_launch(), k_cover_unite<<<tgrid, kCoverThreads, 0, s>>>(reach, n, tile_max, parent,
+                                                               b.tree.leaf_order);
   TCB_CUDA(cudaGetLastError());
 }
 
