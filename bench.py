@@ -412,7 +412,9 @@ def main():
                        "l2": "inputs (444 MB coords + 2.4 GB tree) exceed the 126 MB L2"},
             "stage_ms": {k: round(v / steps_n, 3) for k, v in stage_sum.items()},
             "hbm_gbs_end_to_end": round(total_gbs, 1),
-            "roofline": {"bound": "hbm", "kernel": "k_fd_main (fused traversal + union-find)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "main stage: k_fd_main_fof (fused traversal + union-find) "
+                                   "+ k_cover_* run unions, timed by stage events",
                          "achieved": round(achieved, 1) if achieved else None, "peak": peak,
                          "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
