@@ -59,9 +59,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* smem_w
 // ---------------------------------------------------------------------------
 // Onesweep LSD radix sort (one kernel per digit window, decoupled look-back).
 //
-//   k_sort_hist      ONE read of the keys: the global histogram of every
-//                    digit window that will be sorted (block-private shared
-//                    histograms, one global atomic per bin per block)
+//   k_sort_hist      the global histogram of the first sorted digit window
+//                    (block-private shared histogram, one global atomic per
+//                    bin per block); each onesweep pass adds the histogram of
+//                    the next window from the keys it holds anyway
 //   k_sort_onesweep  per digit window: a tile grabs its id from a counter (so
 //                    look-back only ever waits on tiles already running),
 //                    ranks its keys stably (__match_any_sync + per-warp
@@ -83,23 +84,20 @@ struct PassShifts {
   int count;
 };
 
+// Histogram of the first sorted digit window only; every onesweep pass builds
+// the histogram of the NEXT window from the keys it already holds.
 __global__ void __launch_bounds__(kSortThreads)
-k_sort_hist(const uint64_t* __restrict__ keys, int64_t n, PassShifts ps,
+k_sort_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
             uint32_t* __restrict__ ghist) {
-  __shared__ uint32_t h[kMaxPasses][kRadix];
-  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kSortThreads) (&h[0][0])[i] = 0;
+  __shared__ uint32_t h[kRadix];
+  for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
   __syncthreads();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = __ldcs(keys + i);
-    for (int p = 0; p < ps.count; ++p)
-      atomicAdd(&h[p][static_cast<uint32_t>(k >> ps.shift[p]) & (kRadix - 1)], 1u);
-  }
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&h[static_cast<uint32_t>(__ldcs(keys + i) >> shift) & (kRadix - 1)], 1u);
   __syncthreads();
-  for (int i = threadIdx.x; i < ps.count * kRadix; i += kSortThreads) {
-    const uint32_t v = (&h[0][0])[i];
-    if (v) atomicAdd(ghist + i, v);
-  }
+  for (int i = threadIdx.x; i < kRadix; i += kSortThreads)
+    if (h[i]) atomicAdd(ghist + i, h[i]);
 }
 
 struct OnesweepSmem {
@@ -109,6 +107,7 @@ struct OnesweepSmem {
   uint32_t tile_start[kRadix];
   uint32_t global_start[kRadix];
   uint32_t warp_tot[32];
+  uint32_t next_hist[kRadix];
   int tile;
 };
 
@@ -125,12 +124,14 @@ __global__ void __launch_bounds__(kSortThreads)
 k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
                 uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, int64_t n,
                 int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
-                uint32_t* __restrict__ tile_counter) {
+                uint32_t* __restrict__ tile_counter, int next_shift,
+                uint32_t* __restrict__ ghist_next) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) S.tile = static_cast<int>(atomicAdd(tile_counter, 1u));
   for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
+  S.next_hist[threadIdx.x] = 0;  // kSortThreads == kRadix
   __syncthreads();
   const int tile = S.tile;
 
@@ -145,6 +146,13 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
       k[j] = __ldcs(keys_in + idx);
       v[j] = __ldcs(vals_in + idx);
     }
+  }
+
+  if (next_shift >= 0) {
+#pragma unroll
+    for (int j = 0; j < kIPT; ++j)
+      if (base + j * 32 + lane < n)
+        atomicAdd(&S.next_hist[static_cast<uint32_t>(k[j] >> next_shift) & (kRadix - 1)], 1u);
   }
 
   uint32_t rank[kIPT];
@@ -196,6 +204,7 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
   const uint32_t dbase = block_excl_scan<kSortThreads>(ghist[d], S.warp_tot, nullptr);
   S.tile_start[d] = tstart;
   S.global_start[d] = dbase + excl;
+  if (next_shift >= 0 && S.next_hist[d]) atomicAdd(ghist_next + d, S.next_hist[d]);
   __syncthreads();
 
 #pragma unroll
@@ -303,7 +312,7 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
     uint32_t* ghist = counters + 64;
     TCB_CUDA(cudaMemsetAsync(counters, 0, (64 + kMaxPasses * kRadix) * sizeof(uint32_t), stream));
     note_launch(), k_sort_hist<<<grid_for(n, kSortThreads, 148 * 4), kSortThreads, 0, stream>>>(
-        keys, n, ps, ghist);
+        keys, n, ps.shift[0], ghist);
     TCB_CUDA(cudaFuncSetAttribute(k_sort_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(OnesweepSmem))));
     for (int p = 0; p < ps.count; ++p) {
@@ -314,7 +323,8 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
       TCB_CUDA(cudaMemsetAsync(status, 0, num_tiles * kRadix * sizeof(uint32_t), stream));
       note_launch(), k_sort_onesweep<<<static_cast<unsigned>(num_tiles), kSortThreads,
                                        sizeof(OnesweepSmem), stream>>>(
-          kin, vin, kout, vout, n, ps.shift[p], ghist + p * kRadix, status, counters + p);
+          kin, vin, kout, vout, n, ps.shift[p], ghist + p * kRadix, status, counters + p,
+          p + 1 < ps.count ? ps.shift[p + 1] : -1, ghist + (p + 1) * kRadix);
       TCB_CUDA(cudaGetLastError());
       in_alt = !in_alt;
     }
