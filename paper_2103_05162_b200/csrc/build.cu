@@ -6,12 +6,11 @@
 //   k_morton            fp64 quantization + interleave (geometry.hpp:132-156),
 //                       fused AND/OR reduction of the codes for the sort
 //   radix_sort_pairs    stable (code, index) order (bvh.cpp:27-32)
-//   k_karras            Karras-2012 split search per internal node
-//                       (bvh.cpp:49-86); also writes child payloads, the
-//                       children's max leaf rank and parent links
-//   k_refit             bottom-up boxes with atomic arrival flags
-//                       (bvh.cpp:88-124); points mode also gathers the
+//   k_climb             single bottom-up pass (Apetrei 2014) producing the
+//                       Karras radix tree (bvh.cpp:49-86), its boxes and max
+//                       ranks (bvh.cpp:88-124) and, in points mode, the
 //                       Morton-ordered query points (bvh.cpp:34-39)
+//   k_root_to_zero      moves the root record to node 0
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -141,212 +140,133 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
   return 64 + __clz(static_cast<int>(static_cast<uint32_t>(i) ^ static_cast<uint32_t>(j)));
 }
 
-// Leaves in Morton rank order (bvh.cpp:34-39): leaf_lo[s] / leaf_hi[s] =
-// box of primitive order[s]; in points mode both alias one array whose w
-// component carries the point id (the query points of the traversals).
+// ---------------------------------------------------------------------------
+// Single-pass bottom-up build (Apetrei 2014) of the Karras radix tree
+// (bvh.cpp:49-124): topology, boxes and leaf gather in one kernel.
+//
+// Thread s starts at leaf s (range [s, s]). A node covering [l, r] is the
+// LEFT child of the internal node whose split is r when delta(r) >
+// delta(l-1) (or l == 0), else the RIGHT child of the node whose split is
+// l-1 — the boundaries of a subtree never have equal deltas, so this is
+// exactly the Karras parent. Internal nodes are numbered by their split, so a
+// child knows its parent's record at once and writes its box, link and aux
+// (max rank, or the leaf payload) into its slot there (children-in-parent
+// layout, bvh.cuh). The two children meet at an exchange on the parent's
+// `other` word: the first stores its outer bound and stops; the second reads
+// the sibling's bound (the parent's full range) and its slot, and climbs on
+// with the union box. Only the meeting is ordered: slot stores, then an
+// exchange with release semantics; the second arriver reads the sibling slot
+// through L2 (ld.cg) after the exchange that observed it.
+// Numbering by split puts the root at some index g; k_root_to_zero moves it
+// to node 0 (the traversals' entry) and node 0's record to the spare slot m-1.
+// The tree is the reference's tree node for node; only the numbering of the
+// internal nodes differs (tcg_debug_point_bvh renumbers to Karras indices).
+// ---------------------------------------------------------------------------
+struct ClimbState {
+  int32_t root;         // split index of the root
+  int32_t zero_parent;  // parent of internal node 0 | kUpLeftBit if left child
+};
+
+// Exchange with release semantics: this thread's earlier slot stores are
+// visible (at L2) to whoever observes the exchanged value. No acquire side:
+// the reader goes through L2 (ld.cg) — a full __threadfence would also
+// invalidate the SM's L1 (CCTL.IVALL) on every climbing step.
+__device__ __forceinline__ int32_t atom_exch_release(int32_t* p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.exch.release.gpu.global.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 template <int D, class Src>
 __global__ void __launch_bounds__(256)
-k_gather_leaves(Src src, const int32_t* __restrict__ order, int64_t m, float4* __restrict__ leaf_lo,
-                float4* __restrict__ leaf_hi) {
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
+        const int32_t* __restrict__ prim_aux, int64_t m, float4* nodes,
+        int32_t* __restrict__ other, float4* __restrict__ leaf_pt, ClimbState* state) {
+  using T = NodeTraits<D>;
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (blockIdx.x * static_cast<int64_t>(blockDim.x) >= m) return;
+  bool active = s < m;
+  float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
+  int32_t l = 0, r = 0, link = 0, aux = 0;
+  if (active) {
     const int32_t prim = order[s];
-    float lo[3], hi[3];
     src.box(prim, lo, hi);
-    leaf_lo[s] = make_float4(lo[0], lo[1], D == 3 ? lo[2] : 0.f, __int_as_float(prim));
-    if (leaf_hi != leaf_lo) leaf_hi[s] = make_float4(hi[0], hi[1], D == 3 ? hi[2] : 0.f, 0.f);
-  }
-}
-
-// Subtrees of at most kDirectRange leaves get their boxes straight from the
-// contiguous leaf run (k_small_boxes); only larger nodes are refit bottom-up.
-constexpr int kDirectRange = 32;
-
-template <int D>
-__global__ void __launch_bounds__(256)
-k_karras(const float4* __restrict__ leaf_lo, const float4* __restrict__ leaf_hi,
-         const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
-         const int32_t* __restrict__ prim_aux, int64_t m, float4* __restrict__ nodes,
-         int4* __restrict__ node_info, int32_t* __restrict__ leaf_up,
-         int32_t* __restrict__ starts, int32_t* __restrict__ num_starts) {
-  using T = NodeTraits<D>;
-  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= m - 1) return;
-  const int d = key_delta(codes, m, i, i + 1) > key_delta(codes, m, i, i - 1) ? 1 : -1;
-  const int delta_min = key_delta(codes, m, i, i - d);
-  int64_t lmax = 2;
-  while (key_delta(codes, m, i, i + lmax * d) > delta_min) lmax *= 2;
-  int64_t l = 0;
-  for (int64_t t = lmax / 2; t >= 1; t /= 2)
-    if (key_delta(codes, m, i, i + (l + t) * d) > delta_min) l += t;
-  const int64_t j = i + l * d;
-  const int delta_node = key_delta(codes, m, i, j);
-  int64_t s = 0, t = l;
-  do {
-    t = (t + 1) / 2;
-    if (key_delta(codes, m, i, i + (s + t) * d) > delta_node) s += t;
-  } while (t > 1);
-  const int64_t gamma = i + s * d + (d < 0 ? d : 0);
-  const int64_t lo = i < j ? i : j, hi = i < j ? j : i;
-
-  float* f = reinterpret_cast<float*>(nodes + i * T::kVec);
-  // A leaf child's box goes straight into its slot here (bvh.cpp:34-39's
-  // gather fused in), so the refit only ever waits on internal children.
-  auto leaf_child = [&](int64_t rank, int slot, int32_t& link, int32_t& aux) {
-    link = ~static_cast<int32_t>(rank);
-    const int32_t prim = order[rank];
+    if (leaf_pt) leaf_pt[s] = make_float4(lo[0], lo[1], D == 3 ? lo[2] : 0.f, __int_as_float(prim));
+    l = r = static_cast<int32_t>(s);
+    link = ~l;
     aux = prim_aux ? prim_aux[prim] : prim;
-    const float4 a = leaf_lo[rank], c = leaf_hi[rank];
-    const float blo[3] = {a.x, a.y, a.z}, bhi[3] = {c.x, c.y, c.z};
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      f[slot * 2 * D + k] = blo[k];
-      f[slot * 2 * D + D + k] = bhi[k];
-    }
-  };
-  int32_t left, right, aux_l, aux_r;
-  // Own info (delta = prefix length shared by the whole range, the range);
-  // the parent link of each child is written here, by its parent.
-  node_info[i].y = delta_node;
-  node_info[i].z = static_cast<int32_t>(lo);
-  node_info[i].w = static_cast<int32_t>(hi);
-  const int32_t up_left = static_cast<int32_t>(i) | kUpLeftBit;
-  const int32_t up_right = static_cast<int32_t>(i);
-  if (lo == gamma) {
-    leaf_child(gamma, 0, left, aux_l);
-    leaf_up[gamma] = up_left;
-  } else {
-    left = static_cast<int32_t>(gamma);
-    aux_l = static_cast<int32_t>(gamma);  // max leaf rank of [lo, gamma]
-    node_info[gamma].x = up_left;
   }
-  if (hi == gamma + 1) {
-    leaf_child(gamma + 1, 1, right, aux_r);
-    leaf_up[gamma + 1] = up_right;
-  } else {
-    right = static_cast<int32_t>(gamma + 1);
-    aux_r = static_cast<int32_t>(hi);  // max leaf rank of [gamma+1, hi]
-    node_info[gamma + 1].x = up_right;
-  }
-  *reinterpret_cast<int4*>(f + T::kIntOff) = make_int4(left, right, aux_l, aux_r);
-  if (i == 0) node_info[0].x = kNoParent;
-  // refit climbers start at the large nodes whose two children are leaves or
-  // small subtrees (both slots are complete before k_refit runs)
-  const bool start = (hi - lo + 1 > kDirectRange) && (gamma - lo + 1 <= kDirectRange) &&
-                     (hi - gamma <= kDirectRange);
-  const uint32_t mask = __ballot_sync(__activemask(), start);
-  if (mask) {
-    const int leader = __ffs(mask) - 1;
-    int32_t base = 0;
-    if ((threadIdx.x & 31) == leader) base = atomicAdd(num_starts, __popc(mask));
-    base = __shfl_sync(__activemask(), base, leader);
-    if (start) starts[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1))] = static_cast<int32_t>(i);
-  }
-}
-
-// Box of every non-root internal node with <= kDirectRange leaves, reduced
-// directly over its contiguous leaf run, into its slot of the parent.
-template <int D>
-__global__ void __launch_bounds__(256)
-k_small_boxes(const float4* __restrict__ leaf_lo, const float4* __restrict__ leaf_hi,
-              const int4* __restrict__ node_info, int64_t m, float4* __restrict__ nodes) {
-  using T = NodeTraits<D>;
-  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x + 1; c < m - 1;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int4 info = node_info[c];
-    if (info.w - info.z + 1 > kDirectRange) continue;
-    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int32_t s = info.z; s <= info.w; ++s) {
-      const float4 a = __ldg(leaf_lo + s), b = __ldg(leaf_hi + s);
-      lo[0] = fminf(lo[0], a.x);
-      lo[1] = fminf(lo[1], a.y);
-      lo[2] = fminf(lo[2], a.z);
-      hi[0] = fmaxf(hi[0], b.x);
-      hi[1] = fmaxf(hi[1], b.y);
-      hi[2] = fmaxf(hi[2], b.z);
-    }
-    float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(up_parent(info.x)) * T::kVec);
-    float* slot = pf + (up_is_left(info.x) ? 0 : 2 * D);
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      slot[k] = lo[k];
-      slot[D + k] = hi[k];
-    }
-  }
-}
-
-// Bottom-up refit (bvh.cpp:88-124) of the nodes above kDirectRange leaves.
-// Climbers start at the large nodes whose children are leaves or small
-// subtrees (slots filled by k_karras / k_small_boxes, which run first; k_karras
-// lists them). A finished node writes its box (union of its two slots) into its
-// slot of the parent; if the sibling is a leaf or small the climber continues,
-// otherwise the two climbers meet at an arrival counter and the second one
-// continues. Only that meeting needs ordering: the writer's slot store must be
-// visible before its arrival (release fence, issued once per warp step for all
-// lanes that need it); the second arriver reads the sibling slot through L2
-// (ld.cg), after the atomic that observed the sibling's arrival.
-template <int D>
-__global__ void __launch_bounds__(256)
-k_refit(const int32_t* __restrict__ starts, const int32_t* __restrict__ num_starts,
-        float4* nodes, const int4* __restrict__ node_info, int32_t* __restrict__ arrivals) {
-  using T = NodeTraits<D>;
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int32_t count = *num_starts;
-  if (blockIdx.x * static_cast<int64_t>(blockDim.x) >= count) return;  // whole block idle
-  bool active = t < count;
-  int32_t c = active ? starts[t] : 0;
   while (__any_sync(0xffffffffu, active)) {
-    bool fence = false;
     int32_t p = 0;
+    bool left = false;
     if (active) {
-      if (c == 0) {  // the root's own box is never tested (bvh.hpp:55-58)
-        active = false;
+      left = l == 0 || (r != m - 1 && key_delta(codes, m, r, r + 1) > key_delta(codes, m, l - 1, l));
+      p = left ? r : l - 1;
+      float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
+      float* slot = pf + (left ? 0 : 2 * D);
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        __stcg(slot + k, lo[k]);
+        __stcg(slot + D + k, hi[k]);
+      }
+      int32_t* ip = reinterpret_cast<int32_t*>(pf + T::kIntOff);
+      __stcg(ip + (left ? 0 : 1), link);
+      __stcg(ip + (left ? 2 : 3), aux);
+      if (link == 0) state->zero_parent = p | (left ? kUpLeftBit : 0);
+    }
+    if (active) {
+      const int32_t o = atom_exch_release(other + p, left ? l : r);
+      if (o < 0) {
+        active = false;  // first arrival: the sibling finishes the parent
       } else {
-        const float* cf = reinterpret_cast<const float*>(nodes + static_cast<int64_t>(c) * T::kVec);
-        float lo[3], hi[3];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          lo[k] = fminf(__ldcg(cf + k), __ldcg(cf + 2 * D + k));
-          hi[k] = fmaxf(__ldcg(cf + D + k), __ldcg(cf + 3 * D + k));
-        }
-        p = up_parent(node_info[c].x);
-        float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
-        const int2 pl = *reinterpret_cast<const int2*>(pf + T::kIntOff);
-        const bool is_left = pl.x == c;
-        float* slot = pf + (is_left ? 0 : 2 * D);
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          __stcg(slot + k, lo[k]);
-          __stcg(slot + D + k, hi[k]);
-        }
-        const int32_t sibling = is_left ? pl.y : pl.x;
-        bool ready = sibling < 0;  // a leaf: its slot is already in place
-        if (!ready) {
-          const int4 si = node_info[sibling];
-          ready = si.w - si.z + 1 <= kDirectRange;  // filled by k_small_boxes
-        }
-        if (ready)
-          c = p;
+        if (left)
+          r = o;
         else
-          fence = true;  // meet the sibling's climber
+          l = o;
+        const float* pf = reinterpret_cast<const float*>(nodes + static_cast<int64_t>(p) * T::kVec);
+        const float* sib = pf + (left ? 2 * D : 0);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          lo[k] = fminf(lo[k], __ldcg(sib + k));
+          hi[k] = fmaxf(hi[k], __ldcg(sib + D + k));
+        }
+        link = p;
+        aux = r;  // max leaf rank of [l, r]
+        if (l == 0 && r == m - 1) {
+          state->root = p;
+          active = false;
+        }
       }
     }
-    if (__any_sync(0xffffffffu, fence)) __threadfence();
-    if (fence) {
-      if (atomicAdd(arrivals + p, 1) == 0)
-        active = false;
-      else
-        c = p;
-    }
+  }
+}
+
+// Moves the root record to node 0 and node 0's record to the spare slot m-1,
+// re-pointing the one link that referenced node 0.
+template <int D>
+__global__ void k_root_to_zero(float4* nodes, int64_t m, const ClimbState* state) {
+  using T = NodeTraits<D>;
+  const int32_t root = state->root;
+  if (root == 0) return;
+  const int t = threadIdx.x;  // T::kVec threads
+  const float4 zero_rec = nodes[t];
+  const float4 root_rec = nodes[static_cast<int64_t>(root) * T::kVec + t];
+  __syncthreads();
+  nodes[(m - 1) * T::kVec + t] = zero_rec;
+  nodes[t] = root_rec;
+  __syncthreads();
+  if (t == 0) {
+    int32_t zp = up_parent(state->zero_parent);
+    if (zp == root) zp = 0;  // the root's record now lives at 0
+    int32_t* ip = reinterpret_cast<int32_t*>(reinterpret_cast<float*>(nodes + static_cast<int64_t>(zp) * T::kVec) + T::kIntOff);
+    ip[up_is_left(state->zero_parent) ? 0 : 1] = static_cast<int32_t>(m - 1);
   }
 }
 
 // 1-leaf tree: pseudo root with the leaf on the left and an empty box right.
 template <int D, class Src>
 __global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, float4* nodes,
-                              float4* leaf_pt, int4* node_info, int32_t* leaf_up) {
-  node_info[0] = make_int4(kNoParent, 0, 0, 0);
-  leaf_up[0] = kUpLeftBit;
+                              float4* leaf_pt) {
   using T = NodeTraits<D>;
   float lo[3], hi[3];
   src.box(0, lo, hi);
@@ -371,7 +291,7 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   const int64_t m = src.count;
   BuiltBvh out;
   out.tree.num_leaves = static_cast<int32_t>(m);
-  const int64_t num_nodes = std::max<int64_t>(1, m - 1);
+  const int64_t num_nodes = std::max<int64_t>(1, m);  // m - 1 internal + 1 spare (k_root_to_zero)
   out.tree.nodes = scratch.alloc_n<float4>(num_nodes * NodeTraits<D>::kVec);
   if (points_mode) out.leaf_pt = scratch.alloc_n<float4>(m);
 
@@ -410,33 +330,19 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   if (clock) clock->mark(kStTopo);
   float4* leaf_pt = out.leaf_pt;
   out.codes = codes;
-  out.node_info = scratch.alloc_n<int4>(std::max<int64_t>(1, m - 1));
-  out.leaf_up = scratch.alloc_n<int32_t>(m);
   uint32_t* scene = scratch.alloc_n<uint32_t>(8);
   TCB_CUDA(cudaMemcpyAsync(scene, &d_ctr->bounds_ord[0], 6 * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, st));
   out.scene_ord = scene;
   if (m == 1) {
-    note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt,
-                                                     out.node_info, out.leaf_up);
+    note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
   } else {
-    int32_t* arrivals = scratch.alloc_n<int32_t>(m);  // [m-1] = start count
-    int32_t* starts = scratch.alloc_n<int32_t>(m / 2 + 1);
-    TCB_CUDA(cudaMemsetAsync(arrivals, 0, sizeof(int32_t) * m, st));
-    const unsigned gn = grid_for(m - 1, 256, INT32_MAX);
-    // sorted leaf boxes (points mode: the query points themselves)
-    float4* leaf_lo = points_mode ? leaf_pt : scratch.alloc_n<float4>(m);
-    float4* leaf_hi = points_mode ? leaf_pt : scratch.alloc_n<float4>(m);
-    note_launch(), k_gather_leaves<D><<<grid_for(m, 256), 256, 0, st>>>(boxes, order, m, leaf_lo,
-                                                                         leaf_hi);
-    note_launch(), k_karras<D><<<gn, 256, 0, st>>>(leaf_lo, leaf_hi, codes, order, src.aux, m,
-                                                   out.tree.nodes, out.node_info, out.leaf_up,
-                                                   starts, arrivals + (m - 1));
-    note_launch(), k_small_boxes<D><<<grid_for(m, 256), 256, 0, st>>>(leaf_lo, leaf_hi,
-                                                                       out.node_info, m,
-                                                                       out.tree.nodes);
-    note_launch(), k_refit<D><<<grid_for(m / 2 + 1, 256, INT32_MAX), 256, 0, st>>>(
-        starts, arrivals + (m - 1), out.tree.nodes, out.node_info, arrivals);
+    int32_t* other = scratch.alloc_n<int32_t>(m - 1);
+    auto* state = scratch.alloc_n<ClimbState>(1);
+    TCB_CUDA(cudaMemsetAsync(other, 0xff, sizeof(int32_t) * (m - 1), st));
+    note_launch(), k_climb<D><<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
+        boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, state);
+    note_launch(), k_root_to_zero<D><<<1, NodeTraits<D>::kVec, 0, st>>>(out.tree.nodes, m, state);
   }
   TCB_CUDA(cudaGetLastError());
   return out;

@@ -478,7 +478,8 @@ __device__ __forceinline__ void run_query_queue(int64_t m, unsigned long long* n
 // Device view of a built tree.
 struct DeviceBvh {
   int32_t num_leaves = 0;
-  float4* nodes = nullptr;        // max(1, num_leaves-1) nodes, NodeTraits<D>::kVec float4 each
+  float4* nodes = nullptr;        // num_leaves - 1 nodes (root at 0) + 1 spare slot,
+                                  // NodeTraits<D>::kVec float4 each
   int32_t* leaf_order = nullptr;  // leaf rank -> primitive index (sorted values)
 };
 

@@ -47,7 +47,7 @@ void point_bvh(const float* d_coords, int64_t n, Scratch& scratch, std::vector<f
   src.coords = d_coords;
   src.count = n;
   BuiltBvh b = build_bvh<D>(src, true, ctr, scratch, nullptr);
-  const int64_t nn = n > 1 ? n - 1 : 1;
+  const int64_t nn = n > 1 ? n : 1;  // n - 1 internal nodes + the spare slot
   nodes.resize(static_cast<size_t>(nn * NodeTraits<D>::kVec));
   order.resize(static_cast<size_t>(n));
   TCB_CUDA(cudaMemcpyAsync(nodes.data(), b.tree.nodes, nodes.size() * sizeof(float4),
@@ -101,14 +101,27 @@ TC_EXPORT tc_status tcg_debug_point_bvh(const float* coords, int64_t n, int dim,
         point_bvh<3>(d, n, scratch, nodes, order);
     }
     std::memcpy(leaf_ids, order.data(), sizeof(int32_t) * n);
+    if (n == 1) return TC_OK;
+    // Our internal nodes are numbered by split (root moved to 0, k_climb);
+    // the reference numbers them Karras-style: the root is 0, a left child
+    // is named by the last rank of its range, a right child by the first.
     const int kv = dim == 3 ? 4 : 3;
-    for (int64_t i = 0; i + 1 < n; ++i) {
-      const float* f = reinterpret_cast<const float*>(nodes.data() + i * kv);
+    struct Item {
+      int32_t ours, karras, lo, hi;
+    };
+    std::vector<Item> todo{{0, 0, 0, static_cast<int32_t>(n - 1)}};
+    while (!todo.empty()) {
+      const Item it = todo.back();
+      todo.pop_back();
+      const float* f = reinterpret_cast<const float*>(nodes.data() + static_cast<int64_t>(it.ours) * kv);
       const int32_t* ii = reinterpret_cast<const int32_t*>(f + 4 * dim);
-      left[i] = ii[0];
-      right[i] = ii[1];
-      // Subtree max rank = right child's max (its range is the upper part).
-      max_rank[i] = ii[1] < 0 ? ~ii[1] : ii[3];
+      const int32_t split = ii[0] < 0 ? ~ii[0] : ii[2];  // last rank of the left child
+      const int32_t i = it.karras;
+      left[i] = ii[0] < 0 ? ii[0] : split;
+      right[i] = ii[1] < 0 ? ii[1] : split + 1;
+      max_rank[i] = it.hi;
+      if (ii[0] >= 0) todo.push_back({ii[0], split, it.lo, split});
+      if (ii[1] >= 0) todo.push_back({ii[1], split + 1, split + 1, it.hi});
       // Own box = union of the two child boxes stored in the node.
       for (int k = 0; k < 3; ++k) {
         float lo = 0.f, hi = 0.f;

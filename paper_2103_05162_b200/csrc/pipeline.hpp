@@ -93,10 +93,6 @@ struct BuiltBvh {
   DeviceBvh tree;
   float4* leaf_pt = nullptr;          // points mode only: rank -> (x, y, z, id bits)
   const uint64_t* codes = nullptr;    // sorted Morton codes (leaf rank order)
-  // internal node -> {parent | kUpLeftBit if it is its parent's left child
-  // (kNoParent at the root), common prefix length of its codes, lo, hi rank}
-  int4* node_info = nullptr;
-  int32_t* leaf_up = nullptr;         // leaf rank -> parent | kUpLeftBit
   const uint32_t* scene_ord = nullptr;  // Morton scene box (order-preserving bits, 6)
   int sort_passes = 0;
 };
