@@ -162,6 +162,8 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
 // The tree is the reference's tree node for node; only the numbering of the
 // internal nodes differs (tcg_debug_point_bvh renumbers to Karras indices).
 // ---------------------------------------------------------------------------
+constexpr int kClimbBlock = 256;
+
 struct ClimbState {
   int32_t root;         // split index of the root
   int32_t zero_parent;  // parent of internal node 0 | kUpLeftBit if left child
@@ -178,13 +180,12 @@ __device__ __forceinline__ int32_t atom_exch_release(int32_t* p, int32_t v) {
 }
 
 template <int D, class Src>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kClimbBlock)
 k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
         const int32_t* __restrict__ prim_aux, int64_t m, float4* nodes,
         int32_t* __restrict__ other, float4* __restrict__ leaf_pt, ClimbState* state) {
   using T = NodeTraits<D>;
   const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (blockIdx.x * static_cast<int64_t>(blockDim.x) >= m) return;
   bool active = s < m;
   float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
   int32_t l = 0, r = 0, link = 0, aux = 0;
@@ -196,6 +197,91 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
     link = ~l;
     aux = prim_aux ? prim_aux[prim] : prim;
   }
+
+  // ---- block-local phase: every node whose two children lie inside this
+  // block's 256 leaves is finished here through shared memory — the left
+  // child's thread reads the right child's box and writes the whole record;
+  // no exchange, no fence. Subtrees stay a partition of the block's leaves,
+  // each held by the thread of its first leaf; s_start[end] is the first leaf
+  // of the subtree ending at `end` (a right child's way to its left sibling).
+  {
+    __shared__ float s_box[2 * D][kClimbBlock];
+    __shared__ int32_t s_r[kClimbBlock], s_link[kClimbBlock], s_aux[kClimbBlock];
+    __shared__ int32_t s_code[kClimbBlock], s_start[kClimbBlock];
+    const int t = threadIdx.x;
+    const int64_t b0 = s - t;
+    const int64_t b1 = min(b0 + kClimbBlock - 1, m - 1);
+    auto publish = [&] {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        s_box[k][t] = lo[k];
+        s_box[D + k][t] = hi[k];
+      }
+      s_r[t] = r;
+      s_link[t] = link;
+      s_aux[t] = aux;
+    };
+    if (active) {
+      publish();
+      s_start[t] = l;
+    }
+    while (true) {
+      bool left = false;
+      int32_t p = 0;
+      if (active) {
+        left = l == 0 || (r != m - 1 && key_delta(codes, m, r, r + 1) > key_delta(codes, m, l - 1, l));
+        p = left ? r : l - 1;
+      }
+      s_code[t] = active ? (2 | (left ? 1 : 0)) : 0;  // alive | left child
+      __syncthreads();
+      const bool as_left = active && left && r + 1 <= b1 && s_code[r + 1 - b0] == 2;
+      const bool as_right =
+          active && !left && l - 1 >= b0 && s_code[s_start[l - 1 - b0] - b0] == 3;
+      if (!__syncthreads_or(as_left)) break;
+      if (as_left) {
+        const int u = static_cast<int>(r + 1 - b0);  // the right child's thread
+        float rec[T::kFloats];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          rec[k] = lo[k];
+          rec[D + k] = hi[k];
+          rec[2 * D + k] = s_box[k][u];
+          rec[3 * D + k] = s_box[D + k][u];
+        }
+        const int32_t slink = s_link[u];
+        rec[T::kIntOff + 0] = __int_as_float(link);
+        rec[T::kIntOff + 1] = __int_as_float(slink);
+        rec[T::kIntOff + 2] = __int_as_float(aux);
+        rec[T::kIntOff + 3] = __int_as_float(s_aux[u]);
+        float4* dst = nodes + static_cast<int64_t>(p) * T::kVec;
+#pragma unroll
+        for (int v = 0; v < T::kVec; ++v)
+          __stcg(dst + v, make_float4(rec[4 * v], rec[4 * v + 1], rec[4 * v + 2], rec[4 * v + 3]));
+        if (link == 0) state->zero_parent = p | kUpLeftBit;
+        if (slink == 0) state->zero_parent = p;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          lo[k] = fminf(lo[k], rec[2 * D + k]);
+          hi[k] = fmaxf(hi[k], rec[3 * D + k]);
+        }
+        r = s_r[u];
+        link = p;
+        aux = r;
+        if (l == 0 && r == m - 1) {
+          state->root = p;
+          active = false;
+        }
+      }
+      if (as_right) active = false;  // finished by the left sibling's thread
+      __syncthreads();
+      if (as_left) {
+        publish();
+        s_start[r - b0] = l;
+      }
+    }
+  }
+
+  // ---- global phase: climb through exchanges on the parents' `other` word
   while (__any_sync(0xffffffffu, active)) {
     int32_t p = 0;
     bool left = false;
@@ -340,7 +426,7 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     int32_t* other = scratch.alloc_n<int32_t>(m - 1);
     auto* state = scratch.alloc_n<ClimbState>(1);
     TCB_CUDA(cudaMemsetAsync(other, 0xff, sizeof(int32_t) * (m - 1), st));
-    note_launch(), k_climb<D><<<grid_for(m, 256, INT32_MAX), 256, 0, st>>>(
+    note_launch(), k_climb<D><<<grid_for(m, kClimbBlock, INT32_MAX), kClimbBlock, 0, st>>>(
         boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, state);
     note_launch(), k_root_to_zero<D><<<1, NodeTraits<D>::kVec, 0, st>>>(out.tree.nodes, m, state);
   }
