@@ -223,8 +223,10 @@ constexpr int kStop = 0, kTaken = 1, kWalk = 2;
 // [lo, split], its right child [split + 1, hi]; the root covers [0, n-1]), so
 // that a contained internal child is reported as its unmasked leaf-rank range
 // instead of being walked:
-//     bool visit(int32_t rank, int32_t aux)     leaf `rank` is within eps
-//                                               (false = stop the query)
+//     bool visit(int32_t rank, int32_t aux, bool contained)
+//                                               leaf `rank` is within eps
+//                                               (its whole box when contained;
+//                                               false = stop the query)
 //     int inside(int32_t first, int32_t last)   every rank in [first, last]
 //                                               (first >= min_rank) is a hit:
 //                                               kStop, kTaken, or kWalk (not
@@ -260,7 +262,7 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   if (max_r < min_rank) cr = 0;
   if (cl > 0 && (leaf_l || cl == 2)) {
     if (leaf_l) {
-      if (!visit(~left, aux_l)) return false;
+      if (!visit(~left, aux_l, cl == 2)) return false;
     } else {
       const int a = inside(lo_l, aux_l);
       if (a == kStop) return false;
@@ -269,7 +271,7 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   }
   if (cr > 0 && (leaf_r || cr == 2)) {
     if (leaf_r) {
-      if (!visit(~right, aux_r)) return false;
+      if (!visit(~right, aux_r, cr == 2)) return false;
     } else {
       const int a = inside(lo_r, aux_r);
       if (a == kStop) return false;

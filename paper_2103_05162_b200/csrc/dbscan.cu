@@ -20,6 +20,7 @@
 #include "device_common.cuh"
 #include "pipeline.hpp"
 #include "primitives.cuh"
+#include "cover.cuh"
 
 namespace tcb {
 
@@ -70,7 +71,7 @@ struct CoreQuery {
     return true;
   }
   __device__ bool step() {
-    auto visit = [&](int32_t, int32_t) -> bool {
+    auto visit = [&](int32_t, int32_t, bool) -> bool {
       ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
@@ -151,7 +152,7 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
     const bool core_r = flags[rank] != 0;
     int32_t hint = rank;
     bool settled = false;
-    auto visit = [&](int32_t s, int32_t) -> bool {
+    auto visit = [&](int32_t s, int32_t, bool) -> bool {
       ++pairs;
       resolve_pair_keyed(rank, s, core_r, flags, parent, key, hint, settled);
       return true;
@@ -215,7 +216,7 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
   warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
   if (valid) {
     int32_t hint = rank;
-    auto visit = [&](int32_t s, int32_t) -> bool {
+    auto visit = [&](int32_t s, int32_t, bool) -> bool {
       ++pairs;
       TCB_PROBE_ONLY(++pr[2];)
       uf_unite_hinted_keyed(parent, key, rank, s, hint);
@@ -239,101 +240,6 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
   TCB_PROBE_ONLY(for (int k = 0; k < 6; ++k) flush_counter(&ctr->probe[k], pr[k]);
                  const unsigned wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(pr[6]));
                  if ((threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[6], wmax);)
-}
-
-// ---- covered runs: rank l joins l - 1 iff some recorded run [f, t] has
-// f < l <= t, i.e. iff max(reach[0 .. l-1]) >= l. A max-scan in three
-// kernels over tiles of kCoverTile ranks: tile maxima, a one-block scan of
-// those, then the tile-local scan that performs the unions.
-constexpr int kCoverThreads = 256;
-constexpr int kCoverItems = 8;
-constexpr int kCoverTile = kCoverThreads * kCoverItems;
-
-__device__ __forceinline__ void load_tile(const int32_t* __restrict__ reach, int64_t n,
-                                          int64_t base, int32_t* v) {
-  const int64_t i0 = base + threadIdx.x * kCoverItems;
-  if (i0 + kCoverItems <= n) {
-    const int4 a = __ldg(reinterpret_cast<const int4*>(reach + i0));
-    const int4 b = __ldg(reinterpret_cast<const int4*>(reach + i0) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < kCoverItems; ++k) v[k] = i0 + k < n ? reach[i0 + k] : -1;
-  }
-}
-
-__global__ void __launch_bounds__(kCoverThreads)
-k_cover_tiles(const int32_t* __restrict__ reach, int64_t n, int32_t* __restrict__ tile_max) {
-  __shared__ int32_t red[32];
-  int32_t v[kCoverItems];
-  load_tile(reach, n, blockIdx.x * static_cast<int64_t>(kCoverTile), v);
-  int32_t mx = v[0];
-#pragma unroll
-  for (int k = 1; k < kCoverItems; ++k) mx = max(mx, v[k]);
-  mx = block_reduce(mx, [](int32_t a, int32_t b) { return max(a, b); }, -1, red);
-  if (threadIdx.x == 0) tile_max[blockIdx.x] = mx;
-}
-
-// Exclusive max-scan of the tile maxima, one block (each thread a contiguous
-// chunk).
-__global__ void __launch_bounds__(1024)
-k_cover_carry(int32_t* __restrict__ tile_max, int64_t tiles) {
-  __shared__ int32_t part[1024];
-  const int64_t per = (tiles + blockDim.x - 1) / blockDim.x;
-  const int64_t b = threadIdx.x * per, e = min(b + per, tiles);
-  int32_t mx = -1;
-  for (int64_t t = b; t < e; ++t) mx = max(mx, tile_max[t]);
-  part[threadIdx.x] = mx;
-  __syncthreads();
-  for (int o = 1; o < static_cast<int>(blockDim.x); o <<= 1) {
-    int32_t x = threadIdx.x >= static_cast<unsigned>(o) ? part[threadIdx.x - o] : -1;
-    __syncthreads();
-    part[threadIdx.x] = max(part[threadIdx.x], x);
-    __syncthreads();
-  }
-  int32_t run = threadIdx.x > 0 ? part[threadIdx.x - 1] : -1;
-  for (int64_t t = b; t < e; ++t) {
-    const int32_t x = tile_max[t];
-    tile_max[t] = run;
-    run = max(run, x);
-  }
-}
-
-__global__ void __launch_bounds__(kCoverThreads)
-k_cover_unite(const int32_t* __restrict__ reach, int64_t n, const int32_t* __restrict__ carry,
-              int32_t* __restrict__ parent, const int32_t* __restrict__ key) {
-  __shared__ int32_t warp_max[kCoverThreads / 32];
-  const int64_t base = blockIdx.x * static_cast<int64_t>(kCoverTile);
-  int32_t v[kCoverItems];
-  load_tile(reach, n, base, v);
-  int32_t mine = v[0];
-#pragma unroll
-  for (int k = 1; k < kCoverItems; ++k) mine = max(mine, v[k]);
-  // exclusive max over the threads before this one (warp scan + warp totals)
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int32_t inc = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc = max(inc, x);
-  }
-  if (lane == 31) warp_max[w] = inc;
-  __syncthreads();
-  int32_t run = max(carry[blockIdx.x], __shfl_up_sync(0xffffffffu, inc, 1));
-  if (lane == 0) run = carry[blockIdx.x];
-  for (int k = 0; k < w; ++k) run = max(run, warp_max[k]);
-  const int64_t i0 = base + threadIdx.x * kCoverItems;
-#pragma unroll
-  for (int k = 0; k < kCoverItems; ++k) {
-    const int64_t l = i0 + k;
-    if (l < n && run >= l && l > 0) {
-      const int32_t a = static_cast<int32_t>(l);
-      const int32_t pa = ld_relaxed(parent + a), pb = ld_relaxed(parent + a - 1);
-      if (pa != pb && pa != a - 1 && pb != a) uf_unite_keyed(parent, key, a, a - 1);
-    }
-    run = max(run, v[k]);
-  }
 }
 
 __global__ void k_permute(const uint8_t* __restrict__ src, const int32_t* __restrict__ order,
@@ -449,10 +355,8 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
   cudaStream_t s = scratch.stream();
   const BallTest bt = BallTest::make(eps2);
   const unsigned grid = grid_for(n, kQueryBlock, INT32_MAX);
-  const int64_t tiles = (n + kCoverTile - 1) / kCoverTile;
-  const unsigned tgrid = static_cast<unsigned>(tiles);
-  int32_t* reach = scratch.alloc_n<int32_t>(n + kCoverItems);
-  int32_t* tile_max = scratch.alloc_n<int32_t>(tiles);
+  int32_t* reach = scratch.alloc_n<int32_t>(n + cover_detail::kCoverItems);
+  int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(n));
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
   if (force_core) {
     note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
@@ -468,10 +372,7 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
                                                              noncore_before, reach, d_ctr);
   }
   // covered runs (all-core): join each covered rank to its predecessor
-  note_launch(), k_cover_tiles<<<tgrid, kCoverThreads, 0, s>>>(reach, n, tile_max);
-  note_launch(), k_cover_carry<<<1, 1024, 0, s>>>(tile_max, tiles);
-  note_launch(), k_cover_unite<<<tgrid, kCoverThreads, 0, s>>>(reach, n, tile_max, parent,
-                                                               b.tree.leaf_order);
+  launch_cover_joins(reach, n, tile_max, KeyedJoin{parent, b.tree.leaf_order}, s);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -24,6 +24,8 @@
 #include "device_common.cuh"
 #include "pipeline.hpp"
 #include "primitives.cuh"
+#include "cover.cuh"
+#include "member_tree.cuh"
 
 namespace tcb {
 
@@ -284,6 +286,7 @@ struct DbCoreQuery {
   int minpts;
   uint8_t* __restrict__ flags;
   int32_t* stack;  // per-thread traversal stack, kept outside the struct
+  const MemberTree* mt;
   unsigned long long dists = 0;
   float p[3];
   int32_t id, node, mask_rank = 0;
@@ -315,13 +318,13 @@ struct DbCoreQuery {
           dists += take;
           count += take;
         } else {
-          for (int32_t k = kb; k < ke; ++k) {
-            const float4 m4 = __ldg(sorted_pt + k);
-            const float mp[3] = {m4.x, m4.y, m4.z};
-            ++dists;
-            if (ball_hits<D>(p, mp, mp, bt))
-              if (++count >= minpts) break;
-          }
+          // the member-by-member scan (dbscan.cpp:124-131), answered by the
+          // member tree: same stopping position, same counts
+          int hits;
+          const int64_t pos = member_scan<D>(*mt, kb, ke, p, bt, minpts - count, hits);
+          dists += pos >= 0 ? static_cast<unsigned long long>(pos - kb + 1)
+                            : static_cast<unsigned long long>(ke - kb);
+          count += hits;
         }
       }
       return count < minpts;
@@ -413,9 +416,9 @@ __global__ void __launch_bounds__(kQueryBlock)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
-          uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent) {
+          uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent, MemberTree mt) {
   int32_t stack[kStackDepth];
-  DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, stack};
+  DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, stack, &mt};
   if (persistent)
     run_query_queue(n, &ctr->queue[2], q);
   else
@@ -444,7 +447,203 @@ k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
 }
 
+// densebox_main_phase with contained subtrees (direct launch). A subtree of
+// the mixed tree whose box lies inside the ball holds primitives that each
+// give exactly one pair and one distance evaluation in the reference (a
+// SinglePoint within eps; a DenseBox whose first member is within eps), so a
+// run of primitive ranks [first, last] is counted at once; rep[rank] is the
+// primitive's point (a DenseBox's first member — dense members are core and
+// pre-unioned). Resolution as in k_fd_main: a core query takes runs of core
+// primitives (unite with rep[first], run recorded for the cover pass), a
+// border query counts coreless runs and every run once claimed; other runs
+// are walked. minpts == 2: every run is taken (all pairs are unions).
+template <int D, bool kForceCore>
+__global__ void __launch_bounds__(kQueryBlock)
+k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
+                 const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
+                 const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
+                 BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+                 const int32_t* __restrict__ rep, const int32_t* __restrict__ noncore_before,
+                 int32_t* __restrict__ reach, DevCounters* ctr, MemberTree mt) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = q < n;
+  unsigned long long pairs = 0, dists = 0;
+  float p[3] = {0.f, 0.f, 0.f};
+  int32_t i = 0, own = 0;
+  if (valid) {
+    const float4 qp = qpt[q];
+    i = __float_as_int(qp.w) & 0x7fffffff;
+    own = qrank[q];
+    p[0] = qp.x;
+    p[1] = qp.y;
+    p[2] = qp.z;
+  }
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, own + 1, node, nlo);
+  if (valid) {
+    const bool core_i = kForceCore ? true : flags[i] != 0;
+    int32_t hint = i;
+    bool settled = false;
+    auto pair = [&](int32_t j) {
+      ++pairs;
+      if (kForceCore)
+        uf_unite_hinted(parent, i, j, hint);  // core flags derived at finalize
+      else
+        resolve_pair(i, j, core_i, flags, parent, hint, settled);
+    };
+    auto visit = [&](int32_t, int32_t aux, bool contained) -> bool {
+      if (aux >= 0) {
+        ++dists;
+        pair(aux);
+      } else {
+        const int32_t c = ~aux;
+        const int32_t kb = cell_begin[c], ke = cell_end[c];
+        if (contained) {  // every member within eps: the scan stops at the first
+          ++dists;
+          pair(__float_as_int(__ldg(sorted_pt + kb).w));
+        } else {
+          // scan to the first member within eps (dbscan.cpp:183-193), answered
+          // by the member tree: same member, same evaluation count
+          int hits;
+          const int64_t pos = member_scan<D>(mt, kb, ke, p, bt, 1, hits);
+          if (pos >= 0) {
+            dists += static_cast<unsigned long long>(pos - kb + 1);
+            pair(__float_as_int(__ldg(sorted_pt + pos).w));
+          } else {
+            dists += static_cast<unsigned long long>(ke - kb);
+          }
+        }
+      }
+      return true;
+    };
+    auto inside = [&](int32_t first, int32_t last) -> int {
+      const int32_t cnt = last - first + 1;
+      bool run = kForceCore;
+      if (!kForceCore) {
+        const int32_t nc = __ldg(noncore_before + last + 1) - __ldg(noncore_before + first);
+        if (core_i) {
+          if (nc != 0) return kWalk;
+          run = true;
+        } else if (!settled && nc != cnt) {
+          if (nc != 0) return kWalk;
+          if (ld_relaxed(parent + i) == i) uf_claim(parent, i, uf_find(parent, __ldg(rep + first)));
+          settled = true;
+        }
+      }
+      if (run) {
+        uf_unite_hinted(parent, i, __ldg(rep + first), hint);
+        if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
+      }
+      pairs += static_cast<unsigned long long>(cnt);
+      dists += static_cast<unsigned long long>(cnt);
+      return kTaken;
+    };
+    LocalStack stack;
+    while (bvh_step_ranged<D>(nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
+    }
+  }
+  unsigned long long v = warp_sum(dists);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
+  v = warp_sum(pairs);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
+}
+
+// Member tree levels (member_tree.cuh): level 1 from the points, level l from
+// level l - 1.
+template <int D>
+__global__ void k_member_level(const float4* __restrict__ pts, const float4* __restrict__ child,
+                               float4* __restrict__ out, int64_t count, bool from_points) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < count;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float lo[3], hi[3];
+    if (from_points) {
+      const float4 a = pts[2 * j], b = pts[2 * j + 1];
+      lo[0] = fminf(a.x, b.x);
+      lo[1] = fminf(a.y, b.y);
+      lo[2] = fminf(a.z, b.z);
+      hi[0] = fmaxf(a.x, b.x);
+      hi[1] = fmaxf(a.y, b.y);
+      hi[2] = fmaxf(a.z, b.z);
+    } else if (D == 2) {
+      const float4 a = child[2 * j], b = child[2 * j + 1];
+      lo[0] = fminf(a.x, b.x);
+      lo[1] = fminf(a.y, b.y);
+      hi[0] = fmaxf(a.z, b.z);
+      hi[1] = fmaxf(a.w, b.w);
+    } else {
+      const float4 al = child[4 * j], ah = child[4 * j + 1], bl = child[4 * j + 2],
+                   bh = child[4 * j + 3];
+      lo[0] = fminf(al.x, bl.x);
+      lo[1] = fminf(al.y, bl.y);
+      lo[2] = fminf(al.z, bl.z);
+      hi[0] = fmaxf(ah.x, bh.x);
+      hi[1] = fmaxf(ah.y, bh.y);
+      hi[2] = fmaxf(ah.z, bh.z);
+    }
+    if (D == 2) {
+      out[j] = make_float4(lo[0], lo[1], hi[0], hi[1]);
+    } else {
+      out[2 * j] = make_float4(lo[0], lo[1], lo[2], 0.f);
+      out[2 * j + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+    }
+  }
+}
+
+// rep[rank]: the primitive's point (a DenseBox's first member); ind[rank] = 1
+// for a SinglePoint that is not core (after the core pass), for the
+// noncore prefix counts.
+__global__ void k_prim_reps(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
+                            const int32_t* __restrict__ cell_begin,
+                            const float4* __restrict__ sorted_pt, int64_t m,
+                            int32_t* __restrict__ rep) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t a = prim_aux[order[s]];
+    rep[s] = a >= 0 ? a : __float_as_int(sorted_pt[cell_begin[~a]].w);
+  }
+}
+
+__global__ void k_prim_noncore(const int32_t* __restrict__ order,
+                               const int32_t* __restrict__ prim_aux,
+                               const uint8_t* __restrict__ flags, int64_t m,
+                               int32_t* __restrict__ ind) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s <= m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t v = 0;
+    if (s < m) {
+      const int32_t a = prim_aux[order[s]];
+      v = a >= 0 && !flags[a];
+    }
+    ind[s] = v;
+  }
+}
+
 }  // namespace
+
+template <int D>
+MemberTree build_member_tree(const float4* pts, int64_t n, Scratch& scratch) {
+  MemberTree t;
+  t.pts = pts;
+  constexpr int per = D == 2 ? 1 : 2;  // float4 per box
+  int64_t total = 0;
+  int levels = 0;
+  for (int l = 1; l <= kMemberLevels - 1 && (n >> l) > 0; ++l) {
+    t.off[l] = total;
+    total += per * (n >> l);
+    levels = l;
+  }
+  t.levels = levels;
+  if (levels == 0) return t;
+  float4* boxes = scratch.alloc_n<float4>(total);
+  t.boxes = boxes;
+  for (int l = 1; l <= levels; ++l) {
+    const int64_t count = n >> l;
+    note_launch(), k_member_level<D><<<grid_for(count, 256), 256, 0, scratch.stream()>>>(
+        pts, l > 1 ? boxes + t.off[l - 1] : nullptr, boxes + t.off[l], count, l == 1);
+  }
+  TCB_CUDA(cudaGetLastError());
+  return t;
+}
 
 template <int D>
 void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
@@ -572,14 +771,42 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
                                                  qpt, qrank, parent, flags);
   TCB_CUDA(cudaGetLastError());
 
+  const MemberTree mt = build_member_tree<D>(sorted_pt, n, scratch);
+
   // ---- core pass ----
   clock.mark(kStCore);
   if (minpts > 2)
-    note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, n, sorted_pt, cell_begin,
-                                             cell_end, bt, minpts, flags, ctr, query_mode() == 1);
+    note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, n), kQueryBlock, 0, st>>>(
+        b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr,
+        query_mode() == 1, mt);
   // ---- main pass ----
   clock.mark(kStMain);
-  if (minpts == 2)
+  if (query_mode() != 1) {
+    int32_t* rep = scratch.alloc_n<int32_t>(num_prims);
+    int32_t* reach = scratch.alloc_n<int32_t>(num_prims + 8);
+    int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(num_prims));
+    int32_t* noncore_before = nullptr;
+    TCB_CUDA(cudaMemsetAsync(reach, 0xff, sizeof(int32_t) * num_prims, st));
+    note_launch(), k_prim_reps<<<grid_for(num_prims, 256), 256, 0, st>>>(
+        b.tree.leaf_order, prim_aux, cell_begin, sorted_pt, num_prims, rep);
+    if (minpts > 2) {
+      int32_t* ind = scratch.alloc_n<int32_t>(num_prims + 1);
+      noncore_before = scratch.alloc_n<int32_t>(num_prims + 1);
+      note_launch(), k_prim_noncore<<<grid_for(num_prims + 1, 256), 256, 0, st>>>(
+          b.tree.leaf_order, prim_aux, flags, num_prims, ind);
+      exclusive_scan_i32(ind, noncore_before, num_prims + 1, nullptr, scan_tmp, st);
+    }
+    const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
+    if (minpts == 2)
+      note_launch(), k_db_main_ranged<D, true><<<g, kQueryBlock, 0, st>>>(
+          b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
+          noncore_before, reach, ctr, mt);
+    else
+      note_launch(), k_db_main_ranged<D, false><<<g, kQueryBlock, 0, st>>>(
+          b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
+          noncore_before, reach, ctr, mt);
+    launch_cover_joins(reach, num_prims, tile_max, RepJoin{parent, rep}, st);
+  } else if (minpts == 2)
     note_launch(), k_db_main<D, true><<<query_grid(k_db_main<D, true>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
                                                    cell_begin, cell_end, bt, flags, parent,
                                                    ctr, query_mode() == 1);
