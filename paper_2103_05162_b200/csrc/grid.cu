@@ -625,21 +625,28 @@ MemberTree build_member_tree(const float4* pts, int64_t n, Scratch& scratch) {
   MemberTree t;
   t.pts = pts;
   constexpr int per = D == 2 ? 1 : 2;  // float4 per box
+  int64_t off[kMemberLevels + 1] = {};
   int64_t total = 0;
   int levels = 0;
   for (int l = 1; l <= kMemberLevels - 1 && (n >> l) > 0; ++l) {
-    t.off[l] = total;
+    off[l] = total;
     total += per * (n >> l);
     levels = l;
   }
   t.levels = levels;
   if (levels == 0) return t;
   float4* boxes = scratch.alloc_n<float4>(total);
+  int64_t* d_off = scratch.alloc_n<int64_t>(kMemberLevels + 1);
+  auto* h_off = static_cast<int64_t*>(pinned_staging(sizeof(off)));
+  std::memcpy(h_off, off, sizeof(off));
+  TCB_CUDA(cudaMemcpyAsync(d_off, h_off, sizeof(off), cudaMemcpyHostToDevice, scratch.stream()));
+  TCB_CUDA(cudaStreamSynchronize(scratch.stream()));  // the staging buffer is reused
   t.boxes = boxes;
+  t.off = d_off;
   for (int l = 1; l <= levels; ++l) {
     const int64_t count = n >> l;
     note_launch(), k_member_level<D><<<grid_for(count, 256), 256, 0, scratch.stream()>>>(
-        pts, l > 1 ? boxes + t.off[l - 1] : nullptr, boxes + t.off[l], count, l == 1);
+        pts, l > 1 ? boxes + off[l - 1] : nullptr, boxes + off[l], count, l == 1);
   }
   TCB_CUDA(cudaGetLastError());
   return t;

@@ -31,26 +31,27 @@
 namespace tcb {
 
 constexpr int kMemberLevels = 31;
-constexpr int kMemberLinear = 32;  // member runs up to this long are scanned linearly
+constexpr int kMemberLinear = 32;  // members scanned linearly before the tree takes over
 
 struct MemberTree {
   const float4* pts = nullptr;  // sorted_pt (x, y, z, id)
   const float4* boxes = nullptr;
-  int64_t off[kMemberLevels + 1] = {};  // float4 offset of level l's node 0
-  int levels = 0;                       // highest level built
+  const int64_t* off = nullptr;  // device: float4 offset of level l's node 0
+  int levels = 0;                // highest level built
 };
 
 template <int D>
 __device__ __forceinline__ void member_box(const MemberTree& t, int l, int64_t j, float* lo,
                                            float* hi) {
   if (D == 2) {
-    const float4 b = __ldg(t.boxes + t.off[l] + j);
+    const float4 b = __ldg(t.boxes + __ldg(t.off + l) + j);
     lo[0] = b.x;
     lo[1] = b.y;
     hi[0] = b.z;
     hi[1] = b.w;
   } else {
-    const float4 a = __ldg(t.boxes + t.off[l] + 2 * j), b = __ldg(t.boxes + t.off[l] + 2 * j + 1);
+    const int64_t o = __ldg(t.off + l);
+    const float4 a = __ldg(t.boxes + o + 2 * j), b = __ldg(t.boxes + o + 2 * j + 1);
     lo[0] = a.x;
     lo[1] = a.y;
     lo[2] = a.z;
@@ -68,15 +69,15 @@ __device__ __forceinline__ int64_t member_scan(const MemberTree& t, int64_t a, i
                                                const float* p, const BallTest& bt, int r,
                                                int& hits) {
   hits = 0;
-  if (b - a <= kMemberLinear) {  // short runs: the plain scan is cheaper
-    for (int64_t k = a; k < b; ++k) {
-      const float4 m4 = __ldg(t.pts + k);
-      const float m[3] = {m4.x, m4.y, m4.z};
-      if (ball_hits<D>(p, m, m, bt) && ++hits == r) return k;
-    }
-    return -1;
+  // the first members linearly (a hit is usually close when there is one),
+  // the rest of a long run through the tree
+  const int64_t lin_end = b - a <= kMemberLinear ? b : a + kMemberLinear;
+  for (int64_t k = a; k < lin_end; ++k) {
+    const float4 m4 = __ldg(t.pts + k);
+    const float m[3] = {m4.x, m4.y, m4.z};
+    if (ball_hits<D>(p, m, m, bt) && ++hits == r) return k;
   }
-  int64_t k = a;
+  int64_t k = lin_end;
   while (k < b) {
     int l = k == 0 ? 62 : __ffsll(static_cast<long long>(k)) - 1;  // alignment of k
     const int fit = 63 - __clzll(static_cast<long long>(b - k));    // largest block in [k, b)
