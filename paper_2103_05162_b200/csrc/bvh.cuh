@@ -297,6 +297,73 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   return true;
 }
 
+// bvh_step in the reference's exact visit order (leaf children at once, left
+// then right; internal children right subtree first), with contained
+// internal children taken as runs AT THEIR DFS POSITION: a contained child
+// that is next is taken now; one that waits behind its sibling goes on the
+// stack as a run entry (x = ~first, y = last) and is taken when popped. The
+// sequence of visit / inside calls is therefore the reference's leaf order
+// with each contained subtree's leaves merged into one call — what a query
+// with an order-dependent early exit (the DenseBox core pass) needs.
+//     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
+//     bool inside(int32_t first, int32_t last)    (false = stop the query)
+template <int D, typename Stack, typename Visit, typename Inside>
+__device__ __forceinline__ bool bvh_step_ordered(const float4* __restrict__ nodes, const float* p,
+                                                 const BallTest& bt, int32_t min_rank,
+                                                 int32_t& node, int32_t& nlo, Stack& stack,
+                                                 Visit& visit, Inside& inside) {
+  using T = NodeTraits<D>;
+  float f[T::kFloats];
+  load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
+  const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+  const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+  const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+  const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+  const bool leaf_l = left < 0, leaf_r = right < 0;
+  const int32_t split = leaf_l ? ~left : aux_l;
+  const int32_t max_r = leaf_r ? ~right : aux_r;
+  int cl = ball_classify<D>(p, f, f + D, bt);
+  int cr = ball_classify<D>(p, f + 2 * D, f + 3 * D, bt);
+  if (split < min_rank) cl = 0;
+  if (max_r < min_rank) cr = 0;
+  if (leaf_l && cl > 0 && !visit(~left, aux_l, f, f + D)) return false;
+  if (leaf_r && cr > 0 && !visit(~right, aux_r, f + 2 * D, f + 3 * D)) return false;
+  const bool go_l = !leaf_l && cl > 0, go_r = !leaf_r && cr > 0;
+  const int32_t lo_l = nlo > min_rank ? nlo : min_rank;
+  const int32_t lo_r = split + 1 > min_rank ? split + 1 : min_rank;
+  // the next subtree in DFS order: right first, the left one waits
+  bool have_next = false;
+  if (go_r) {
+    if (go_l) stack.push(cl == 2 ? make_int2(~lo_l, aux_l) : make_int2(left, nlo));
+    if (cr == 2) {
+      if (!inside(lo_r, aux_r)) return false;
+    } else {
+      node = right;
+      nlo = split + 1;
+      have_next = true;
+    }
+  } else if (go_l) {
+    if (cl == 2) {
+      if (!inside(lo_l, aux_l)) return false;
+    } else {
+      node = left;
+      have_next = true;
+    }
+  }
+  while (!have_next) {
+    int2 e;
+    if (!stack.pop(e)) return false;
+    if (e.x < 0) {
+      if (!inside(~e.x, e.y)) return false;
+    } else {
+      node = e.x;
+      nlo = e.y;
+      have_next = true;
+    }
+  }
+  return true;
+}
+
 // Traversal stacks of (node, first leaf rank) entries for bvh_step_ranged.
 struct LocalStack {  // per-thread local memory
   int2 e[kStackDepth];
@@ -375,6 +442,7 @@ __device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp,
   warp_start_node<D>(nodes, qp.p, valid, bt, valid ? qp.mask_rank : 0, node, nlo);
   if (valid) {
     qp.node = node;
+    qp.nlo = nlo;
     while (qp.step()) {
     }
     qp.end();

@@ -285,12 +285,15 @@ struct DbCoreQuery {
   BallTest bt;
   int minpts;
   uint8_t* __restrict__ flags;
-  int32_t* stack;  // per-thread traversal stack, kept outside the struct
+  LocalStack* stack;  // per-thread traversal stack, kept outside the struct
   const MemberTree* mt;
+  const int32_t* __restrict__ qoff;  // rank -> points before it (exclusive prefix)
+  int64_t n_points;
+  int32_t num_prims;
   unsigned long long dists = 0;
   float p[3];
-  int32_t id, node, mask_rank = 0;
-  int count, top;
+  int32_t id, node, nlo, mask_rank = 0;
+  int count;
   __device__ bool begin(int64_t q) {
     const float4 qp = qpt[q];
     id = __float_as_int(qp.w);
@@ -300,7 +303,8 @@ struct DbCoreQuery {
     p[2] = qp.z;
     count = 0;
     node = 0;
-    top = 0;
+    nlo = 0;
+    stack->top = 0;
     return true;
   }
   __device__ bool step() {
@@ -329,7 +333,23 @@ struct DbCoreQuery {
       }
       return count < minpts;
     };
-    return bvh_step<D>(nodes, p, bt, 0, node, top, stack, visit);
+    // a contained subtree: every point of its primitives is within eps, and
+    // the reference counts one hit and one evaluation per point in DFS order
+    // (a fully inside DenseBox included), so it adds its point count — up to
+    // the minpts stop, taken at the subtree's own DFS position
+    auto inside = [&](int32_t first, int32_t last) -> bool {
+      const int64_t end = last + 1 < num_prims ? __ldg(qoff + last + 1) : n_points;
+      const int64_t pts = end - __ldg(qoff + first);
+      if (count + pts >= minpts) {
+        dists += static_cast<unsigned long long>(minpts - count);
+        count = minpts;
+        return false;
+      }
+      dists += static_cast<unsigned long long>(pts);
+      count += static_cast<int>(pts);
+      return true;
+    };
+    return bvh_step_ordered<D>(nodes, p, bt, 0, node, nlo, *stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[id] = 1;
@@ -354,7 +374,7 @@ struct DbMainQuery {
   int32_t* stack;  // per-thread traversal stack, kept outside the struct
   unsigned long long dists = 0, pairs = 0;
   float p[3];
-  int32_t i, own, hint, node, mask_rank;
+  int32_t i, own, hint, node, nlo, mask_rank;
   int top;
   bool core_i, settled;
   __device__ bool begin(int64_t q) {
@@ -416,9 +436,11 @@ __global__ void __launch_bounds__(kQueryBlock)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
-          uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent, MemberTree mt) {
-  int32_t stack[kStackDepth];
-  DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, stack, &mt};
+          uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent, MemberTree mt,
+          const int32_t* __restrict__ qoff, int32_t num_prims) {
+  LocalStack stack;
+  DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
+                   qoff, n, num_prims};
   if (persistent)
     run_query_queue(n, &ctr->queue[2], q);
   else
@@ -785,7 +807,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   if (minpts > 2)
     note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, n), kQueryBlock, 0, st>>>(
         b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr,
-        query_mode() == 1, mt);
+        query_mode() == 1, mt, qoff, num_prims);
   // ---- main pass ----
   clock.mark(kStMain);
   if (query_mode() != 1) {
