@@ -268,3 +268,45 @@ def test_c3_full_size_properties():
     assert s0["pair_resolutions"] == 898_475_393
     assert s0["core_count"] == s1["core_count"] == 4_243_007
     assert s0["cluster_count"] == s1["cluster_count"] == 5000
+
+
+# ---------------- contained subtrees / member tree vs the reference ----------------
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("case", ["taxi2d", "blobs3d", "lattice2d"])
+def test_densebox_large_cells_exact_counters(case):
+    """DenseBox with large dense cells (hundreds to thousands of members): the
+    member-tree scans (first hit / minpts-th hit in member order) and the
+    contained-subtree runs must reproduce the reference's counters exactly,
+    together with the clustering itself."""
+    if case == "taxi2d":
+        c, eps, mp = Dataset.taxi_like(400_000, seed=3).coords(), 0.001, 300
+    elif case == "blobs3d":
+        c = Dataset.blobs(20, 15000, 3, 1.0, 0.15, 9).coords()
+        eps, mp = 0.2, 150
+    else:
+        rng = np.random.default_rng(4)
+        g = np.stack(np.meshgrid(np.arange(300), np.arange(300)), -1).reshape(-1, 2)
+        c = (g * 0.01 + rng.uniform(-0.004, 0.004, g.shape)).astype(np.float32)
+        eps, mp = 0.1, 20
+    got = tb.cluster(Dataset.from_array(c), eps, mp, Algorithm.DENSEBOX)
+    want = ref.dbscan(c, eps, mp, 1, threads=0)
+    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], case)
+    for k in ("pair_resolutions", "distance_evaluations", "cluster_count", "core_count",
+              "noise_count"):
+        assert got.stats[k] == want["stats"][k], (case, k, got.stats[k], want["stats"][k])
+    assert got.stats["dense_point_fraction"] > 0.2, case
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("minpts", [2, 7, 60])
+def test_fdbscan_contained_runs_exact_counters(minpts):
+    """FDBSCAN on dense clumps, where most pairs come from contained subtrees
+    (rank runs): pair and distance counters and the clustering equal the
+    reference's for the minpts == 2 path and the minpts > 2 path."""
+    c = Dataset.blobs(30, 8000, 3, 1.0, 0.05, 13).coords()
+    got = tb.cluster(Dataset.from_array(c), 0.03, minpts, Algorithm.FDBSCAN)
+    want = ref.dbscan(c, 0.03, minpts, 0, threads=0)
+    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], f"fd{minpts}")
+    for k in ("pair_resolutions", "distance_evaluations", "cluster_count", "core_count",
+              "noise_count"):
+        assert got.stats[k] == want["stats"][k], (minpts, k, got.stats[k], want["stats"][k])
