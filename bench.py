@@ -283,6 +283,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the Morton-range sharded path")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the Morton-range sharded path even at N=1 (its overhead vs the "
+                         "direct path)")
     args = ap.parse_args()
 
     rank = env_int("RANK", 0)
@@ -302,7 +305,7 @@ def main():
         local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    if world > 1 or args.sharded:
         backend = os.environ.get("TCB_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -310,7 +313,7 @@ def main():
             dist.init_process_group(backend)
 
     n = args.points
-    if world > 1 and not args.replicas:
+    if (world > 1 and not args.replicas) or args.sharded:
         return run_sharded(args, rank, world, dev, n)
     # Synthetic HACC-like halos; each rank its own cloud.
     ds = tb.Dataset.hacc_like(n, seed=11 + rank)

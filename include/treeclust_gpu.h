@@ -45,6 +45,15 @@ tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
                              uint8_t* d_core, void* stream,
                              tc_cluster_stats* stats);
 
+/* FDBSCAN with caller keys: d_keys[i] is a unique int32 key of point i (e.g.
+ * its global id across shards); clusters are represented by the key of their
+ * minimum-key core, so d_labels[i] = that key (or -1 for noise). With keys
+ * 0..n-1 this is tcg_cluster_device(FDBSCAN). Used by the sharded path to
+ * label a local (own + ghost) set directly in global ids. */
+tc_status tcg_cluster_keyed_device(const float* d_coords, const int32_t* d_keys, int64_t n,
+                                   int dim, float eps, int minpts, int32_t* d_labels,
+                                   uint8_t* d_core, void* stream, tc_cluster_stats* stats);
+
 /* Per-stage device milliseconds of the last tcg_cluster_device / tc_cluster
  * call on this host thread (the tc_cluster_stats phases split finer):
  * [0] bounds+morton  [1] sort  [2] topology+refit  [3] grid (DenseBox)

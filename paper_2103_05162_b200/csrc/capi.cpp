@@ -448,6 +448,21 @@ TC_EXPORT tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim
   });
 }
 
+TC_EXPORT tc_status tcg_cluster_keyed_device(const float* d_coords, const int32_t* d_keys,
+                                             int64_t n, int dim, float eps, int minpts,
+                                             int32_t* d_labels, uint8_t* d_core, void* stream,
+                                             tc_cluster_stats* stats) {
+  if (!d_keys) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    tcb::RunOutput ro;
+    tcb::run_device(d_coords, n, dim, eps, minpts, TC_ALGO_FDBSCAN, 0, d_labels, d_core,
+                    static_cast<cudaStream_t>(stream), stats != nullptr, stats ? &ro : nullptr,
+                    nullptr, d_keys);
+    if (stats) *stats = ro.stats;
+    return TC_OK;
+  });
+}
+
 TC_EXPORT int tcg_last_stage_ms(double* out, int cap) {
   if (!out || cap <= 0) return 0;
   return tcb::get_last_stage_ms(out, cap);

@@ -253,6 +253,13 @@ __global__ void k_permute(const uint8_t* __restrict__ src, const int32_t* __rest
   }
 }
 
+__global__ void k_gather_keys(const int32_t* __restrict__ keys, const int32_t* __restrict__ order,
+                              int64_t n, int32_t* __restrict__ out) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[s] = keys[order[s]];
+}
+
 __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -282,8 +289,8 @@ k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_
 // set is its minimum-key rank, so label = key[root] = minimum original index.
 __global__ void __launch_bounds__(256)
 k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
-                 const int32_t* __restrict__ key, int64_t n, int32_t* __restrict__ labels,
-                 uint8_t* __restrict__ core_out, DevCounters* ctr) {
+                 const int32_t* __restrict__ key, const int32_t* __restrict__ order, int64_t n,
+                 int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr) {
   long long noise = 0, clusters = 0, cores = 0;
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -292,12 +299,12 @@ k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags
     while (p != (q = ld_relaxed(parent + p))) p = q;
     st_relaxed(parent + s, p);
     const bool core = flags[s] != 0;
-    const int32_t i = key[s];
+    const int32_t i = order[s];
     const int32_t lab = (core || p != s) ? key[p] : -1;  // dbscan.cpp:215
     labels[i] = lab;
     core_out[i] = core ? 1 : 0;
     noise += lab == -1;
-    clusters += lab == i;
+    clusters += lab != -1 && p == s;  // label[i] == i (keys are unique)
     cores += core;
   }
   noise = warp_sum(noise);
@@ -349,8 +356,8 @@ void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
 }
 
 template <int D>
-void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
-                       uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
+void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double eps2,
+                       bool force_core, uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        Scratch& scratch) {
   cudaStream_t s = scratch.stream();
   const BallTest bt = BallTest::make(eps2);
@@ -360,7 +367,7 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
   if (force_core) {
     note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, n, bt, parent, b.tree.leaf_order, reach, d_ctr);
+        b.tree.nodes, b.leaf_pt, n, bt, parent, key, reach, d_ctr);
   } else {
     int32_t* ind = scratch.alloc_n<int32_t>(n + 1);
     int32_t* noncore_before = scratch.alloc_n<int32_t>(n + 1);
@@ -368,11 +375,11 @@ void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_cor
     note_launch(), k_noncore_ind<<<grid_for(n + 1, 256), 256, 0, s>>>(flags, n, ind);
     exclusive_scan_i32(ind, noncore_before, n + 1, nullptr, scan_tmp, s);
     note_launch(), k_fd_main<D><<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags,
-                                                             parent, b.tree.leaf_order,
+                                                             parent, key,
                                                              noncore_before, reach, d_ctr);
   }
   // covered runs (all-core): join each covered rank to its predecessor
-  launch_cover_joins(reach, n, tile_max, KeyedJoin{parent, b.tree.leaf_order}, s);
+  launch_cover_joins(reach, n, tile_max, KeyedJoin{parent, key}, s);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -382,18 +389,25 @@ void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t*
   TCB_CUDA(cudaGetLastError());
 }
 
+void gather_rank_keys(const int32_t* keys, const int32_t* order, int64_t n, int32_t* out,
+                      cudaStream_t s) {
+  note_launch(), k_gather_keys<<<grid_for(n, 256), 256, 0, s>>>(keys, order, n, out);
+  TCB_CUDA(cudaGetLastError());
+}
+
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
   note_launch(), k_init_uf<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
   TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(n), s));
   TCB_CUDA(cudaGetLastError());
 }
 
-void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key, int64_t n,
+void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
+                           const int32_t* order, int64_t n,
                            int32_t* labels, uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
                            bool force_core) {
   if (force_core) note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
-  note_launch(), k_finalize_ranks<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, key, n, labels,
-                                                                   core_out, d_ctr);
+  note_launch(), k_finalize_ranks<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, key, order, n,
+                                                                   labels, core_out, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -408,9 +422,9 @@ template void fdbscan_core_pass<2>(const BuiltBvh&, int64_t, double, int, uint8_
                                    DevCounters*, cudaStream_t);
 template void fdbscan_core_pass<3>(const BuiltBvh&, int64_t, double, int, uint8_t*,
                                    DevCounters*, cudaStream_t);
-template void fdbscan_main_pass<2>(const BuiltBvh&, int64_t, double, bool, uint8_t*,
-                                   int32_t*, DevCounters*, Scratch&);
-template void fdbscan_main_pass<3>(const BuiltBvh&, int64_t, double, bool, uint8_t*,
-                                   int32_t*, DevCounters*, Scratch&);
+template void fdbscan_main_pass<2>(const BuiltBvh&, const int32_t*, int64_t, double, bool,
+                                   uint8_t*, int32_t*, DevCounters*, Scratch&);
+template void fdbscan_main_pass<3>(const BuiltBvh&, const int32_t*, int64_t, double, bool,
+                                   uint8_t*, int32_t*, DevCounters*, Scratch&);
 
 }  // namespace tcb

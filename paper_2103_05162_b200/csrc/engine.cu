@@ -133,7 +133,8 @@ int get_last_stage_ms(double* out, int cap) {
 // ---------------------------------------------------------------------------
 template <int D>
 void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
-                 uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock) {
+                 uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
+                 const int32_t* d_keys) {
   cudaStream_t st = scratch.stream();
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
   PrimSource src;
@@ -144,21 +145,27 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
 
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
+  const int32_t* key = b.tree.leaf_order;  // rank -> original index
+  if (d_keys) {
+    int32_t* k = scratch.alloc_n<int32_t>(n);
+    gather_rank_keys(d_keys, b.tree.leaf_order, n, k, st);
+    key = k;
+  }
   clock.mark(kStCore);
   init_union_find(parent, flags, n, st);
   if (minpts > 2) fdbscan_core_pass<D>(b, n, eps2, minpts, flags, ctr, st);
   clock.mark(kStMain);
-  fdbscan_main_pass<D>(b, n, eps2, minpts == 2, flags, parent, ctr, scratch);
+  fdbscan_main_pass<D>(b, key, n, eps2, minpts == 2, flags, parent, ctr, scratch);
   clock.mark(kStFinal);
-  finalize_labels_ranks(parent, flags, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
+  finalize_labels_ranks(parent, flags, key, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
                         minpts == 2);
   clock.finish();
 }
 
 template void run_fdbscan<2>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
-                             Scratch&, StageClock&);
+                             Scratch&, StageClock&, const int32_t*);
 template void run_fdbscan<3>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
-                             Scratch&, StageClock&);
+                             Scratch&, StageClock&, const int32_t*);
 
 // ---------------------------------------------------------------------------
 // Entry
@@ -166,7 +173,7 @@ template void run_fdbscan<3>(const float*, int64_t, float, int, int32_t*, uint8_
 void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
                 tc_algorithm algo, int64_t oracle_cap, int32_t* d_labels, uint8_t* d_core,
                 cudaStream_t stream, bool want_stats, RunOutput* out,
-                const std::function<void(cudaStream_t)>& tail) {
+                const std::function<void(cudaStream_t)>& tail, const int32_t* d_keys) {
   if (dim != 2 && dim != 3) throw InvalidArgument{"PointSet: dimension must be 2 or 3"};
   if (n < 1) throw InvalidArgument{"PointSet: empty"};
   if (!(eps > 0.f) || !std::isfinite(eps))
@@ -175,6 +182,7 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
   if (n > std::numeric_limits<int32_t>::max())
     throw InvalidArgument{"dbscan_run: more than 2^31-1 points"};
   if (!d_coords || !d_labels || !d_core) throw InvalidArgument{"null buffer"};
+  if (d_keys && algo != TC_ALGO_FDBSCAN) throw InvalidArgument{"keys need FDBSCAN"};
 
   reset_launch_count();
   Scratch scratch(stream);
@@ -186,9 +194,9 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
   switch (algo) {
     case TC_ALGO_FDBSCAN:
       if (dim == 2)
-        run_fdbscan<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock);
+        run_fdbscan<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys);
       else
-        run_fdbscan<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock);
+        run_fdbscan<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys);
       break;
     case TC_ALGO_DENSEBOX:
       if (dim == 2)

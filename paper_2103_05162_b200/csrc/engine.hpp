@@ -44,7 +44,8 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
                 tc_algorithm algo, int64_t oracle_cap, int32_t* d_labels,
                 uint8_t* d_core, cudaStream_t stream, bool want_stats,
                 RunOutput* out,
-                const std::function<void(cudaStream_t)>& tail = nullptr);
+                const std::function<void(cudaStream_t)>& tail = nullptr,
+                const int32_t* d_keys = nullptr);
 
 // Kernel-launch accounting (thread-local; reset at the start of run_device).
 void note_launch();

@@ -115,17 +115,23 @@ void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s);
 // force_core (minpts == 2) uses the contained-subtree pass (k_fd_main_fof) and
 // allocates its run-coverage scratch from `scratch`.
+// key[rank]: the element's key; roots are the minimum-key element of a set.
 template <int D>
-void fdbscan_main_pass(const BuiltBvh& b, int64_t n, double eps2, bool force_core,
-                       uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
+void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double eps2,
+                       bool force_core, uint8_t* flags, int32_t* parent, DevCounters* d_ctr,
                        Scratch& scratch);
+// out[rank] = keys[order[rank]]
+void gather_rank_keys(const int32_t* keys, const int32_t* order, int64_t n, int32_t* out,
+                      cudaStream_t s);
 // Moves per-point bytes between input order and leaf-rank order:
 // to_rank: dst[r] = src[order[r]]; else dst[order[r]] = src[r].
 void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t* dst,
                    bool to_rank, cudaStream_t s);
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
 // FDBSCAN: parent / flags indexed by leaf rank, key[rank] = original index.
-void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key, int64_t n,
+// labels[order[rank]] = key of the rank's root (or -1).
+void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
+                           const int32_t* order, int64_t n,
                            int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
                            cudaStream_t s, bool force_core);
 // force_core (minpts == 2): core flags are derived here from the union-find
@@ -135,9 +141,12 @@ void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,
                      cudaStream_t s, bool force_core);
 
 // ---- whole FDBSCAN pipeline over the point BVH (engine.cu) ----
+// d_keys (optional): unique int32 key per point; labels are then the key of
+// each cluster's minimum-key core instead of its minimum index.
 template <int D>
 void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
-                 uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock);
+                 uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
+                 const int32_t* d_keys = nullptr);
 
 // ---- DenseBox (grid.cu) ----
 template <int D>

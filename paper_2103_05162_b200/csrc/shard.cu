@@ -134,8 +134,10 @@ void given_core(const float* d_coords, int64_t n, float eps, const uint8_t* d_co
   init_union_find(parent, flags, n, st);
   permute_flags(d_core_in, b.tree.leaf_order, n, flags, /*to_rank=*/true, st);
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
-  fdbscan_main_pass<D>(b, n, eps2, /*force_core=*/false, flags, parent, ctr, scratch);
-  finalize_labels_ranks(parent, flags, b.tree.leaf_order, n, d_labels, d_core_out, ctr, st,
+  fdbscan_main_pass<D>(b, b.tree.leaf_order, n, eps2, /*force_core=*/false, flags, parent, ctr,
+                       scratch);
+  finalize_labels_ranks(parent, flags, b.tree.leaf_order, b.tree.leaf_order, n, d_labels,
+                        d_core_out, ctr, st,
                         /*force_core=*/false);
   if (stats) {
     DevCounters h;

@@ -26,6 +26,12 @@ GPUs, gloo in the CPU tests); every data-path stage runs in the C-ABI library
    are global minimum ids) — the cluster representative is then the global
    minimum core id, exactly the 1-GPU label; own points are relabelled.
 
+minpts == 2 skips steps 5-6: every within-eps pair is a core-core union and
+"core" is "has a neighbour", exact for own points, so one keyed local run
+(tcg_cluster_keyed_device: own + ghost points, labels = global id of the
+cluster's minimum-id point) replaces the flag exchange, the global-id sort and
+the second tree build; step 7 takes its labels as they are.
+
 Result per rank: (global ids, labels, core flags) of the points it owns.
 """
 from __future__ import annotations
@@ -105,6 +111,20 @@ class DeviceEngine:
         self._count()
         return labels
 
+    def cluster_keyed(self, x, keys, eps, minpts):
+        """FDBSCAN of x with labels = key of the cluster's minimum-key core."""
+        n, d = x.shape
+        labels = torch.empty(n, dtype=torch.int32, device=x.device)
+        core = torch.empty(n, dtype=torch.uint8, device=x.device)
+        keys = keys.contiguous()
+        _check(lib.tcg_cluster_keyed_device(C.c_void_p(x.data_ptr()), C.c_void_p(keys.data_ptr()),
+                                            n, d, C.c_float(eps), int(minpts),
+                                            C.c_void_p(labels.data_ptr()),
+                                            C.c_void_p(core.data_ptr()), self._s(), None),
+               "tcg_cluster_keyed_device")
+        self._count()
+        return labels, core
+
     def union_edges(self, edges, n):
         root = torch.empty(n, dtype=torch.int32, device=self.device)
         edges = edges.to(device=self.device, dtype=torch.int32).contiguous()
@@ -168,6 +188,55 @@ def _all_to_all(t, send_counts, group):
     return out.to(dev), recv
 
 
+def _merge_edges(edges, root_gid, engine, group):
+    """Global merge: all-gather the (global id, local root id) edges, union
+    them (min-id hooking, so the global representative is the minimum id),
+    and map this rank's local roots to global representatives."""
+    all_edges = torch.cat(_all_gather_var(edges, group))
+    if all_edges.shape[0]:
+        uniq, comp = torch.unique(all_edges.view(-1), return_inverse=True)
+        root = engine.union_edges(comp.view(-1, 2), uniq.shape[0]).to(torch.int64)
+        rep = uniq[root]  # compact ids are ordered like global ids: min id wins
+        last = uniq.shape[0] - 1
+        pos = torch.searchsorted(uniq, root_gid.clamp(min=0))
+        hit = (root_gid >= 0) & (pos <= last) & (uniq[pos.clamp(max=last)] == root_gid)
+        root_gid = torch.where(hit, rep[pos.clamp(max=last)], root_gid)
+    return root_gid
+
+
+def _unpack(rows, dim):
+    """(coords f32 [n, dim], gid i64 [n]) from int32 rows [n, dim + 2]. Copies
+    the column slices (an empty slice keeps a storage offset that a dtype view
+    rejects)."""
+    x = rows[:, :dim].clone(memory_format=torch.contiguous_format).view(torch.float32)
+    g = rows[:, dim:].clone(memory_format=torch.contiguous_format).view(torch.int64).view(-1)
+    return x, g
+
+
+class _StageMarks:
+    """Per-stage CUDA-event times of cluster_sharded (TCB_SHARD_TIMING=1)."""
+
+    def __init__(self, dev):
+        import os
+        self.on = os.environ.get("TCB_SHARD_TIMING") == "1" and dev.type == "cuda"
+        self.ev = []
+        if self.on:
+            self.mark("1")
+
+    def mark(self, name):
+        if self.on:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.ev.append((name, e))
+
+    def report(self, rank):
+        if not self.on:
+            return
+        torch.cuda.synchronize()
+        parts = [f"{a}:{ea.elapsed_time(eb):.2f}" for (a, ea), (_, eb) in zip(self.ev, self.ev[1:])]
+        print(f"[shard rank {rank}] stage ms " + " ".join(parts), flush=True)
+
+
 # ---------------------------------------------------------------------------
 def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples=4096):
     """Clusters the union of every rank's (x, gid) points.
@@ -184,6 +253,7 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     rank = dist.get_rank(group)
     dev = x.device
     n, dim = x.shape
+    marks = _StageMarks(dev)
 
     # 1. global scene box
     if n:
@@ -195,15 +265,18 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     lo = _all_reduce(lo.clone(), dist.ReduceOp.MIN, group)
     hi = _all_reduce(hi.clone(), dist.ReduceOp.MAX, group)
 
+    marks.mark("2")
     # 2. codes and splitters
     codes = engine.morton(x, lo, hi) if n else torch.empty(0, dtype=torch.int64, device=dev)
-    scodes = torch.sort(codes).values
     k = min(n, samples)
-    if k:
-        pos = torch.div(torch.arange(k, device=dev) * n + n // 2, k, rounding_mode="floor")
-        sample = scodes[pos.clamp(max=n - 1)]
+    if k and world > 1:
+        # a pseudo-random subsample (fixed seed) stands in for the local
+        # distribution; only load balance depends on it, never correctness
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234 + rank)
+        sample = codes[torch.randint(0, n, (k,), device=dev, generator=g)]
     else:
-        sample = scodes[:0]
+        sample = codes[:0]
     allsamp = torch.sort(torch.cat(_all_gather_var(sample, group))).values
     m = allsamp.shape[0]
     if world > 1 and m:
@@ -213,19 +286,31 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
         splitters = torch.empty(0, dtype=torch.int64, device=dev)
     owner = torch.bucketize(codes, splitters, right=True)
 
-    # 3. redistribution by Morton range
-    order = torch.argsort(owner, stable=True)
-    counts = torch.bincount(owner, minlength=world).tolist() if n else [0] * world
-    payload = torch.cat([x[order].view(torch.int32), gid[order].view(torch.int32).view(-1, 2)], 1)
-    recv, _ = _all_to_all(payload, counts, group)
-    own_x = recv[:, :dim].contiguous().view(torch.float32)
-    own_gid = recv[:, dim:].contiguous().view(torch.int64).view(-1)
+    marks.mark("3")
+    # 3. redistribution by Morton range (the codes travel along: step 4
+    #    orders the own points by them)
+    if world == 1:
+        own_x, own_gid, own_codes = x.contiguous(), gid, codes
+    else:
+        order = torch.argsort(owner, stable=True)
+        counts = torch.bincount(owner, minlength=world).tolist() if n else [0] * world
+        payload = torch.cat([x[order].view(torch.int32), gid[order].view(torch.int32).view(-1, 2),
+                             codes[order].view(torch.int32).view(-1, 2)], 1)
+        recv, _ = _all_to_all(payload, counts, group)
+        own_x, own_gid = _unpack(recv[:, :dim + 2], dim)
+        own_codes = recv[:, dim + 2:].clone(memory_format=torch.contiguous_format).view(
+            torch.int64).view(-1)
     n_own = own_x.shape[0]
 
-    # 4. region boxes and the eps halo
-    if n_own:
-        oc = engine.morton(own_x, lo, hi)
-        perm = torch.argsort(oc)
+    marks.mark("4")
+    # 4. region boxes and the eps halo (a single rank has no peers)
+    if world == 1:
+        ghost_x = own_x[:0]
+        ghost_gid = own_gid[:0]
+        send_idx = torch.empty(0, dtype=torch.int64, device=dev)
+        send_counts = [0]
+    elif n_own:
+        perm = torch.argsort(own_codes)
         xs = own_x[perm]
         nb = (n_own + block - 1) // block
         padn = nb * block - n_own
@@ -235,27 +320,53 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
         boxes = torch.cat([blo, bhi], 1)
     else:
         boxes = torch.empty((0, 2 * dim), dtype=torch.float32, device=dev)
-    peer_boxes = _all_gather_var(boxes, group)
-    send_idx, send_counts = [], []
-    for j in range(world):
-        if j == rank or n_own == 0 or peer_boxes[j].shape[0] == 0:
-            send_counts.append(0)
-            continue
-        pb = peer_boxes[j]
-        mask = engine.near_boxes(own_x, eps, pb[:, :dim], pb[:, dim:])
-        idx = torch.nonzero(mask, as_tuple=False).view(-1)
-        send_idx.append(idx)
-        send_counts.append(int(idx.shape[0]))
-    send_idx = torch.cat(send_idx) if send_idx else torch.empty(0, dtype=torch.int64, device=dev)
-    halo_payload = torch.cat([own_x[send_idx].view(torch.int32),
-                              own_gid[send_idx].view(torch.int32).view(-1, 2)], 1)
-    ghost, _ = _all_to_all(halo_payload, send_counts, group)
-    ghost_x = ghost[:, :dim].contiguous().view(torch.float32)
-    ghost_gid = ghost[:, dim:].contiguous().view(torch.int64).view(-1)
+    if world > 1:
+        peer_boxes = _all_gather_var(boxes, group)
+        send_idx, send_counts = [], []
+        for j in range(world):
+            if j == rank or n_own == 0 or peer_boxes[j].shape[0] == 0:
+                send_counts.append(0)
+                continue
+            pb = peer_boxes[j]
+            mask = engine.near_boxes(own_x, eps, pb[:, :dim], pb[:, dim:])
+            idx = torch.nonzero(mask, as_tuple=False).view(-1)
+            send_idx.append(idx)
+            send_counts.append(int(idx.shape[0]))
+        send_idx = torch.cat(send_idx) if send_idx else torch.empty(0, dtype=torch.int64, device=dev)
+        halo_payload = torch.cat([own_x[send_idx].view(torch.int32),
+                                  own_gid[send_idx].view(torch.int32).view(-1, 2)], 1)
+        ghost, _ = _all_to_all(halo_payload, send_counts, group)
+        ghost_x, ghost_gid = _unpack(ghost, dim)
+
+    marks.mark("5")
+    lgid = torch.cat([own_gid, ghost_gid])
+    if minpts == 2 and hasattr(engine, "cluster_keyed") and \
+            (lgid.shape[0] == 0 or int(lgid.max().item()) < 2**31):
+        # minpts == 2 (friends-of-friends): every within-eps pair is a
+        # core-core union and core == "has a neighbour", exact for own points
+        # (complete neighbourhoods); no flag exchange is needed. One local run
+        # keyed by global id labels the own + ghost set in global ids.
+        lx = torch.cat([own_x, ghost_x]).contiguous()
+        if lx.shape[0] == 0:
+            e = torch.empty(0, dtype=torch.int64, device=dev)
+            _all_gather_var(torch.empty((0, 2), dtype=torch.int64, device=dev), group)
+            return e, e.to(torch.int32), e.to(torch.uint8)
+        lab, lcore = engine.cluster_keyed(lx, lgid.to(torch.int32), eps, 2)
+        lab = lab.to(torch.int64)
+        marks.mark("7")
+        own_lab, own_core = lab[:n_own], lcore[:n_own]
+        g_lab = lab[n_own:]
+        e_lab = own_lab[send_idx]
+        gsel, esel = g_lab >= 0, e_lab >= 0
+        edges = torch.cat([torch.stack([ghost_gid[gsel], g_lab[gsel]], 1),
+                           torch.stack([own_gid[send_idx][esel], e_lab[esel]], 1)])
+        root_gid = _merge_edges(edges, own_lab, engine, group)
+        marks.mark("end")
+        marks.report(rank)
+        return own_gid, root_gid, own_core
 
     # 5. local set ordered by global id; exact own flags; owners' ghost flags
     lx = torch.cat([own_x, ghost_x])
-    lgid = torch.cat([own_gid, ghost_gid])
     lorder = torch.argsort(lgid)
     lx = lx[lorder].contiguous()
     lgid = lgid[lorder]
@@ -274,9 +385,11 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     core = local_core.clone()
     core[ghost_pos] = ghost_core.view(-1)
 
+    marks.mark("6")
     # 6. local main pass with the true flags
     lab = engine.cluster_given_core(lx, eps, core).to(torch.int64)
 
+    marks.mark("7")
     # 7. cross-shard edges (global ids) and the global merge
     exported = torch.zeros(nl, dtype=torch.bool, device=dev)
     exported[own_pos[send_idx]] = True
@@ -284,14 +397,9 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     is_ghost[ghost_pos] = True
     sel = (core.bool() & (is_ghost | exported)).nonzero(as_tuple=False).view(-1)
     edges = torch.stack([lgid[sel], lgid[lab[sel]]], 1)
-    all_edges = torch.cat(_all_gather_var(edges, group))
     own_lab = lab[own_pos]
     root_gid = torch.where(own_lab >= 0, lgid[own_lab.clamp(min=0)], torch.full_like(own_lab, -1))
-    if all_edges.shape[0]:
-        uniq, comp = torch.unique(all_edges.view(-1), return_inverse=True)
-        root = engine.union_edges(comp.view(-1, 2), uniq.shape[0]).to(torch.int64)
-        rep = uniq[root]  # compact ids are ordered like global ids: min id wins
-        pos = torch.searchsorted(uniq, root_gid.clamp(min=0))
-        hit = (root_gid >= 0) & (pos < uniq.shape[0]) & (uniq[pos.clamp(max=uniq.shape[0] - 1)] == root_gid)
-        root_gid = torch.where(hit, rep[pos.clamp(max=uniq.shape[0] - 1)], root_gid)
+    root_gid = _merge_edges(edges, root_gid, engine, group)
+    marks.mark("end")
+    marks.report(rank)
     return own_gid, root_gid, own_core

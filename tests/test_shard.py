@@ -54,6 +54,19 @@ class OracleEngine:
         cnt = (self._d2(x.numpy(), x.numpy()) <= e2).sum(1)
         return torch.from_numpy((cnt >= minpts).astype(np.uint8))
 
+    def cluster_keyed(self, x, keys, eps, minpts):
+        """Labels = key of the cluster's minimum-key core (FoF when minpts == 2)."""
+        r = oracle.dbscan(x.numpy(), eps, minpts, 0)
+        lab = r["labels"].astype(np.int64)
+        core = r["core"].astype(bool)
+        k = keys.numpy().astype(np.int64)
+        big = np.iinfo(np.int64).max
+        best = np.full(len(lab), big, np.int64)
+        cm = core & (lab >= 0)
+        np.minimum.at(best, lab[cm], k[cm])
+        out = np.where(lab >= 0, best[np.maximum(lab, 0)], -1)
+        return torch.from_numpy(out.astype(np.int32)), torch.from_numpy(r["core"].astype(np.uint8))
+
     def cluster_given_core(self, x, eps, core):
         e2 = np.float64(np.float32(eps)) ** 2
         adj = self._d2(x.numpy(), x.numpy()) <= e2
@@ -192,3 +205,19 @@ def test_sharded_device_engine_world2(dim, eps, minpts):
     coords = blob_mix(40 + dim, 6000, dim)
     labels, core = run_sharded(coords, eps, minpts, world=2, use_gpu=True)
     check_against_oracle(coords, eps, minpts, labels, core)
+
+
+@pytest.mark.parametrize("minpts", [2, 4])
+def test_sharded_world1(minpts):
+    """A single rank: no exchange at all, the local run is the whole result."""
+    coords = blob_mix(21, 1200, 3)
+    labels, core = run_sharded(coords, 0.35, minpts, world=1)
+    check_against_oracle(coords, 0.35, minpts, labels, core)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("minpts", [2, 6])
+def test_sharded_device_engine_world1(minpts):
+    coords = blob_mix(44, 8000, 3)
+    labels, core = run_sharded(coords, 0.3, minpts, world=1, use_gpu=True)
+    check_against_oracle(coords, 0.3, minpts, labels, core)
