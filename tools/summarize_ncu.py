@@ -3,7 +3,8 @@
 `--set full` capture. Also writes profiles/traffic.json, which bench.py reads
 for roofline.traffic (DRAM bytes per launch of the dominant kernel).
 
-  python tools/summarize_ncu.py <tag> <launches.csv> <full_raw.csv> [kernel-substring]
+  python tools/summarize_ncu.py <tag> <launches.csv> <full_raw.csv[,more.csv]> [kernel-substring]
+                                [--no-traffic]
 """
 import collections
 import csv
@@ -67,8 +68,10 @@ def to_bytes(val, unit):
 
 
 def main():
-    tag, lpath, fpath = sys.argv[1:4]
-    kfilter = sys.argv[4] if len(sys.argv) > 4 else "k_fd_main"
+    argv = [a for a in sys.argv[1:] if a != "--no-traffic"]
+    write_traffic = "--no-traffic" not in sys.argv
+    tag, lpath, fpaths = argv[0:3]
+    kfilter = argv[3] if len(argv) > 3 else "k_fd_main"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     lines = [f"# ncu summary {tag}", ""]
     agg = launches(lpath)
@@ -80,7 +83,8 @@ def main():
         lines.append(f"| `{k}` | {c} | {v / c / 1e3:.1f} | {v / tot * 100:.1f}% |")
     lines += ["", "## `--set full` captures", ""]
     traffic = None
-    for rec in full(fpath):
+    recs = [r for fp in fpaths.split(",") for r in full(fp)]
+    for rec in recs:
         lines.append(f"### `{rec['kernel']}`")
         for m, label in METRICS:
             if label in rec:
@@ -90,7 +94,7 @@ def main():
             traffic = to_bytes(*rec["DRAM read"]) + to_bytes(*rec["DRAM write"])
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    if traffic is not None:
+    if traffic is not None and write_traffic:
         with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
             json.dump({"k_fd_main_dram_bytes_per_launch": traffic, "source": f"{tag} ncu --set full",
                        "kernel": kfilter}, f, indent=1)
