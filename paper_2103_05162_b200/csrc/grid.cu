@@ -286,16 +286,18 @@ struct DbCoreQuery {
   int minpts;
   uint8_t* __restrict__ flags;
   LocalStack* stack;  // per-thread traversal stack, kept outside the struct
-  const MemberTree* mt;
+  const MemberTree* mt;   // members in member order
+  const MemberTree* smt;  // the same cells' members in spatial order
   const int32_t* __restrict__ qoff;  // rank -> points before it (exclusive prefix)
   int64_t n_points;
   int32_t num_prims;
+  const int32_t* __restrict__ list;  // query slots to run (the SinglePoint ones)
   unsigned long long dists = 0;
   float p[3];
   int32_t id, node, nlo, mask_rank = 0;
   int count;
   __device__ bool begin(int64_t q) {
-    const float4 qp = qpt[q];
+    const float4 qp = qpt[list ? list[q] : q];
     id = __float_as_int(qp.w);
     if (id < 0) return false;  // member of a dense cell
     p[0] = qp.x;
@@ -322,13 +324,23 @@ struct DbCoreQuery {
           dists += take;
           count += take;
         } else {
-          // the member-by-member scan (dbscan.cpp:124-131), answered by the
-          // member tree: same stopping position, same counts
-          int hits;
-          const int64_t pos = member_scan<D>(*mt, kb, ke, p, bt, minpts - count, hits);
-          dists += pos >= 0 ? static_cast<unsigned long long>(pos - kb + 1)
-                            : static_cast<unsigned long long>(ke - kb);
-          count += hits;
+          // the member-by-member scan (dbscan.cpp:124-131): when the box holds
+          // fewer hits than still needed the scan runs to the end (count them
+          // in the spatial tree); otherwise find the stopping member in
+          // member order (the index tree) — at most once per query
+          const int rem = minpts - count;
+          const int total = ke - kb <= kMemberLinear ? rem  // short: scan it directly
+                                                     : member_count<D>(*smt, kb, ke, p, bt, rem);
+          if (total < rem) {
+            dists += static_cast<unsigned long long>(ke - kb);
+            count += total;
+          } else {  // (a short box comes here directly and may still fall short)
+            int hits;
+            const int64_t pos = member_scan<D>(*mt, kb, ke, p, bt, rem, hits);
+            dists += pos >= 0 ? static_cast<unsigned long long>(pos - kb + 1)
+                              : static_cast<unsigned long long>(ke - kb);
+            count += hits;
+          }
         }
       }
       return count < minpts;
@@ -437,14 +449,15 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
           uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent, MemberTree mt,
-          const int32_t* __restrict__ qoff, int32_t num_prims) {
+          MemberTree smt, const int32_t* __restrict__ qoff, int32_t num_prims,
+          const int32_t* __restrict__ list, int64_t m) {
   LocalStack stack;
   DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
-                   qoff, n, num_prims};
+                   &smt, qoff, n, num_prims, list};
   if (persistent)
-    run_query_queue(n, &ctr->queue[2], q);
+    run_query_queue(m, &ctr->queue[2], q);
   else
-    run_query_warpstart<D>(n, q, nodes, bt);
+    run_query_warpstart<D>(m, q, nodes, bt);
   unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
 }
@@ -570,6 +583,42 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
 }
 
+// Spatial order of the members inside each cell: key = cell index (high 32
+// bits) | Morton code of the point's position inside its cell (low bits).
+// Any order inside a cell is valid for counting; this one makes the blocks of
+// the spatial member tree compact.
+template <int D>
+__global__ void k_spatial_keys(const float4* __restrict__ sorted_pt,
+                               const int32_t* __restrict__ cell_of_sorted,
+                               const GridParams* __restrict__ gp, int64_t n,
+                               uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  const float inv_h = static_cast<float>(1.0 / gp->h);
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 q = sorted_pt[k];
+    const float c[3] = {q.x, q.y, q.z};
+    uint64_t code = 0;
+    constexpr int bits = D == 2 ? 16 : 10;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const float t = (c[a] - gp->origin[a]) * inv_h;
+      float f = t - floorf(t);  // position inside the cell, approximately
+      f = fminf(fmaxf(f, 0.f), 0.999999f);
+      const uint64_t v = static_cast<uint64_t>(f * static_cast<float>(1 << bits));
+      code |= D == 2 ? (spread2(v) << a) : (spread3(v) << a);
+    }
+    keys[k] = (static_cast<uint64_t>(cell_of_sorted[k]) << 32) | code;
+    vals[k] = static_cast<int32_t>(k);
+  }
+}
+
+__global__ void k_gather_pts(const float4* __restrict__ src, const int32_t* __restrict__ perm,
+                             int64_t n, float4* __restrict__ dst) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[j] = src[perm[j]];
+}
+
 // Member tree levels (member_tree.cuh): level 1 from the points, level l from
 // level l - 1.
 template <int D>
@@ -623,6 +672,23 @@ __global__ void k_prim_reps(const int32_t* __restrict__ order, const int32_t* __
     const int32_t a = prim_aux[order[s]];
     rep[s] = a >= 0 ? a : __float_as_int(sorted_pt[cell_begin[~a]].w);
   }
+}
+
+// Query slots of the SinglePoint primitives, in rank order (the only queries
+// of densebox_mark_cores: dense members are core already, dbscan.cpp:118).
+__global__ void k_single_ind(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
+                             int64_t m, int32_t* __restrict__ ind) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    ind[s] = prim_aux[order[s]] >= 0;
+}
+
+__global__ void k_single_slots(const int32_t* __restrict__ ind, const int32_t* __restrict__ pos,
+                               const int32_t* __restrict__ qoff, int64_t m,
+                               int32_t* __restrict__ list) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (ind[s]) list[pos[s]] = qoff[s];
 }
 
 __global__ void k_prim_noncore(const int32_t* __restrict__ order,
@@ -801,13 +867,40 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   TCB_CUDA(cudaGetLastError());
 
   const MemberTree mt = build_member_tree<D>(sorted_pt, n, scratch);
+  // the core pass also gets the members in spatial order per cell (same cell
+  // segments) to count the hits of a long cut box without member order
+  MemberTree smt;
+  if (minpts > 2) {
+    uint64_t* sk = scratch.alloc_n<uint64_t>(n);
+    int32_t* sv = scratch.alloc_n<int32_t>(n);
+    note_launch(), k_spatial_keys<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted,
+                                                                     gp, n, sk, sv);
+    uint64_t cells_pow2 = 1;
+    while (cells_pow2 < static_cast<uint64_t>(num_cells)) cells_pow2 <<= 1;
+    const uint64_t or_all = ((cells_pow2 - 1) << 32) | 0xffffffffull;
+    const bool alt = radix_sort_pairs(sk, sv, keys, vals, n, 0, or_all, sort_tmp, st);
+    const int32_t* sperm = alt ? vals : sv;
+    float4* spt = scratch.alloc_n<float4>(n);
+    note_launch(), k_gather_pts<<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, sperm, n, spt);
+    smt = build_member_tree<D>(spt, n, scratch);
+  }
 
   // ---- core pass ----
   clock.mark(kStCore);
-  if (minpts > 2)
-    note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, n), kQueryBlock, 0, st>>>(
+  if (minpts > 2 && sparse_points > 0) {
+    // only SinglePoint queries run: a compact slot list keeps the warps full
+    int32_t* ind = scratch.alloc_n<int32_t>(num_prims);
+    int32_t* pos = scratch.alloc_n<int32_t>(num_prims);
+    int32_t* list = scratch.alloc_n<int32_t>(sparse_points);
+    note_launch(), k_single_ind<<<grid_for(num_prims, 256), 256, 0, st>>>(b.tree.leaf_order,
+                                                                          prim_aux, num_prims, ind);
+    exclusive_scan_i32(ind, pos, num_prims, nullptr, scan_tmp, st);
+    note_launch(), k_single_slots<<<grid_for(num_prims, 256), 256, 0, st>>>(ind, pos, qoff,
+                                                                            num_prims, list);
+    note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, sparse_points), kQueryBlock, 0, st>>>(
         b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr,
-        query_mode() == 1, mt, qoff, num_prims);
+        query_mode() == 1, mt, smt, qoff, num_prims, list, sparse_points);
+  }
   // ---- main pass ----
   clock.mark(kStMain);
   if (query_mode() != 1) {

@@ -118,6 +118,49 @@ __device__ __forceinline__ int64_t member_scan(const MemberTree& t, int64_t a, i
   return -1;
 }
 
+// Number of members of [a, b) within eps of p, counting stops at `cap`
+// (returns min(hits, cap) when it stops early). Order-free: for a member tree
+// over a spatially ordered copy of the members (same cell segments), where
+// blocks are compact and most are skipped or counted whole.
+template <int D>
+__device__ __forceinline__ int member_count(const MemberTree& t, int64_t a, int64_t b,
+                                            const float* p, const BallTest& bt, int cap) {
+  int hits = 0;
+  int64_t k = a;
+  while (k < b) {
+    int l = k == 0 ? 62 : __ffsll(static_cast<long long>(k)) - 1;
+    const int fit = 63 - __clzll(static_cast<long long>(b - k));
+    if (fit < l) l = fit;
+    if (l > t.levels) l = t.levels;
+    int2 st[2 * kMemberLevels + 2];
+    int top = 0;
+    st[top++] = make_int2(l, static_cast<int32_t>(k >> l));
+    while (top) {
+      const int2 e = st[--top];
+      const int64_t j = e.y;
+      if (e.x == 0) {
+        const float4 m4 = __ldg(t.pts + j);
+        const float m[3] = {m4.x, m4.y, m4.z};
+        if (ball_hits<D>(p, m, m, bt) && ++hits >= cap) return hits;
+        continue;
+      }
+      float lo[3], hi[3];
+      member_box<D>(t, e.x, j, lo, hi);
+      const int c = ball_classify<D>(p, lo, hi, bt);
+      if (c == 0) continue;
+      if (c == 2) {
+        hits += 1 << e.x;
+        if (hits >= cap) return hits;
+        continue;
+      }
+      st[top++] = make_int2(e.x - 1, static_cast<int32_t>(2 * j + 1));
+      st[top++] = make_int2(e.x - 1, static_cast<int32_t>(2 * j));
+    }
+    k += int64_t{1} << l;
+  }
+  return hits;
+}
+
 // Host: builds the levels over n sorted points (scratch-allocated boxes).
 template <int D>
 MemberTree build_member_tree(const float4* pts, int64_t n, Scratch& scratch);
