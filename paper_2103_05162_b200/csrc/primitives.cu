@@ -15,7 +15,14 @@ namespace {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / kWarp;
-constexpr int kIPT = 16;
+#ifndef TCB_SORT_IPT
+#define TCB_SORT_IPT 16
+#endif
+#ifndef TCB_SORT_LOOKBACK
+#define TCB_SORT_LOOKBACK 4
+#endif
+constexpr int kIPT = TCB_SORT_IPT;
+constexpr int kLookback = TCB_SORT_LOOKBACK;
 constexpr int kTile = kSortThreads * kIPT;  // 4096 keys per tile
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
@@ -191,13 +198,26 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
   }
   uint32_t* my = status + static_cast<int64_t>(tile) * kRadix + d;
   st_status(my, (tile == 0 ? kFlagInc : kFlagAgg) | tile_count);
+  // decoupled look-back, kLookback predecessors per round trip
   uint32_t excl = 0;
   for (int t = tile - 1; t >= 0;) {
-    const uint32_t s = ld_status(status + static_cast<int64_t>(t) * kRadix + d);
-    if ((s & ~kCountMask) == 0) continue;  // predecessor not published yet
-    excl += s & kCountMask;
-    if (s & kFlagInc) break;
-    --t;
+    uint32_t sv[kLookback];
+#pragma unroll
+    for (int j = 0; j < kLookback; ++j)
+      sv[j] = t - j >= 0 ? ld_status(status + static_cast<int64_t>(t - j) * kRadix + d)
+                         : kFlagInc;  // before tile 0: an inclusive zero
+    bool done = false;
+    int used = 0;
+#pragma unroll
+    for (int j = 0; j < kLookback; ++j) {
+      if (done || used < j) break;
+      if ((sv[j] & ~kCountMask) == 0) break;  // not published yet: retry from here
+      excl += sv[j] & kCountMask;
+      used = j + 1;
+      if (sv[j] & kFlagInc) done = true;
+    }
+    if (done) break;
+    t -= used;
   }
   if (tile > 0) st_status(my, kFlagInc | (excl + tile_count));
   const uint32_t tstart = block_excl_scan<kSortThreads>(tile_count, S.warp_tot, nullptr);

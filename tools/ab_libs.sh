@@ -7,6 +7,6 @@ for L in paper_2103_05162_b200/ab/*.so; do
 import sys, json
 for l in sys.stdin:
     if l.startswith('{'):
-        d = json.loads(l); print(d['config'], d['ms_best'], d['stage_ms'].get('core'), d['stage_ms'].get('main'), d['stats']['pair_resolutions'], d['stats']['distance_evaluations'], d.get('cross_check'))
+        d = json.loads(l); print(d['config'], d['ms_best'], {k: v for k, v in d['stage_ms'].items() if v > 0.05}, d['stats']['pair_resolutions'], d['stats']['distance_evaluations'], d.get('cross_check'))
 "
 done
