@@ -208,9 +208,14 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
     __shared__ float s_box[2 * D][kClimbBlock];
     __shared__ int32_t s_r[kClimbBlock], s_link[kClimbBlock], s_aux[kClimbBlock];
     __shared__ int32_t s_code[kClimbBlock], s_start[kClimbBlock];
+    __shared__ int32_t s_delta[kClimbBlock + 1];  // delta(b0 - 1 + j), j = 0..256
     const int t = threadIdx.x;
     const int64_t b0 = s - t;
     const int64_t b1 = min(b0 + kClimbBlock - 1, m - 1);
+    // every boundary delta a subtree inside the block can ask for, computed once
+    s_delta[t + 1] = key_delta(codes, m, b0 + t, b0 + t + 1);
+    if (t == 0) s_delta[0] = b0 > 0 ? key_delta(codes, m, b0 - 1, b0) : -1;
+    __syncthreads();
     auto publish = [&] {
 #pragma unroll
       for (int k = 0; k < D; ++k) {
@@ -229,7 +234,7 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
       bool left = false;
       int32_t p = 0;
       if (active) {
-        left = l == 0 || (r != m - 1 && key_delta(codes, m, r, r + 1) > key_delta(codes, m, l - 1, l));
+        left = l == 0 || (r != m - 1 && s_delta[r - b0 + 1] > s_delta[l - b0]);
         p = left ? r : l - 1;
       }
       s_code[t] = active ? (2 | (left ? 1 : 0)) : 0;  // alive | left child
