@@ -189,10 +189,44 @@ struct DeviceCall {
 };
 
 // One algorithm on a dataset already resident on the device.
+// FDBSCAN results reach the host chunk by chunk: each finalized chunk is
+// copied on a second stream while the next one is computed.
+struct ChunkedCopy {
+  cudaStream_t cp = nullptr;
+  std::vector<cudaEvent_t> events;
+  ChunkedCopy() { TCB_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking)); }
+  ~ChunkedCopy() {
+    if (cp) {
+      cudaStreamSynchronize(cp);
+      cudaStreamDestroy(cp);
+    }
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+  }
+};
+
 void device_cluster(DeviceCall& call, const float* d_coords, int64_t n, int dim, float eps,
                     int minpts, tc_algorithm algo, int64_t cap, int32_t* d_labels,
                     uint8_t* d_core, tc_result* res) {
   tcb::RunOutput ro;
+  if (res && algo == TC_ALGO_FDBSCAN) {
+    ChunkedCopy cc;
+    tcb::ChunkSink sink = [&](int64_t i0, int64_t i1, cudaStream_t s) {
+      cudaEvent_t e;
+      TCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      cc.events.push_back(e);
+      TCB_CUDA(cudaEventRecord(e, s));
+      TCB_CUDA(cudaStreamWaitEvent(cc.cp, e, 0));
+      TCB_CUDA(cudaMemcpyAsync(res->labels.ptr + i0, d_labels + i0, sizeof(int32_t) * (i1 - i0),
+                               cudaMemcpyDeviceToHost, cc.cp));
+      TCB_CUDA(cudaMemcpyAsync(res->core.ptr + i0, d_core + i0, static_cast<size_t>(i1 - i0),
+                               cudaMemcpyDeviceToHost, cc.cp));
+    };
+    tcb::run_device(d_coords, n, dim, eps, minpts, algo, cap, d_labels, d_core, call.st, true,
+                    &ro, nullptr, nullptr, &sink);
+    TCB_CUDA(cudaStreamSynchronize(cc.cp));
+    res->stats = ro.stats;
+    return;
+  }
   tcb::run_device(d_coords, n, dim, eps, minpts, algo, cap, d_labels, d_core, call.st, true, &ro,
                   [&](cudaStream_t s) {
                     if (!res) return;

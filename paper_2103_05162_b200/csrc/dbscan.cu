@@ -318,6 +318,36 @@ k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags
 }
 
 __global__ void __launch_bounds__(256)
+k_finalize_gather(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
+                  const int32_t* __restrict__ key, const int32_t* __restrict__ rank_of,
+                  int64_t i0, int64_t i1, int32_t* __restrict__ labels,
+                  uint8_t* __restrict__ core_out, DevCounters* ctr) {
+  long long noise = 0, clusters = 0, cores = 0;
+  for (int64_t i = i0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < i1;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t s = __ldg(rank_of + i);
+    int32_t p = ld_relaxed(parent + s);
+    int32_t q;
+    while (p != (q = ld_relaxed(parent + p))) p = q;
+    const bool core = flags[s] != 0;
+    const int32_t lab = (core || p != s) ? __ldg(key + p) : -1;  // dbscan.cpp:215
+    labels[i] = lab;
+    core_out[i] = core ? 1 : 0;
+    noise += lab == -1;
+    clusters += lab != -1 && p == s;
+    cores += core;
+  }
+  noise = warp_sum(noise);
+  clusters = warp_sum(clusters);
+  cores = warp_sum(cores);
+  if ((threadIdx.x & 31) == 0) {
+    if (noise) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->noise), noise);
+    if (clusters) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->clusters), clusters);
+    if (cores) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->cores), cores);
+  }
+}
+
+__global__ void __launch_bounds__(256)
 k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int64_t n,
            int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr) {
   long long noise = 0, clusters = 0, cores = 0;
@@ -408,6 +438,20 @@ void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
   if (force_core) note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
   note_launch(), k_finalize_ranks<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, key, order, n,
                                                                    labels, core_out, d_ctr);
+  TCB_CUDA(cudaGetLastError());
+}
+
+void finalize_labels_gather(int32_t* parent, const uint8_t* flags, const int32_t* key,
+                            const int32_t* rank_of, int64_t i0, int64_t i1, int32_t* labels,
+                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s) {
+  if (i1 <= i0) return;
+  note_launch(), k_finalize_gather<<<grid_for(i1 - i0, 256), 256, 0, s>>>(
+      parent, flags, key, rank_of, i0, i1, labels, core_out, d_ctr);
+  TCB_CUDA(cudaGetLastError());
+}
+
+void flatten_mark(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
+  note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
   TCB_CUDA(cudaGetLastError());
 }
 

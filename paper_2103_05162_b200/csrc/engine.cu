@@ -134,12 +134,13 @@ int get_last_stage_ms(double* out, int cap) {
 template <int D>
 void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
                  uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
-                 const int32_t* d_keys) {
+                 const int32_t* d_keys, const ChunkSink* sink) {
   cudaStream_t st = scratch.stream();
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
   PrimSource src;
   src.coords = d_coords;
   src.count = n;
+  src.want_rank_of = sink != nullptr;
   clock.mark(kStBounds);
   BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock);
 
@@ -157,15 +158,28 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   clock.mark(kStMain);
   fdbscan_main_pass<D>(b, key, n, eps2, minpts == 2, flags, parent, ctr, scratch);
   clock.mark(kStFinal);
-  finalize_labels_ranks(parent, flags, key, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
-                        minpts == 2);
+  if (sink) {
+    // gather form, in chunks of output positions: each finished chunk goes
+    // to the sink (tc_cluster copies it to the host while the next runs)
+    if (minpts == 2) flatten_mark(parent, flags, n, st);
+    const int64_t chunks = n < (int64_t{1} << 22) ? 1 : 8;
+    const int64_t per = (n + chunks - 1) / chunks;
+    for (int64_t i0 = 0; i0 < n; i0 += per) {
+      const int64_t i1 = i0 + per < n ? i0 + per : n;
+      finalize_labels_gather(parent, flags, key, b.rank_of, i0, i1, d_labels, d_core, ctr, st);
+      (*sink)(i0, i1, st);
+    }
+  } else {
+    finalize_labels_ranks(parent, flags, key, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
+                          minpts == 2);
+  }
   clock.finish();
 }
 
 template void run_fdbscan<2>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
-                             Scratch&, StageClock&, const int32_t*);
+                             Scratch&, StageClock&, const int32_t*, const ChunkSink*);
 template void run_fdbscan<3>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
-                             Scratch&, StageClock&, const int32_t*);
+                             Scratch&, StageClock&, const int32_t*, const ChunkSink*);
 
 // ---------------------------------------------------------------------------
 // Entry
@@ -173,7 +187,8 @@ template void run_fdbscan<3>(const float*, int64_t, float, int, int32_t*, uint8_
 void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
                 tc_algorithm algo, int64_t oracle_cap, int32_t* d_labels, uint8_t* d_core,
                 cudaStream_t stream, bool want_stats, RunOutput* out,
-                const std::function<void(cudaStream_t)>& tail, const int32_t* d_keys) {
+                const std::function<void(cudaStream_t)>& tail, const int32_t* d_keys,
+                const ChunkSink* sink) {
   if (dim != 2 && dim != 3) throw InvalidArgument{"PointSet: dimension must be 2 or 3"};
   if (n < 1) throw InvalidArgument{"PointSet: empty"};
   if (!(eps > 0.f) || !std::isfinite(eps))
@@ -194,9 +209,11 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
   switch (algo) {
     case TC_ALGO_FDBSCAN:
       if (dim == 2)
-        run_fdbscan<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys);
+        run_fdbscan<2>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys,
+                       sink);
       else
-        run_fdbscan<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys);
+        run_fdbscan<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys,
+                       sink);
       break;
     case TC_ALGO_DENSEBOX:
       if (dim == 2)

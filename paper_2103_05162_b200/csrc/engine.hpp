@@ -36,6 +36,11 @@ struct RunOutput {
   double stage_ms[kNumStages]{};
 };
 
+// Called with [i0, i1) once labels/core flags of those points are final
+// (enqueued on the given stream): lets tc_cluster overlap the device->host
+// copy of early chunks with the finalize of later ones.
+using ChunkSink = std::function<void(int64_t i0, int64_t i1, cudaStream_t)>;
+
 // Full device pipeline. d_coords/d_labels/d_core are device pointers.
 // want_stats: synchronize at the end and fill `out`.
 // `tail` (optional) is invoked after the last kernel is enqueued and before
@@ -45,7 +50,7 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
                 uint8_t* d_core, cudaStream_t stream, bool want_stats,
                 RunOutput* out,
                 const std::function<void(cudaStream_t)>& tail = nullptr,
-                const int32_t* d_keys = nullptr);
+                const int32_t* d_keys = nullptr, const ChunkSink* sink = nullptr);
 
 // Kernel-launch accounting (thread-local; reset at the start of run_device).
 void note_launch();

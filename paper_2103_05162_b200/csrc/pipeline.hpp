@@ -87,11 +87,13 @@ struct PrimSource {
   const float4* hi = nullptr;
   const int32_t* aux = nullptr;   // leaf payload per primitive (nullptr: primitive index)
   int64_t count = 0;
+  bool want_rank_of = false;      // also produce primitive -> leaf rank
 };
 
 struct BuiltBvh {
   DeviceBvh tree;
   float4* leaf_pt = nullptr;          // points mode only: rank -> (x, y, z, id bits)
+  int32_t* rank_of = nullptr;         // primitive -> leaf rank (PrimSource::want_rank_of)
   const uint64_t* codes = nullptr;    // sorted Morton codes (leaf rank order)
   const uint32_t* scene_ord = nullptr;  // Morton scene box (order-preserving bits, 6)
   int sort_passes = 0;
@@ -129,6 +131,15 @@ void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t*
                    bool to_rank, cudaStream_t s);
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
 // FDBSCAN: parent / flags indexed by leaf rank, key[rank] = original index.
+// Gather form of finalize_labels_ranks for output positions [i0, i1):
+// labels[i] = key of the root of rank_of[i] (or -1). Lets the caller copy
+// finished chunks to the host while later chunks are computed.
+void finalize_labels_gather(int32_t* parent, const uint8_t* flags, const int32_t* key,
+                            const int32_t* rank_of, int64_t i0, int64_t i1, int32_t* labels,
+                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s);
+// minpts == 2: the union-find flatten + derived core flags of finalize_labels_ranks.
+void flatten_mark(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
+
 // labels[order[rank]] = key of the rank's root (or -1).
 void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
                            const int32_t* order, int64_t n,
@@ -146,7 +157,7 @@ void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,
 template <int D>
 void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
                  uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
-                 const int32_t* d_keys = nullptr);
+                 const int32_t* d_keys = nullptr, const ChunkSink* sink = nullptr);
 
 // ---- DenseBox (grid.cu) ----
 template <int D>
