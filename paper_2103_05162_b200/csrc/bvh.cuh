@@ -365,6 +365,7 @@ __device__ __forceinline__ bool bvh_step_ordered(const float4* __restrict__ node
 }
 
 // Traversal stacks of (node, first leaf rank) entries for bvh_step_ranged.
+// (caching the top entry in registers measured slower: +14% on the C2 main pass)
 struct LocalStack {  // per-thread local memory
   int2 e[kStackDepth];
   int top = 0;
@@ -374,6 +375,7 @@ struct LocalStack {  // per-thread local memory
     v = e[--top];
     return true;
   }
+  __device__ __forceinline__ void reset() { top = 0; }
 };
 
 

@@ -67,7 +67,7 @@ struct CoreQuery {
     count = 0;
     node = 0;
     nlo = 0;
-    stack->top = 0;
+    stack->reset();
     return true;
   }
   __device__ bool step() {

@@ -306,7 +306,7 @@ struct DbCoreQuery {
     count = 0;
     node = 0;
     nlo = 0;
-    stack->top = 0;
+    stack->reset();
     return true;
   }
   __device__ bool step() {
