@@ -54,6 +54,17 @@ tc_status tcg_cluster_keyed_device(const float* d_coords, const int32_t* d_keys,
                                    int dim, float eps, int minpts, int32_t* d_labels,
                                    uint8_t* d_core, void* stream, tc_cluster_stats* stats);
 
+/* Binary point files (the reference's .bin layout, io.cpp:106-134) straight
+ * to the device: tcg_binary_info reads the header;
+ * tcg_load_binary_device reads the coordinates in chunks through two
+ * page-locked staging buffers, each chunk's host->device copy overlapping the
+ * next read, into d_coords (n*dim floats), and synchronizes `stream`.
+ * Errors as tc_dataset_load: unreadable / truncated / bad header -> TC_ERR_IO.
+ * Coordinates are validated by the clustering call itself. */
+tc_status tcg_binary_info(const char* path, int64_t* n, int* dim);
+tc_status tcg_load_binary_device(const char* path, float* d_coords, int64_t n, int dim,
+                                 void* stream);
+
 /* Per-stage device milliseconds of the last tcg_cluster_device / tc_cluster
  * call on this host thread (the tc_cluster_stats phases split finer):
  * [0] bounds+morton  [1] sort  [2] topology+refit  [3] grid (DenseBox)

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     device_count,
     last_launch_count,
     last_stage_ms,
+    load_device,
     status_string,
     verify,
 )

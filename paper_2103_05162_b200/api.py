@@ -220,6 +220,21 @@ def cluster_device(coords, eps: float, minpts: int, algorithm: Algorithm = Algor
     return labels, core, (st.to_dict() if st is not None else None)
 
 
+def load_device(path: str, device=None):
+    """``tcg_binary_info`` + ``tcg_load_binary_device``: a .bin point file to a
+    (n, dim) float32 CUDA tensor, file reads overlapped with the copies."""
+    import torch
+
+    n, d = C.c_int64(), C.c_int()
+    _check(lib.tcg_binary_info(path.encode(), C.byref(n), C.byref(d)), "tcg_binary_info")
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    out = torch.empty((n.value, d.value), dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream(dev)
+    _check(lib.tcg_load_binary_device(path.encode(), C.c_void_p(out.data_ptr()), n.value, d.value,
+                                      C.c_void_p(s.cuda_stream)), "tcg_load_binary_device")
+    return out
+
+
 def verify(ds: Dataset, eps: float, minpts: int, threads: int = 0, oracle_cap: int = 0):
     """``tc_verify`` -> (Status, report text)."""
     buf = C.create_string_buffer(8192)

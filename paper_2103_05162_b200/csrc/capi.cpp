@@ -497,6 +497,23 @@ TC_EXPORT tc_status tcg_cluster_keyed_device(const float* d_coords, const int32_
   });
 }
 
+TC_EXPORT tc_status tcg_binary_info(const char* path, int64_t* n, int* dim) {
+  if (!path || !n || !dim) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    tcb::binary_info(path, n, dim);
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tcg_load_binary_device(const char* path, float* d_coords, int64_t n, int dim,
+                                           void* stream) {
+  if (!path || !d_coords || n < 1 || (dim != 2 && dim != 3)) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    tcb::load_binary_device(path, d_coords, n, dim, static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
+}
+
 TC_EXPORT int tcg_last_stage_ms(double* out, int cap) {
   if (!out || cap <= 0) return 0;
   return tcb::get_last_stage_ms(out, cap);

@@ -8,6 +8,9 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <stdexcept>
+
+#include "engine.hpp"
 
 namespace tcb {
 
@@ -338,6 +341,62 @@ HostPoints read_binary(const std::string& path) {
 }
 
 }  // namespace
+
+void binary_info(const std::string& path, int64_t* n, int* dim) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) io_fail(path, "cannot open for reading");
+  uint32_t hdr[2] = {0, 0};
+  in.read(reinterpret_cast<char*>(hdr), sizeof hdr);
+  if (!in) io_fail(path, "truncated header");
+  if (hdr[0] == 0 || (hdr[1] != 2 && hdr[1] != 3)) io_fail(path, "invalid header (n or dim)");
+  *n = hdr[0];
+  *dim = static_cast<int>(hdr[1]);
+}
+
+// load_binary (io.cpp:106-122) straight into device memory: the file is read
+// in chunks into two page-locked staging buffers, each chunk's host->device
+// copy running while the next chunk is read.
+void load_binary_device(const std::string& path, float* d_coords, int64_t n, int dim,
+                        cudaStream_t stream) {
+  int64_t fn = 0;
+  int fdim = 0;
+  binary_info(path, &fn, &fdim);
+  if (fn != n || fdim != dim) throw std::invalid_argument("load_binary_device: shape mismatch");
+  std::ifstream in(path, std::ios::binary);
+  if (!in) io_fail(path, "cannot open for reading");
+  in.seekg(8);
+  constexpr size_t kChunk = size_t{32} << 20;  // bytes per staging buffer
+  struct Staging {
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    ~Staging() {
+      for (int k = 0; k < 2; ++k) {
+        if (done[k]) {
+          cudaEventSynchronize(done[k]);
+          cudaEventDestroy(done[k]);
+        }
+        if (buf[k]) cudaFreeHost(buf[k]);
+      }
+    }
+  } stg;
+  for (int k = 0; k < 2; ++k) {
+    TCB_CUDA(cudaMallocHost(&stg.buf[k], kChunk));
+    TCB_CUDA(cudaEventCreateWithFlags(&stg.done[k], cudaEventDisableTiming));
+  }
+  const size_t total = static_cast<size_t>(n) * dim * sizeof(float);
+  auto* dst = reinterpret_cast<char*>(d_coords);
+  size_t off = 0;
+  for (int k = 0; off < total; k ^= 1) {
+    const size_t len = total - off < kChunk ? total - off : kChunk;
+    TCB_CUDA(cudaEventSynchronize(stg.done[k]));  // the copy out of this buffer finished
+    in.read(static_cast<char*>(stg.buf[k]), static_cast<std::streamsize>(len));
+    if (!in) io_fail(path, "truncated coordinate data");
+    TCB_CUDA(cudaMemcpyAsync(dst + off, stg.buf[k], len, cudaMemcpyHostToDevice, stream));
+    TCB_CUDA(cudaEventRecord(stg.done[k], stream));
+    off += len;
+  }
+  TCB_CUDA(cudaStreamSynchronize(stream));
+}
 
 HostPoints load_points(const std::string& path, int format) {
   const bool binary = format == 2 || (format != 1 && is_binary_path(path));

@@ -4,6 +4,8 @@
 // byte-identical to the reference's for the same arguments.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -57,5 +59,11 @@ HostPoints gen_taxi_like(int64_t n, uint64_t seed);
 // File formats (io.cpp:51-148). Errors throw std::runtime_error.
 HostPoints load_points(const std::string& path, int format /* 0 auto, 1 csv, 2 bin */);
 void save_points(const std::string& path, int format, int dim, const float* coords, int64_t n);
+// Header of a binary point file (io.cpp:106-115): n and dim.
+void binary_info(const std::string& path, int64_t* n, int* dim);
+// A binary point file straight into d_coords (n*dim floats), reads overlapped
+// with the host->device copies; synchronizes `stream` before returning.
+void load_binary_device(const std::string& path, float* d_coords, int64_t n, int dim,
+                        cudaStream_t stream);
 
 }  // namespace tcb

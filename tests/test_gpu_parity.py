@@ -310,3 +310,26 @@ def test_fdbscan_contained_runs_exact_counters(minpts):
     for k in ("pair_resolutions", "distance_evaluations", "cluster_count", "core_count",
               "noise_count"):
         assert got.stats[k] == want["stats"][k], (minpts, k, got.stats[k], want["stats"][k])
+
+
+def test_load_binary_device_matches_host_load(tmp_path):
+    """§8f row f1: a .bin file streamed to the device equals tc_dataset_load's
+    points; bad files fail like tc_dataset_load (TC_ERR_IO)."""
+    import torch
+
+    ds = Dataset.hacc_like(3_000_000, seed=5)  # > 2 staging chunks of 32 MiB
+    path = str(tmp_path / "pts.bin")
+    ds.save(path)
+    x = tb.load_device(path)
+    assert x.shape == (3_000_000, 3)
+    assert torch.equal(x.cpu(), torch.from_numpy(Dataset.load(path).coords()))
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"\x05\x00\x00\x00\x07\x00\x00\x00")  # dim 7
+    with pytest.raises(TreeclustError) as e:
+        tb.load_device(str(bad))
+    assert e.value.status == Status.IO
+    trunc = tmp_path / "trunc.bin"
+    trunc.write_bytes(open(path, "rb").read()[:1000])
+    with pytest.raises(TreeclustError) as e:
+        tb.load_device(str(trunc))
+    assert e.value.status == Status.IO
