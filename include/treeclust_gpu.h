@@ -122,6 +122,21 @@ tc_status tcg_cluster_given_core_device(const float* d_coords, int64_t n, int di
                                         uint8_t* d_core_out, void* stream,
                                         tc_cluster_stats* stats);
 
+/* Local context of one shard (own + ghost points): ONE point BVH serving the
+ * core pass and, after the caller exchanged ghost flags with their owners,
+ * the main pass. Labels are the key (e.g. global id) of each cluster's
+ * minimum-key core, -1 for noise; d_keys must be unique. All calls use the
+ * stream given at creation; free the context before destroying that stream. */
+typedef struct tcg_local tcg_local;
+tc_status tcg_local_create(const float* d_coords, const int32_t* d_keys, int64_t n, int dim,
+                           float eps, void* stream, tcg_local** out);
+/* Exact core flags (fdbscan_mark_cores over the local set), input order. */
+tc_status tcg_local_core_flags(tcg_local* ctx, int minpts, uint8_t* d_core);
+/* Main pass + finalize with the given core flags (input order). */
+tc_status tcg_local_cluster(tcg_local* ctx, const uint8_t* d_core_in, int32_t* d_labels,
+                            uint8_t* d_core_out);
+void tcg_local_free(tcg_local* ctx);
+
 /* Connected components of m edges (2*m int32 endpoints in [0, n)): d_root[i]
  * = the minimum index of i's component (min-index hooking + flatten). Used
  * for the cross-shard merge of (ghost, local root) edges. */

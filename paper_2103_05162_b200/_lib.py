@@ -78,6 +78,10 @@ SIGNATURES = {
     "tcg_core_flags_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, C.c_int, _P, _P]),
     "tcg_binary_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "tcg_load_binary_device": (C.c_int, [C.c_char_p, _P, C.c_int64, C.c_int, _P]),
+    "tcg_local_create": (C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_float, _P, _PP]),
+    "tcg_local_core_flags": (C.c_int, [_P, C.c_int, _P]),
+    "tcg_local_cluster": (C.c_int, [_P, _P, _P, _P]),
+    "tcg_local_free": (None, [_P]),
     "tcg_cluster_keyed_device": (C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_float, C.c_int, _P, _P,
                                          _P, C.POINTER(TcClusterStats)]),
     "tcg_cluster_given_core_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P,

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <memory>
 #include <limits>
 
 #include "device_common.cuh"
@@ -152,6 +153,54 @@ void given_core(const float* d_coords, int64_t n, float eps, const uint8_t* d_co
   }
 }
 
+// ---- local context: one point BVH of a shard's own + ghost set serving the
+// core pass, the ghost-flag exchange (done by the caller) and the main pass
+struct LocalCtx {
+  cudaStream_t st;
+  Scratch scratch;
+  DevCounters* ctr = nullptr;
+  BuiltBvh b;
+  const int32_t* key = nullptr;  // rank -> caller key
+  int64_t n = 0;
+  int dim = 0;
+  double eps2 = 0.0;
+  explicit LocalCtx(cudaStream_t s) : st(s), scratch(s) {}
+};
+
+template <int D>
+void local_build(LocalCtx& c, const float* d_coords, const int32_t* d_keys) {
+  c.ctr = c.scratch.alloc_n<DevCounters>(1);
+  TCB_CUDA(cudaMemsetAsync(c.ctr, 0, sizeof(DevCounters), c.st));
+  PrimSource src;
+  src.coords = d_coords;
+  src.count = c.n;
+  c.b = build_bvh<D>(src, true, c.ctr, c.scratch, nullptr);
+  int32_t* k = c.scratch.alloc_n<int32_t>(c.n);
+  gather_rank_keys(d_keys, c.b.tree.leaf_order, c.n, k, c.st);
+  c.key = k;
+}
+
+template <int D>
+void local_core(LocalCtx& c, int minpts, uint8_t* d_core) {
+  Scratch tmp(c.st);
+  uint8_t* flags = tmp.alloc_n<uint8_t>(c.n);  // rank space
+  TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(c.n), c.st));
+  fdbscan_core_pass<D>(c.b, c.n, c.eps2, minpts, flags, c.ctr, c.st);
+  permute_flags(flags, c.b.tree.leaf_order, c.n, d_core, /*to_rank=*/false, c.st);
+}
+
+template <int D>
+void local_cluster(LocalCtx& c, const uint8_t* d_core_in, int32_t* d_labels, uint8_t* d_core_out) {
+  Scratch tmp(c.st);
+  int32_t* parent = tmp.alloc_n<int32_t>(c.n);
+  uint8_t* flags = tmp.alloc_n<uint8_t>(c.n);
+  init_union_find(parent, flags, c.n, c.st);
+  permute_flags(d_core_in, c.b.tree.leaf_order, c.n, flags, /*to_rank=*/true, c.st);
+  fdbscan_main_pass<D>(c.b, c.key, c.n, c.eps2, /*force_core=*/false, flags, parent, c.ctr, tmp);
+  finalize_labels_ranks(parent, flags, c.key, c.b.tree.leaf_order, c.n, d_labels, d_core_out,
+                        c.ctr, c.st, /*force_core=*/false);
+}
+
 __global__ void k_unite_pairs(const int32_t* __restrict__ edges, int64_t m, int32_t* parent) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < m;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -255,6 +304,57 @@ TC_EXPORT tc_status tcg_cluster_given_core_device(const float* d_coords, int64_t
       given_core<3>(d_coords, n, eps, d_core_in, d_labels, d_core_out, st, stats);
   });
 }
+
+struct tcg_local : tcb::LocalCtx {
+  using LocalCtx::LocalCtx;
+};
+
+TC_EXPORT tc_status tcg_local_create(const float* d_coords, const int32_t* d_keys, int64_t n,
+                                     int dim, float eps, void* stream, tcg_local** out) {
+  if (bad_shape(d_coords, n, dim) || n < 1 || !d_keys || !out || !(eps > 0.f) ||
+      !std::isfinite(eps))
+    return TC_ERR_INVALID_ARGUMENT;
+  tcg_local* c = nullptr;
+  const tc_status st = run_guarded([&] {
+    reset_launch_count();
+    auto ctx = std::make_unique<tcg_local>(static_cast<cudaStream_t>(stream));
+    ctx->n = n;
+    ctx->dim = dim;
+    ctx->eps2 = static_cast<double>(eps) * static_cast<double>(eps);
+    if (dim == 2)
+      local_build<2>(*ctx, d_coords, d_keys);
+    else
+      local_build<3>(*ctx, d_coords, d_keys);
+    c = ctx.release();
+  });
+  if (st == TC_OK) *out = c;
+  return st;
+}
+
+TC_EXPORT tc_status tcg_local_core_flags(tcg_local* ctx, int minpts, uint8_t* d_core) {
+  if (!ctx || !d_core || minpts < 2) return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    reset_launch_count();
+    if (ctx->dim == 2)
+      local_core<2>(*ctx, minpts, d_core);
+    else
+      local_core<3>(*ctx, minpts, d_core);
+  });
+}
+
+TC_EXPORT tc_status tcg_local_cluster(tcg_local* ctx, const uint8_t* d_core_in, int32_t* d_labels,
+                                      uint8_t* d_core_out) {
+  if (!ctx || !d_core_in || !d_labels || !d_core_out) return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    reset_launch_count();
+    if (ctx->dim == 2)
+      local_cluster<2>(*ctx, d_core_in, d_labels, d_core_out);
+    else
+      local_cluster<3>(*ctx, d_core_in, d_labels, d_core_out);
+  });
+}
+
+TC_EXPORT void tcg_local_free(tcg_local* ctx) { delete ctx; }
 
 TC_EXPORT tc_status tcg_union_edges_device(const int32_t* d_edges, int64_t m, int32_t n,
                                            int32_t* d_root, void* stream) {

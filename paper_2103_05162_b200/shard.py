@@ -26,7 +26,9 @@ GPUs, gloo in the CPU tests); every data-path stage runs in the C-ABI library
    are global minimum ids) — the cluster representative is then the global
    minimum core id, exactly the 1-GPU label; own points are relabelled.
 
-minpts == 2 skips steps 5-6: every within-eps pair is a core-core union and
+Steps 5-6 run on one local context (tcg_local_*: own + ghost points keyed by
+global id, one tree for both passes, labels in global ids). minpts == 2
+skips steps 5-6: every within-eps pair is a core-core union and
 "core" is "has a neighbour", exact for own points, so one keyed local run
 (tcg_cluster_keyed_device: own + ghost points, labels = global id of the
 cluster's minimum-id point) replaces the flag exchange, the global-id sort and
@@ -125,6 +127,10 @@ class DeviceEngine:
         self._count()
         return labels, core
 
+    def local(self, x, keys, eps):
+        """A LocalContext over (x, keys): one tree for the core and main passes."""
+        return LocalContext(self, x, keys, eps)
+
     def union_edges(self, edges, n):
         root = torch.empty(n, dtype=torch.int32, device=self.device)
         edges = edges.to(device=self.device, dtype=torch.int32).contiguous()
@@ -133,6 +139,49 @@ class DeviceEngine:
                "tcg_union_edges_device")
         self._count()
         return root
+
+
+class LocalContext:
+    """tcg_local_*: the local (own + ghost) point set of a shard, its BVH built
+    once; core_flags() then cluster() with the owners' ghost flags. Labels
+    are keys (global ids)."""
+
+    def __init__(self, engine, x, keys, eps):
+        self.engine = engine
+        self.x = x.contiguous()
+        self.keys = keys.contiguous()
+        self.n = x.shape[0]
+        h = C.c_void_p()
+        _check(lib.tcg_local_create(C.c_void_p(self.x.data_ptr()), C.c_void_p(self.keys.data_ptr()),
+                                    self.n, x.shape[1], C.c_float(eps), engine._s(), C.byref(h)),
+               "tcg_local_create")
+        engine._count()
+        self.h = h
+
+    def core_flags(self, minpts):
+        core = torch.empty(self.n, dtype=torch.uint8, device=self.x.device)
+        _check(lib.tcg_local_core_flags(self.h, int(minpts), C.c_void_p(core.data_ptr())),
+               "tcg_local_core_flags")
+        self.engine._count()
+        return core
+
+    def cluster(self, core):
+        core = core.contiguous()
+        labels = torch.empty(self.n, dtype=torch.int32, device=self.x.device)
+        core_out = torch.empty(self.n, dtype=torch.uint8, device=self.x.device)
+        _check(lib.tcg_local_cluster(self.h, C.c_void_p(core.data_ptr()),
+                                     C.c_void_p(labels.data_ptr()), C.c_void_p(core_out.data_ptr())),
+               "tcg_local_cluster")
+        self.engine._count()
+        return labels
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            lib.tcg_local_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 # ---------------------------------------------------------------------------
@@ -361,6 +410,38 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
         edges = torch.cat([torch.stack([ghost_gid[gsel], g_lab[gsel]], 1),
                            torch.stack([own_gid[send_idx][esel], e_lab[esel]], 1)])
         root_gid = _merge_edges(edges, own_lab, engine, group)
+        marks.mark("end")
+        marks.report(rank)
+        return own_gid, root_gid, own_core
+
+    if hasattr(engine, "local") and (lgid.shape[0] == 0 or int(lgid.max().item()) < 2**31):
+        # 5. one local context (own + ghost points, keyed by global id): exact
+        #    own flags, owners' flags for the ghosts, then the main pass on the
+        #    same tree; labels come out as global ids
+        lx = torch.cat([own_x, ghost_x]).contiguous()
+        nl = lx.shape[0]
+        if nl == 0:
+            e = torch.empty(0, dtype=torch.int64, device=dev)
+            _all_gather_var(torch.empty((0, 2), dtype=torch.int64, device=dev), group)
+            return e, e.to(torch.int32), e.to(torch.uint8)
+        ctx = engine.local(lx, lgid.to(torch.int32), eps)
+        local_core = ctx.core_flags(minpts)
+        own_core = local_core[:n_own]
+        ghost_core, _ = _all_to_all(own_core[send_idx].view(-1, 1), send_counts, group)
+        core = local_core.clone()
+        core[n_own:] = ghost_core.view(-1)
+        marks.mark("6")
+        lab = ctx.cluster(core).to(torch.int64)
+        ctx.close()
+        marks.mark("7")
+        # 7. cross-shard edges: every core that is a ghost here or was sent
+        #    away as one, with its local label (a global id)
+        touched = torch.zeros(nl, dtype=torch.bool, device=dev)
+        touched[n_own:] = True
+        touched[send_idx] = True
+        sel = (core.bool() & touched).nonzero(as_tuple=False).view(-1)
+        edges = torch.stack([lgid[sel], lab[sel]], 1)
+        root_gid = _merge_edges(edges, lab[:n_own], engine, group)
         marks.mark("end")
         marks.report(rank)
         return own_gid, root_gid, own_core

@@ -67,6 +67,31 @@ class OracleEngine:
         out = np.where(lab >= 0, best[np.maximum(lab, 0)], -1)
         return torch.from_numpy(out.astype(np.int32)), torch.from_numpy(r["core"].astype(np.uint8))
 
+    def local(self, x, keys, eps):
+        """Test double of tcg_local_*: core flags, then the main pass with the
+        given flags, labels = key of the cluster's minimum-key core."""
+        eng = self
+
+        class Local:
+            def core_flags(self, minpts):
+                return eng.core_flags(x, eps, minpts)
+
+            def cluster(self, core):
+                lab = eng.cluster_given_core(x, eps, core).numpy().astype(np.int64)
+                k = keys.numpy().astype(np.int64)
+                c = core.numpy().astype(bool)
+                big = np.iinfo(np.int64).max
+                best = np.full(len(lab), big, np.int64)
+                cm = c & (lab >= 0)
+                np.minimum.at(best, lab[cm], k[cm])
+                out = np.where(lab >= 0, best[np.maximum(lab, 0)], -1)
+                return torch.from_numpy(out.astype(np.int32))
+
+            def close(self):
+                pass
+
+        return Local()
+
     def cluster_given_core(self, x, eps, core):
         e2 = np.float64(np.float32(eps)) ** 2
         adj = self._d2(x.numpy(), x.numpy()) <= e2
