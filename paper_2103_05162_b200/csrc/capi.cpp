@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -159,6 +161,19 @@ tc_status publish(tcb::HostPoints&& pts, tc_dataset** out) {
   *out = ds.release();
   return TC_OK;
 }
+
+// TCB_HOST_TIMING=1: host wall-clock marks of tc_cluster on stderr.
+struct HostTimer {
+  bool on = std::getenv("TCB_HOST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tc_cluster] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // RAII stream + device buffers for one ABI call.
 struct DeviceCall {
@@ -357,15 +372,19 @@ TC_EXPORT tc_status tc_cluster(const tc_dataset* ds, float eps, int minpts, tc_a
     }
     if (!(eps > 0.f) || !std::isfinite(eps) || minpts < 2) return TC_ERR_INVALID_ARGUMENT;
     const int64_t n = ds->n;
+    HostTimer ht;
     auto res = std::make_unique<tc_result>(n);
+    ht.mark("result alloc");
     DeviceCall call;
     float* d_coords = call.alloc<float>(n * ds->dim);
     int32_t* d_labels = call.alloc<int32_t>(n);
     uint8_t* d_core = call.alloc<uint8_t>(n);
+    ht.mark("stream + device alloc");
     TCB_CUDA(cudaMemcpyAsync(d_coords, ds->coords.ptr, sizeof(float) * n * ds->dim,
                              cudaMemcpyHostToDevice, call.st));
     device_cluster(call, d_coords, n, ds->dim, eps, minpts, algorithm, oracle_cap, d_labels,
                    d_core, res.get());
+    ht.mark("H2D + device + D2H");
     if (algorithm == TC_ALGO_BRUTEFORCE) {  // the reference leaves timers/counters at 0
       tc_cluster_stats& s = res->stats;
       s.build_seconds = s.preprocess_seconds = s.main_seconds = s.finalize_seconds = 0.0;
@@ -373,6 +392,7 @@ TC_EXPORT tc_status tc_cluster(const tc_dataset* ds, float eps, int minpts, tc_a
       s.pair_resolutions = s.distance_evaluations = 0;
     }
     *out = res.release();
+    ht.mark("release");
     return TC_OK;
   });
 }
