@@ -115,9 +115,10 @@ k_cover_unite(const int32_t* __restrict__ reach, int64_t n, const int32_t* __res
 struct KeyedJoin {
   int32_t* parent;
   const int32_t* key;
+  uint8_t* mark = nullptr;  // see uf_unite_keyed
   __device__ __forceinline__ void operator()(int32_t a) const {
     const int32_t pa = ld_relaxed(parent + a), pb = ld_relaxed(parent + a - 1);
-    if (pa != pb && pa != a - 1 && pb != a) uf_unite_keyed(parent, key, a, a - 1);
+    if (pa != pb && pa != a - 1 && pb != a) uf_unite_keyed(parent, key, a, a - 1, mark);
   }
 };
 

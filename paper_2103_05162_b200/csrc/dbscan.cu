@@ -200,7 +200,7 @@ template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
               BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
-              int32_t* __restrict__ reach, DevCounters* ctr) {
+              int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -219,13 +219,13 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
     auto visit = [&](int32_t s, int32_t, bool) -> bool {
       ++pairs;
       TCB_PROBE_ONLY(++pr[2];)
-      uf_unite_hinted_keyed(parent, key, rank, s, hint);
+      uf_unite_hinted_keyed(parent, key, rank, s, hint, mark);
       return true;
     };
     auto inside = [&](int32_t first, int32_t last) -> int {
       pairs += static_cast<unsigned long long>(last - first + 1);
       TCB_PROBE_ONLY(++pr[1]; pr[4] += last - first + 1;)
-      uf_unite_hinted_keyed(parent, key, rank, first, hint);
+      uf_unite_hinted_keyed(parent, key, rank, first, hint, mark);
       if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
       return kTaken;
     };
@@ -290,7 +290,8 @@ k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_
 __global__ void __launch_bounds__(256)
 k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
                  const int32_t* __restrict__ key, const int32_t* __restrict__ order, int64_t n,
-                 int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr) {
+                 int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr,
+                 bool derive_core) {
   long long noise = 0, clusters = 0, cores = 0;
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -298,7 +299,7 @@ k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags
     int32_t q;
     while (p != (q = ld_relaxed(parent + p))) p = q;
     st_relaxed(parent + s, p);
-    const bool core = flags[s] != 0;
+    const bool core = flags[s] != 0 || (derive_core && p != s);
     const int32_t i = order[s];
     const int32_t lab = (core || p != s) ? key[p] : -1;  // dbscan.cpp:215
     labels[i] = lab;
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(256)
 k_finalize_gather(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
                   const int32_t* __restrict__ key, const int32_t* __restrict__ rank_of,
                   int64_t i0, int64_t i1, int32_t* __restrict__ labels,
-                  uint8_t* __restrict__ core_out, DevCounters* ctr) {
+                  uint8_t* __restrict__ core_out, DevCounters* ctr, bool derive_core) {
   long long noise = 0, clusters = 0, cores = 0;
   for (int64_t i = i0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < i1;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -329,7 +330,7 @@ k_finalize_gather(int32_t* __restrict__ parent, const uint8_t* __restrict__ flag
     int32_t p = ld_relaxed(parent + s);
     int32_t q;
     while (p != (q = ld_relaxed(parent + p))) p = q;
-    const bool core = flags[s] != 0;
+    const bool core = flags[s] != 0 || (derive_core && p != s);
     const int32_t lab = (core || p != s) ? __ldg(key + p) : -1;  // dbscan.cpp:215
     labels[i] = lab;
     core_out[i] = core ? 1 : 0;
@@ -397,7 +398,7 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
   if (force_core) {
     note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, n, bt, parent, key, reach, d_ctr);
+        b.tree.nodes, b.leaf_pt, n, bt, parent, key, reach, flags, d_ctr);
   } else {
     int32_t* ind = scratch.alloc_n<int32_t>(n + 1);
     int32_t* noncore_before = scratch.alloc_n<int32_t>(n + 1);
@@ -409,7 +410,7 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
                                                              noncore_before, reach, d_ctr);
   }
   // covered runs (all-core): join each covered rank to its predecessor
-  launch_cover_joins(reach, n, tile_max, KeyedJoin{parent, key}, s);
+  launch_cover_joins(reach, n, tile_max, KeyedJoin{parent, key, force_core ? flags : nullptr}, s);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -435,18 +436,21 @@ void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
                            const int32_t* order, int64_t n,
                            int32_t* labels, uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
                            bool force_core) {
-  if (force_core) note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
+  // force_core (minpts == 2): a rank is core iff its set has >= 2 elements —
+  // a non-root, or a root marked by a hook (uf_unite_keyed's mark)
   note_launch(), k_finalize_ranks<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, key, order, n,
-                                                                   labels, core_out, d_ctr);
+                                                                   labels, core_out, d_ctr,
+                                                                   force_core);
   TCB_CUDA(cudaGetLastError());
 }
 
 void finalize_labels_gather(int32_t* parent, const uint8_t* flags, const int32_t* key,
                             const int32_t* rank_of, int64_t i0, int64_t i1, int32_t* labels,
-                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s) {
+                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
+                            bool force_core) {
   if (i1 <= i0) return;
   note_launch(), k_finalize_gather<<<grid_for(i1 - i0, 256), 256, 0, s>>>(
-      parent, flags, key, rank_of, i0, i1, labels, core_out, d_ctr);
+      parent, flags, key, rank_of, i0, i1, labels, core_out, d_ctr, force_core);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -190,8 +190,11 @@ __device__ __forceinline__ void uf_unite_hinted(int32_t* parent, int32_t i, int3
 // key[rank] = original index, and the higher-key root is hooked under the
 // lower-key one, so every representative is the minimum original index of its
 // set — the reference's labels (union_find.hpp:51-64).
+// `mark` (optional): the surviving root of every successful hook gets
+// mark[root] = 1, so "element of a set of >= 2" is (mark[r] || parent[r] != r)
+// without a pass over the structure (minpts == 2 core flags).
 __device__ __forceinline__ int32_t uf_unite_keyed(int32_t* parent, const int32_t* __restrict__ key,
-                                                  int32_t a, int32_t b) {
+                                                  int32_t a, int32_t b, uint8_t* mark = nullptr) {
   while (true) {
     a = uf_find(parent, a);
     b = uf_find(parent, b);
@@ -201,15 +204,19 @@ __device__ __forceinline__ int32_t uf_unite_keyed(int32_t* parent, const int32_t
       a = b;
       b = t;
     }
-    if (atomicCAS(parent + b, b, a) == b) return a;
+    if (atomicCAS(parent + b, b, a) == b) {
+      if (mark) mark[a] = 1;
+      return a;
+    }
   }
 }
 
 __device__ __forceinline__ void uf_unite_hinted_keyed(int32_t* parent, const int32_t* key,
-                                                      int32_t a, int32_t b, int32_t& hint) {
+                                                      int32_t a, int32_t b, int32_t& hint,
+                                                      uint8_t* mark = nullptr) {
   const int32_t pb = ld_cached(parent + b);  // any past parent of b is proof enough
   if (pb == hint || b == hint) return;
-  hint = uf_unite_keyed(parent, key, a, b);
+  hint = uf_unite_keyed(parent, key, a, b, mark);
 }
 
 // One-shot border claim (union_find.hpp:69-73).

@@ -161,12 +161,12 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   if (sink) {
     // gather form, in chunks of output positions: each finished chunk goes
     // to the sink (tc_cluster copies it to the host while the next runs)
-    if (minpts == 2) flatten_mark(parent, flags, n, st);
     const int64_t chunks = n < (int64_t{1} << 22) ? 1 : 8;
     const int64_t per = (n + chunks - 1) / chunks;
     for (int64_t i0 = 0; i0 < n; i0 += per) {
       const int64_t i1 = i0 + per < n ? i0 + per : n;
-      finalize_labels_gather(parent, flags, key, b.rank_of, i0, i1, d_labels, d_core, ctr, st);
+      finalize_labels_gather(parent, flags, key, b.rank_of, i0, i1, d_labels, d_core, ctr, st,
+                             minpts == 2);
       (*sink)(i0, i1, st);
     }
   } else {

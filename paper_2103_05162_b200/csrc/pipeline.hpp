@@ -136,7 +136,8 @@ void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s)
 // finished chunks to the host while later chunks are computed.
 void finalize_labels_gather(int32_t* parent, const uint8_t* flags, const int32_t* key,
                             const int32_t* rank_of, int64_t i0, int64_t i1, int32_t* labels,
-                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s);
+                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
+                            bool force_core);
 // minpts == 2: the union-find flatten + derived core flags of finalize_labels_ranks.
 void flatten_mark(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
 
