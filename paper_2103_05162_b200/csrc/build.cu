@@ -262,7 +262,7 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
         rec[T::kIntOff + 3] = __int_as_float(s_aux[u]);
         float4* dst = nodes + static_cast<int64_t>(p) * T::kVec;
 #pragma unroll
-        for (int v = 0; v < T::kVec; ++v)
+        for (int v = 0; v < (D == 3 ? 4 : 3); ++v)  // (a 2D record's last float4 is padding)
           __stcg(dst + v, make_float4(rec[4 * v], rec[4 * v + 1], rec[4 * v + 2], rec[4 * v + 3]));
         if (link == 0) state->zero_parent = p | kUpLeftBit;
         if (slink == 0) state->zero_parent = p;

@@ -5,7 +5,7 @@
 // (bvh.hpp:60-71). Here every internal node stores BOTH children's boxes,
 // their child links and, per child, one aux int:
 //     3D: 64 B = 4 x float4   [L.lo xyz, L.hi xyz, R.lo xyz, R.hi xyz | l, r, auxL, auxR]
-//     2D: 48 B = 3 x float4   [L.lo xy,  L.hi xy,  R.lo xy,  R.hi xy  | l, r, auxL, auxR]
+//     2D: 64 B = 4 x float4   [L.lo xy,  L.hi xy,  R.lo xy,  R.hi xy  | l, r, auxL, auxR | pad]
 // so one node fetch (two 32 B sectors) decides both children with no second
 // dependent load. Child links: >= 0 internal node index, < 0 = ~leaf_rank
 // (bvh.hpp:91). aux for an internal child = its max leaf rank (the right end
@@ -25,19 +25,20 @@
 
 namespace tcb {
 
+// Both layouts take 64 B: the 2D record (48 B of payload) is padded so that
+// every record is 32-byte aligned and loads as two 256-bit loads.
 template <int D>
 struct NodeTraits {
-  static constexpr int kVec = D == 3 ? 4 : 3;  // float4 per node
+  static constexpr int kVec = 4;          // float4 per node
   static constexpr int kFloats = kVec * 4;
-  static constexpr int kIntOff = 4 * D;        // float index of the int4 part
+  static constexpr int kIntOff = 4 * D;   // float index of the int4 part
 };
 
 constexpr int kStackDepth = 128;
 
-// One node record into registers. 3D records (64 B, 32-byte aligned) take two
-// 256-bit loads (sm_100 LDG.256): half the load requests of float4 loads on
-// the L1 pipe that bounds the traversal. 2D records (48 B) are only 16-byte
-// aligned and keep three 128-bit loads.
+// One node record into registers: two 256-bit loads (sm_100 LDG.256; 64 B
+// records are 32-byte aligned): half the load requests of float4 loads on
+// the L1 pipe that bounds the traversal. A 2D record only needs 48 B of it.
 __device__ __forceinline__ void ld_nc_v8(const float* src, float* f) {
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]), "=f"(f[4]), "=f"(f[5]), "=f"(f[6]),
@@ -47,19 +48,16 @@ __device__ __forceinline__ void ld_nc_v8(const float* src, float* f) {
 
 template <int D>
 __device__ __forceinline__ void load_node(const float4* __restrict__ src, float* f) {
+  const float* s = reinterpret_cast<const float*>(src);
+  ld_nc_v8(s, f);
   if (D == 3) {
-    const float* s = reinterpret_cast<const float*>(src);
-    ld_nc_v8(s, f);
     ld_nc_v8(s + 8, f + 8);
-  } else {
-#pragma unroll
-    for (int v = 0; v < 3; ++v) {
-      const float4 q = __ldg(src + v);
-      f[4 * v + 0] = q.x;
-      f[4 * v + 1] = q.y;
-      f[4 * v + 2] = q.z;
-      f[4 * v + 3] = q.w;
-    }
+  } else {  // floats 8..11 (the int4 part); 12..15 are padding
+    const float4 q = __ldg(src + 2);
+    f[8] = q.x;
+    f[9] = q.y;
+    f[10] = q.z;
+    f[11] = q.w;
   }
 }  // bvh.hpp:82-84 (keys are 64 + 32 bits)
 

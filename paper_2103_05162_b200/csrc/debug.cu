@@ -105,7 +105,7 @@ TC_EXPORT tc_status tcg_debug_point_bvh(const float* coords, int64_t n, int dim,
     // Our internal nodes are numbered by split (root moved to 0, k_climb);
     // the reference numbers them Karras-style: the root is 0, a left child
     // is named by the last rank of its range, a right child by the first.
-    const int kv = dim == 3 ? 4 : 3;
+    const int kv = 4;  // NodeTraits<D>::kVec
     struct Item {
       int32_t ours, karras, lo, hi;
     };
