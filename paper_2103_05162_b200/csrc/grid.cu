@@ -583,8 +583,10 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
 }
 
-// Spatial order of the members inside each cell: key = cell index (high 32
-// bits) | Morton code of the point's position inside its cell (low bits).
+// Spatial order of the members inside each cell: key = cell index (high
+// bits) | 12-bit Morton code of the point's position inside its cell (a
+// 64 x 64 / 16^3 sub-grid: enough coherence for the tree, few sort passes).
+constexpr int kSpatialBits = 12;
 // Any order inside a cell is valid for counting; this one makes the blocks of
 // the spatial member tree compact.
 template <int D>
@@ -598,7 +600,7 @@ __global__ void k_spatial_keys(const float4* __restrict__ sorted_pt,
     const float4 q = sorted_pt[k];
     const float c[3] = {q.x, q.y, q.z};
     uint64_t code = 0;
-    constexpr int bits = D == 2 ? 16 : 10;
+    constexpr int bits = D == 2 ? 6 : 4;  // kSpatialBits per cell in total
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       const float t = (c[a] - gp->origin[a]) * inv_h;
@@ -607,7 +609,7 @@ __global__ void k_spatial_keys(const float4* __restrict__ sorted_pt,
       const uint64_t v = static_cast<uint64_t>(f * static_cast<float>(1 << bits));
       code |= D == 2 ? (spread2(v) << a) : (spread3(v) << a);
     }
-    keys[k] = (static_cast<uint64_t>(cell_of_sorted[k]) << 32) | code;
+    keys[k] = (static_cast<uint64_t>(cell_of_sorted[k]) << kSpatialBits) | code;
     vals[k] = static_cast<int32_t>(k);
   }
 }
@@ -877,7 +879,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
                                                                      gp, n, sk, sv);
     uint64_t cells_pow2 = 1;
     while (cells_pow2 < static_cast<uint64_t>(num_cells)) cells_pow2 <<= 1;
-    const uint64_t or_all = ((cells_pow2 - 1) << 32) | 0xffffffffull;
+    const uint64_t or_all = ((cells_pow2 - 1) << kSpatialBits) | ((1ull << kSpatialBits) - 1);
     const bool alt = radix_sort_pairs(sk, sv, keys, vals, n, 0, or_all, sort_tmp, st);
     const int32_t* sperm = alt ? vals : sv;
     float4* spt = scratch.alloc_n<float4>(n);
