@@ -333,3 +333,44 @@ def test_load_binary_device_matches_host_load(tmp_path):
     with pytest.raises(TreeclustError) as e:
         tb.load_device(str(trunc))
     assert e.value.status == Status.IO
+
+
+@pytest.mark.parametrize("minpts", [2, 6])
+def test_keyed_and_local_context_label_in_keys(minpts):
+    """tcg_cluster_keyed_device and the tcg_local_* context (the sharded
+    path's local runs): with arbitrary unique keys, a cluster is labelled by
+    the key of its minimum-key core, and the partition equals tc_cluster's."""
+    import torch
+    from paper_2103_05162_b200.shard import DeviceEngine
+
+    c = Dataset.blobs(12, 3000, 3, 1.0, 0.12, 17).coords()
+    eps = 0.09
+    want = tb.cluster(Dataset.from_array(c), eps, minpts, Algorithm.FDBSCAN)
+    rng = np.random.default_rng(3)
+    keys = rng.permutation(np.arange(10**6, 10**6 + 7 * len(c), 7)).astype(np.int32)
+    eng = DeviceEngine("cuda:0")
+    x = torch.from_numpy(c).cuda()
+    kd = torch.from_numpy(keys).cuda()
+    core = want.core_flags.astype(bool)
+    lab_w = want.labels
+    # expected: key of the minimum-key core of each reference cluster
+    best = {}
+    for i in np.nonzero(core)[0]:
+        best[lab_w[i]] = min(best.get(lab_w[i], 2**31), int(keys[i]))
+    if minpts == 2:
+        lab, cf = eng.cluster_keyed(x, kd, eps, minpts)
+    else:
+        ctx = eng.local(x, kd, eps)
+        cf = ctx.core_flags(minpts)
+        lab = ctx.cluster(cf)
+        ctx.close()
+    lab = lab.cpu().numpy()
+    assert np.array_equal(cf.cpu().numpy(), want.core_flags)
+    assert np.array_equal(lab == -1, lab_w == -1)
+    for i in np.nonzero(core)[0]:
+        assert lab[i] == best[lab_w[i]], i
+    # borders: a core's cluster within eps (any valid claim)
+    border = (~core) & (lab_w != -1)
+    inv = {v: k for k, v in best.items()}
+    for i in np.nonzero(border)[0]:
+        assert lab[i] in inv, i
