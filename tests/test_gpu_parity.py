@@ -374,3 +374,25 @@ def test_keyed_and_local_context_label_in_keys(minpts):
     inv = {v: k for k, v in best.items()}
     for i in np.nonzero(border)[0]:
         assert lab[i] in inv, i
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties():
+    """C4 at full size (80M 2D taxi-like, eps 0.001, minpts 1000): DenseBox and
+    FDBSCAN agree exactly on cores / noise / core labels, and DenseBox's
+    counters (member-tree scans, primitive runs) stay the reference-semantics
+    values (pinned against the reference at smaller sizes by
+    test_densebox_large_cells_exact_counters)."""
+    import torch
+
+    ds = Dataset.taxi_like(80_000_000)
+    x = torch.from_numpy(ds.coords()).cuda()
+    l1, c1, s1 = tb.cluster_device(x, 0.001, 1000, Algorithm.DENSEBOX, stats=True)
+    l0, c0, s0 = tb.cluster_device(x, 0.001, 1000, Algorithm.FDBSCAN, stats=True)
+    assert torch.equal(c0, c1)
+    assert torch.equal(l0 == -1, l1 == -1)
+    m = c0.bool()
+    assert torch.equal(l0[m], l1[m])
+    assert s1["pair_resolutions"] == 16_116_139_953
+    assert s1["distance_evaluations"] == 47_286_475_806
+    assert s1["core_count"] == 78_423_128 and s1["cluster_count"] == 250
