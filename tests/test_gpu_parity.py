@@ -396,3 +396,33 @@ def test_c4_full_size_properties():
     assert s1["pair_resolutions"] == 16_116_139_953
     assert s1["distance_evaluations"] == 47_286_475_806
     assert s1["core_count"] == 78_423_128 and s1["cluster_count"] == 250
+
+
+@pytest.mark.parametrize("minpts", [2, 5, 3000])
+def test_massive_duplicates_and_flat_axis(minpts):
+    """Stress of the contained-run paths: 1.5M copies of one point plus a flat
+    (z = 0) uniform background. All copies form one cluster whose pair count is
+    n(n-1)/2 (every pair of copies), counted exactly through rank runs."""
+    rng = np.random.default_rng(8)
+    dup = np.tile(np.array([[-5.0, -5.0, 0.0]], np.float32), (1_500_000, 1))
+    bg = np.concatenate([rng.uniform(0, 100, (200_000, 2)), np.zeros((200_000, 1))], 1)
+    c = np.concatenate([dup, bg.astype(np.float32)])
+    eps = 0.05
+    got = tb.cluster(Dataset.from_array(c), eps, minpts, Algorithm.FDBSCAN)
+    nd = len(dup)
+    assert (got.labels[:nd] == 0).all() and (got.core_flags[:nd] == 1).all()
+    # background pairs: brute force on the sparse part only (no background
+    # point is within eps of the duplicate point here)
+    b = bg.astype(np.float32).astype(np.float64)
+    assert np.sqrt(((b[:, :2] + 5.0) ** 2).sum(1)).min() > eps
+    want_bg = tb.cluster(Dataset.from_array(bg.astype(np.float32)), eps, minpts, Algorithm.FDBSCAN)
+    assert got.stats["pair_resolutions"] == nd * (nd - 1) // 2 + want_bg.stats["pair_resolutions"]
+    assert np.array_equal(got.core_flags[nd:], want_bg.core_flags)
+    lab = got.labels[nd:]
+    wl = want_bg.labels
+    assert np.array_equal(lab == -1, wl == -1)
+    cm = want_bg.core_flags == 1
+    assert np.array_equal(lab[cm], wl[cm] + nd)
+    db = tb.cluster(Dataset.from_array(c), eps, minpts, Algorithm.DENSEBOX)
+    assert np.array_equal(db.core_flags, got.core_flags)
+    assert np.array_equal(db.labels[got.core_flags == 1], got.labels[got.core_flags == 1])
