@@ -432,6 +432,11 @@ __device__ __forceinline__ void warp_start_node(const float4* __restrict__ nodes
   }
 }
 
+// One query per thread, started at the warp's common start node. Q provides
+// begin(q) (false: no query), step(), end(), p[3], node, nlo and mask_rank
+// (the query's min_rank). Starting below the root skips only nodes with a
+// single live child, so the order of the query's visit calls is the same as
+// from the root (the DenseBox core pass depends on that order).
 template <int D, class Q>
 __device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp,
                                                     const float4* __restrict__ nodes,
@@ -460,90 +465,6 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
   }
 }
 
-// ---------------------------------------------------------------------------
-// Persistent, warp-refilled query driver.
-//
-// Per-query work varies by orders of magnitude (a point in a halo core has
-// thousands of neighbours, a background point none), so one-query-per-thread
-// launches leave most lanes of a warp idle while the longest query runs
-// (ncu, round 1: 5.6 active threads / warp). Instead each warp owns a chunk of
-// kQueryChunk Morton-consecutive queries (grabbed with one atomic) and refills
-// every lane the moment its query finishes; all lanes advance one node per
-// iteration. Chunks are handed out in rank order, so the queries in flight
-// stay a narrow, L2-resident window of the tree.
-//
-// Q provides:  bool begin(int64_t q)  start query q (false: nothing to do)
-//              bool step()            one node; false when the query is done
-//              void end()             finish the current query
-// ---------------------------------------------------------------------------
-constexpr int kQueryChunk = 256;
-
-// One query per thread, grid covers all queries (the plain launch).
-template <class Q>
-__device__ __forceinline__ void run_query_direct(int64_t m, Q& qp) {
-  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (q < m && qp.begin(q)) {
-    while (qp.step()) {
-    }
-    qp.end();
-  }
-}
-
-// One query per thread started at the warp's common start node
-// (warp_start_node, defined below). Q also exposes p[3], node and
-// mask_rank (the query's min_rank). Starting below the root skips only nodes
-// with a single live child, so the order of the query's visit calls is the
-// same as from the root (the DenseBox core pass depends on that order).
-template <int D, class Q>
-__device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp,
-                                                    const float4* __restrict__ nodes,
-                                                    const BallTest& bt);
-
-// Query scheduling mode of the traversal kernels: 0 = one query per thread,
-// 1 = persistent warp-refilled queue. Chosen once per process (TCB_QUERY_MODE).
-int query_mode();
-
-__device__ __forceinline__ uint32_t lanemask_lt_u32() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-template <class Q>
-__device__ __forceinline__ void run_query_queue(int64_t m, unsigned long long* next_chunk, Q& qp) {
-  const int lane = threadIdx.x & 31;
-  long long cur = 0, end = 0;  // warp-uniform chunk [cur, end)
-  bool exhausted = false;      // warp-uniform
-  bool busy = false;
-  while (true) {
-    const uint32_t idle = __ballot_sync(0xffffffffu, !busy);
-    if (idle) {
-      if (cur >= end && !exhausted) {
-        long long base = 0;
-        if (lane == 0) base = static_cast<long long>(atomicAdd(next_chunk, kQueryChunk));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= m) {
-          exhausted = true;
-        } else {
-          cur = base;
-          end = base + kQueryChunk < m ? base + kQueryChunk : m;
-        }
-      }
-      if (cur >= end) {
-        if (idle == 0xffffffffu && exhausted) break;
-      } else {
-        const long long q = cur + __popc(idle & lanemask_lt_u32());
-        if (!busy && q < end) busy = qp.begin(q);
-        cur += __popc(idle);
-        if (cur > end) cur = end;
-      }
-    }
-    if (busy && !qp.step()) {
-      qp.end();
-      busy = false;
-    }
-  }
-}
 
 // Device view of a built tree.
 struct DeviceBvh {

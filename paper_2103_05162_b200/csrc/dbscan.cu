@@ -96,22 +96,18 @@ struct CoreQuery {
 template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent) {
+          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
   LocalStack stack;
   CoreQuery<D> q{nodes, leaf_pt, bt, minpts, flags, &stack};
-  if (persistent) {
-    run_query_queue(m, &ctr->queue[0], q);
-  } else {
-    // one query per thread, started at the warp's common start node
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    const bool valid = r < m;
-    if (valid) q.begin(r);
-    warp_start_node<D>(nodes, q.p, valid, bt, 0, q.node, q.nlo);
-    if (valid) {
-      while (q.step()) {
-      }
-      q.end();
+  // one query per thread, started at the warp's common start node
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
+  if (valid) q.begin(r);
+  warp_start_node<D>(nodes, q.p, valid, bt, 0, q.node, q.nlo);
+  if (valid) {
+    while (q.step()) {
     }
+    q.end();
   }
   flush_counter(&ctr->dists, q.dists);
 }
@@ -381,8 +377,8 @@ k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int6
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s) {
-  note_launch(), k_fd_core<D><<<query_grid(k_fd_core<D>, n), kQueryBlock, 0, s>>>(
-      b.tree.nodes, b.leaf_pt, n, BallTest::make(eps2), minpts, flags, d_ctr, query_mode() == 1);
+  note_launch(), k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
+      b.tree.nodes, b.leaf_pt, n, BallTest::make(eps2), minpts, flags, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -110,13 +110,6 @@ void note_launch() { ++t_launches; }
 void reset_launch_count() { t_launches = 0; }
 int64_t launch_count() { return t_launches; }
 
-int query_mode() {
-  static const int mode = [] {
-    const char* v = std::getenv("TCB_QUERY_MODE");
-    return v ? std::atoi(v) : 0;
-  }();
-  return mode;
-}
 
 void set_last_stage_ms(const double* ms) {
   for (int s = 0; s < kNumStages; ++s) t_last_stage_ms[s] = ms[s];

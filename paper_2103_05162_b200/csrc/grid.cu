@@ -16,7 +16,7 @@
 // contiguous run of queries, so each warp shares one neighbourhood.
 //   k_dense_union     union_dense_cells (dbscan.cpp:90-108): direct hooks
 //   k_db_core         densebox_mark_cores (dbscan.cpp:110-139)
-//   k_db_main         densebox_main_phase (dbscan.cpp:141-200)
+//   k_db_main_ranged  densebox_main_phase (dbscan.cpp:141-200)
 #include <cfloat>
 #include <cmath>
 #include <cstring>
@@ -368,119 +368,22 @@ struct DbCoreQuery {
   }
 };
 
-// densebox_main_phase query (dbscan.cpp:141-200): masked at the rank of the
-// query's own primitive (its own leaf skipped); a SinglePoint leaf is one
-// pair, a DenseBox leaf contributes the first member within eps only — every
-// member is a core of one pre-unioned cluster, so one link joins them all.
-template <int D, bool kForceCore>
-struct DbMainQuery {
-  const float4* __restrict__ nodes;
-  const float4* __restrict__ qpt;
-  const int32_t* __restrict__ qrank;
-  const float4* __restrict__ sorted_pt;
-  const int32_t* __restrict__ cell_begin;
-  const int32_t* __restrict__ cell_end;
-  BallTest bt;
-  const uint8_t* __restrict__ flags;
-  int32_t* __restrict__ parent;
-  int32_t* stack;  // per-thread traversal stack, kept outside the struct
-  unsigned long long dists = 0, pairs = 0;
-  float p[3];
-  int32_t i, own, hint, node, nlo, mask_rank;
-  int top;
-  bool core_i, settled;
-  __device__ bool begin(int64_t q) {
-    const float4 qp = qpt[q];
-    i = __float_as_int(qp.w) & 0x7fffffff;
-    own = qrank[q];
-    mask_rank = own;
-    p[0] = qp.x;
-    p[1] = qp.y;
-    p[2] = qp.z;
-    core_i = kForceCore ? true : flags[i] != 0;
-    hint = i;
-    settled = false;
-    node = 0;
-    top = 0;
-    return true;
-  }
-  __device__ void pair(int32_t j) {
-    ++pairs;
-    if (kForceCore)
-      uf_unite_hinted(parent, i, j, hint);  // core flags derived at finalize
-    else
-      resolve_pair(i, j, core_i, flags, parent, hint, settled);
-  }
-  __device__ bool step() {
-    auto visit = [&](int32_t s, int32_t aux, const float* lo, const float* hi) -> bool {
-      if (s == own) return true;
-      if (aux >= 0) {
-        ++dists;
-        pair(aux);
-      } else {
-        const int32_t c = ~aux;
-        const int32_t kb = cell_begin[c], ke = cell_end[c];
-        if (box_inside_ball<D>(p, lo, hi, bt)) {
-          // every member is within eps: the scan stops at the first one
-          ++dists;
-          pair(__float_as_int(__ldg(sorted_pt + kb).w));
-        } else {
-          for (int32_t k = kb; k < ke; ++k) {
-            const float4 m4 = __ldg(sorted_pt + k);
-            const float mp[3] = {m4.x, m4.y, m4.z};
-            ++dists;
-            if (ball_hits<D>(p, mp, mp, bt)) {
-              pair(__float_as_int(m4.w));
-              break;  // dbscan.cpp:183-193
-            }
-          }
-        }
-      }
-      return true;
-    };
-    return bvh_step<D>(nodes, p, bt, own, node, top, stack, visit);
-  }
-  __device__ void end() {}
-};
-
 template <int D>
 __global__ void __launch_bounds__(kQueryBlock)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
-          uint8_t* __restrict__ flags, DevCounters* ctr, bool persistent, MemberTree mt,
+          uint8_t* __restrict__ flags, DevCounters* ctr, MemberTree mt,
           MemberTree smt, const int32_t* __restrict__ qoff, int32_t num_prims,
           const int32_t* __restrict__ list, int64_t m) {
   LocalStack stack;
   DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
                    &smt, qoff, n, num_prims, list};
-  if (persistent)
-    run_query_queue(m, &ctr->queue[2], q);
-  else
-    run_query_warpstart<D>(m, q, nodes, bt);
+  run_query_warpstart<D>(m, q, nodes, bt);
   unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
 }
 
-template <int D, bool kForceCore>
-__global__ void __launch_bounds__(kQueryBlock)
-k_db_main(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
-          const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
-          const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
-          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-          DevCounters* ctr, bool persistent) {
-  int32_t stack[kStackDepth];
-  DbMainQuery<D, kForceCore> q{nodes, qpt, qrank, sorted_pt, cell_begin, cell_end, bt, flags,
-                               parent, stack};
-  if (persistent)
-    run_query_queue(n, &ctr->queue[3], q);
-  else
-    run_query_warpstart<D>(n, q, nodes, bt);
-  unsigned long long v = warp_sum(q.dists);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
-  v = warp_sum(q.pairs);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
-}
 
 // densebox_main_phase with contained subtrees (direct launch). A subtree of
 // the mixed tree whose box lies inside the ball holds primitives that each
@@ -899,45 +802,36 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
     exclusive_scan_i32(ind, pos, num_prims, nullptr, scan_tmp, st);
     note_launch(), k_single_slots<<<grid_for(num_prims, 256), 256, 0, st>>>(ind, pos, qoff,
                                                                             num_prims, list);
-    note_launch(), k_db_core<D><<<query_grid(k_db_core<D>, sparse_points), kQueryBlock, 0, st>>>(
-        b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr,
-        query_mode() == 1, mt, smt, qoff, num_prims, list, sparse_points);
+    note_launch(), k_db_core<D><<<grid_for(sparse_points, kQueryBlock, INT32_MAX), kQueryBlock, 0, st>>>(
+        b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr, mt, smt,
+        qoff, num_prims, list, sparse_points);
   }
   // ---- main pass ----
   clock.mark(kStMain);
-  if (query_mode() != 1) {
-    int32_t* rep = scratch.alloc_n<int32_t>(num_prims);
-    int32_t* reach = scratch.alloc_n<int32_t>(num_prims + 8);
-    int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(num_prims));
-    int32_t* noncore_before = nullptr;
-    TCB_CUDA(cudaMemsetAsync(reach, 0xff, sizeof(int32_t) * num_prims, st));
-    note_launch(), k_prim_reps<<<grid_for(num_prims, 256), 256, 0, st>>>(
-        b.tree.leaf_order, prim_aux, cell_begin, sorted_pt, num_prims, rep);
-    if (minpts > 2) {
-      int32_t* ind = scratch.alloc_n<int32_t>(num_prims + 1);
-      noncore_before = scratch.alloc_n<int32_t>(num_prims + 1);
-      note_launch(), k_prim_noncore<<<grid_for(num_prims + 1, 256), 256, 0, st>>>(
-          b.tree.leaf_order, prim_aux, flags, num_prims, ind);
-      exclusive_scan_i32(ind, noncore_before, num_prims + 1, nullptr, scan_tmp, st);
-    }
-    const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
-    if (minpts == 2)
-      note_launch(), k_db_main_ranged<D, true><<<g, kQueryBlock, 0, st>>>(
-          b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
-          noncore_before, reach, ctr, mt);
-    else
-      note_launch(), k_db_main_ranged<D, false><<<g, kQueryBlock, 0, st>>>(
-          b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
-          noncore_before, reach, ctr, mt);
-    launch_cover_joins(reach, num_prims, tile_max, RepJoin{parent, rep}, st);
-  } else if (minpts == 2)
-    note_launch(), k_db_main<D, true><<<query_grid(k_db_main<D, true>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
-                                                   cell_begin, cell_end, bt, flags, parent,
-                                                   ctr, query_mode() == 1);
+  int32_t* rep = scratch.alloc_n<int32_t>(num_prims);
+  int32_t* reach = scratch.alloc_n<int32_t>(num_prims + 8);
+  int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(num_prims));
+  int32_t* noncore_before = nullptr;
+  TCB_CUDA(cudaMemsetAsync(reach, 0xff, sizeof(int32_t) * num_prims, st));
+  note_launch(), k_prim_reps<<<grid_for(num_prims, 256), 256, 0, st>>>(
+      b.tree.leaf_order, prim_aux, cell_begin, sorted_pt, num_prims, rep);
+  if (minpts > 2) {
+    int32_t* ind = scratch.alloc_n<int32_t>(num_prims + 1);
+    noncore_before = scratch.alloc_n<int32_t>(num_prims + 1);
+    note_launch(), k_prim_noncore<<<grid_for(num_prims + 1, 256), 256, 0, st>>>(
+        b.tree.leaf_order, prim_aux, flags, num_prims, ind);
+    exclusive_scan_i32(ind, noncore_before, num_prims + 1, nullptr, scan_tmp, st);
+  }
+  const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
+  if (minpts == 2)
+    note_launch(), k_db_main_ranged<D, true><<<g, kQueryBlock, 0, st>>>(
+        b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
+        noncore_before, reach, ctr, mt);
   else
-    note_launch(), k_db_main<D, false><<<query_grid(k_db_main<D, false>, n), kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
-                                                    cell_begin, cell_end, bt, flags, parent,
-                                                    ctr, query_mode() == 1);
+    note_launch(), k_db_main_ranged<D, false><<<g, kQueryBlock, 0, st>>>(
+        b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
+        noncore_before, reach, ctr, mt);
+  launch_cover_joins(reach, num_prims, tile_max, RepJoin{parent, rep}, st);
   TCB_CUDA(cudaGetLastError());
   clock.mark(kStFinal);
   finalize_labels(parent, flags, n, d_labels, d_core, ctr, st, minpts == 2);

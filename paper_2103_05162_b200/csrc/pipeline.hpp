@@ -25,7 +25,6 @@ struct DevCounters {
   int32_t count_a;             // generic device-side counts (cells, prims ...)
   int32_t count_b;
   int32_t pad;
-  unsigned long long queue[4];  // chunk counters of the persistent query kernels
   unsigned long long probe[8];  // -DTCB_PROBE builds only (make probe): work counters
 };
 
@@ -202,26 +201,7 @@ __device__ __forceinline__ void publish_and_or(uint64_t a, uint64_t o, DevCounte
 
 #endif
 
-// Grid of a persistent kernel: every SM filled to the kernel's occupancy.
-template <typename Kernel>
-inline unsigned persistent_grid(Kernel kernel, int block) {
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
-  if (per_sm < 1) per_sm = 1;
-  return static_cast<unsigned>(sms * per_sm);
-}
-
-int query_mode();
-
 inline unsigned grid_for(int64_t work, int block, int64_t max_blocks = 148 * 64);
-
-// Grid of a traversal kernel under the current query scheduling mode.
-template <typename Kernel>
-inline unsigned query_grid(Kernel kernel, int64_t n) {
-  return query_mode() == 1 ? persistent_grid(kernel, 128) : grid_for(n, 128, INT32_MAX);
-}
 
 inline unsigned grid_for(int64_t work, int block, int64_t max_blocks) {
   int64_t b = (work + block - 1) / block;
