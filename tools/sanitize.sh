@@ -18,6 +18,30 @@ for algo, mp in ((0, 4), (1, 4)):
     print("2d", algo, mp, r.stats["cluster_count"])
 st, rep = tb.verify(ds, 0.3, 5)
 print("verify", int(st))
+# dense cells with long member runs (member trees, spatial tree, runs)
+rng = np.random.default_rng(4)
+g = np.stack(np.meshgrid(np.arange(60), np.arange(60)), -1).reshape(-1, 2)
+lat = (g * 0.01 + rng.uniform(-0.004, 0.004, g.shape)).astype(np.float32)
+lat = np.concatenate([lat, np.repeat(lat[:50], 40, axis=0)])
+for mp in (2, 20, 200):
+    r = tb.cluster(tb.Dataset.from_array(lat), 0.1, mp, tb.Algorithm.DENSEBOX)
+    print("dense", mp, r.stats["cluster_count"], r.stats["distance_evaluations"])
+# keyed run, local context, binary load to the device
+import torch
+from paper_2103_05162_b200.shard import DeviceEngine
+eng = DeviceEngine("cuda:0")
+x = torch.from_numpy(ds.coords()).cuda()
+keys = torch.arange(5000, 5000 + x.shape[0], dtype=torch.int32, device="cuda")
+lab, core = eng.cluster_keyed(x, keys, 0.3, 2)
+ctx = eng.local(x, keys, 0.3)
+cf = ctx.core_flags(5)
+lab2 = ctx.cluster(cf)
+ctx.close()
+torch.cuda.synchronize()
+print("keyed", int((lab >= 0).sum()), int((lab2 >= 0).sum()))
+ds.save("/tmp/san.bin")
+y = tb.load_device("/tmp/san.bin")
+print("load", bool(torch.equal(y, x)))
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 $CS --tool $tool --error-exitcode 9 python /tmp/san_run.py > gpurun_out/sanitize_$tool.log 2>&1
