@@ -1,15 +1,20 @@
 // FDBSCAN passes over the point BVH, and label finalization.
 //
-//   k_fd_core   fdbscan_mark_cores (dbscan.cpp:36-58): one thread per leaf
-//               rank (Morton order, so a warp's queries are spatial
-//               neighbours and walk nearly the same nodes), unmasked query,
-//               early exit once minpts neighbours (self included) are seen.
-//   k_fd_main   fdbscan_main_phase (dbscan.cpp:60-88): rank-masked query so
-//               every unordered within-eps pair is found exactly once, each
-//               pair resolved on the spot with the lock-free union-find; no
-//               neighbour list is ever stored.
-//   k_finalize  UnionFind::flatten + finalize_labels + the stats loop
-//               (union_find.hpp:77-86, dbscan.cpp:202-219, :274-282).
+//   k_fd_core      fdbscan_mark_cores (dbscan.cpp:36-58): one thread per leaf
+//                  rank (Morton order, so a warp's queries are spatial
+//                  neighbours and walk nearly the same nodes), unmasked
+//                  query from the warp's start node, early exit once minpts
+//                  neighbours (self included) are seen.
+//   k_fd_main_fof  fdbscan_main_phase (dbscan.cpp:60-88) for minpts == 2:
+//                  rank-masked query so every unordered within-eps pair is
+//                  found exactly once, each pair resolved on the spot with the
+//                  lock-free union-find, contained subtrees taken as runs;
+//                  no neighbour list is ever stored.
+//   k_fd_main      the same for minpts > 2 (pairs resolved per
+//                  dbscan.hpp:82-99 with final core flags).
+//   cover.cuh      the runs' unions (max-scan over the recorded runs).
+//   k_finalize*    UnionFind::flatten + finalize_labels + the stats loop
+//                  (union_find.hpp:77-86, dbscan.cpp:202-219, :274-282).
 //
 // For point leaves the leaf box test IS the exact distance test (the box is
 // degenerate and box_distance_sq reduces to distance_sq term by term, the
