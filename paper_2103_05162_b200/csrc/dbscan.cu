@@ -31,7 +31,7 @@ namespace tcb {
 
 namespace {
 
-constexpr int kQueryBlock = 128;
+constexpr int kQueryBlock = 128;  // 64 / 256 measured equal or slower
 
 template <int D>
 __device__ __forceinline__ void load_query(const float4* leaf_pt, int64_t r, float* p,
