@@ -198,3 +198,38 @@ def test_product_path_has_no_oracle_dependency():
                     "from oracle" not in txt and "liboracle" not in txt, f
     libs = os.popen(f"ldd {LIB_PATH}").read()
     assert "oracle" not in libs and "treeclust_ref" not in libs
+
+
+def test_additive_entry_points_validate_before_device_work(tmp_path):
+    """tcg_binary_info / tcg_load_binary_device / tcg_cluster_keyed_device /
+    tcg_local_*: header parsing and argument checks are host-side and need no
+    GPU; errors map like the reference ABI's (bad file -> TC_ERR_IO, null or
+    invalid argument -> TC_ERR_INVALID_ARGUMENT)."""
+    ds = Dataset.blobs(2, 50, 3, 5.0, 0.3, 7)
+    path = str(tmp_path / "p.bin")
+    ds.save(path)
+    n, d = C.c_int64(), C.c_int()
+    assert lib.tcg_binary_info(path.encode(), C.byref(n), C.byref(d)) == Status.OK
+    assert (n.value, d.value) == (100, 3)
+    assert lib.tcg_binary_info(b"/nonexistent.bin", C.byref(n), C.byref(d)) == Status.IO
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"\x05\x00\x00\x00\x07\x00\x00\x00")
+    assert lib.tcg_binary_info(str(bad).encode(), C.byref(n), C.byref(d)) == Status.IO
+    assert lib.tcg_binary_info(None, C.byref(n), C.byref(d)) == Status.INVALID_ARGUMENT
+    assert lib.tcg_load_binary_device(path.encode(), None, 100, 3, None) == Status.INVALID_ARGUMENT
+    assert lib.tcg_load_binary_device(path.encode(), C.c_void_p(16), 100, 4, None) == \
+        Status.INVALID_ARGUMENT
+    st = tb.api.TcClusterStats()
+    assert lib.tcg_cluster_keyed_device(C.c_void_p(16), None, 10, 3, C.c_float(0.1), 2,
+                                        C.c_void_p(16), C.c_void_p(16), None,
+                                        C.byref(st)) == Status.INVALID_ARGUMENT
+    h = C.c_void_p()
+    assert lib.tcg_local_create(None, C.c_void_p(16), 10, 3, C.c_float(0.1), None,
+                                C.byref(h)) == Status.INVALID_ARGUMENT
+    assert lib.tcg_local_create(C.c_void_p(16), C.c_void_p(16), 10, 3, C.c_float(-1.0), None,
+                                C.byref(h)) == Status.INVALID_ARGUMENT
+    assert h.value is None  # *out untouched on failure
+    assert lib.tcg_local_core_flags(None, 5, C.c_void_p(16)) == Status.INVALID_ARGUMENT
+    assert lib.tcg_local_cluster(None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16)) == \
+        Status.INVALID_ARGUMENT
+    lib.tcg_local_free(None)  # no-op
