@@ -93,10 +93,13 @@ struct BallTest {
   }
 };
 
-template <int D>
+// kFast: 1 = bt.fast known true, 0 = known false, -1 = test at run time
+// (kernels on the hot path are instantiated for both and launched by the host
+// with the right one, which drops the fp64-only branch from their loops).
+template <int D, int kFast = -1>
 __device__ __forceinline__ bool ball_hits(const float* p, const float* lo, const float* hi,
                                           const BallTest& bt) {
-  if (bt.fast) {
+  if (kFast == 1 || (kFast == -1 && bt.fast)) {
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -193,10 +196,10 @@ __device__ __forceinline__ bool bvh_step(const float4* __restrict__ nodes, const
 // degenerate box any answer > 0 means "within eps". The fp32 estimates use
 // fused multiply-adds: one rounding per term instead of two, inside the same
 // error bound as the unfused chain the band was sized for.
-template <int D>
+template <int D, int kFast = -1>
 __device__ __forceinline__ int ball_classify(const float* p, const float* lo, const float* hi,
                                              const BallTest& bt) {
-  if (!bt.fast) return ball_hits<D>(p, lo, hi, bt) ? 1 : 0;
+  if (kFast == 0 || (kFast == -1 && !bt.fast)) return ball_hits<D, 0>(p, lo, hi, bt) ? 1 : 0;
   float sn = 0.f, sf = 0.f;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -237,7 +240,7 @@ constexpr int kStop = 0, kTaken = 1, kWalk = 2;
 // leaves are reported is not the reference's DFS order (callers only depend
 // on the set, or, for early exit, on the count — see CoreQuery).
 
-template <int D, typename Stack, typename Visit, typename Inside>
+template <int D, typename Stack, typename Visit, typename Inside, int kFast = -1>
 __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes, const float* p,
                                                 const BallTest& bt, int32_t min_rank,
                                                 int32_t& node, int32_t& nlo, Stack& stack,
@@ -254,8 +257,8 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   const int32_t max_r = leaf_r ? ~right : aux_r;
   const int32_t lo_l = nlo > min_rank ? nlo : min_rank;
   const int32_t lo_r = split + 1 > min_rank ? split + 1 : min_rank;
-  int cl = ball_classify<D>(p, f, f + D, bt);
-  int cr = ball_classify<D>(p, f + 2 * D, f + 3 * D, bt);
+  int cl = ball_classify<D, kFast>(p, f, f + D, bt);
+  int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
   if (split < min_rank) cl = 0;
   if (max_r < min_rank) cr = 0;
   if (cl > 0 && (leaf_l || cl == 2)) {

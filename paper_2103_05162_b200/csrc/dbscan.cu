@@ -54,7 +54,7 @@ __device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned 
 // reference would have stopped inside it after exactly minpts - count more
 // leaf hits, so the distance counter (one per hit, dists == count) is still
 // the reference's.
-template <int D>
+template <int D, int kFast>
 struct CoreQuery {
   const float4* __restrict__ nodes;
   const float4* __restrict__ leaf_pt;
@@ -91,19 +91,20 @@ struct CoreQuery {
       count += static_cast<int>(k);
       return kTaken;
     };
-    return bvh_step_ranged<D>(nodes, p, bt, 0, node, nlo, *stack, visit, inside);
+    return bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, 0, node, nlo, *stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[id] = 1;
   }
 };
 
-template <int D>
+template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
   LocalStack stack;
-  CoreQuery<D> q{nodes, leaf_pt, bt, minpts, flags, &stack};
+  CoreQuery<D, kFast> q{nodes, leaf_pt, bt, minpts, flags, &stack};
   // one query per thread, started at the warp's common start node
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
@@ -131,7 +132,7 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
 //   border query, no core leaf or already settled (claimed): every pair is a
 //                 no-op, counted only; all leaves core: claimed by the run;
 //   otherwise the subtree is walked leaf by leaf (per-pair rule).
-template <int D>
+template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
@@ -174,7 +175,8 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
       return kTaken;
     };
     LocalStack stack;
-    while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
+    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
     }
   }
   flush_counter(&ctr->pairs, pairs);
@@ -197,7 +199,7 @@ __global__ void k_noncore_ind(const uint8_t* __restrict__ flags, int64_t n,
 // partition as uniting r with each leaf (each leaf is joined to r through the
 // run); pairs counted per leaf, so pair_resolutions / distance_evaluations
 // stay exact.
-template <int D>
+template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
               BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
@@ -231,7 +233,8 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
       return kTaken;
     };
     LocalStack stack;
-    while (bvh_step_ranged<D>(nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
+    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
       TCB_PROBE_ONLY(++pr[0];)
     }
     TCB_PROBE_ONLY(++pr[0]; pr[5] += pairs == 0; pr[6] = pr[0]; if (pairs == 0) pr[3] = pr[0];)
@@ -382,8 +385,10 @@ k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int6
 template <int D>
 void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
                        uint8_t* flags, DevCounters* d_ctr, cudaStream_t s) {
-  note_launch(), k_fd_core<D><<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-      b.tree.nodes, b.leaf_pt, n, BallTest::make(eps2), minpts, flags, d_ctr);
+  const BallTest bt = BallTest::make(eps2);
+  auto core = bt.fast ? k_fd_core<D, 1> : k_fd_core<D, 0>;
+  note_launch(), core<<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
+      b.tree.nodes, b.leaf_pt, n, bt, minpts, flags, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -398,17 +403,18 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
   int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(n));
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
   if (force_core) {
-    note_launch(), k_fd_main_fof<D><<<grid, kQueryBlock, 0, s>>>(
-        b.tree.nodes, b.leaf_pt, n, bt, parent, key, reach, flags, d_ctr);
+    auto fof = bt.fast ? k_fd_main_fof<D, 1> : k_fd_main_fof<D, 0>;
+    note_launch(), fof<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, parent, key,
+                                                   reach, flags, d_ctr);
   } else {
     int32_t* ind = scratch.alloc_n<int32_t>(n + 1);
     int32_t* noncore_before = scratch.alloc_n<int32_t>(n + 1);
     void* scan_tmp = scratch.alloc(scan_scratch_bytes(n + 1));
     note_launch(), k_noncore_ind<<<grid_for(n + 1, 256), 256, 0, s>>>(flags, n, ind);
     exclusive_scan_i32(ind, noncore_before, n + 1, nullptr, scan_tmp, s);
-    note_launch(), k_fd_main<D><<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags,
-                                                             parent, key,
-                                                             noncore_before, reach, d_ctr);
+    auto main = bt.fast ? k_fd_main<D, 1> : k_fd_main<D, 0>;
+    note_launch(), main<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags, parent,
+                                                    key, noncore_before, reach, d_ctr);
   }
   // covered runs (all-core): join each covered rank to its predecessor
   launch_cover_joins(reach, n, tile_max, KeyedJoin{parent, key, force_core ? flags : nullptr}, s);
