@@ -308,7 +308,7 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
 // with an order-dependent early exit (the DenseBox core pass) needs.
 //     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
 //     bool inside(int32_t first, int32_t last)    (false = stop the query)
-template <int D, typename Stack, typename Visit, typename Inside>
+template <int D, typename Stack, typename Visit, typename Inside, int kFast = -1>
 __device__ __forceinline__ bool bvh_step_ordered(const float4* __restrict__ nodes, const float* p,
                                                  const BallTest& bt, int32_t min_rank,
                                                  int32_t& node, int32_t& nlo, Stack& stack,
@@ -323,8 +323,8 @@ __device__ __forceinline__ bool bvh_step_ordered(const float4* __restrict__ node
   const bool leaf_l = left < 0, leaf_r = right < 0;
   const int32_t split = leaf_l ? ~left : aux_l;
   const int32_t max_r = leaf_r ? ~right : aux_r;
-  int cl = ball_classify<D>(p, f, f + D, bt);
-  int cr = ball_classify<D>(p, f + 2 * D, f + 3 * D, bt);
+  int cl = ball_classify<D, kFast>(p, f, f + D, bt);
+  int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
   if (split < min_rank) cl = 0;
   if (max_r < min_rank) cr = 0;
   if (leaf_l && cl > 0 && !visit(~left, aux_l, f, f + D)) return false;

@@ -275,7 +275,7 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
 // densebox_mark_cores query (dbscan.cpp:110-139): unmasked; a SinglePoint
 // leaf is one neighbour, a DenseBox leaf is scanned member by member until
 // minpts is reached. Dense members are core already and skip (dbscan.cpp:118).
-template <int D>
+template <int D, int kFast>
 struct DbCoreQuery {
   const float4* __restrict__ nodes;
   const float4* __restrict__ qpt;
@@ -361,14 +361,15 @@ struct DbCoreQuery {
       count += static_cast<int>(pts);
       return true;
     };
-    return bvh_step_ordered<D>(nodes, p, bt, 0, node, nlo, *stack, visit, inside);
+    return bvh_step_ordered<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, 0, node, nlo, *stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[id] = 1;
   }
 };
 
-template <int D>
+template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
@@ -377,7 +378,7 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
           MemberTree smt, const int32_t* __restrict__ qoff, int32_t num_prims,
           const int32_t* __restrict__ list, int64_t m) {
   LocalStack stack;
-  DbCoreQuery<D> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
+  DbCoreQuery<D, kFast> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
                    &smt, qoff, n, num_prims, list};
   run_query_warpstart<D>(m, q, nodes, bt);
   unsigned long long v = warp_sum(q.dists);
@@ -395,7 +396,7 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
 // primitives (unite with rep[first], run recorded for the cover pass), a
 // border query counts coreless runs and every run once claimed; other runs
 // are walked. minpts == 2: every run is taken (all pairs are unions).
-template <int D, bool kForceCore>
+template <int D, bool kForceCore, int kFast>
 __global__ void __launch_bounds__(kQueryBlock)
 k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
                  const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
@@ -477,7 +478,8 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
       return kTaken;
     };
     LocalStack stack;
-    while (bvh_step_ranged<D>(nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
+    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
     }
   }
   unsigned long long v = warp_sum(dists);
@@ -802,7 +804,8 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
     exclusive_scan_i32(ind, pos, num_prims, nullptr, scan_tmp, st);
     note_launch(), k_single_slots<<<grid_for(num_prims, 256), 256, 0, st>>>(ind, pos, qoff,
                                                                             num_prims, list);
-    note_launch(), k_db_core<D><<<grid_for(sparse_points, kQueryBlock, INT32_MAX), kQueryBlock, 0, st>>>(
+    auto core = bt.fast ? k_db_core<D, 1> : k_db_core<D, 0>;
+    note_launch(), core<<<grid_for(sparse_points, kQueryBlock, INT32_MAX), kQueryBlock, 0, st>>>(
         b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr, mt, smt,
         qoff, num_prims, list, sparse_points);
   }
@@ -823,14 +826,11 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
     exclusive_scan_i32(ind, noncore_before, num_prims + 1, nullptr, scan_tmp, st);
   }
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
-  if (minpts == 2)
-    note_launch(), k_db_main_ranged<D, true><<<g, kQueryBlock, 0, st>>>(
-        b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
-        noncore_before, reach, ctr, mt);
-  else
-    note_launch(), k_db_main_ranged<D, false><<<g, kQueryBlock, 0, st>>>(
-        b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin, cell_end, bt, flags, parent, rep,
-        noncore_before, reach, ctr, mt);
+  auto main = minpts == 2 ? (bt.fast ? k_db_main_ranged<D, true, 1> : k_db_main_ranged<D, true, 0>)
+                          : (bt.fast ? k_db_main_ranged<D, false, 1> : k_db_main_ranged<D, false, 0>);
+  note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin,
+                                                cell_end, bt, flags, parent, rep, noncore_before,
+                                                reach, ctr, mt);
   launch_cover_joins(reach, num_prims, tile_max, RepJoin{parent, rep}, st);
   TCB_CUDA(cudaGetLastError());
   clock.mark(kStFinal);
