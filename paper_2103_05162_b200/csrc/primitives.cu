@@ -18,6 +18,9 @@ constexpr int kSortWarps = kSortThreads / kWarp;
 #ifndef TCB_SORT_IPT
 #define TCB_SORT_IPT 16
 #endif
+#ifndef TCB_SORT_MINB  // 3 resident tiles per SM (ptxas caps registers at 85;
+#define TCB_SORT_MINB 3   // measured on C2: 2.84 ms vs 3.14 ms uncapped at 2/SM)
+#endif
 #ifndef TCB_SORT_LOOKBACK
 #define TCB_SORT_LOOKBACK 4
 #endif
@@ -127,7 +130,7 @@ __device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, TCB_SORT_MINB)
 k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
                 uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, int64_t n,
                 int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
