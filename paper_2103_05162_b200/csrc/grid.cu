@@ -296,6 +296,8 @@ struct DbCoreQuery {
   float p[3];
   int32_t id, node, nlo, mask_rank = 0;
   int count;
+  // the stopping scan of a long cut DenseBox, left to the warp (k_db_core)
+  int32_t pend_kb = -1, pend_ke = 0, pend_rem = 0;
   __device__ bool begin(int64_t q) {
     const float4 qp = qpt[list ? list[q] : q];
     id = __float_as_int(qp.w);
@@ -306,6 +308,7 @@ struct DbCoreQuery {
     count = 0;
     node = 0;
     nlo = 0;
+    pend_kb = -1;
     stack->reset();
     return true;
   }
@@ -326,15 +329,21 @@ struct DbCoreQuery {
         } else {
           // the member-by-member scan (dbscan.cpp:124-131): when the box holds
           // fewer hits than still needed the scan runs to the end (count them
-          // in the spatial tree); otherwise find the stopping member in
-          // member order (the index tree) — at most once per query
+          // in the spatial tree); otherwise the scan stops at the rem-th hit
+          // in member order and the query is core — at most once per query,
+          // found by the whole warp after the traversals (k_db_core)
           const int rem = minpts - count;
-          const int total = ke - kb <= kMemberLinear ? rem  // short: scan it directly
-                                                     : member_count<D>(*smt, kb, ke, p, bt, rem);
+          const bool is_short = ke - kb <= kMemberLinear;
+          const int total = is_short ? rem : member_count<D>(*smt, kb, ke, p, bt, rem);
           if (total < rem) {
             dists += static_cast<unsigned long long>(ke - kb);
             count += total;
-          } else {  // (a short box comes here directly and may still fall short)
+          } else if (!is_short) {
+            pend_kb = kb;
+            pend_ke = ke;
+            pend_rem = rem;
+            count = minpts;
+          } else {  // a short box, scanned here (it may still fall short)
             int hits;
             const int64_t pos = member_scan<D>(*mt, kb, ke, p, bt, rem, hits);
             dists += pos >= 0 ? static_cast<unsigned long long>(pos - kb + 1)
@@ -381,6 +390,41 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
   DbCoreQuery<D, kFast> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
                    &smt, qoff, n, num_prims, list};
   run_query_warpstart<D>(m, q, nodes, bt);
+  // The stopping scans: position of the rem-th member within eps of p in
+  // member order, 32 members per step across the warp (same predicate as the
+  // per-member loop; the members of a cell are in random spatial order, so a
+  // box tree over them prunes nothing and one lane would test them one by one).
+  const int lane = threadIdx.x & 31;
+  const bool valid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x < m;
+  unsigned pend = __ballot_sync(0xffffffffu, valid && q.pend_kb >= 0);
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const float pp[3] = {__shfl_sync(0xffffffffu, q.p[0], src),
+                         __shfl_sync(0xffffffffu, q.p[1], src),
+                         D == 3 ? __shfl_sync(0xffffffffu, q.p[2], src) : 0.f};
+    const int32_t kb = __shfl_sync(0xffffffffu, q.pend_kb, src);
+    const int32_t ke = __shfl_sync(0xffffffffu, q.pend_ke, src);
+    int need = __shfl_sync(0xffffffffu, q.pend_rem, src);
+    int64_t pos = -1;
+    for (int32_t base = kb; base < ke; base += 32) {
+      bool hit = false;
+      if (base + lane < ke) {
+        const float4 m4 = __ldg(mt.pts + base + lane);
+        const float mp[3] = {m4.x, m4.y, m4.z};
+        hit = ball_hits<D, kFast>(pp, mp, mp, bt);
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, hit);
+      const int c = __popc(b);
+      if (c >= need) {
+        pos = base + static_cast<int>(__fns(b, 0, need));
+        break;
+      }
+      need -= c;
+    }
+    // pos >= 0: the spatial count found >= rem hits in the same cell
+    if (lane == src) q.dists += static_cast<unsigned long long>(pos >= 0 ? pos - kb + 1 : ke - kb);
+  }
   unsigned long long v = warp_sum(q.dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
 }
