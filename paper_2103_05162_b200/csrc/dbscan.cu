@@ -165,7 +165,7 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
       if (core_r) {
         if (noncore != 0) return kWalk;
         uf_unite_hinted_keyed(parent, key, rank, first, hint);
-        if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
+        record_run(reach, first, last);
       } else if (!settled && noncore != size) {
         if (noncore != 0) return kWalk;
         if (ld_relaxed(parent + rank) == rank) uf_claim(parent, rank, uf_find(parent, first));
@@ -229,7 +229,7 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
       pairs += static_cast<unsigned long long>(last - first + 1);
       TCB_PROBE_ONLY(++pr[1]; pr[4] += last - first + 1;)
       uf_unite_hinted_keyed(parent, key, rank, first, hint, mark);
-      if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
+      record_run(reach, first, last);
       return kTaken;
     };
     LocalStack stack;

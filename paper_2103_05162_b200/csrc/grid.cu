@@ -515,7 +515,7 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
       }
       if (run) {
         uf_unite_hinted(parent, i, __ldg(rep + first), hint);
-        if (last > first && ld_cached(reach + first) < last) atomicMax(reach + first, last);
+        record_run(reach, first, last);
       }
       pairs += static_cast<unsigned long long>(cnt);
       dists += static_cast<unsigned long long>(cnt);
