@@ -414,8 +414,17 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   uint64_t* keys_alt = scratch.alloc_n<uint64_t>(m);
   int32_t* vals_alt = scratch.alloc_n<int32_t>(m);
   void* sort_tmp = scratch.alloc(radix_sort_scratch_bytes(m));
-  bool in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, m, key_and, key_or,
-                                 sort_tmp, st, &out.sort_passes);
+  // Morton codes are nearly unique at their top 40 bits (C2: groups of <= 6
+  // points), so the LSD passes skip the low 24 bits and one fix-up pass
+  // orders the small groups; a long group (many coincident points) falls
+  // back to the full sort of freshly computed codes. Same order either way.
+  bool in_alt = false;
+  if (!radix_sort_pairs_prefix(keys, vals, keys_alt, vals_alt, m, key_and, key_or, sort_tmp, st,
+                               &in_alt, &out.sort_passes)) {
+    note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
+    in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, m, key_and, key_or, sort_tmp, st,
+                              &out.sort_passes);
+  }
   const uint64_t* codes = in_alt ? keys_alt : keys;
   int32_t* order = in_alt ? vals_alt : vals;
   out.tree.leaf_order = order;

@@ -316,7 +316,7 @@ size_t radix_sort_scratch_bytes(int64_t n) {
   const int64_t t = num_sort_tiles(std::max<int64_t>(n, 1));
   // status words (tiles x radix) + per-pass tile counters + global histograms
   return static_cast<size_t>(t) * kRadix * sizeof(uint32_t) + 64 * sizeof(uint32_t) +
-         kMaxPasses * kRadix * sizeof(uint32_t) + 256;
+         kMaxPasses * kRadix * sizeof(uint32_t) + 256 + 64;  // + the prefix sort's flag
 }
 
 bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
@@ -354,6 +354,71 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
   }
   if (passes_run) *passes_run = n > 1 ? ps.count : 0;
   return in_alt;
+}
+
+namespace {
+
+// Fix-up of radix_sort_pairs_prefix: element k finds its group [b, e) of equal
+// key >> cut (at most kFixMax long), counts the group members ordered before
+// it by (key, val) and writes itself there. Singletons (nearly every element
+// of a Morton order cut at 24 bits) just copy through.
+__global__ void __launch_bounds__(256)
+k_sort_fixup(const uint64_t* __restrict__ kin, const int32_t* __restrict__ vin,
+             uint64_t* __restrict__ kout, int32_t* __restrict__ vout, int64_t n, int cut,
+             uint32_t* __restrict__ too_long) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = kin[k];
+    const int32_t v = vin[k];
+    const uint64_t top = key >> cut;
+    int64_t b = k, e = k + 1;
+    while (b > 0 && k - b < kFixMax && (kin[b - 1] >> cut) == top) --b;
+    while (e < n && e - k < kFixMax && (kin[e] >> cut) == top) ++e;
+    if (e - b > kFixMax) {
+      *too_long = 1;
+      continue;
+    }
+    int64_t r = b;
+    for (int64_t j = b; j < e; ++j) {
+      const uint64_t kj = kin[j];
+      r += kj < key || (kj == key && vin[j] < v);
+    }
+    kout[r] = key;
+    vout[r] = v;
+  }
+}
+
+}  // namespace
+
+bool radix_sort_pairs_prefix(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
+                             int32_t* vals_alt, int64_t n, uint64_t and_all, uint64_t or_all,
+                             void* scratch, cudaStream_t stream, bool* in_alt,
+                             int* passes_run) {
+  constexpr uint64_t low = (uint64_t{1} << kFixBits) - 1;
+  // the low windows look constant to the LSD passes
+  const uint64_t or_top = (or_all & ~low) | (and_all & low);
+  int passes = 0;
+  bool alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, n, and_all, or_top, scratch, stream,
+                              &passes);
+  if (((and_all ^ or_all) & low) != 0 && n > 1) {
+    // the fix-up flag lives past the sort's own scratch
+    uint32_t* flag = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) +
+                                                 radix_sort_scratch_bytes(n) - 64);
+    TCB_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), stream));
+    note_launch(), k_sort_fixup<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(
+        alt ? keys_alt : keys, alt ? vals_alt : vals, alt ? keys : keys_alt, alt ? vals : vals_alt,
+        n, kFixBits, flag);
+    TCB_CUDA(cudaGetLastError());
+    alt = !alt;
+    ++passes;
+    auto* h = static_cast<uint32_t*>(pinned_staging(64));
+    TCB_CUDA(cudaMemcpyAsync(h, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+    TCB_CUDA(cudaStreamSynchronize(stream));
+    if (*h) return false;
+  }
+  *in_alt = alt;
+  if (passes_run) *passes_run = passes;
+  return true;
 }
 
 size_t scan_scratch_bytes(int64_t n) {

@@ -23,6 +23,22 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
                       uint64_t or_all, void* scratch, cudaStream_t stream,
                       int* passes_run = nullptr);
 
+// radix_sort_pairs for keys whose low bits rarely matter (Morton codes):
+// the LSD passes sort only the bits at and above kFixBits, and one fix-up
+// pass orders each group of equal (key >> kFixBits) by (key, val), each
+// element placing itself by its rank inside the group. Groups longer than
+// kFixMax make it return false (the result is then garbage and the caller
+// sorts the original keys with radix_sort_pairs); this synchronizes the
+// stream once to read that verdict. vals must be 0..n-1 in order on input.
+// On success the sorted pairs are in (keys, vals) when *in_alt is false,
+// else in the *_alt buffers.
+constexpr int kFixBits = 24;
+constexpr int kFixMax = 256;
+bool radix_sort_pairs_prefix(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
+                             int32_t* vals_alt, int64_t n, uint64_t and_all, uint64_t or_all,
+                             void* scratch, cudaStream_t stream, bool* in_alt,
+                             int* passes_run = nullptr);
+
 // Exclusive scan of n int32 counts into out (may alias in); writes the total
 // to *d_total (device pointer) when non-null.
 size_t scan_scratch_bytes(int64_t n);

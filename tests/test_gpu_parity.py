@@ -86,6 +86,31 @@ def test_device_bvh_is_the_reference_tree():
             assert np.array_equal(t[k], w[k]), (d, k)
 
 
+@pytest.mark.parametrize("d", [2, 3])
+def test_morton_prefix_sort_fixup_and_fallback(d):
+    """The build sorts Morton codes on their top bits and fixes equal-prefix
+    groups afterwards (radix_sort_pairs_prefix); groups longer than kFixMax
+    fall back to the full sort. Both must give the reference's tree."""
+    rng = np.random.default_rng(17 + d)
+    wide = rng.uniform(-5, 5, (40000, d))
+    cases = {
+        # many small groups at the cut (tight pairs / triples)
+        "pairs": np.concatenate([wide, wide[:5000] + rng.normal(0, 1e-6, (5000, d))]),
+        # one group of 600 coincident points: fallback
+        "dups600": np.concatenate([wide, np.repeat(wide[:1], 600, axis=0)]),
+        # 3000 distinct points inside one top-bits cell: fallback
+        "clump": np.concatenate([wide, rng.normal(1.0, 1e-7, (3000, d))]),
+        # groups just under the cap
+        "dups200": np.concatenate([wide, np.repeat(wide[:20], 200, axis=0)]),
+    }
+    for name, pts in cases.items():
+        pts = pts.astype(np.float32)
+        t = tb.api.debug_point_bvh(pts)
+        w = oracle.point_bvh(pts)
+        for k in ("leaf_ids", "left", "right", "max_rank", "boxes"):
+            assert np.array_equal(t[k], w[k]), (name, d, k)
+
+
 def test_radix_sort_is_stable_and_exact():
     rng = np.random.default_rng(7)
     cases = [

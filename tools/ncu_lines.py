@@ -1,7 +1,7 @@
 """Per-source-line totals (instructions executed, warp stall samples) of one
 kernel from `ncu -i REP --page source --csv --print-source cuda,sass`.
 
-  python tools/ncu_lines.py gpurun_out/x.ncu-rep [top]
+  python tools/ncu_lines.py gpurun_out/x.ncu-rep [top] [kernel-regex]
 """
 import csv
 import io
@@ -10,8 +10,10 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if len(sys.argv) > 3:
+    cmd += ["--kernel-name", "regex:" + sys.argv[3]]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 agg = {}
 path = None
