@@ -407,20 +407,28 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
     const int32_t ke = __shfl_sync(0xffffffffu, q.pend_ke, src);
     int need = __shfl_sync(0xffffffffu, q.pend_rem, src);
     int64_t pos = -1;
-    for (int32_t base = kb; base < ke; base += 32) {
-      bool hit = false;
-      if (base + lane < ke) {
-        const float4 m4 = __ldg(mt.pts + base + lane);
-        const float mp[3] = {m4.x, m4.y, m4.z};
-        hit = ball_hits<D, kFast>(pp, mp, mp, bt);
+    constexpr int kChunks = 4;  // 128 members in flight per round trip
+    for (int32_t base = kb; base < ke && pos < 0; base += 32 * kChunks) {
+      float4 m4[kChunks];
+#pragma unroll
+      for (int u = 0; u < kChunks; ++u) {
+        const int32_t k = base + 32 * u + lane;
+        m4[u] = k < ke ? __ldg(mt.pts + k) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      const unsigned b = __ballot_sync(0xffffffffu, hit);
-      const int c = __popc(b);
-      if (c >= need) {
-        pos = base + static_cast<int>(__fns(b, 0, need));
-        break;
+#pragma unroll
+      for (int u = 0; u < kChunks; ++u) {
+        const int32_t k = base + 32 * u + lane;
+        const float mp[3] = {m4[u].x, m4[u].y, m4[u].z};
+        const bool hit = k < ke && ball_hits<D, kFast>(pp, mp, mp, bt);
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        const int c = __popc(b);
+        if (pos < 0) {
+          if (c >= need)
+            pos = base + 32 * u + static_cast<int>(__fns(b, 0, need));
+          else
+            need -= c;
+        }
       }
-      need -= c;
     }
     // pos >= 0: the spatial count found >= rem hits in the same cell
     if (lane == src) q.dists += static_cast<unsigned long long>(pos >= 0 ? pos - kb + 1 : ke - kb);
