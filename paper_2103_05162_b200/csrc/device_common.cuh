@@ -177,7 +177,7 @@ __device__ __forceinline__ int32_t uf_unite(int32_t* parent, int32_t i, int32_t 
 // where a query meets hundreds of neighbours that joined its set long ago.
 __device__ __forceinline__ void uf_unite_hinted(int32_t* parent, int32_t i, int32_t j,
                                                 int32_t& hint) {
-  const int32_t pj = ld_relaxed(parent + j);
+  const int32_t pj = ld_cached(parent + j);  // any past parent of j is proof enough
   if (pj == hint || j == hint) return;
   hint = uf_unite(parent, i, j);
 }
