@@ -26,6 +26,11 @@ lat = np.concatenate([lat, np.repeat(lat[:50], 40, axis=0)])
 for mp in (2, 20, 200):
     r = tb.cluster(tb.Dataset.from_array(lat), 0.1, mp, tb.Algorithm.DENSEBOX)
     print("dense", mp, r.stats["cluster_count"], r.stats["distance_evaluations"])
+# Morton prefix sort: small equal-prefix groups (fix-up) and a > 256 group (fallback)
+wide = rng.uniform(-5, 5, (3000, 3))
+for pts in (np.concatenate([wide, wide[:500] + 1e-6]), np.concatenate([wide, np.repeat(wide[:1], 400, axis=0)])):
+    r = tb.cluster(tb.Dataset.from_array(pts.astype(np.float32)), 0.3, 3, tb.Algorithm.FDBSCAN)
+    print("prefix", r.stats["cluster_count"], r.stats["pair_resolutions"])
 # keyed run, local context, binary load to the device
 import torch
 from paper_2103_05162_b200.shard import DeviceEngine
