@@ -183,7 +183,7 @@ template <int D, class Src>
 __global__ void __launch_bounds__(kClimbBlock)
 k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
         const int32_t* __restrict__ prim_aux, int64_t m, float4* nodes,
-        int32_t* __restrict__ other, float4* __restrict__ leaf_pt, int32_t* __restrict__ rank_of,
+        int32_t* __restrict__ other, float4* __restrict__ leaf_pt,
         ClimbState* state) {
   using T = NodeTraits<D>;
   const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -194,7 +194,6 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
     const int32_t prim = order[s];
     src.box(prim, lo, hi);
     if (leaf_pt) leaf_pt[s] = make_float4(lo[0], lo[1], D == 3 ? lo[2] : 0.f, __int_as_float(prim));
-    if (rank_of) rank_of[prim] = static_cast<int32_t>(s);
     l = r = static_cast<int32_t>(s);
     link = ~l;
     aux = prim_aux ? prim_aux[prim] : prim;
@@ -436,10 +435,6 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   TCB_CUDA(cudaMemcpyAsync(scene, &d_ctr->bounds_ord[0], 6 * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, st));
   out.scene_ord = scene;
-  if (src.want_rank_of) {
-    out.rank_of = scratch.alloc_n<int32_t>(m);
-    if (m == 1) TCB_CUDA(cudaMemsetAsync(out.rank_of, 0, sizeof(int32_t), st));
-  }
   if (m == 1) {
     note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
   } else {
@@ -447,7 +442,7 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     auto* state = scratch.alloc_n<ClimbState>(1);
     TCB_CUDA(cudaMemsetAsync(other, 0xff, sizeof(int32_t) * (m - 1), st));
     note_launch(), k_climb<D><<<grid_for(m, kClimbBlock, INT32_MAX), kClimbBlock, 0, st>>>(
-        boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, out.rank_of, state);
+        boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, state);
     note_launch(), k_root_to_zero<D><<<1, NodeTraits<D>::kVec, 0, st>>>(out.tree.nodes, m, state);
   }
   TCB_CUDA(cudaGetLastError());

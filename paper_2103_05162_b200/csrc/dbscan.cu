@@ -20,6 +20,7 @@
 // degenerate and box_distance_sq reduces to distance_sq term by term, the
 // subtraction merely negated), so a visited leaf is a within-eps neighbour
 // and its distance is not recomputed.
+#include <algorithm>
 #include <cmath>
 
 #include "device_common.cuh"
@@ -288,29 +289,67 @@ k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_
   }
 }
 
-// Rank-space finalize (FDBSCAN): flatten over ranks; outputs scattered back
-// to input order through key[rank] = original index. The representative of a
-// set is its minimum-key rank, so label = key[root] = minimum original index.
-__global__ void __launch_bounds__(256)
-k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
-                 const int32_t* __restrict__ key, const int32_t* __restrict__ order, int64_t n,
-                 int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr,
-                 bool derive_core) {
+// Rank-space finalize (FDBSCAN): flatten over ranks (union_find.hpp:77-86,
+// dbscan.cpp:202-219); the representative of a set is its minimum-key rank,
+// so label = key[root] = minimum original index. The outputs go to input
+// order through a
+// permutation, and 4-byte / 1-byte stores to random positions are partial
+// sector writes that DRAM pays for one by one. Pass 1 (rank order) finalizes
+// each rank and files an entry (destination | core <<
+// 31, label) into the bucket of its destination: buckets are 2^shift
+// consecutive output positions, and since the destinations are a
+// permutation bucket b holds exactly its window's size, so it owns entries
+// [b << shift, ...) with a per-bucket cursor and no histogram pass. A block's
+// entries for one bucket are consecutive (a per-block shared count, one
+// global atomic per bucket). Pass 2 walks the entries in bucket order: its
+// label / core stores stay inside a few small windows at a time, so L2 merges
+// them into whole sectors.
+constexpr int kFinThreads = 1024;
+constexpr int kFinItems = 8;
+constexpr int kFinMaxBuckets = 2048;
+
+__global__ void __launch_bounds__(kFinThreads)
+k_fin_bucket(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
+             const int32_t* __restrict__ key, const int32_t* __restrict__ order, int64_t n,
+             int shift, int nb, uint32_t* __restrict__ cursor, uint2* __restrict__ entries,
+             DevCounters* ctr, bool derive_core) {
+  __shared__ uint32_t s_cnt[kFinMaxBuckets];
+  for (int b = threadIdx.x; b < nb; b += kFinThreads) s_cnt[b] = 0;
+  __syncthreads();
   long long noise = 0, clusters = 0, cores = 0;
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int32_t p = ld_relaxed(parent + s);
-    int32_t q;
-    while (p != (q = ld_relaxed(parent + p))) p = q;
-    st_relaxed(parent + s, p);
-    const bool core = flags[s] != 0 || (derive_core && p != s);
-    const int32_t i = order[s];
-    const int32_t lab = (core || p != s) ? key[p] : -1;  // dbscan.cpp:215
-    labels[i] = lab;
-    core_out[i] = core ? 1 : 0;
-    noise += lab == -1;
-    clusters += lab != -1 && p == s;  // label[i] == i (keys are unique)
-    cores += core;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (kFinThreads * kFinItems);
+  uint2 e[kFinItems];
+  uint32_t loc[kFinItems];
+#pragma unroll
+  for (int j = 0; j < kFinItems; ++j) {
+    const int64_t s = base + j * kFinThreads + threadIdx.x;
+    e[j].x = 0xffffffffu;
+    if (s < n) {
+      int32_t p = ld_relaxed(parent + s);
+      int32_t q;
+      while (p != (q = ld_relaxed(parent + p))) p = q;
+      st_relaxed(parent + s, p);
+      const bool core = flags[s] != 0 || (derive_core && p != s);
+      const int32_t lab = (core || p != s) ? __ldg(key + p) : -1;  // dbscan.cpp:215
+      noise += lab == -1;
+      clusters += lab != -1 && p == s;
+      cores += core;
+      // destination < 2^31 - 1 (n <= INT32_MAX), so its bit 31 carries the
+      // core flag and 0xffffffff marks an empty slot
+      const uint32_t i = static_cast<uint32_t>(__ldg(order + s));
+      e[j] = make_uint2(i | (core ? 0x80000000u : 0u), static_cast<uint32_t>(lab));
+      loc[j] = atomicAdd(&s_cnt[i >> shift], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += kFinThreads)
+    if (s_cnt[b]) s_cnt[b] = atomicAdd(cursor + b, s_cnt[b]);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kFinItems; ++j) {
+    if (e[j].x == 0xffffffffu) continue;
+    const uint32_t b = (e[j].x & 0x7fffffffu) >> shift;
+    entries[(static_cast<int64_t>(b) << shift) + s_cnt[b] + loc[j]] = e[j];
   }
   noise = warp_sum(noise);
   clusters = warp_sum(clusters);
@@ -322,35 +361,53 @@ k_finalize_ranks(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags
   }
 }
 
-__global__ void __launch_bounds__(256)
-k_finalize_gather(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
-                  const int32_t* __restrict__ key, const int32_t* __restrict__ rank_of,
-                  int64_t i0, int64_t i1, int32_t* __restrict__ labels,
-                  uint8_t* __restrict__ core_out, DevCounters* ctr, bool derive_core) {
-  long long noise = 0, clusters = 0, cores = 0;
-  for (int64_t i = i0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < i1;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t s = __ldg(rank_of + i);
-    int32_t p = ld_relaxed(parent + s);
-    int32_t q;
-    while (p != (q = ld_relaxed(parent + p))) p = q;
-    const bool core = flags[s] != 0 || (derive_core && p != s);
-    const int32_t lab = (core || p != s) ? __ldg(key + p) : -1;  // dbscan.cpp:215
-    labels[i] = lab;
-    core_out[i] = core ? 1 : 0;
-    noise += lab == -1;
-    clusters += lab != -1 && p == s;
-    cores += core;
+// Pass 2 for windows of at most kFinWindow outputs: block b gathers bucket b's
+// entries into shared memory and writes its window out coalesced.
+constexpr int kFinWindow = 32768;
+
+__global__ void __launch_bounds__(kFinThreads)
+k_fin_window(const uint2* __restrict__ entries, int64_t n, int shift, int b0,
+             int32_t* __restrict__ labels, uint8_t* __restrict__ core_out) {
+  extern __shared__ __align__(16) unsigned char fin_smem[];
+  int32_t* s_lab = reinterpret_cast<int32_t*>(fin_smem);
+  uint8_t* s_core = fin_smem + sizeof(int32_t) * kFinWindow;
+  const int64_t base = static_cast<int64_t>(b0 + blockIdx.x) << shift;
+  const int64_t rest = n - base;
+  const int cnt = static_cast<int>(rest < (int64_t{1} << shift) ? rest : (int64_t{1} << shift));
+  for (int k = threadIdx.x; k < cnt; k += kFinThreads) {
+    const uint2 v = __ldcs(entries + base + k);
+    const int w = static_cast<int>((v.x & 0x7fffffffu) - base);
+    s_lab[w] = static_cast<int32_t>(v.y);
+    s_core[w] = static_cast<uint8_t>(v.x >> 31);
   }
-  noise = warp_sum(noise);
-  clusters = warp_sum(clusters);
-  cores = warp_sum(cores);
-  if ((threadIdx.x & 31) == 0) {
-    if (noise) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->noise), noise);
-    if (clusters) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->clusters), clusters);
-    if (cores) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->cores), cores);
+  __syncthreads();
+  if (cnt == (1 << shift)) {  // full window: 16-byte stores (base is 16-aligned)
+    int4* dl = reinterpret_cast<int4*>(labels + base);
+    const int4* sl = reinterpret_cast<const int4*>(s_lab);
+    for (int k = threadIdx.x; k < cnt / 4; k += kFinThreads) __stcs(dl + k, sl[k]);
+    int4* dc = reinterpret_cast<int4*>(core_out + base);
+    const int4* sc = reinterpret_cast<const int4*>(s_core);
+    for (int k = threadIdx.x; k < cnt / 16; k += kFinThreads) __stcs(dc + k, sc[k]);
+  } else {
+    for (int k = threadIdx.x; k < cnt; k += kFinThreads) {
+      labels[base + k] = s_lab[k];
+      core_out[base + k] = s_core[k];
+    }
   }
 }
+
+__global__ void __launch_bounds__(256)
+k_fin_scatter(const uint2* __restrict__ entries, int64_t e0, int64_t e1,
+              int32_t* __restrict__ labels, uint8_t* __restrict__ core_out) {
+  for (int64_t k = e0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < e1;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint2 v = __ldcs(entries + k);
+    const uint32_t i = v.x & 0x7fffffffu;
+    labels[i] = static_cast<int32_t>(v.y);
+    core_out[i] = static_cast<uint8_t>(v.x >> 31);
+  }
+}
+
 
 __global__ void __launch_bounds__(256)
 k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int64_t n,
@@ -439,32 +496,46 @@ void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s)
   TCB_CUDA(cudaGetLastError());
 }
 
-void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
-                           const int32_t* order, int64_t n,
-                           int32_t* labels, uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
-                           bool force_core) {
-  // force_core (minpts == 2): a rank is core iff its set has >= 2 elements —
-  // a non-root, or a root marked by a hook (uf_unite_keyed's mark)
-  note_launch(), k_finalize_ranks<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, key, order, n,
-                                                                   labels, core_out, d_ctr,
-                                                                   force_core);
+
+void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* key,
+                              const int32_t* order, int64_t n, int32_t* labels,
+                              uint8_t* core_out, DevCounters* d_ctr, Scratch& scratch,
+                              bool force_core, const ChunkSink* sink) {
+  cudaStream_t s = scratch.stream();
+  int shift = 12;
+  while (((n + (int64_t{1} << shift) - 1) >> shift) > kFinMaxBuckets) ++shift;
+  const int nb = static_cast<int>((n + (int64_t{1} << shift) - 1) >> shift);
+  uint32_t* cursor = scratch.alloc_n<uint32_t>(nb);
+  uint2* entries = scratch.alloc_n<uint2>(n);
+  TCB_CUDA(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * nb, s));
+  const int64_t tile = int64_t{kFinThreads} * kFinItems;
+  note_launch(), k_fin_bucket<<<static_cast<unsigned>((n + tile - 1) / tile), kFinThreads, 0, s>>>(
+      parent, flags, key, order, n, shift, nb, cursor, entries, d_ctr, force_core);
   TCB_CUDA(cudaGetLastError());
+  // pass 2, in chunks of whole buckets when a sink copies finished output
+  // ranges to the host while the next chunk is written
+  const int chunks = sink && n >= (int64_t{1} << 22) ? 8 : 1;
+  const int per = (nb + chunks - 1) / chunks;
+  for (int b0 = 0; b0 < nb; b0 += per) {
+    const int64_t e0 = static_cast<int64_t>(b0) << shift;
+    const int64_t e1 = std::min<int64_t>(static_cast<int64_t>(b0 + per) << shift, n);
+    if ((1 << shift) <= kFinWindow) {
+      constexpr size_t smem = (sizeof(int32_t) + 1) * kFinWindow;
+      TCB_CUDA(cudaFuncSetAttribute(k_fin_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      const int blocks = std::min(per, nb - b0);
+      note_launch(), k_fin_window<<<blocks, kFinThreads, smem, s>>>(entries, n, shift, b0, labels,
+                                                                   core_out);
+    } else {  // wide windows: stores straight to global (L2 still merges a window)
+      note_launch(), k_fin_scatter<<<grid_for(e1 - e0, 256), 256, 0, s>>>(entries, e0, e1, labels,
+                                                                         core_out);
+    }
+    TCB_CUDA(cudaGetLastError());
+    if (sink) (*sink)(e0, e1, s);
+  }
 }
 
-void finalize_labels_gather(int32_t* parent, const uint8_t* flags, const int32_t* key,
-                            const int32_t* rank_of, int64_t i0, int64_t i1, int32_t* labels,
-                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
-                            bool force_core) {
-  if (i1 <= i0) return;
-  note_launch(), k_finalize_gather<<<grid_for(i1 - i0, 256), 256, 0, s>>>(
-      parent, flags, key, rank_of, i0, i1, labels, core_out, d_ctr, force_core);
-  TCB_CUDA(cudaGetLastError());
-}
 
-void flatten_mark(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
-  note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
-  TCB_CUDA(cudaGetLastError());
-}
 
 void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n, int32_t* labels,
                      uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s, bool force_core) {

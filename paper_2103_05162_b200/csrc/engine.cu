@@ -133,7 +133,6 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   PrimSource src;
   src.coords = d_coords;
   src.count = n;
-  src.want_rank_of = sink != nullptr;
   clock.mark(kStBounds);
   BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock);
 
@@ -151,21 +150,11 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   clock.mark(kStMain);
   fdbscan_main_pass<D>(b, key, n, eps2, minpts == 2, flags, parent, ctr, scratch);
   clock.mark(kStFinal);
-  if (sink) {
-    // gather form, in chunks of output positions: each finished chunk goes
-    // to the sink (tc_cluster copies it to the host while the next runs)
-    const int64_t chunks = n < (int64_t{1} << 22) ? 1 : 8;
-    const int64_t per = (n + chunks - 1) / chunks;
-    for (int64_t i0 = 0; i0 < n; i0 += per) {
-      const int64_t i1 = i0 + per < n ? i0 + per : n;
-      finalize_labels_gather(parent, flags, key, b.rank_of, i0, i1, d_labels, d_core, ctr, st,
-                             minpts == 2);
-      (*sink)(i0, i1, st);
-    }
-  } else {
-    finalize_labels_ranks(parent, flags, key, b.tree.leaf_order, n, d_labels, d_core, ctr, st,
-                          minpts == 2);
-  }
+  // whole-sector output writes through destination buckets; with a sink
+  // (tc_cluster) the output is finished in 8 ranges, each copied to the host
+  // while the next is written
+  finalize_labels_bucketed(parent, flags, key, b.tree.leaf_order, n, d_labels, d_core, ctr,
+                           scratch, minpts == 2, sink);
   clock.finish();
 }
 

@@ -86,13 +86,11 @@ struct PrimSource {
   const float4* hi = nullptr;
   const int32_t* aux = nullptr;   // leaf payload per primitive (nullptr: primitive index)
   int64_t count = 0;
-  bool want_rank_of = false;      // also produce primitive -> leaf rank
 };
 
 struct BuiltBvh {
   DeviceBvh tree;
   float4* leaf_pt = nullptr;          // points mode only: rank -> (x, y, z, id bits)
-  int32_t* rank_of = nullptr;         // primitive -> leaf rank (PrimSource::want_rank_of)
   const uint64_t* codes = nullptr;    // sorted Morton codes (leaf rank order)
   const uint32_t* scene_ord = nullptr;  // Morton scene box (order-preserving bits, 6)
   int sort_passes = 0;
@@ -129,22 +127,15 @@ void gather_rank_keys(const int32_t* keys, const int32_t* order, int64_t n, int3
 void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t* dst,
                    bool to_rank, cudaStream_t s);
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
-// FDBSCAN: parent / flags indexed by leaf rank, key[rank] = original index.
-// Gather form of finalize_labels_ranks for output positions [i0, i1):
-// labels[i] = key of the root of rank_of[i] (or -1). Lets the caller copy
-// finished chunks to the host while later chunks are computed.
-void finalize_labels_gather(int32_t* parent, const uint8_t* flags, const int32_t* key,
-                            const int32_t* rank_of, int64_t i0, int64_t i1, int32_t* labels,
-                            uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s,
-                            bool force_core);
-// minpts == 2: the union-find flatten + derived core flags of finalize_labels_ranks.
-void flatten_mark(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
-
-// labels[order[rank]] = key of the rank's root (or -1).
-void finalize_labels_ranks(int32_t* parent, uint8_t* flags, const int32_t* key,
-                           const int32_t* order, int64_t n,
-                           int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
-                           cudaStream_t s, bool force_core);
+// FDBSCAN finalize in rank space: labels[order[rank]] = key of the rank's
+// root (or -1), core flags likewise, through destination buckets
+// (k_fin_bucket, then k_fin_window / k_fin_scatter, dbscan.cu): whole-sector
+// output writes. With a sink, the output is written in 8 contiguous ranges,
+// each handed to the sink once final.
+void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* key,
+                              const int32_t* order, int64_t n, int32_t* labels,
+                              uint8_t* core_out, DevCounters* d_ctr, Scratch& scratch,
+                              bool force_core, const ChunkSink* sink = nullptr);
 // force_core (minpts == 2): core flags are derived here from the union-find
 // structure instead of being stored per pair in the main pass.
 void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,

@@ -137,9 +137,8 @@ void given_core(const float* d_coords, int64_t n, float eps, const uint8_t* d_co
   const double eps2 = static_cast<double>(eps) * static_cast<double>(eps);
   fdbscan_main_pass<D>(b, b.tree.leaf_order, n, eps2, /*force_core=*/false, flags, parent, ctr,
                        scratch);
-  finalize_labels_ranks(parent, flags, b.tree.leaf_order, b.tree.leaf_order, n, d_labels,
-                        d_core_out, ctr, st,
-                        /*force_core=*/false);
+  finalize_labels_bucketed(parent, flags, b.tree.leaf_order, b.tree.leaf_order, n, d_labels,
+                           d_core_out, ctr, scratch, /*force_core=*/false);
   if (stats) {
     DevCounters h;
     TCB_CUDA(cudaMemcpyAsync(&h, ctr, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -197,8 +196,8 @@ void local_cluster(LocalCtx& c, const uint8_t* d_core_in, int32_t* d_labels, uin
   init_union_find(parent, flags, c.n, c.st);
   permute_flags(d_core_in, c.b.tree.leaf_order, c.n, flags, /*to_rank=*/true, c.st);
   fdbscan_main_pass<D>(c.b, c.key, c.n, c.eps2, /*force_core=*/false, flags, parent, c.ctr, tmp);
-  finalize_labels_ranks(parent, flags, c.key, c.b.tree.leaf_order, c.n, d_labels, d_core_out,
-                        c.ctr, c.st, /*force_core=*/false);
+  finalize_labels_bucketed(parent, flags, c.key, c.b.tree.leaf_order, c.n, d_labels, d_core_out,
+                           c.ctr, tmp, /*force_core=*/false);
 }
 
 __global__ void k_unite_pairs(const int32_t* __restrict__ edges, int64_t m, int32_t* parent) {
