@@ -122,14 +122,17 @@ struct KeyedJoin {
   }
 };
 
-// primitive ranks mapped to a representative point (DenseBox): rep[rank]
-struct RepJoin {
+// DenseBox: primitive ranks mapped to their first query slot (slot-space
+// union-find keyed by point id, see k_queries in grid.cu)
+struct SlotJoin {
   int32_t* parent;
-  const int32_t* rep;
+  const int32_t* key;
+  const int32_t* qoff;
+  uint8_t* mark = nullptr;
   __device__ __forceinline__ void operator()(int32_t l) const {
-    const int32_t a = __ldg(rep + l), b = __ldg(rep + l - 1);
+    const int32_t a = __ldg(qoff + l), b = __ldg(qoff + l - 1);
     const int32_t pa = ld_relaxed(parent + a), pb = ld_relaxed(parent + b);
-    if (pa != pb && pa != b && pb != a) uf_unite(parent, a, b);
+    if (pa != pb && pa != b && pb != a) uf_unite_keyed(parent, key, a, b, mark);
   }
 };
 

@@ -306,7 +306,7 @@ k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_
 // them into whole sectors.
 constexpr int kFinThreads = 1024;
 constexpr int kFinItems = 8;
-constexpr int kFinMaxBuckets = 2048;
+constexpr int kFinMaxBuckets = 4096;
 
 __global__ void __launch_bounds__(kFinThreads)
 k_fin_bucket(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
@@ -502,7 +502,11 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
                               uint8_t* core_out, DevCounters* d_ctr, Scratch& scratch,
                               bool force_core, const ChunkSink* sink) {
   cudaStream_t s = scratch.stream();
+  // <= 2048 windows (>= 4 entries per block and bucket in pass 1), but up to
+  // 4096 when that keeps the windows within shared memory (pass 2)
   int shift = 12;
+  while (((n + (int64_t{1} << shift) - 1) >> shift) > kFinMaxBuckets / 2) ++shift;
+  if (shift > 15 && ((n + (int64_t{1} << 15) - 1) >> 15) <= kFinMaxBuckets) shift = 15;
   while (((n + (int64_t{1} << shift) - 1) >> shift) > kFinMaxBuckets) ++shift;
   const int nb = static_cast<int>((n + (int64_t{1} << shift) - 1) >> shift);
   uint32_t* cursor = scratch.alloc_n<uint32_t>(nb);

@@ -241,15 +241,18 @@ k_leaf_counts(const int32_t* __restrict__ order, const int32_t* __restrict__ pri
 }
 
 // Query slots in leaf order: qpt = (coords, id | dense<<31), qrank = own leaf
-// rank. Also union_dense_cells: every dense member is core and hooked straight
-// under the cell's first (= minimum-index) member.
+// rank, key = point id. The DenseBox union-find lives in this SLOT space
+// (like FDBSCAN's rank space: a query's neighbours are slot-local), hooked by
+// key so roots are still minimum point ids. Also union_dense_cells: every
+// dense member is core and hooked straight under the slot of the cell's first
+// (= minimum-index) member.
 template <int D>
 __global__ void __launch_bounds__(256)
 k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_of_sorted,
           const int32_t* __restrict__ cell_begin, const uint8_t* __restrict__ cell_dense,
           const int32_t* __restrict__ prim_off, const int32_t* __restrict__ rank_of_prim,
           const int32_t* __restrict__ qoff, int64_t n, float4* __restrict__ qpt,
-          int32_t* __restrict__ qrank, int32_t* __restrict__ parent,
+          int32_t* __restrict__ qrank, int32_t* __restrict__ key, int32_t* __restrict__ parent,
           uint8_t* __restrict__ flags) {
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -262,10 +265,11 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
     const int32_t dst = qoff[s] + (dense ? off : 0);
     float4 pt = sorted_pt[k];
     const int32_t i = __float_as_int(pt.w);
+    key[dst] = i;
     if (dense) {
       pt.w = __int_as_float(i | static_cast<int32_t>(0x80000000u));
-      flags[i] = 1;
-      parent[i] = __float_as_int(sorted_pt[b].w);  // dbscan.cpp:98-104
+      flags[dst] = 1;
+      parent[dst] = qoff[s];  // the cell's first (minimum-index) member (dbscan.cpp:98-104)
     }
     qpt[dst] = pt;
     qrank[dst] = s;
@@ -294,12 +298,13 @@ struct DbCoreQuery {
   const int32_t* __restrict__ list;  // query slots to run (the SinglePoint ones)
   unsigned long long dists = 0;
   float p[3];
-  int32_t id, node, nlo, mask_rank = 0;
+  int32_t id, slot, node, nlo, mask_rank = 0;
   int count;
   // the stopping scan of a long cut DenseBox, left to the warp (k_db_core)
   int32_t pend_kb = -1, pend_ke = 0, pend_rem = 0;
   __device__ bool begin(int64_t q) {
-    const float4 qp = qpt[list ? list[q] : q];
+    slot = list ? list[q] : static_cast<int32_t>(q);
+    const float4 qp = qpt[slot];
     id = __float_as_int(qp.w);
     if (id < 0) return false;  // member of a dense cell
     p[0] = qp.x;
@@ -374,7 +379,7 @@ struct DbCoreQuery {
         nodes, p, bt, 0, node, nlo, *stack, visit, inside);
   }
   __device__ void end() {
-    if (count >= minpts) flags[id] = 1;
+    if (count >= minpts) flags[slot] = 1;
   }
 };
 
@@ -442,10 +447,11 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
 // the mixed tree whose box lies inside the ball holds primitives that each
 // give exactly one pair and one distance evaluation in the reference (a
 // SinglePoint within eps; a DenseBox whose first member is within eps), so a
-// run of primitive ranks [first, last] is counted at once; rep[rank] is the
-// primitive's point (a DenseBox's first member — dense members are core and
-// pre-unioned). Resolution as in k_fd_main: a core query takes runs of core
-// primitives (unite with rep[first], run recorded for the cover pass), a
+// run of primitive ranks [first, last] is counted at once; qoff[rank] is the
+// slot of the primitive's point (a DenseBox's first member — dense members
+// are core and pre-unioned). Resolution as in k_fd_main: a core query takes
+// runs of core primitives (unite with qoff[first], run recorded for the
+// cover pass), a
 // border query counts coreless runs and every run once claimed; other runs
 // are walked. minpts == 2: every run is taken (all pairs are unions).
 template <int D, bool kForceCore, int kFast>
@@ -453,17 +459,18 @@ __global__ void __launch_bounds__(kQueryBlock)
 k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
                  const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
                  const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
-                 BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
-                 const int32_t* __restrict__ rep, const int32_t* __restrict__ noncore_before,
-                 int32_t* __restrict__ reach, DevCounters* ctr, MemberTree mt) {
+                 BallTest bt, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+                 const int32_t* __restrict__ key, const int32_t* __restrict__ qoff,
+                 const int32_t* __restrict__ noncore_before, int32_t* __restrict__ reach,
+                 DevCounters* ctr, MemberTree mt) {
   const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = q < n;
   unsigned long long pairs = 0, dists = 0;
   float p[3] = {0.f, 0.f, 0.f};
-  int32_t i = 0, own = 0;
+  const int32_t i = static_cast<int32_t>(q);  // this query's slot
+  int32_t own = 0;
   if (valid) {
     const float4 qp = qpt[q];
-    i = __float_as_int(qp.w) & 0x7fffffff;
     own = qrank[q];
     p[0] = qp.x;
     p[1] = qp.y;
@@ -475,23 +482,26 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
     const bool core_i = kForceCore ? true : flags[i] != 0;
     int32_t hint = i;
     bool settled = false;
+    // j: the neighbour's slot (a SinglePoint's is qoff[rank]; a DenseBox
+    // member's is qoff[rank] + its offset in the cell)
     auto pair = [&](int32_t j) {
       ++pairs;
-      if (kForceCore)
-        uf_unite_hinted(parent, i, j, hint);  // core flags derived at finalize
+      if (kForceCore)  // core flags derived at finalize from the hook marks
+        uf_unite_hinted_keyed(parent, key, i, j, hint, flags);
       else
-        resolve_pair(i, j, core_i, flags, parent, hint, settled);
+        resolve_pair_keyed(i, j, core_i, flags, parent, key, hint, settled);
     };
-    auto visit = [&](int32_t, int32_t aux, bool contained) -> bool {
+    auto visit = [&](int32_t s, int32_t aux, bool contained) -> bool {
+      const int32_t base = __ldg(qoff + s);
       if (aux >= 0) {
         ++dists;
-        pair(aux);
+        pair(base);
       } else {
         const int32_t c = ~aux;
         const int32_t kb = cell_begin[c], ke = cell_end[c];
         if (contained) {  // every member within eps: the scan stops at the first
           ++dists;
-          pair(__float_as_int(__ldg(sorted_pt + kb).w));
+          pair(base);
         } else {
           // scan to the first member within eps (dbscan.cpp:183-193), answered
           // by the member tree: same member, same evaluation count
@@ -499,7 +509,7 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
           const int64_t pos = member_scan<D>(mt, kb, ke, p, bt, 1, hits);
           if (pos >= 0) {
             dists += static_cast<unsigned long long>(pos - kb + 1);
-            pair(__float_as_int(__ldg(sorted_pt + pos).w));
+            pair(base + static_cast<int32_t>(pos - kb));
           } else {
             dists += static_cast<unsigned long long>(ke - kb);
           }
@@ -517,12 +527,13 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
           run = true;
         } else if (!settled && nc != cnt) {
           if (nc != 0) return kWalk;
-          if (ld_relaxed(parent + i) == i) uf_claim(parent, i, uf_find(parent, __ldg(rep + first)));
+          if (ld_relaxed(parent + i) == i) uf_claim(parent, i, uf_find(parent, __ldg(qoff + first)));
           settled = true;
         }
       }
       if (run) {
-        uf_unite_hinted(parent, i, __ldg(rep + first), hint);
+        uf_unite_hinted_keyed(parent, key, i, __ldg(qoff + first), hint,
+                              kForceCore ? flags : nullptr);
         record_run(reach, first, last);
       }
       pairs += static_cast<unsigned long long>(cnt);
@@ -619,20 +630,6 @@ __global__ void k_member_level(const float4* __restrict__ pts, const float4* __r
   }
 }
 
-// rep[rank]: the primitive's point (a DenseBox's first member); ind[rank] = 1
-// for a SinglePoint that is not core (after the core pass), for the
-// noncore prefix counts.
-__global__ void k_prim_reps(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
-                            const int32_t* __restrict__ cell_begin,
-                            const float4* __restrict__ sorted_pt, int64_t m,
-                            int32_t* __restrict__ rep) {
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t a = prim_aux[order[s]];
-    rep[s] = a >= 0 ? a : __float_as_int(sorted_pt[cell_begin[~a]].w);
-  }
-}
-
 // Query slots of the SinglePoint primitives, in rank order (the only queries
 // of densebox_mark_cores: dense members are core already, dbscan.cpp:118).
 __global__ void k_single_ind(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
@@ -650,17 +647,17 @@ __global__ void k_single_slots(const int32_t* __restrict__ ind, const int32_t* _
     if (ind[s]) list[pos[s]] = qoff[s];
 }
 
+// ind[rank] = 1 for a SinglePoint that is not core (after the core pass), for
+// the noncore prefix counts.
 __global__ void k_prim_noncore(const int32_t* __restrict__ order,
                                const int32_t* __restrict__ prim_aux,
-                               const uint8_t* __restrict__ flags, int64_t m,
+                               const uint8_t* __restrict__ flags,
+                               const int32_t* __restrict__ qoff, int64_t m,
                                int32_t* __restrict__ ind) {
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s <= m;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int32_t v = 0;
-    if (s < m) {
-      const int32_t a = prim_aux[order[s]];
-      v = a >= 0 && !flags[a];
-    }
+    if (s < m) v = prim_aux[order[s]] >= 0 && !flags[qoff[s]];
     ind[s] = v;
   }
 }
@@ -817,12 +814,13 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   exclusive_scan_i32(qcount, qoff, num_prims, nullptr, scan_tmp, st);
   float4* qpt = scratch.alloc_n<float4>(n);
   int32_t* qrank = scratch.alloc_n<int32_t>(n);
+  int32_t* qkey = scratch.alloc_n<int32_t>(n);
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
   init_union_find(parent, flags, n, st);
   note_launch(), k_queries<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
                                                  cell_dense, prim_off, rank_of_prim, qoff, n,
-                                                 qpt, qrank, parent, flags);
+                                                 qpt, qrank, qkey, parent, flags);
   TCB_CUDA(cudaGetLastError());
 
   const MemberTree mt = build_member_tree<D>(sorted_pt, n, scratch);
@@ -863,30 +861,29 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   }
   // ---- main pass ----
   clock.mark(kStMain);
-  int32_t* rep = scratch.alloc_n<int32_t>(num_prims);
   int32_t* reach = scratch.alloc_n<int32_t>(num_prims + 8);
   int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(num_prims));
   int32_t* noncore_before = nullptr;
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, sizeof(int32_t) * num_prims, st));
-  note_launch(), k_prim_reps<<<grid_for(num_prims, 256), 256, 0, st>>>(
-      b.tree.leaf_order, prim_aux, cell_begin, sorted_pt, num_prims, rep);
   if (minpts > 2) {
     int32_t* ind = scratch.alloc_n<int32_t>(num_prims + 1);
     noncore_before = scratch.alloc_n<int32_t>(num_prims + 1);
     note_launch(), k_prim_noncore<<<grid_for(num_prims + 1, 256), 256, 0, st>>>(
-        b.tree.leaf_order, prim_aux, flags, num_prims, ind);
+        b.tree.leaf_order, prim_aux, flags, qoff, num_prims, ind);
     exclusive_scan_i32(ind, noncore_before, num_prims + 1, nullptr, scan_tmp, st);
   }
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
   auto main = minpts == 2 ? (bt.fast ? k_db_main_ranged<D, true, 1> : k_db_main_ranged<D, true, 0>)
                           : (bt.fast ? k_db_main_ranged<D, false, 1> : k_db_main_ranged<D, false, 0>);
   note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin,
-                                                cell_end, bt, flags, parent, rep, noncore_before,
-                                                reach, ctr, mt);
-  launch_cover_joins(reach, num_prims, tile_max, RepJoin{parent, rep}, st);
+                                                cell_end, bt, flags, parent, qkey, qoff,
+                                                noncore_before, reach, ctr, mt);
+  launch_cover_joins(reach, num_prims, tile_max,
+                     SlotJoin{parent, qkey, qoff, minpts == 2 ? flags : nullptr}, st);
   TCB_CUDA(cudaGetLastError());
   clock.mark(kStFinal);
-  finalize_labels(parent, flags, n, d_labels, d_core, ctr, st, minpts == 2);
+  finalize_labels_bucketed(parent, flags, qkey, qkey, n, d_labels, d_core, ctr, scratch,
+                           minpts == 2);
   clock.finish();
 }
 
