@@ -13,7 +13,7 @@
 //   k_fd_main      the same for minpts > 2 (pairs resolved per
 //                  dbscan.hpp:82-99 with final core flags).
 //   cover.cuh      the runs' unions (max-scan over the recorded runs).
-//   k_finalize*    UnionFind::flatten + finalize_labels + the stats loop
+//   k_fin_*        UnionFind::flatten + finalize_labels + the stats loop
 //                  (union_find.hpp:77-86, dbscan.cpp:202-219, :274-282).
 //
 // For point leaves the leaf box test IS the exact distance test (the box is
@@ -271,24 +271,6 @@ __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
     parent[i] = static_cast<int32_t>(i);
 }
 
-// minpts == 2: a point is core iff some other point lies within eps, i.e.
-// iff it shares a union-find set with another point. Flatten, and mark every
-// non-root point and the root it hangs under (the reference sets both flags
-// per pair instead, dbscan.hpp:85-88; the final flags are the same).
-__global__ void __launch_bounds__(256)
-k_flatten_mark(int32_t* __restrict__ parent, uint8_t* __restrict__ flags, int64_t n) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int32_t p = ld_relaxed(parent + i);
-    if (p == static_cast<int32_t>(i)) continue;
-    int32_t q;
-    while (p != (q = ld_relaxed(parent + p))) p = q;
-    st_relaxed(parent + i, p);
-    flags[i] = 1;
-    if (!flags[p]) flags[p] = 1;
-  }
-}
-
 // Rank-space finalize (FDBSCAN): flatten over ranks (union_find.hpp:77-86,
 // dbscan.cpp:202-219); the representative of a set is its minimum-key rank,
 // so label = key[root] = minimum original index. The outputs go to input
@@ -408,35 +390,6 @@ k_fin_scatter(const uint2* __restrict__ entries, int64_t e0, int64_t e1,
   }
 }
 
-
-__global__ void __launch_bounds__(256)
-k_finalize(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags, int64_t n,
-           int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, DevCounters* ctr) {
-  long long noise = 0, clusters = 0, cores = 0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int32_t p = ld_relaxed(parent + i);
-    int32_t q;
-    while (p != (q = ld_relaxed(parent + p))) p = q;
-    st_relaxed(parent + i, p);
-    const bool core = flags[i] != 0;
-    const int32_t lab = (core || p != i) ? p : -1;  // dbscan.cpp:215
-    labels[i] = lab;
-    core_out[i] = core ? 1 : 0;
-    noise += lab == -1;
-    clusters += lab == static_cast<int32_t>(i);
-    cores += core;
-  }
-  noise = warp_sum(noise);
-  clusters = warp_sum(clusters);
-  cores = warp_sum(cores);
-  if ((threadIdx.x & 31) == 0) {
-    if (noise) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->noise), noise);
-    if (clusters) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->clusters), clusters);
-    if (cores) atomicAdd(reinterpret_cast<unsigned long long*>(&ctr->cores), cores);
-  }
-}
-
 }  // namespace
 
 template <int D>
@@ -540,13 +493,6 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
 }
 
 
-
-void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n, int32_t* labels,
-                     uint8_t* core_out, DevCounters* d_ctr, cudaStream_t s, bool force_core) {
-  if (force_core) note_launch(), k_flatten_mark<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n);
-  note_launch(), k_finalize<<<grid_for(n, 256), 256, 0, s>>>(parent, flags, n, labels, core_out, d_ctr);
-  TCB_CUDA(cudaGetLastError());
-}
 
 template void fdbscan_core_pass<2>(const BuiltBvh&, int64_t, double, int, uint8_t*,
                                    DevCounters*, cudaStream_t);

@@ -136,11 +136,6 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
                               const int32_t* order, int64_t n, int32_t* labels,
                               uint8_t* core_out, DevCounters* d_ctr, Scratch& scratch,
                               bool force_core, const ChunkSink* sink = nullptr);
-// force_core (minpts == 2): core flags are derived here from the union-find
-// structure instead of being stored per pair in the main pass.
-void finalize_labels(int32_t* parent, uint8_t* flags, int64_t n,
-                     int32_t* labels, uint8_t* core_out, DevCounters* d_ctr,
-                     cudaStream_t s, bool force_core);
 
 // ---- whole FDBSCAN pipeline over the point BVH (engine.cu) ----
 // d_keys (optional): unique int32 key per point; labels are then the key of
