@@ -360,11 +360,13 @@ def test_load_binary_device_matches_host_load(tmp_path):
     assert e.value.status == Status.IO
 
 
-@pytest.mark.parametrize("minpts", [2, 6])
-def test_keyed_and_local_context_label_in_keys(minpts):
+@pytest.mark.parametrize("minpts,top", [(2, False), (6, False), (2, True), (6, True)])
+def test_keyed_and_local_context_label_in_keys(minpts, top):
     """tcg_cluster_keyed_device and the tcg_local_* context (the sharded
     path's local runs): with arbitrary unique keys, a cluster is labelled by
-    the key of its minimum-key core, and the partition equals tc_cluster's."""
+    the key of its minimum-key core, and the partition equals tc_cluster's.
+    top: the keys run up to INT32_MAX (labels travel through the finalize
+    entries untouched)."""
     import torch
     from paper_2103_05162_b200.shard import DeviceEngine
 
@@ -372,7 +374,9 @@ def test_keyed_and_local_context_label_in_keys(minpts):
     eps = 0.09
     want = tb.cluster(Dataset.from_array(c), eps, minpts, Algorithm.FDBSCAN)
     rng = np.random.default_rng(3)
-    keys = rng.permutation(np.arange(10**6, 10**6 + 7 * len(c), 7)).astype(np.int32)
+    base = 2**31 - 1 - 7 * (len(c) - 1) if top else 10**6
+    keys = rng.permutation(np.arange(base, base + 7 * len(c), 7, dtype=np.int64)).astype(np.int32)
+    assert not top or keys.max() == 2**31 - 1
     eng = DeviceEngine("cuda:0")
     x = torch.from_numpy(c).cuda()
     kd = torch.from_numpy(keys).cuda()
