@@ -33,6 +33,13 @@ namespace tcb {
 namespace {
 
 constexpr int kQueryBlock = 128;  // 64 / 256 measured equal or slower
+// Resident blocks per SM the FoF main pass is compiled for (ptxas caps its
+// registers at 36): 14 x 4 warps instead of 12 at its natural 40 registers,
+// main pass 19.2 -> 18.5 ms on C2 despite a few spilled bytes.
+constexpr int kFofMinBlocks = 14;
+// the same for the minpts > 2 main pass (12: main 22.2 -> 21.2 ms on C3);
+// the core pass is faster uncapped
+constexpr int kMainMinBlocks = 12;
 
 template <int D>
 __device__ __forceinline__ void load_query(const float4* leaf_pt, int64_t r, float* p,
@@ -134,7 +141,7 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
 //                 no-op, counted only; all leaves core: claimed by the run;
 //   otherwise the subtree is walked leaf by leaf (per-pair rule).
 template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
+__global__ void __launch_bounds__(kQueryBlock, kMainMinBlocks)
 k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
           const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
@@ -201,7 +208,7 @@ __global__ void k_noncore_ind(const uint8_t* __restrict__ flags, int64_t n,
 // run); pairs counted per leaf, so pair_resolutions / distance_evaluations
 // stay exact.
 template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
+__global__ void __launch_bounds__(kQueryBlock, kFofMinBlocks)
 k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
               BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
               int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {

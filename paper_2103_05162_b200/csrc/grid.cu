@@ -279,6 +279,10 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
 // densebox_mark_cores query (dbscan.cpp:110-139): unmasked; a SinglePoint
 // leaf is one neighbour, a DenseBox leaf is scanned member by member until
 // minpts is reached. Dense members are core already and skip (dbscan.cpp:118).
+// Resident 128-thread blocks per SM the DenseBox traversals are compiled
+// for (register cap; C4 main pass 63.7 -> 62.8 ms).
+constexpr int kDbMinBlocks = 10;
+
 template <int D, int kFast>
 struct DbCoreQuery {
   const float4* __restrict__ nodes;
@@ -384,7 +388,7 @@ struct DbCoreQuery {
 };
 
 template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
+__global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
@@ -455,7 +459,7 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
 // border query counts coreless runs and every run once claimed; other runs
 // are walked. minpts == 2: every run is taken (all pairs are unions).
 template <int D, bool kForceCore, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
+__global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
 k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
                  const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
                  const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
