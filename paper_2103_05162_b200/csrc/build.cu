@@ -162,7 +162,7 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
 // The tree is the reference's tree node for node; only the numbering of the
 // internal nodes differs (tcg_debug_point_bvh renumbers to Karras indices).
 // ---------------------------------------------------------------------------
-constexpr int kClimbBlock = 256;  // 512 measured slower (more rounds per block)
+constexpr int kClimbBlock = 128;  // 256: topology 3.04 vs 2.90 ms on C2; 512 slower still
 
 struct ClimbState {
   int32_t root;         // split index of the root
@@ -200,7 +200,7 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
   }
 
   // ---- block-local phase: every node whose two children lie inside this
-  // block's 256 leaves is finished here through shared memory — the left
+  // block's leaves is finished here through shared memory — the left
   // child's thread reads the right child's box and writes the whole record;
   // no exchange, no fence. Subtrees stay a partition of the block's leaves,
   // each held by the thread of its first leaf; s_start[end] is the first leaf
@@ -209,7 +209,7 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
     __shared__ float s_box[2 * D][kClimbBlock];
     __shared__ int32_t s_r[kClimbBlock], s_link[kClimbBlock], s_aux[kClimbBlock];
     __shared__ int32_t s_code[kClimbBlock], s_start[kClimbBlock];
-    __shared__ int32_t s_delta[kClimbBlock + 1];  // delta(b0 - 1 + j), j = 0..256
+    __shared__ int32_t s_delta[kClimbBlock + 1];  // delta(b0 - 1 + j), j = 0..kClimbBlock
     const int t = threadIdx.x;
     const int64_t b0 = s - t;
     const int64_t b1 = min(b0 + kClimbBlock - 1, m - 1);
