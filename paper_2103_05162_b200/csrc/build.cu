@@ -162,7 +162,7 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
 // The tree is the reference's tree node for node; only the numbering of the
 // internal nodes differs (tcg_debug_point_bvh renumbers to Karras indices).
 // ---------------------------------------------------------------------------
-constexpr int kClimbBlock = 128;  // 256: topology 3.04 vs 2.90 ms on C2; 512 slower still
+constexpr int kClimbBlock = 128;  // 256: topology 3.04 vs 2.90 ms on C2; 64: 3.06; 512 slower still
 
 struct ClimbState {
   int32_t root;         // split index of the root
