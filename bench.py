@@ -21,8 +21,10 @@ scaling; `--replicas` instead runs N independent 37M clouds. Timed as the max
 over ranks. (TCB_BENCH_BACKEND=gloo TCB_BENCH_SAME_DEVICE=1 lets a 1-GPU box
 smoke-test the N>1 protocol with every rank on cuda:0.)
 `--impl reference` times the reference's own CPU implementation
-(oracle/_ref = /root/reference/proj compiled unmodified, via its C ABI) on the
-host cores, on a bounded sample of the same workload (same density).
+(oracle/_ref = /root/reference/proj compiled unmodified) through its public C
+ABI on the host cores, on the same 37M-point workload: input from the oracle's
+byte-identical generator, loaded with the reference's tc_dataset_load; the
+product library is never loaded on that arm.
 """
 from __future__ import annotations
 
@@ -46,7 +48,6 @@ UNIT = "Mpoints/s"
 # algorithmic bytes per point, 3D FDBSCAN minpts=2, one pass.
 B_ALG_TOTAL = 183
 B_ALG_MAIN = 53  # per traversal pass: leaf coords + node + flag + 2 x parent
-REF_SAMPLE_N = 4_000_000  # bounded CPU sample (same density as C2)
 
 
 def env_int(name, default):
@@ -128,58 +129,81 @@ def load_traffic():
         return None
 
 
-def cpu_reference_run(n_sample, steps, warmup, threads=0):
-    """Times the unmodified reference (oracle/_ref) through its own C ABI."""
-    import ctypes as C
-    import paper_2103_05162_b200 as tb
-    from oracle import ref
+def reference_input(n):
+    """C2's input for the reference arm, made WITHOUT the product library: the
+    oracle's byte-identical HACC-like generator (sha256 pinned in
+    tests/golden/bench_inputs.json), written in the reference's .bin format and
+    loaded through the reference's own tc_dataset_load (REF capi.cpp:84-96)."""
+    import shutil
+    import tempfile
+    from oracle import oracle, ref
 
-    L = ref.lib()
-    L.tc_dataset_create.argtypes = [C.POINTER(C.c_float), C.c_int64, C.c_int,
-                                    C.POINTER(C.c_void_p)]
-    L.tc_cluster.argtypes = [C.c_void_p, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int64,
-                             C.POINTER(C.c_void_p)]
-    L.tc_result_free.argtypes = [C.c_void_p]
-    L.tc_dataset_free.argtypes = [C.c_void_p]
-    sample = tb.Dataset.hacc_like(n_sample).coords()
-    ds = C.c_void_p()
-    assert L.tc_dataset_create(sample.ctypes.data_as(C.POINTER(C.c_float)), n_sample, 3,
-                               C.byref(ds)) == 0
-    times = []
+    coords = oracle.hacc_like(n)
+    tmp = tempfile.mkdtemp(prefix="tcb_ref_")
+    try:
+        path = os.path.join(tmp, "c2.bin")
+        oracle.write_bin(path, coords)
+        del coords
+        return ref.RefDataset.load(path)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+def cpu_reference_times(ds, steps, warmup, threads=0):
+    """Wall seconds of the unmodified reference's tc_cluster (REF
+    capi.cpp:150-184) on dataset `ds`, plus the last run's stats."""
+    times, stats = [], None
     for it in range(warmup + steps):
-        res = C.c_void_p()
-        t0 = time.perf_counter()
-        st = L.tc_cluster(ds, C.c_float(EPS), MINPTS, ALGO, threads, 0, C.byref(res))
-        dt = time.perf_counter() - t0
-        assert st == 0, st
-        L.tc_result_free(res)
+        dt, stats, _, _ = ds.cluster(EPS, MINPTS, ALGO, threads)
         if it >= warmup:
             times.append(dt)
-    L.tc_dataset_free(ds)
-    return times
+    return times, stats
+
+
+def cpu_desc(threads_used):
+    from oracle import ref
+    return {"cores": threads_used, "host_threads": os.cpu_count() or 1,
+            "cpu_model": ref.host_cpu_model()}
 
 
 def run_reference_arm(args, rank, world):
+    """`--impl reference`: the reference's own CPU path (oracle/_ref = the
+    unmodified /root/reference/proj compiled from its sources) through its
+    public C ABI, on the SAME workload as our arm (C2: 37M HACC-like points,
+    eps 0.042, minpts 2, FDBSCAN), threads=0 (all host cores). Rank 0 only."""
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
     steps = max(1, args.steps)
-    times = cpu_reference_run(REF_SAMPLE_N, steps, args.warmup)
+    n = args.points
+    t_gen = time.perf_counter()
+    ds = reference_input(n)
+    t_gen = time.perf_counter() - t_gen
+    times, stats = cpu_reference_times(ds, steps, args.warmup)
+    ds.close()
     t = sum(times) / len(times)
-    value = REF_SAMPLE_N / t / 1e6
-    sample = (f"hacc_like n={REF_SAMPLE_N} (same density as the 37M config), eps={EPS}, "
-              f"minpts={MINPTS}, FDBSCAN, tc_cluster(threads=0) of the unmodified reference")
+    value = n / t / 1e6
+    desc = cpu_desc(os.cpu_count() or 1)
+    sample = (f"the full workload: hacc_like n={n} (oracle generator, .bin via the reference's "
+              f"tc_dataset_load, {t_gen:.1f} s), eps={EPS}, minpts={MINPTS}, FDBSCAN, reference "
+              f"tc_cluster(threads=0) on {desc['host_threads']} host threads "
+              f"({desc['cpu_model']}); per-run s: min {min(times):.2f} max {max(times):.2f}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 coords / f64 distances", "data": "synthetic",
-        "config": {"workload": "C2-sample: 3D HACC-like halos, eps=0.042, minpts=2, FDBSCAN",
-                   "points_per_step": REF_SAMPLE_N, "algorithm": "FDBSCAN"},
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores,
-                         "kind": "reference", "sample": sample},
+        "config": {"workload": "C2: 3D HACC-like halos, 37M points, eps=0.042, minpts=2, "
+                               "FDBSCAN" if n == N_POINTS else f"C2-shaped, n={n}",
+                   "points_per_rank": n, "algorithm": "FDBSCAN", "eps": EPS, "minpts": MINPTS,
+                   "parallelism": "host threads (reference parallel_for)"},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": desc["cores"],
+                         "cpu_model": desc["cpu_model"], "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "stage_s": {k: round(stats[k], 3) for k in ("build_seconds", "preprocess_seconds",
+                                                     "main_seconds", "finalize_seconds")},
+        "stats": {k: int(stats[k]) for k in ("pair_resolutions", "cluster_count", "core_count",
+                                            "noise_count")},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -379,17 +403,23 @@ def main():
         e2e_s = float(t.item())
     e2e_value = n * world / e2e_s / 1e6
 
-    # ---- CPU baseline: the unmodified reference on the host cores ----
+    # ---- CPU baseline: the unmodified reference on the host cores, on the
+    # same 37M input (one run, threads=0) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            times = cpu_reference_run(REF_SAMPLE_N, 2, 0)
-            tcpu = sum(times) / len(times)
-            cpu = {"value": round(REF_SAMPLE_N / tcpu / 1e6, 4), "unit": UNIT,
-                   "cores": os.cpu_count() or 1, "kind": "reference",
-                   "sample": f"hacc_like n={REF_SAMPLE_N} (C2 density), eps={EPS}, minpts={MINPTS}, "
-                             "FDBSCAN, reference tc_cluster(threads=0), mean of 2 runs, "
-                             f"{tcpu:.2f} s each"}
+            from oracle import ref
+            rds = ref.RefDataset.from_array(ds.coords())
+            times, rstats = cpu_reference_times(rds, 1, 0)
+            rds.close()
+            tcpu = times[0]
+            desc = cpu_desc(os.cpu_count() or 1)
+            same = rstats["pair_resolutions"] == (last_stats or {}).get("pair_resolutions")
+            cpu = {"value": round(n / tcpu / 1e6, 4), "unit": UNIT, "cores": desc["cores"],
+                   "cpu_model": desc["cpu_model"], "kind": "reference",
+                   "sample": f"the full workload (n={n}, eps={EPS}, minpts={MINPTS}, FDBSCAN): "
+                             f"one reference tc_cluster(threads=0) run, {tcpu:.2f} s; "
+                             f"pair_resolutions equal to ours: {same}"}
         except Exception as e:  # the reference .so may be absent on a bare box
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1,
                    "kind": "reference", "sample": f"unavailable: {e}"}

@@ -23,8 +23,8 @@
 extern "C" {
 #endif
 
-/* Library / device information. Returns the CUDA device count (0 when no
- * usable device / driver), and fills name (NUL-terminated) for device 0. */
+/* Library / device information: the CUDA device count (0 when no usable
+ * device / driver) and the library version string. */
 int tcg_device_count(void);
 const char* tcg_version(void);
 
@@ -89,10 +89,11 @@ tc_status tcg_generate_taxi_like(int64_t n, uint64_t seed, tc_dataset** out);
 tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n,
                               float* eps, int* minpts, tc_dataset** out);
 
-/* ---- dataset from caller memory without validation copy (host) ---- */
-/* Same as tc_dataset_create but the dataset's coords live in page-locked
- * (pinned) host memory, so tc_cluster's host->device copy runs at full PCIe
- * / C2C rate. */
+/* ---- dataset creation (host) ---- */
+/* Identical to tc_dataset_create (kept for source compatibility with earlier
+ * builds): every dataset of 1 MiB or more is allocated page-locked by
+ * tc_dataset_create already, so tc_cluster's host->device copy runs at full
+ * PCIe / C2C rate either way. */
 tc_status tcg_dataset_create_pinned(const float* coords, int64_t n, int dim,
                                     tc_dataset** out);
 
@@ -142,6 +143,24 @@ void tcg_local_free(tcg_local* ctx);
  * for the cross-shard merge of (ghost, local root) edges. */
 tc_status tcg_union_edges_device(const int32_t* d_edges, int64_t m, int32_t n, int32_t* d_root,
                                  void* stream);
+
+/* ---- device parity checker ---- */
+
+/* check_equivalence (REF oracle.cpp:120-163) of clusterings a and b of the
+ * same n points, all on the device: checks run in the reference's order and
+ * *check receives the first that fails (0 pass, 1 core flags differ, 2 noise
+ * sets differ, 3 core partitions differ, 4 / 5 invalid border label in a / b)
+ * and *at the point index the reference's scan reports for it. Synchronizes
+ * `stream`. */
+tc_status tcg_check_equivalence_device(const float* d_coords, int64_t n, int dim, float eps,
+                                       const int32_t* d_labels_a, const uint8_t* d_core_a,
+                                       const int32_t* d_labels_b, const uint8_t* d_core_b,
+                                       void* stream, int* check, int64_t* at);
+/* borders_valid (REF oracle.cpp:72-116) of one clustering: *at = the smallest
+ * index of a border point with no same-label core within eps, or -1. */
+tc_status tcg_first_bad_border_device(const float* d_coords, int64_t n, int dim, float eps,
+                                      const int32_t* d_labels, const uint8_t* d_core,
+                                      void* stream, int64_t* at);
 
 /* ---- stage probes for parity tests (each runs one device stage on host
  *      inputs and copies the result back) ---- */

@@ -38,6 +38,8 @@ def lib() -> C.CDLL:
                                     u8p, i64p]
         L.oracle_check_equivalence.argtypes = [f32p, C.c_int64, C.c_int, C.c_float, i32p, u8p,
                                                i32p, u8p, C.c_char_p, C.c_int64]
+        L.oracle_gen_hacc_like.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_uint64, f32p]
+        L.oracle_gen_taxi_like.argtypes = [C.c_int64, C.c_uint64, f32p]
         _lib = L
     return _lib
 
@@ -116,3 +118,32 @@ def check_equivalence(coords, eps, la, ca, lb, cb):
                                         _p(la, C.c_int32), _p(ca, C.c_uint8), _p(lb, C.c_int32),
                                         _p(cb, C.c_uint8), msg, len(msg))
     return bool(ok), msg.value.decode()
+
+
+def hacc_like(n: int, box_len=None, halo_frac=0.23, seed=11) -> np.ndarray:
+    """SURVEY §8d HACC-like halos (C2/C3/C5 inputs); box_len defaults to the
+    C2 density, 36.8 * (n / 37e6)^(1/3)."""
+    if box_len is None:
+        box_len = 36.8 * (n / 37e6) ** (1.0 / 3.0)
+    out = np.empty((n, 3), np.float32)
+    if lib().oracle_gen_hacc_like(n, float(box_len), float(halo_frac), seed,
+                                  _p(out, C.c_float)) != 0:
+        raise ValueError("invalid argument")
+    return out
+
+
+def taxi_like(n: int, seed=5) -> np.ndarray:
+    """SURVEY §8d taxi-like 2D road points (C4 input)."""
+    out = np.empty((n, 2), np.float32)
+    if lib().oracle_gen_taxi_like(n, seed, _p(out, C.c_float)) != 0:
+        raise ValueError("invalid argument")
+    return out
+
+
+def write_bin(path: str, coords) -> None:
+    """The reference's binary point format (REF io.cpp:124-134): u32 n, u32 dim,
+    n*dim little-endian f32."""
+    a = np.ascontiguousarray(coords, np.float32)
+    with open(path, "wb") as f:
+        f.write(np.array(a.shape, dtype="<u4").tobytes())
+        f.write(a.astype("<f4", copy=False).tobytes())

@@ -154,3 +154,118 @@ def random_instance(seed, min_n=50, max_n=2000):
     lib().ref_random_instance(seed, min_n, max_n, C.byref(dim), C.byref(eps), C.byref(minpts),
                               _ptr(coords, C.c_float))
     return coords, eps.value, minpts.value
+
+
+# ---------------------------------------------------------------------------
+# The reference's own public C ABI (REF include/treeclust.h:52-103), for the
+# CPU baseline: bench.py's reference arm loads its input through
+# tc_dataset_load and times tc_cluster exactly as a reference caller would.
+# ---------------------------------------------------------------------------
+class RefStats(C.Structure):
+    """tc_cluster_stats (REF include/treeclust.h:38-50)."""
+
+    _fields_ = [("build_seconds", C.c_double), ("preprocess_seconds", C.c_double),
+                ("main_seconds", C.c_double), ("finalize_seconds", C.c_double),
+                ("preprocess_skipped", C.c_int), ("dense_point_fraction", C.c_double),
+                ("pair_resolutions", C.c_uint64), ("distance_evaluations", C.c_uint64),
+                ("cluster_count", C.c_int64), ("core_count", C.c_int64),
+                ("noise_count", C.c_int64)]
+
+    def to_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+def _capi():
+    L = lib()
+    if not getattr(L, "_capi_ready", False):
+        V, PP = C.c_void_p, C.POINTER(C.c_void_p)
+        L.tc_dataset_load.argtypes = [C.c_char_p, C.c_int, PP]
+        L.tc_dataset_create.argtypes = [C.POINTER(C.c_float), C.c_int64, C.c_int, PP]
+        L.tc_dataset_size.restype = C.c_int64
+        L.tc_dataset_size.argtypes = [V]
+        L.tc_dataset_free.argtypes = [V]
+        L.tc_cluster.argtypes = [V, C.c_float, C.c_int, C.c_int, C.c_int, C.c_int64, PP]
+        L.tc_result_stats.argtypes = [V, C.POINTER(RefStats)]
+        L.tc_result_labels.restype = C.POINTER(C.c_int32)
+        L.tc_result_labels.argtypes = [V]
+        L.tc_result_core_flags.restype = C.POINTER(C.c_uint8)
+        L.tc_result_core_flags.argtypes = [V]
+        L.tc_result_free.argtypes = [V]
+        L._capi_ready = True
+    return L
+
+
+class RefDataset:
+    """A reference tc_dataset handle (tc_dataset_load / tc_dataset_create)."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def load(cls, path: str) -> "RefDataset":
+        h = C.c_void_p()
+        st = _capi().tc_dataset_load(path.encode(), 0, C.byref(h))
+        if st != 0:
+            raise RuntimeError(f"reference tc_dataset_load({path}) -> status {st}")
+        return cls(h)
+
+    @classmethod
+    def from_array(cls, coords) -> "RefDataset":
+        a, p = _f32(coords)
+        h = C.c_void_p()
+        st = _capi().tc_dataset_create(p, a.shape[0], a.shape[1], C.byref(h))
+        if st != 0:
+            raise RuntimeError(f"reference tc_dataset_create -> status {st}")
+        return cls(h)
+
+    @property
+    def size(self) -> int:
+        return int(_capi().tc_dataset_size(self.h))
+
+    def cluster(self, eps, minpts, algo, threads=0, want_labels=False):
+        """Reference tc_cluster (REF capi.cpp:150-184). Returns (wall seconds of
+        the call, stats dict, labels or None, core flags or None)."""
+        import time
+
+        L = _capi()
+        res = C.c_void_p()
+        t0 = time.perf_counter()
+        st = L.tc_cluster(self.h, C.c_float(eps), int(minpts), int(algo), int(threads), 0,
+                          C.byref(res))
+        dt = time.perf_counter() - t0
+        if st != 0:
+            raise RuntimeError(f"reference tc_cluster -> status {st}")
+        try:
+            s = RefStats()
+            L.tc_result_stats(res, C.byref(s))
+            labels = core = None
+            if want_labels:
+                n = self.size
+                labels = np.ctypeslib.as_array(L.tc_result_labels(res), shape=(n,)).copy()
+                core = np.ctypeslib.as_array(L.tc_result_core_flags(res), shape=(n,)).copy()
+            return dt, s.to_dict(), labels, core
+        finally:
+            L.tc_result_free(res)
+
+    def close(self):
+        if self.h:
+            _capi().tc_dataset_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def host_cpu_model() -> str:
+    """`lscpu` model name of this host (for the cpu_baseline record)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"

@@ -781,3 +781,115 @@ int oracle_check_equivalence(const float* coords, int64_t n, int dim, float eps,
   }
   return pass;
 }
+
+/* ---- benchmark inputs -------------------------------------
+ * Test/bench infrastructure: the reference arm of bench.py and the full-size
+ * parity tests generate their inputs here, so they never load the product
+ * library. SplitMix64 follows REF rng.hpp:11-47; the HACC-like and taxi-like
+ * recipes are the SURVEY §8d specifications (the reference ships neither).
+ * Output must be byte-identical to the product's tcg_generate_* (checked by
+ * tests/test_oracle.py against the sha256 in tests/golden/generators.json). */
+
+typedef struct {
+  uint64_t state;
+  int have_spare;
+  double spare;
+} Rng;
+
+static uint64_t rng_next(Rng* r) { /* REF rng.hpp:15-20 */
+  uint64_t z = (r->state += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static double rng_unit(Rng* r) { return (double)(rng_next(r) >> 11) * 0x1.0p-53; } /* :23 */
+static double rng_range(Rng* r, double lo, double hi) { return lo + (hi - lo) * rng_unit(r); }
+static double rng_gauss(Rng* r) { /* REF rng.hpp:28-41 (Box-Muller, cached half) */
+  if (r->have_spare) {
+    r->have_spare = 0;
+    return r->spare;
+  }
+  double u1 = rng_unit(r), u2 = rng_unit(r);
+  while (u1 == 0.0) u1 = rng_unit(r);
+  const double mag = sqrt(-2.0 * log(u1)), ang = 2.0 * 3.141592653589793 * u2;
+  r->spare = mag * sin(ang);
+  r->have_spare = 1;
+  return mag * cos(ang);
+}
+
+int oracle_gen_hacc_like(int64_t n, double box_len, double halo_frac, uint64_t seed,
+                         float* out) {
+  if (n < 1 || !(box_len > 0.0) || !(halo_frac >= 0.0 && halo_frac <= 1.0)) return 1;
+  Rng r = {seed, 0, 0.0};
+  const int64_t n_halo = (int64_t)(halo_frac * (double)n);
+  float* w = out;
+  for (int64_t i = 0; i < (n - n_halo) * 3; ++i) *w++ = (float)rng_range(&r, 0.0, box_len);
+  for (int64_t made = 0; made < n_halo;) {
+    int64_t m = (int64_t)(20.0 / pow(1.0 - rng_unit(&r), 1.0 / 0.9));
+    if (m > 200000) m = 200000;
+    if (m > n_halo - made) m = n_halo - made;
+    if (m < 1) m = 1;
+    const double a = 0.010 * cbrt((double)m / 20.0);
+    double c[3];
+    for (int k = 0; k < 3; ++k) c[k] = rng_range(&r, a, box_len - a);
+    for (int64_t p = 0; p < m; ++p) {
+      double rad;
+      do { /* Plummer radius, redrawn beyond 10a */
+        double uu;
+        do uu = rng_unit(&r); while (uu == 0.0);
+        rad = a / sqrt(pow(uu, -2.0 / 3.0) - 1.0);
+      } while (!(rad <= 10.0 * a));
+      const double z = rng_range(&r, -1.0, 1.0);
+      const double phi = rng_range(&r, 0.0, 2.0 * 3.141592653589793);
+      const double s = sqrt(1.0 - z * z);
+      *w++ = (float)(c[0] + rad * s * cos(phi));
+      *w++ = (float)(c[1] + rad * s * sin(phi));
+      *w++ = (float)(c[2] + rad * z);
+    }
+    made += m;
+  }
+  return 0;
+}
+
+int oracle_gen_taxi_like(int64_t n, uint64_t seed, float* out) {
+  enum { CITIES = 8, SEGMENTS = 300 };
+  if (n < 1) return 1;
+  Rng r = {seed, 0, 0.0};
+  double city[CITIES][2], seg[SEGMENTS][4], cdf[SEGMENTS], total = 0.0;
+  for (int c = 0; c < CITIES; ++c)
+    for (int k = 0; k < 2; ++k) city[c][k] = rng_range(&r, 0.2, 0.8);
+  for (int s = 0; s < SEGMENTS; ++s) {
+    const int c = (int)(rng_next(&r) % CITIES);
+    const double ax = city[c][0] + 0.08 * rng_gauss(&r);
+    const double ay = city[c][1] + 0.08 * rng_gauss(&r);
+    const double ang = rng_range(&r, 0.0, 3.141592653589793);
+    const double len = -0.02 * log(1.0 - rng_unit(&r));
+    seg[s][0] = ax;
+    seg[s][1] = ay;
+    seg[s][2] = len * cos(ang);
+    seg[s][3] = len * sin(ang);
+    total += pow((double)(s + 1), -0.8); /* Zipf(0.8) weights */
+    cdf[s] = total;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double x, y;
+    if (rng_unit(&r) < 0.98) {
+      const double pick = rng_unit(&r) * total;
+      int lo = 0, hi = SEGMENTS; /* first cdf entry > pick */
+      while (lo < hi) {
+        const int mid = (lo + hi) / 2;
+        if (cdf[mid] > pick) hi = mid; else lo = mid + 1;
+      }
+      const double* g = seg[lo < SEGMENTS ? lo : SEGMENTS - 1];
+      const double t = rng_unit(&r);
+      x = g[0] + t * g[2] + 1e-4 * rng_gauss(&r);
+      y = g[1] + t * g[3] + 1e-4 * rng_gauss(&r);
+    } else {
+      x = rng_unit(&r);
+      y = rng_unit(&r);
+    }
+    out[2 * i] = (float)(x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x));
+    out[2 * i + 1] = (float)(y < 0.0 ? 0.0 : (y > 1.0 ? 1.0 : y));
+  }
+  return 0;
+}

@@ -243,6 +243,56 @@ def verify(ds: Dataset, eps: float, minpts: int, threads: int = 0, oracle_cap: i
     return Status(st), buf.value.decode("utf-8", "replace")
 
 
+EQUIVALENCE_CHECKS = ("PASS", "core flags differ", "noise sets differ", "core partitions differ",
+                      "first clustering has an invalid border label",
+                      "second clustering has an invalid border label")
+
+
+def _dev_ptrs(coords, *arrays):
+    import torch
+
+    if not (coords.is_cuda and coords.dtype == torch.float32 and coords.dim() == 2
+            and coords.is_contiguous()):
+        raise TreeclustError(Status.INVALID_ARGUMENT, "device coords")
+    for a in arrays:
+        if not (a.is_cuda and a.is_contiguous() and a.shape[0] == coords.shape[0]):
+            raise TreeclustError(Status.INVALID_ARGUMENT, "device arrays")
+    return [C.c_void_p(a.data_ptr()) for a in (coords,) + arrays]
+
+
+def check_equivalence_device(coords, eps, labels_a, core_a, labels_b, core_b, stream=None):
+    """``tcg_check_equivalence_device`` (REF oracle.cpp:120-163 on the GPU):
+    returns (check code, point index, message) with check 0 = PASS."""
+    import torch
+
+    ptrs = _dev_ptrs(coords, labels_a, core_a, labels_b, core_b)
+    s = stream if stream is not None else torch.cuda.current_stream(coords.device)
+    chk, at = C.c_int(), C.c_int64()
+    _check(lib.tcg_check_equivalence_device(ptrs[0], coords.shape[0], coords.shape[1],
+                                            C.c_float(eps), *ptrs[1:], C.c_void_p(s.cuda_stream),
+                                            C.byref(chk), C.byref(at)),
+           "tcg_check_equivalence_device")
+    msg = EQUIVALENCE_CHECKS[chk.value]
+    if chk.value:
+        msg += f" (first divergence at point {at.value})"
+    return chk.value, at.value, msg
+
+
+def first_bad_border(coords, eps, labels, core, stream=None) -> int:
+    """``tcg_first_bad_border_device`` (REF oracle.cpp:72-116): smallest border
+    index with no same-label core within eps, or -1."""
+    import torch
+
+    ptrs = _dev_ptrs(coords, labels, core)
+    s = stream if stream is not None else torch.cuda.current_stream(coords.device)
+    at = C.c_int64()
+    _check(lib.tcg_first_bad_border_device(ptrs[0], coords.shape[0], coords.shape[1],
+                                           C.c_float(eps), ptrs[1], ptrs[2],
+                                           C.c_void_p(s.cuda_stream), C.byref(at)),
+           "tcg_first_bad_border_device")
+    return at.value
+
+
 def last_stage_ms() -> dict:
     arr = (C.c_double * len(STAGES))()
     k = lib.tcg_last_stage_ms(arr, len(STAGES))

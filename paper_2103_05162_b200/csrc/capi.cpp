@@ -252,40 +252,24 @@ void device_cluster(DeviceCall& call, const float* d_coords, int64_t n, int dim,
   if (res) res->stats = ro.stats;
 }
 
-// ---- check_equivalence (oracle.cpp:120-163) on host arrays + device border check ----
+// check_equivalence (oracle.cpp:120-163) on the device, message text as the
+// reference's index_message (oracle.cpp:64-68).
 struct Equivalence {
   bool pass = true;
   std::string message = "PASS";
 };
 
-std::string at_point(const char* what, int64_t i) {
-  std::ostringstream os;
-  os << what << " (first divergence at point " << i << ")";
-  return os.str();
-}
-
-Equivalence check_equivalence(const int32_t* la, const uint8_t* ca, const int32_t* lb,
-                              const uint8_t* cb, int64_t n, int64_t bad_a, int64_t bad_b) {
+Equivalence device_equivalence(const float* d_coords, int64_t n, int dim, float eps,
+                               const int32_t* la, const uint8_t* ca, const int32_t* lb,
+                               const uint8_t* cb, cudaStream_t st) {
+  const tcb::EqVerdict v = tcb::check_equivalence_device(d_coords, n, dim, eps, la, ca, lb, cb, st);
   Equivalence r;
-  auto fail = [&](std::string m) {
+  if (v.check != 0) {
+    std::ostringstream os;
+    os << tcb::equivalence_message(v.check) << " (first divergence at point " << v.at << ")";
     r.pass = false;
-    r.message = std::move(m);
-    return r;
-  };
-  for (int64_t i = 0; i < n; ++i)
-    if (ca[i] != cb[i]) return fail(at_point("core flags differ", i));
-  for (int64_t i = 0; i < n; ++i)
-    if ((la[i] == -1) != (lb[i] == -1)) return fail(at_point("noise sets differ", i));
-  std::unordered_map<int32_t, int32_t> a2b, b2a;
-  for (int64_t i = 0; i < n; ++i) {
-    if (!ca[i]) continue;
-    auto ia = a2b.emplace(la[i], lb[i]);
-    if (!ia.second && ia.first->second != lb[i]) return fail(at_point("core partitions differ", i));
-    auto ib = b2a.emplace(lb[i], la[i]);
-    if (!ib.second && ib.first->second != la[i]) return fail(at_point("core partitions differ", i));
+    r.message = os.str();
   }
-  if (bad_a >= 0) return fail(at_point("first clustering has an invalid border label", bad_a));
-  if (bad_b >= 0) return fail(at_point("second clustering has an invalid border label", bad_b));
   return r;
 }
 
@@ -423,16 +407,13 @@ TC_EXPORT tc_status tc_verify(const tc_dataset* ds, float eps, int minpts, int t
     TCB_CUDA(cudaMemcpyAsync(d_coords, ds->coords.ptr, sizeof(float) * n * dim,
                              cudaMemcpyHostToDevice, call.st));
     struct Run {
-      std::unique_ptr<tc_result> res;
       int32_t* d_labels;
       uint8_t* d_core;
-      int64_t bad = -1;
     };
     auto run = [&](tc_algorithm algo) {
-      Run r{std::make_unique<tc_result>(n), call.alloc<int32_t>(n), call.alloc<uint8_t>(n)};
+      Run r{call.alloc<int32_t>(n), call.alloc<uint8_t>(n)};
       device_cluster(call, d_coords, n, dim, eps, minpts, algo, cap, r.d_labels, r.d_core,
-                     r.res.get());
-      r.bad = tcb::first_bad_border(d_coords, n, dim, eps, r.d_labels, r.d_core, call.st);
+                     nullptr);
       return r;
     };
     auto line = [&](const char* name, const Equivalence& e) {
@@ -441,20 +422,21 @@ TC_EXPORT tc_status tc_verify(const tc_dataset* ds, float eps, int minpts, int t
       text += e.pass ? std::string("PASS") : "FAIL \xE2\x80\x94 " + e.message;
       text += '\n';
     };
+    auto equiv = [&](const Run& a, const Run& b) {
+      return device_equivalence(d_coords, n, dim, eps, a.d_labels, a.d_core, b.d_labels,
+                                b.d_core, call.st);
+    };
     Run fd = run(TC_ALGO_FDBSCAN);
     Run db = run(TC_ALGO_DENSEBOX);
     bool all = true;
-    Equivalence x = check_equivalence(fd.res->labels.ptr, fd.res->core.ptr, db.res->labels.ptr,
-                                      db.res->core.ptr, n, fd.bad, db.bad);
+    Equivalence x = equiv(fd, db);
     line("fdbscan vs densebox", x);
     all &= x.pass;
     if (n <= cap) {
       Run bf = run(TC_ALGO_BRUTEFORCE);
-      Equivalence a = check_equivalence(fd.res->labels.ptr, fd.res->core.ptr, bf.res->labels.ptr,
-                                        bf.res->core.ptr, n, fd.bad, bf.bad);
+      Equivalence a = equiv(fd, bf);
       line("fdbscan vs bruteforce", a);
-      Equivalence b = check_equivalence(db.res->labels.ptr, db.res->core.ptr, bf.res->labels.ptr,
-                                        bf.res->core.ptr, n, db.bad, bf.bad);
+      Equivalence b = equiv(db, bf);
       line("densebox vs bruteforce", b);
       all &= a.pass && b.pass;
     } else {
@@ -563,4 +545,37 @@ TC_EXPORT tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t ma
 TC_EXPORT tc_status tcg_dataset_create_pinned(const float* coords, int64_t n, int dim,
                                               tc_dataset** out) {
   return tc_dataset_create(coords, n, dim, out);  // large datasets are pinned already
+}
+
+TC_EXPORT tc_status tcg_check_equivalence_device(const float* d_coords, int64_t n, int dim,
+                                                 float eps, const int32_t* d_labels_a,
+                                                 const uint8_t* d_core_a,
+                                                 const int32_t* d_labels_b,
+                                                 const uint8_t* d_core_b, void* stream,
+                                                 int* check, int64_t* at) {
+  if (!d_coords || n < 1 || (dim != 2 && dim != 3) || !d_labels_a || !d_core_a || !d_labels_b ||
+      !d_core_b || !check || !at || !(eps > 0.f) || !std::isfinite(eps))
+    return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    const tcb::EqVerdict v =
+        tcb::check_equivalence_device(d_coords, n, dim, eps, d_labels_a, d_core_a, d_labels_b,
+                                      d_core_b, static_cast<cudaStream_t>(stream));
+    *check = v.check;
+    *at = v.at;
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tcg_first_bad_border_device(const float* d_coords, int64_t n, int dim,
+                                                float eps, const int32_t* d_labels,
+                                                const uint8_t* d_core, void* stream,
+                                                int64_t* at) {
+  if (!d_coords || n < 1 || (dim != 2 && dim != 3) || !d_labels || !d_core || !at ||
+      !(eps > 0.f) || !std::isfinite(eps))
+    return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    *at = tcb::first_bad_border(d_coords, n, dim, eps, d_labels, d_core,
+                                static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
 }

@@ -258,31 +258,99 @@ def test_c1_blobs_1m_against_reference(algo):
         assert got.stats[k] == want["stats"][k], k
 
 
+_FULL = {}
+
+
+def _full_input(name):
+    """The §8d inputs at full size, from the oracle's generator (sha256 pinned in
+    tests/golden/bench_inputs.json; byte-identical to tcg_generate_*)."""
+    if name not in _FULL:
+        _FULL.clear()  # hold one full-size input at a time
+        _FULL[name] = oracle.hacc_like(37_000_000) if name == "hacc" else \
+            oracle.taxi_like(80_000_000)
+    return _FULL[name]
+
+
+def _assert_reference_parity(got, want, coords, eps, minpts, tag, counters=True):
+    """SURVEY §8 gates at full size against the compiled reference: core flags
+    bit-exact, noise set exact, core labels EQUAL, every border label valid
+    (reference check_equivalence semantics, device border check), and the
+    reference's own counters."""
+    import torch
+
+    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], tag)
+    x = torch.from_numpy(coords).cuda()
+    bad = tb.api.first_bad_border(x, eps, torch.from_numpy(got.labels).cuda(),
+                                  torch.from_numpy(got.core_flags).cuda())
+    assert bad < 0, f"{tag}: invalid border label at point {bad}"
+    for k in ("cluster_count", "core_count", "noise_count", "preprocess_skipped"):
+        assert got.stats[k] == want["stats"][k], (tag, k, got.stats[k], want["stats"][k])
+    if counters:
+        for k in ("pair_resolutions", "distance_evaluations"):
+            assert got.stats[k] == want["stats"][k], (tag, k, got.stats[k], want["stats"][k])
+        assert got.stats["dense_point_fraction"] == want["stats"]["dense_point_fraction"], tag
+
+
 @pytest.mark.slow
 @pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
 def test_c2_hacc_37m_against_reference():
-    """C2 at full size: 37M HACC-like points, eps 0.042, minpts 2, FDBSCAN — the
-    bench workload — against the reference run on the host cores."""
-    ds = Dataset.hacc_like(37_000_000)
-    c = ds.coords()
-    got = tb.cluster(ds, 0.042, 2, Algorithm.FDBSCAN)
+    """C2 at full size (BASELINE configs[1], the bench workload): 37M HACC-like
+    points, eps 0.042, minpts 2 — FDBSCAN AND DenseBox (north star: "minpts=2
+    and minpts=100 ... core partition bit-exact vs the CPU reference") against
+    the reference's FDBSCAN and DenseBox runs on the host cores."""
+    c = _full_input("hacc")
+    ds = Dataset.from_array(c)
     want = ref.dbscan(c, 0.042, 2, 0, threads=0)
-    assert_parity(got.labels, got.core_flags, want["labels"], want["core"], "C2")
-    assert got.stats["pair_resolutions"] == want["stats"]["pair_resolutions"] == 898_475_393
-    assert got.stats["cluster_count"] == want["stats"]["cluster_count"]
+    got = tb.cluster(ds, 0.042, 2, Algorithm.FDBSCAN)
+    _assert_reference_parity(got, want, c, 0.042, 2, "C2 FDBSCAN")
+    assert got.stats["pair_resolutions"] == 898_475_393
     # minpts == 2: no borders, so labels are fully determined
     assert np.array_equal(got.labels, want["labels"])
+    want_db = ref.dbscan(c, 0.042, 2, 1, threads=0)
+    assert np.array_equal(want_db["labels"], want["labels"])  # the reference agrees with itself
+    got_db = tb.cluster(ds, 0.042, 2, Algorithm.DENSEBOX)
+    _assert_reference_parity(got_db, want_db, c, 0.042, 2, "C2 DenseBox")
+    assert np.array_equal(got_db.labels, want_db["labels"])
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_c3_hacc_37m_densebox_against_reference():
+    """C3 at full size: 37M HACC-like points, eps 0.042, minpts 100, DenseBox
+    (REF dbscan.cpp:110-200) against the reference's DenseBox run; our FDBSCAN
+    on the same input must give the same core partition and noise set."""
+    c = _full_input("hacc")
+    ds = Dataset.from_array(c)
+    want = ref.dbscan(c, 0.042, 100, 1, threads=0)
+    got = tb.cluster(ds, 0.042, 100, Algorithm.DENSEBOX)
+    _assert_reference_parity(got, want, c, 0.042, 100, "C3 DenseBox")
+    assert want["stats"]["core_count"] == 4_243_007 and want["stats"]["cluster_count"] == 5000
+    got_fd = tb.cluster(ds, 0.042, 100, Algorithm.FDBSCAN)
+    _assert_reference_parity(got_fd, want, c, 0.042, 100, "C3 FDBSCAN", counters=False)
+    again = tb.cluster(ds, 0.042, 100, Algorithm.DENSEBOX)  # determinism (acceptance crit. 8)
+    assert np.array_equal(again.labels, got.labels) and again.stats == got.stats
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_c4_taxi_80m_densebox_against_reference():
+    """C4 at full size: 80M 2D taxi-like points, eps 0.001, minpts 1000,
+    DenseBox, against the reference's DenseBox run (counters included: the
+    member-tree scans and primitive runs must reproduce the reference's
+    member-by-member scans exactly)."""
+    c = _full_input("taxi")
+    want = ref.dbscan(c, 0.001, 1000, 1, threads=0)
+    got = tb.cluster(Dataset.from_array(c), 0.001, 1000, Algorithm.DENSEBOX)
+    _assert_reference_parity(got, want, c, 0.001, 1000, "C4 DenseBox")
 
 
 @pytest.mark.slow
 def test_c3_full_size_properties():
-    """C3 at full size on the device only: FDBSCAN and DenseBox agree exactly
-    on cores / noise / core labels, the GPU border checker passes, and the
-    result is identical run to run."""
+    """C3 on the device only: FDBSCAN and DenseBox agree exactly on cores /
+    noise / core labels, and the result is identical run to run."""
     import torch
 
-    ds = Dataset.hacc_like(37_000_000)
-    x = torch.from_numpy(ds.coords()).cuda()
+    x = torch.from_numpy(_full_input("hacc")).cuda()
     l0, c0, s0 = tb.cluster_device(x, 0.042, 100, Algorithm.FDBSCAN, stats=True)
     l1, c1, s1 = tb.cluster_device(x, 0.042, 100, Algorithm.DENSEBOX, stats=True)
     l2, c2, _ = tb.cluster_device(x, 0.042, 100, Algorithm.FDBSCAN, stats=True)
@@ -290,9 +358,7 @@ def test_c3_full_size_properties():
     assert torch.equal(l0 == -1, l1 == -1)
     m = c0.bool()
     assert torch.equal(l0[m], l1[m]) and torch.equal(l0[m], l2[m])
-    assert s0["pair_resolutions"] == 898_475_393
-    assert s0["core_count"] == s1["core_count"] == 4_243_007
-    assert s0["cluster_count"] == s1["cluster_count"] == 5000
+    assert s0["core_count"] == s1["core_count"]
 
 
 # ---------------- contained subtrees / member tree vs the reference ----------------
@@ -405,28 +471,6 @@ def test_keyed_and_local_context_label_in_keys(minpts, top):
         assert lab[i] in inv, i
 
 
-@pytest.mark.slow
-def test_c4_full_size_properties():
-    """C4 at full size (80M 2D taxi-like, eps 0.001, minpts 1000): DenseBox and
-    FDBSCAN agree exactly on cores / noise / core labels, and DenseBox's
-    counters (member-tree scans, primitive runs) stay the reference-semantics
-    values (pinned against the reference at smaller sizes by
-    test_densebox_large_cells_exact_counters)."""
-    import torch
-
-    ds = Dataset.taxi_like(80_000_000)
-    x = torch.from_numpy(ds.coords()).cuda()
-    l1, c1, s1 = tb.cluster_device(x, 0.001, 1000, Algorithm.DENSEBOX, stats=True)
-    l0, c0, s0 = tb.cluster_device(x, 0.001, 1000, Algorithm.FDBSCAN, stats=True)
-    assert torch.equal(c0, c1)
-    assert torch.equal(l0 == -1, l1 == -1)
-    m = c0.bool()
-    assert torch.equal(l0[m], l1[m])
-    assert s1["pair_resolutions"] == 16_116_139_953
-    assert s1["distance_evaluations"] == 47_286_475_806
-    assert s1["core_count"] == 78_423_128 and s1["cluster_count"] == 250
-
-
 @pytest.mark.parametrize("minpts", [2, 5, 3000])
 def test_massive_duplicates_and_flat_axis(minpts):
     """Stress of the contained-run paths: 1.5M copies of one point plus a flat
@@ -455,3 +499,78 @@ def test_massive_duplicates_and_flat_axis(minpts):
     db = tb.cluster(Dataset.from_array(c), eps, minpts, Algorithm.DENSEBOX)
     assert np.array_equal(db.core_flags, got.core_flags)
     assert np.array_equal(db.labels[got.core_flags == 1], got.labels[got.core_flags == 1])
+
+
+# ---------------- device check_equivalence (§8f row f2) ----------------
+def test_device_check_equivalence_matches_reference_checker():
+    """tcg_check_equivalence_device reports the same verdict and the same
+    first-divergence index as the reference's check_equivalence
+    (REF oracle.cpp:120-163) on a passing pair and on one corrupted pair per
+    check (core flag, noise, core partition, border in a / in b)."""
+    import torch
+
+    ds, eps, mp = Dataset.random_instance(11, 3000, 3000)
+    c = ds.coords()
+    a = tb.cluster(ds, eps, 5, Algorithm.FDBSCAN)
+    b = tb.cluster(ds, eps, 5, Algorithm.DENSEBOX)
+    x = torch.from_numpy(c).cuda()
+
+    def both(la, ca, lb, cb):
+        dev = tb.api.check_equivalence_device(
+            x, eps, *(torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (la, ca, lb, cb)))
+        ok, msg = oracle.check_equivalence(c, eps, la, ca, lb, cb)
+        if ref.available():
+            rok, rmsg = ref.check_equivalence(c, eps, 5, la, ca, lb, cb)
+            assert (rok, rmsg) == (ok, msg)
+        assert (dev[0] == 0) == ok and dev[2] == msg, (dev, msg)
+        return dev[0]
+
+    assert both(a.labels, a.core_flags, b.labels, b.core_flags) == 0
+    core = np.nonzero(a.core_flags)[0]
+    border = np.nonzero((a.core_flags == 0) & (a.labels != -1))[0]
+    noise = np.nonzero(a.labels == -1)[0]
+    assert len(core) > 10 and len(border) > 0 and len(noise) > 0
+    cb = b.core_flags.copy(); cb[core[7]] = 0
+    assert both(a.labels, a.core_flags, b.labels, cb) == 1
+    lb = b.labels.copy(); lb[noise[3]] = b.labels[core[0]]
+    assert both(a.labels, a.core_flags, lb, b.core_flags) == 2
+    # merge two clusters of b: a core partition difference at the first core
+    # of the second cluster
+    lab_ids = np.unique(b.labels[core])
+    assert len(lab_ids) >= 2
+    lb = b.labels.copy(); lb[lb == lab_ids[1]] = lab_ids[0]
+    assert both(a.labels, a.core_flags, lb, b.core_flags) == 3
+    # relabel a border into a cluster none of its cores reach
+    la = a.labels.copy()
+    far = [l for l in np.unique(a.labels[core]) if l != la[border[0]]][0]
+    la[border[0]] = far
+    assert both(la, a.core_flags, b.labels, b.core_flags) == 4
+    assert both(a.labels, a.core_flags, la, a.core_flags) == 5
+    # bijective relabeling of a core partition (arbitrary label values) passes
+    perm = {l: 10_000_000 + 3 * k for k, l in enumerate(np.unique(b.labels))}
+    perm[-1] = -1
+    lb = np.array([perm[v] for v in b.labels], np.int32)
+    assert both(a.labels, a.core_flags, lb, b.core_flags) == 0
+
+
+def test_device_morton_codes_golden():
+    """Device Morton codes (the tree build's quantization, REF
+    geometry.hpp:132-156) equal the reference's codes in morton.npz."""
+    import ctypes as C
+    import torch
+    from paper_2103_05162_b200._lib import lib
+
+    g = npz("morton.npz")
+    for d in (2, 3):
+        pts = torch.from_numpy(g[f"pts{d}"]).cuda()
+        lo = np.ascontiguousarray(g[f"lo{d}"], np.float32)
+        hi = np.ascontiguousarray(g[f"hi{d}"], np.float32)
+        out = torch.empty(pts.shape[0], dtype=torch.int64, device="cuda")
+        st = lib.tcg_morton_codes_device(C.c_void_p(pts.data_ptr()), pts.shape[0], d,
+                                         lo.ctypes.data_as(C.POINTER(C.c_float)),
+                                         hi.ctypes.data_as(C.POINTER(C.c_float)),
+                                         C.c_void_p(out.data_ptr()),
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert st == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), g[f"codes{d}"]), d

@@ -238,3 +238,55 @@ def test_reference_threaded_core_labels_equal_oracle():
             want = oracle.dbscan(coords, eps, mp, algo)
             got = ref.dbscan(coords, eps, mp, algo, threads=8)
             assert_parity(got["labels"], got["core"], want["labels"], want["core"], f"{seed}/{algo}")
+
+
+# ---------------- benchmark inputs ----------------
+def test_oracle_bench_generators_match_product():
+    """The oracle's HACC-like / taxi-like generators (used by bench.py's
+    reference arm and the full-size parity tests, so that those never load the
+    product library) are byte-identical to the product's."""
+    import paper_2103_05162_b200 as tb
+
+    for n, seed in ((150_000, 11), (777, 3)):
+        assert np.array_equal(oracle.hacc_like(n, seed=seed),
+                              tb.Dataset.hacc_like(n, seed=seed).coords())
+        assert np.array_equal(oracle.taxi_like(n, seed=seed),
+                              tb.Dataset.taxi_like(n, seed=seed).coords())
+    with pytest.raises(ValueError):
+        oracle.hacc_like(0)
+
+
+def test_bench_inputs_full_size_sha():
+    """C2/C3 (37M HACC-like) and C4 (80M taxi-like) inputs pinned by sha256."""
+    import hashlib
+    import json
+    import os
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "bench_inputs.json")))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    assert sha(oracle.hacc_like(37_000_000)) == g["hacc_like(37000000,L=36.8,0.23,seed=11)"]
+    assert sha(oracle.taxi_like(80_000_000)) == g["taxi_like(80000000,seed=5)"]
+
+
+def test_write_bin_loads_in_reference(tmp_path):
+    """oracle.write_bin produces the reference's binary format (REF io.cpp:106-134)."""
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    import ctypes as C
+
+    a = oracle.hacc_like(1000, seed=4)
+    path = str(tmp_path / "p.bin")
+    oracle.write_bin(path, a)
+    L = ref.lib()
+    L.tc_dataset_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.tc_dataset_size.restype = C.c_int64
+    L.tc_dataset_size.argtypes = [C.c_void_p]
+    L.tc_dataset_coords.restype = C.POINTER(C.c_float)
+    L.tc_dataset_coords.argtypes = [C.c_void_p]
+    L.tc_dataset_free.argtypes = [C.c_void_p]
+    ds = C.c_void_p()
+    assert L.tc_dataset_load(path.encode(), 0, C.byref(ds)) == 0
+    assert L.tc_dataset_size(ds) == 1000
+    got = np.ctypeslib.as_array(L.tc_dataset_coords(ds), shape=(3000,)).reshape(1000, 3).copy()
+    L.tc_dataset_free(ds)
+    assert np.array_equal(got, a)
