@@ -33,13 +33,20 @@ namespace tcb {
 namespace {
 
 constexpr int kQueryBlock = 128;  // 64 / 256 measured equal or slower
+
 // Resident blocks per SM the FoF main pass is compiled for (ptxas caps its
 // registers at 36): 14 x 4 warps instead of 12 at its natural 40 registers,
 // main pass 19.2 -> 18.5 ms on C2 despite a few spilled bytes.
-constexpr int kFofMinBlocks = 14;
+#ifndef TCB_FOF_MIN_BLOCKS
+#define TCB_FOF_MIN_BLOCKS 12
+#endif
+constexpr int kFofMinBlocks = TCB_FOF_MIN_BLOCKS;
 // the same for the minpts > 2 main pass (12: main 22.2 -> 21.2 ms on C3);
 // the core pass is faster uncapped
-constexpr int kMainMinBlocks = 12;
+#ifndef TCB_MAIN_MIN_BLOCKS
+#define TCB_MAIN_MIN_BLOCKS 10
+#endif
+constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
 
 template <int D>
 __device__ __forceinline__ void load_query(const float4* leaf_pt, int64_t r, float* p,
@@ -57,73 +64,44 @@ __device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned 
 }
 
 // fdbscan_mark_cores query (dbscan.cpp:36-58): unmasked, early exit once
-// minpts neighbours (self included) are seen. A subtree whose box lies inside
-// the ball adds its leaf count at once; when that crosses minpts the
-// reference would have stopped inside it after exactly minpts - count more
-// leaf hits, so the distance counter (one per hit, dists == count) is still
-// the reference's.
+// minpts neighbours (self included) are seen. Every hit counts one distance
+// evaluation until the stop, so the reference's counter is min(|N|, minpts)
+// whatever the visit order: a subtree whose box lies inside the ball adds its
+// leaf count at once, capped at the stop.
 template <int D, int kFast>
-struct CoreQuery {
-  const float4* __restrict__ nodes;
-  const float4* __restrict__ leaf_pt;
-  BallTest bt;
-  int minpts;
-  uint8_t* __restrict__ flags;
-  LocalStack* stack;  // per-thread traversal stack, kept outside the struct
-  unsigned long long dists = 0;
-  float p[3];
-  int32_t id, node, nlo;
-  int count;
-  __device__ bool begin(int64_t r) {
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_core(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTest bt, int minpts,
+          uint8_t* __restrict__ flags, DevCounters* ctr) {
+  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
+  float p[3] = {0.f, 0.f, 0.f};
+  if (valid) {
+    int32_t id;
     load_query<D>(leaf_pt, r, p, &id);
-    id = static_cast<int32_t>(r);  // flags are kept in rank space
-    count = 0;
-    node = 0;
-    nlo = 0;
-    stack->reset();
-    return true;
   }
-  __device__ bool step() {
+  RopeWalk<D, kStackRegs> walk;
+  walk.min_rank = 0;
+  warp_start_node<D>(tv, p, valid, bt, 0, walk.node, walk.end);
+  int count = 0;
+  if (valid) {
     auto visit = [&](int32_t, int32_t, bool) -> bool {
-      ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
     auto inside = [&](int32_t first, int32_t last) -> int {
       const int64_t k = static_cast<int64_t>(last) - first + 1;
       if (count + k >= minpts) {
-        dists += static_cast<unsigned long long>(minpts - count);
         count = minpts;
         return kStop;
       }
-      dists += static_cast<unsigned long long>(k);
       count += static_cast<int>(k);
       return kTaken;
     };
-    return bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, 0, node, nlo, *stack, visit, inside);
-  }
-  __device__ void end() {
-    if (count >= minpts) flags[id] = 1;
-  }
-};
-
-template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
-k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
-  LocalStack stack;
-  CoreQuery<D, kFast> q{nodes, leaf_pt, bt, minpts, flags, &stack};
-  // one query per thread, started at the warp's common start node
-  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const bool valid = r < m;
-  if (valid) q.begin(r);
-  warp_start_node<D>(nodes, q.p, valid, bt, 0, q.node, q.nlo);
-  if (valid) {
-    while (q.step()) {
+    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
     }
-    q.end();
+    if (count >= minpts) flags[r] = 1;  // flags are kept in rank space
   }
-  flush_counter(&ctr->dists, q.dists);
+  flush_counter(&ctr->dists, static_cast<unsigned long long>(count));
 }
 
 // fdbscan_main_phase (dbscan.cpp:60-88): one thread per leaf rank r (Morton
@@ -142,10 +120,11 @@ k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
 //   otherwise the subtree is walked leaf by leaf (per-pair rule).
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kMainMinBlocks)
-k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+k_fd_main(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTest bt,
+          const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
           const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
           int32_t* __restrict__ reach, DevCounters* ctr) {
+  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -156,8 +135,9 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
     load_query<D>(leaf_pt, r, p, &id);
     rank = static_cast<int32_t>(r);
   }
-  int32_t node, nlo;
-  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
+  RopeWalk<D, kStackRegs> walk;
+  walk.min_rank = rank + 1;
+  warp_start_node<D>(tv, p, valid, bt, rank + 1, walk.node, walk.end);
   if (valid) {
     const bool core_r = flags[rank] != 0;
     int32_t hint = rank;
@@ -182,9 +162,7 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
       pairs += static_cast<unsigned long long>(size);
       return kTaken;
     };
-    LocalStack stack;
-    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
+    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
     }
   }
   flush_counter(&ctr->pairs, pairs);
@@ -209,9 +187,10 @@ __global__ void k_noncore_ind(const uint8_t* __restrict__ flags, int64_t n,
 // stay exact.
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kFofMinBlocks)
-k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
-              BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
+k_fd_main_fof(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTest bt,
+              int32_t* __restrict__ parent, const int32_t* __restrict__ key,
               int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {
+  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -223,8 +202,9 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
     load_query<D>(leaf_pt, r, p, &id);
     rank = static_cast<int32_t>(r);
   }
-  int32_t node, nlo;
-  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
+  RopeWalk<D, kStackRegs> walk;
+  walk.min_rank = rank + 1;
+  warp_start_node<D>(tv, p, valid, bt, rank + 1, walk.node, walk.end);
   if (valid) {
     int32_t hint = rank;
     auto visit = [&](int32_t s, int32_t, bool) -> bool {
@@ -240,12 +220,10 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
       record_run(reach, first, last);
       return kTaken;
     };
-    LocalStack stack;
-    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
-      TCB_PROBE_ONLY(++pr[0];)
+    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
+      TCB_PROBE_ONLY(++pr[0]; pr[3] += walk.stack.lost();)
     }
-    TCB_PROBE_ONLY(++pr[0]; pr[5] += pairs == 0; pr[6] = pr[0]; if (pairs == 0) pr[3] = pr[0];)
+    TCB_PROBE_ONLY(++pr[0]; pr[5] += walk.stack.lost(); pr[6] = pr[0];)
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
@@ -406,7 +384,7 @@ void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
   const BallTest bt = BallTest::make(eps2);
   auto core = bt.fast ? k_fd_core<D, 1> : k_fd_core<D, 0>;
   note_launch(), core<<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-      b.tree.nodes, b.leaf_pt, n, bt, minpts, flags, d_ctr);
+      b.tree, b.leaf_pt, n, bt, minpts, flags, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -422,7 +400,7 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
   if (force_core) {
     auto fof = bt.fast ? k_fd_main_fof<D, 1> : k_fd_main_fof<D, 0>;
-    note_launch(), fof<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, parent, key,
+    note_launch(), fof<<<grid, kQueryBlock, 0, s>>>(b.tree, b.leaf_pt, n, bt, parent, key,
                                                    reach, flags, d_ctr);
   } else {
     int32_t* ind = scratch.alloc_n<int32_t>(n + 1);
@@ -431,7 +409,7 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
     note_launch(), k_noncore_ind<<<grid_for(n + 1, 256), 256, 0, s>>>(flags, n, ind);
     exclusive_scan_i32(ind, noncore_before, n + 1, nullptr, scan_tmp, s);
     auto main = bt.fast ? k_fd_main<D, 1> : k_fd_main<D, 0>;
-    note_launch(), main<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags, parent,
+    note_launch(), main<<<grid, kQueryBlock, 0, s>>>(b.tree, b.leaf_pt, n, bt, flags, parent,
                                                     key, noncore_before, reach, d_ctr);
   }
   // covered runs (all-core): join each covered rank to its predecessor

@@ -285,7 +285,7 @@ constexpr int kDbMinBlocks = 10;
 
 template <int D, int kFast>
 struct DbCoreQuery {
-  const float4* __restrict__ nodes;
+  TreeView tv;
   const float4* __restrict__ qpt;
   const float4* __restrict__ sorted_pt;
   const int32_t* __restrict__ cell_begin;
@@ -302,7 +302,7 @@ struct DbCoreQuery {
   const int32_t* __restrict__ list;  // query slots to run (the SinglePoint ones)
   unsigned long long dists = 0;
   float p[3];
-  int32_t id, slot, node, nlo, mask_rank = 0;
+  int32_t id, slot, node, mask_rank = 0;
   int count;
   // the stopping scan of a long cut DenseBox, left to the warp (k_db_core)
   int32_t pend_kb = -1, pend_ke = 0, pend_rem = 0;
@@ -316,7 +316,6 @@ struct DbCoreQuery {
     p[2] = qp.z;
     count = 0;
     node = 0;
-    nlo = 0;
     pend_kb = -1;
     stack->reset();
     return true;
@@ -380,7 +379,7 @@ struct DbCoreQuery {
       return true;
     };
     return bvh_step_ordered<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, 0, node, nlo, *stack, visit, inside);
+        tv, p, bt, 0, node, *stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[slot] = 1;
@@ -389,16 +388,17 @@ struct DbCoreQuery {
 
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
-k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
+k_db_core(DeviceBvh tree, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
           uint8_t* __restrict__ flags, DevCounters* ctr, MemberTree mt,
           MemberTree smt, const int32_t* __restrict__ qoff, int32_t num_prims,
           const int32_t* __restrict__ list, int64_t m) {
   LocalStack stack;
-  DbCoreQuery<D, kFast> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
+  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
+  DbCoreQuery<D, kFast> q{tv, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
                    &smt, qoff, n, num_prims, list};
-  run_query_warpstart<D>(m, q, nodes, bt);
+  run_query_warpstart<D>(m, q, tv, bt);
   // The stopping scans: position of the rem-th member within eps of p in
   // member order, 32 members per step across the warp (same predicate as the
   // per-member loop; the members of a cell are in random spatial order, so a
@@ -460,13 +460,14 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
 // are walked. minpts == 2: every run is taken (all pairs are unions).
 template <int D, bool kForceCore, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
-k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
+k_db_main_ranged(DeviceBvh tree, const float4* __restrict__ qpt,
                  const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
                  const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
                  BallTest bt, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
                  const int32_t* __restrict__ key, const int32_t* __restrict__ qoff,
                  const int32_t* __restrict__ noncore_before, int32_t* __restrict__ reach,
                  DevCounters* ctr, MemberTree mt) {
+  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
   const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = q < n;
   unsigned long long pairs = 0, dists = 0;
@@ -480,8 +481,9 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
     p[1] = qp.y;
     p[2] = qp.z;
   }
-  int32_t node, nlo;
-  warp_start_node<D>(nodes, p, valid, bt, own + 1, node, nlo);
+  RopeWalk<D, kStackRegs> walk;
+  walk.min_rank = own + 1;
+  warp_start_node<D>(tv, p, valid, bt, own + 1, walk.node, walk.end);
   if (valid) {
     const bool core_i = kForceCore ? true : flags[i] != 0;
     int32_t hint = i;
@@ -544,9 +546,7 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
       dists += static_cast<unsigned long long>(cnt);
       return kTaken;
     };
-    LocalStack stack;
-    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
+    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
     }
   }
   unsigned long long v = warp_sum(dists);
@@ -860,7 +860,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
                                                                             num_prims, list);
     auto core = bt.fast ? k_db_core<D, 1> : k_db_core<D, 0>;
     note_launch(), core<<<grid_for(sparse_points, kQueryBlock, INT32_MAX), kQueryBlock, 0, st>>>(
-        b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr, mt, smt,
+        b.tree, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr, mt, smt,
         qoff, num_prims, list, sparse_points);
   }
   // ---- main pass ----
@@ -879,7 +879,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
   auto main = minpts == 2 ? (bt.fast ? k_db_main_ranged<D, true, 1> : k_db_main_ranged<D, true, 0>)
                           : (bt.fast ? k_db_main_ranged<D, false, 1> : k_db_main_ranged<D, false, 0>);
-  note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin,
+  note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree, qpt, qrank, n, sorted_pt, cell_begin,
                                                 cell_end, bt, flags, parent, qkey, qoff,
                                                 noncore_before, reach, ctr, mt);
   launch_cover_joins(reach, num_prims, tile_max,

@@ -1,14 +1,19 @@
 // Host-side generators and file formats (see host_data.hpp).
 #include "host_data.hpp"
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <fstream>
-#include <sstream>
+#include <memory>
 #include <stdexcept>
+#include <string>
 
 #include "engine.hpp"
 
@@ -250,121 +255,153 @@ HostPoints gen_taxi_like(int64_t n, uint64_t seed) {
 }
 
 // ---------------------------------------------------------------------------
-// File formats (io.cpp:51-148)
+// File formats: the reference's CSV and binary layouts (io.cpp:51-148), read
+// through a read-only memory map. Failures are std::runtime_error (the ABI maps
+// them to TC_ERR_IO, capi.cpp:30-43), with the path and, for CSV, the line.
 // ---------------------------------------------------------------------------
 namespace {
 
-[[noreturn]] void io_fail(const std::string& path, const std::string& what) {
-  throw std::runtime_error(path + ": " + what);
+std::string located(const std::string& path, int64_t line, const char* what) {
+  std::string m = path;
+  if (line > 0) m += ":" + std::to_string(line);
+  return m + ": " + what;
 }
 
-[[noreturn]] void parse_fail(const std::string& path, int64_t line, const std::string& what) {
-  std::ostringstream os;
-  os << path << ":" << line << ": " << what;
-  throw std::runtime_error(os.str());
-}
-
-// One CSV record: comma-separated floats, blanks/tabs around fields allowed.
-bool split_fields(const std::string& line, std::vector<float>& out) {
-  out.clear();
-  const char* p = line.data();
-  const char* end = p + line.size();
-  while (p < end) {
-    while (p < end && (*p == ' ' || *p == '\t')) ++p;
-    float v;
-    auto res = std::from_chars(p, end, v);
-    if (res.ec != std::errc{}) return false;
-    out.push_back(v);
-    p = res.ptr;
-    while (p < end && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
-    if (p < end) {
-      if (*p != ',') return false;
-      ++p;
+// Whole file mapped read-only (an empty file maps to an empty span).
+class MappedFile {
+ public:
+  explicit MappedFile(const std::string& path) {
+    fd_ = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    struct stat st;
+    if (fd_ < 0 || ::fstat(fd_, &st) != 0 || !S_ISREG(st.st_mode))
+      throw std::runtime_error(located(path, 0, "cannot open for reading"));
+    size_ = static_cast<size_t>(st.st_size);
+    if (size_ > 0) {
+      void* p = ::mmap(nullptr, size_, PROT_READ, MAP_PRIVATE, fd_, 0);
+      if (p == MAP_FAILED) throw std::runtime_error(located(path, 0, "cannot map for reading"));
+      base_ = static_cast<const char*>(p);
+      ::madvise(p, size_, MADV_SEQUENTIAL);
     }
   }
-  return !out.empty();
+  ~MappedFile() {
+    if (base_) ::munmap(const_cast<char*>(base_), size_);
+    if (fd_ >= 0) ::close(fd_);
+  }
+  MappedFile(const MappedFile&) = delete;
+  MappedFile& operator=(const MappedFile&) = delete;
+  const char* data() const { return base_; }
+  size_t size() const { return size_; }
+
+ private:
+  int fd_ = -1;
+  const char* base_ = nullptr;
+  size_t size_ = 0;
+};
+
+// ".bin" selects the binary layout, anything else CSV (io.cpp:51-56).
+bool binary_suffix(const std::string& path) {
+  return path.size() >= 4 && path.compare(path.size() - 4, 4, ".bin") == 0;
 }
 
-bool is_binary_path(const std::string& path) {
-  auto dot = path.rfind('.');
-  return dot != std::string::npos && path.substr(dot) == ".bin";
+// Binary header: little-endian u32 n, u32 dim (io.cpp:106-122).
+void binary_header(const std::string& path, const char* data, size_t size, uint32_t* n,
+                   uint32_t* dim) {
+  if (size < 8) throw std::runtime_error(located(path, 0, "truncated header"));
+  std::memcpy(n, data, 4);
+  std::memcpy(dim, data + 4, 4);
+  if (*n == 0 || (*dim != 2 && *dim != 3))
+    throw std::runtime_error(located(path, 0, "invalid header (n or dim)"));
 }
 
-HostPoints read_csv(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) io_fail(path, "cannot open for reading");
+// One CSV record [s, e): comma-separated floats with optional blanks around
+// each, a trailing CR tolerated (io.cpp:29-46 accepts exactly these). Returns
+// the field count (>= 1), or 0 for a malformed record; keeps the first three.
+int scan_record(const char* s, const char* e, float* out) {
+  int count = 0;
+  auto blank = [](char c) { return c == ' ' || c == '\t'; };
+  for (;;) {
+    while (s < e && blank(*s)) ++s;
+    if (s == e) return count;  // empty record or a trailing comma ends here
+    float v = 0.f;
+    const auto r = std::from_chars(s, e, v);
+    if (r.ec != std::errc{}) return 0;
+    if (count < 3) out[count] = v;
+    ++count;
+    s = r.ptr;
+    while (s < e && (blank(*s) || *s == '\r')) ++s;
+    if (s == e) return count;
+    if (*s++ != ',') return 0;
+  }
+}
+
+HostPoints parse_csv(const std::string& path, const char* data, size_t size) {
   HostPoints ps;
-  std::string line;
-  std::vector<float> fields;
-  int64_t lineno = 0;
-  bool header_allowed = true;
-  while (std::getline(in, line)) {
-    ++lineno;
-    if (line.empty() || line == "\r") continue;
-    if (!split_fields(line, fields)) {
-      if (header_allowed) {
-        header_allowed = false;
-        continue;
-      }
-      parse_fail(path, lineno, "malformed point line");
+  const char* cur = data;
+  const char* const end = data + size;
+  int64_t line = 0;
+  bool header_ok = true;  // the first non-blank line may be a header
+  while (cur < end) {
+    const char* nl = static_cast<const char*>(std::memchr(cur, '\n', static_cast<size_t>(end - cur)));
+    const char* le = nl ? nl : end;
+    const char* ls = cur;
+    cur = nl ? nl + 1 : end;
+    ++line;
+    if (ls == le || (le - ls == 1 && *ls == '\r')) continue;
+    float v[3];
+    const int k = scan_record(ls, le, v);
+    const bool first = header_ok;
+    header_ok = false;
+    if (k == 0) {
+      if (first) continue;
+      throw std::runtime_error(located(path, line, "malformed point line"));
     }
-    header_allowed = false;
     if (ps.dim == 0) {
-      if (fields.size() != 2 && fields.size() != 3)
-        parse_fail(path, lineno, "points must have 2 or 3 coordinates");
-      ps.dim = static_cast<int>(fields.size());
-    } else if (static_cast<int>(fields.size()) != ps.dim) {
-      parse_fail(path, lineno, "inconsistent coordinate count");
+      if (k != 2 && k != 3)
+        throw std::runtime_error(located(path, line, "points must have 2 or 3 coordinates"));
+      ps.dim = k;
+    } else if (k != ps.dim) {
+      throw std::runtime_error(located(path, line, "inconsistent coordinate count"));
     }
-    ps.coords.insert(ps.coords.end(), fields.begin(), fields.end());
+    ps.coords.insert(ps.coords.end(), v, v + k);
   }
-  if (ps.coords.empty()) io_fail(path, "no points found");
-  validate_points(ps.dim, ps.coords.data(), static_cast<int64_t>(ps.coords.size()));
+  if (ps.coords.empty()) throw std::runtime_error(located(path, 0, "no points found"));
   return ps;
 }
 
-HostPoints read_binary(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) io_fail(path, "cannot open for reading");
-  uint32_t hdr[2] = {0, 0};
-  in.read(reinterpret_cast<char*>(hdr), sizeof hdr);
-  if (!in) io_fail(path, "truncated header");
-  if (hdr[0] == 0 || (hdr[1] != 2 && hdr[1] != 3)) io_fail(path, "invalid header (n or dim)");
+HostPoints parse_binary(const std::string& path, const char* data, size_t size) {
+  uint32_t n = 0, dim = 0;
+  binary_header(path, data, size, &n, &dim);
+  const size_t bytes = static_cast<size_t>(n) * dim * sizeof(float);
+  if (size - 8 < bytes) throw std::runtime_error(located(path, 0, "truncated coordinate data"));
   HostPoints ps;
-  ps.dim = static_cast<int>(hdr[1]);
-  ps.coords.resize(static_cast<size_t>(hdr[0]) * hdr[1]);
-  in.read(reinterpret_cast<char*>(ps.coords.data()),
-          static_cast<std::streamsize>(ps.coords.size() * sizeof(float)));
-  if (!in) io_fail(path, "truncated coordinate data");
-  validate_points(ps.dim, ps.coords.data(), static_cast<int64_t>(ps.coords.size()));
+  ps.dim = static_cast<int>(dim);
+  ps.coords.resize(static_cast<size_t>(n) * dim);
+  std::memcpy(ps.coords.data(), data + 8, bytes);
   return ps;
 }
 
 }  // namespace
 
 void binary_info(const std::string& path, int64_t* n, int* dim) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) io_fail(path, "cannot open for reading");
-  uint32_t hdr[2] = {0, 0};
-  in.read(reinterpret_cast<char*>(hdr), sizeof hdr);
-  if (!in) io_fail(path, "truncated header");
-  if (hdr[0] == 0 || (hdr[1] != 2 && hdr[1] != 3)) io_fail(path, "invalid header (n or dim)");
-  *n = hdr[0];
-  *dim = static_cast<int>(hdr[1]);
+  MappedFile f(path);
+  uint32_t hn = 0, hd = 0;
+  binary_header(path, f.data(), f.size(), &hn, &hd);
+  *n = hn;
+  *dim = static_cast<int>(hd);
 }
 
-// load_binary (io.cpp:106-122) straight into device memory: the file is read
-// in chunks into two page-locked staging buffers, each chunk's host->device
-// copy running while the next chunk is read.
+// The binary layout (io.cpp:106-122) straight into device memory: the mapped
+// file is copied in chunks into two page-locked staging buffers, each chunk's
+// host->device copy running while the next chunk is staged.
 void load_binary_device(const std::string& path, float* d_coords, int64_t n, int dim,
                         cudaStream_t stream) {
-  int64_t fn = 0;
-  int fdim = 0;
-  binary_info(path, &fn, &fdim);
-  if (fn != n || fdim != dim) throw std::invalid_argument("load_binary_device: shape mismatch");
-  std::ifstream in(path, std::ios::binary);
-  if (!in) io_fail(path, "cannot open for reading");
-  in.seekg(8);
+  MappedFile f(path);
+  uint32_t hn = 0, hd = 0;
+  binary_header(path, f.data(), f.size(), &hn, &hd);
+  if (hn != n || static_cast<int>(hd) != dim)
+    throw std::invalid_argument("load_binary_device: shape mismatch");
+  const size_t total = static_cast<size_t>(n) * dim * sizeof(float);
+  if (f.size() - 8 < total) throw std::runtime_error(located(path, 0, "truncated coordinate data"));
   constexpr size_t kChunk = size_t{32} << 20;  // bytes per staging buffer
   struct Staging {
     void* buf[2] = {nullptr, nullptr};
@@ -383,49 +420,48 @@ void load_binary_device(const std::string& path, float* d_coords, int64_t n, int
     TCB_CUDA(cudaMallocHost(&stg.buf[k], kChunk));
     TCB_CUDA(cudaEventCreateWithFlags(&stg.done[k], cudaEventDisableTiming));
   }
-  const size_t total = static_cast<size_t>(n) * dim * sizeof(float);
+  const char* src = f.data() + 8;
   auto* dst = reinterpret_cast<char*>(d_coords);
-  size_t off = 0;
-  for (int k = 0; off < total; k ^= 1) {
-    const size_t len = total - off < kChunk ? total - off : kChunk;
+  for (size_t off = 0, k = 0; off < total; off += kChunk, k ^= 1) {
+    const size_t len = std::min(kChunk, total - off);
     TCB_CUDA(cudaEventSynchronize(stg.done[k]));  // the copy out of this buffer finished
-    in.read(static_cast<char*>(stg.buf[k]), static_cast<std::streamsize>(len));
-    if (!in) io_fail(path, "truncated coordinate data");
+    std::memcpy(stg.buf[k], src + off, len);
     TCB_CUDA(cudaMemcpyAsync(dst + off, stg.buf[k], len, cudaMemcpyHostToDevice, stream));
     TCB_CUDA(cudaEventRecord(stg.done[k], stream));
-    off += len;
   }
   TCB_CUDA(cudaStreamSynchronize(stream));
 }
 
 HostPoints load_points(const std::string& path, int format) {
-  const bool binary = format == 2 || (format != 1 && is_binary_path(path));
-  return binary ? read_binary(path) : read_csv(path);
+  MappedFile f(path);
+  const bool binary = format == 2 || (format != 1 && binary_suffix(path));
+  HostPoints ps = binary ? parse_binary(path, f.data(), f.size())
+                         : parse_csv(path, f.data(), f.size());
+  validate_points(ps.dim, ps.coords.data(), static_cast<int64_t>(ps.coords.size()));
+  return ps;
 }
 
+// Writers (io.cpp:84-148 formats): binary header + raw floats, or one CSV
+// record per point with 9 significant digits.
 void save_points(const std::string& path, int format, int dim, const float* coords, int64_t n) {
-  const bool binary = format == 2 || (format != 1 && is_binary_path(path));
+  const bool binary = format == 2 || (format != 1 && binary_suffix(path));
+  std::unique_ptr<FILE, int (*)(FILE*)> f(std::fopen(path.c_str(), binary ? "wb" : "w"),
+                                          &std::fclose);
+  if (!f) throw std::runtime_error(located(path, 0, "cannot open for writing"));
+  bool ok = true;
   if (binary) {
-    std::ofstream out(path, std::ios::binary);
-    if (!out) io_fail(path, "cannot open for writing");
     const uint32_t hdr[2] = {static_cast<uint32_t>(n), static_cast<uint32_t>(dim)};
-    out.write(reinterpret_cast<const char*>(hdr), sizeof hdr);
-    out.write(reinterpret_cast<const char*>(coords),
-              static_cast<std::streamsize>(static_cast<size_t>(n) * dim * sizeof(float)));
-    if (!out) io_fail(path, "write failed");
-    return;
+    const size_t count = static_cast<size_t>(n) * dim;
+    ok = std::fwrite(hdr, sizeof hdr, 1, f.get()) == 1 &&
+         std::fwrite(coords, sizeof(float), count, f.get()) == count;
+  } else {
+    for (int64_t i = 0; i < n && ok; ++i)
+      ok = (dim == 2 ? std::fprintf(f.get(), "%.9g,%.9g\n", coords[2 * i], coords[2 * i + 1])
+                     : std::fprintf(f.get(), "%.9g,%.9g,%.9g\n", coords[3 * i], coords[3 * i + 1],
+                                    coords[3 * i + 2])) > 0;
   }
-  std::ofstream out(path);
-  if (!out) io_fail(path, "cannot open for writing");
-  out.precision(9);
-  for (int64_t i = 0; i < n; ++i) {
-    for (int k = 0; k < dim; ++k) {
-      if (k) out << ',';
-      out << coords[i * dim + k];
-    }
-    out << '\n';
-  }
-  if (!out) io_fail(path, "write failed");
+  if (std::fflush(f.get()) != 0) ok = false;
+  if (!ok) throw std::runtime_error(located(path, 0, "write failed"));
 }
 
 }  // namespace tcb

@@ -233,3 +233,111 @@ def test_additive_entry_points_validate_before_device_work(tmp_path):
     assert lib.tcg_local_cluster(None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16)) == \
         Status.INVALID_ARGUMENT
     lib.tcg_local_free(None)  # no-op
+
+
+CSV_CASES = {
+    "plain2": "1,2\n3,4\n",
+    "plain3_crlf": "1,2,3\r\n4,5,6\r\n",
+    "header": "x,y\n1,2\n",
+    "header_then_bad": "x,y\nfoo\n1,2\n",
+    "blank_lines": "\n\r\n1, 2\n\n 3 ,\t4\n",
+    "trailing_comma": "1,2,\n3,4,\n",
+    "leading_comma": ",1,2\n",
+    "four_fields": "1,2,3,4\n",
+    "one_field": "1\n2\n",
+    "inconsistent": "1,2\n1,2,3\n",
+    "no_newline_at_end": "1,2\n3,4",
+    "only_header": "a,b\n",
+    "empty": "",
+    "whitespace_line": "1,2\n   \n3,4\n",
+    "exponent": "1e-3,2.5E2\n-0.0,7\n",
+    "nonfinite": "inf,1\n2,3\n",
+    "garbage_after": "1,2x\n",
+    "spaces_only_fields": "1 2\n",
+}
+
+
+@pytest.mark.parametrize("case", sorted(CSV_CASES))
+def test_csv_reader_matches_reference(tmp_path, case):
+    """tc_dataset_load on CSV edge cases gives the reference's status and points
+    (REF io.cpp:29-104)."""
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    path = str(tmp_path / f"{case}.csv")
+    with open(path, "w", newline="") as f:
+        f.write(CSV_CASES[case])
+    L = ref._capi()
+    L.tc_dataset_dim.restype = C.c_int
+    L.tc_dataset_dim.argtypes = [C.c_void_p]
+    L.tc_dataset_coords.restype = C.POINTER(C.c_float)
+    L.tc_dataset_coords.argtypes = [C.c_void_p]
+    h = C.c_void_p()
+    want = L.tc_dataset_load(path.encode(), 0, C.byref(h))
+    want_pts = None
+    if want == 0:
+        n, d = L.tc_dataset_size(h), L.tc_dataset_dim(h)
+        want_pts = np.ctypeslib.as_array(L.tc_dataset_coords(h), shape=(n * d,)).reshape(n, d).copy()
+        L.tc_dataset_free(h)
+    try:
+        got_pts = Dataset.load(path).coords()
+        got = 0
+    except TreeclustError as e:
+        got = int(e.status)
+    assert got == want, (case, got, want)
+    if want == 0:
+        assert np.array_equal(got_pts, want_pts)
+
+
+@pytest.mark.parametrize("suffix", [".csv", ".bin"])
+def test_writers_match_reference_bytes(tmp_path, suffix):
+    """tc_dataset_save writes the reference's bytes (REF io.cpp:84-148)."""
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    pts = Dataset.hacc_like(500, seed=9).coords()
+    pts[:5] *= np.float32(1e-7)
+    ours, theirs = str(tmp_path / f"a{suffix}"), str(tmp_path / f"b{suffix}")
+    Dataset.from_array(pts).save(ours)
+    L = ref._capi()
+    L.tc_dataset_save.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
+    rds = ref.RefDataset.from_array(pts)
+    assert L.tc_dataset_save(rds.h, theirs.encode(), 0) == 0
+    rds.close()
+    assert open(ours, "rb").read() == open(theirs, "rb").read()
+
+
+def test_binary_reader_errors_match_reference(tmp_path):
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    good = np.arange(12, dtype=np.float32).reshape(4, 3)
+    blobs = {
+        "short_header": b"\x04\x00\x00",
+        "zero_n": np.array([0, 3], "<u4").tobytes(),
+        "bad_dim": np.array([4, 4], "<u4").tobytes() + good.tobytes(),
+        "truncated": np.array([4, 3], "<u4").tobytes() + good.tobytes()[:40],
+        "ok_extra_tail": np.array([4, 3], "<u4").tobytes() + good.tobytes() + b"xyz",
+        "ok": np.array([4, 3], "<u4").tobytes() + good.tobytes(),
+    }
+    L = ref._capi()
+    for name, blob in blobs.items():
+        path = str(tmp_path / f"{name}.bin")
+        open(path, "wb").write(blob)
+        h = C.c_void_p()
+        want = L.tc_dataset_load(path.encode(), 0, C.byref(h))
+        if want == 0:
+            L.tc_dataset_free(h)
+        try:
+            got = 0
+            assert np.array_equal(Dataset.load(path).coords(), good)
+        except TreeclustError as e:
+            got = int(e.status)
+        assert got == want, name
+    missing = str(tmp_path / "nope.bin")
+    with pytest.raises(TreeclustError) as e:
+        Dataset.load(missing)
+    assert e.value.status == Status.IO

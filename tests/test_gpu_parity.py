@@ -328,7 +328,10 @@ def test_c3_hacc_37m_densebox_against_reference():
     got_fd = tb.cluster(ds, 0.042, 100, Algorithm.FDBSCAN)
     _assert_reference_parity(got_fd, want, c, 0.042, 100, "C3 FDBSCAN", counters=False)
     again = tb.cluster(ds, 0.042, 100, Algorithm.DENSEBOX)  # determinism (acceptance crit. 8)
-    assert np.array_equal(again.labels, got.labels) and again.stats == got.stats
+    assert np.array_equal(again.labels, got.labels)
+    assert np.array_equal(again.core_flags, got.core_flags)
+    for k, v in got.stats.items():
+        assert k.endswith("_seconds") or again.stats[k] == v, k
 
 
 @pytest.mark.slow
