@@ -38,15 +38,18 @@ const char* tcg_version(void);
  * The call is stream-ordered: with stats == NULL it returns once the work is
  * enqueued, except for the few small device->host reads that size later
  * launches (DenseBox cell/primitive counts). Scratch comes from the stream-
- * ordered CUDA memory pool (cudaMallocAsync) and is released before return. */
+ * ordered memory pool (tcg_set_pool_release_threshold) and is released before
+ * return. */
 tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
                              float eps, int minpts, tc_algorithm algorithm,
                              int64_t oracle_cap, int32_t* d_labels,
                              uint8_t* d_core, void* stream,
                              tc_cluster_stats* stats);
 
-/* FDBSCAN with caller keys: d_keys[i] is a unique int32 key of point i (e.g.
- * its global id across shards); clusters are represented by the key of their
+/* FDBSCAN with caller keys: d_keys[i] is a unique non-negative int32 key of
+ * point i (e.g. its global id across shards; a negative key could collide
+ * with the noise label -1 and is rejected with TC_ERR_INVALID_ARGUMENT after
+ * one device check and synchronization); clusters are represented by the key of their
  * minimum-key core, so d_labels[i] = that key (or -1 for noise). With keys
  * 0..n-1 this is tcg_cluster_device(FDBSCAN). Used by the sharded path to
  * label a local (own + ghost) set directly in global ids. */
@@ -75,6 +78,16 @@ int tcg_last_stage_ms(double* out, int cap);
 /* Number of kernels the last tcg_cluster_device / tc_cluster call on this
  * host thread launched (all of them are this library's own sm_100a kernels). */
 int64_t tcg_last_launch_count(void);
+
+/* ---- memory held between calls ----
+ * Device scratch comes from the library's own stream-ordered pool per device
+ * (the process's default CUDA pool is never modified). The pool keeps up to
+ * `bytes` reserved between calls (default 24 GiB; more is returned to the
+ * driver at the next synchronization). Large host buffers (datasets, results)
+ * are page-locked and up to 4 GiB of them are cached for reuse.
+ * tcg_release_cached_memory frees both caches now. */
+tc_status tcg_set_pool_release_threshold(uint64_t bytes);
+void tcg_release_cached_memory(void);
 
 /* ---- benchmark generators (host, SplitMix64) ---- */
 
@@ -126,7 +139,8 @@ tc_status tcg_cluster_given_core_device(const float* d_coords, int64_t n, int di
 /* Local context of one shard (own + ghost points): ONE point BVH serving the
  * core pass and, after the caller exchanged ghost flags with their owners,
  * the main pass. Labels are the key (e.g. global id) of each cluster's
- * minimum-key core, -1 for noise; d_keys must be unique. All calls use the
+ * minimum-key core, -1 for noise; d_keys must be unique and non-negative
+ * (negative: TC_ERR_INVALID_ARGUMENT). All calls use the
  * stream given at creation; free the context before destroying that stream. */
 typedef struct tcg_local tcg_local;
 tc_status tcg_local_create(const float* d_coords, const int32_t* d_keys, int64_t n, int dim,

@@ -99,6 +99,8 @@ SIGNATURES = {
                                                _P, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
     "tcg_first_bad_border_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P,
                                               C.POINTER(C.c_int64)]),
+    "tcg_set_pool_release_threshold": (C.c_int, [C.c_uint64]),
+    "tcg_release_cached_memory": (None, []),
     "tcg_dataset_create_pinned": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int, _PP]),
 }
 

@@ -41,8 +41,8 @@ struct NodeTraits {
 };
 
 constexpr int kStackDepth = 128;
-// Register-stack entries of the clustering traversals (RopeWalk); deeper
-// pending subtrees are recovered through ropes.
+// Register-stack entries of the clustering traversals (RangedWalk); deeper
+// pending subtrees spill to local memory.
 #ifndef TCB_STACK_REGS
 #define TCB_STACK_REGS 6
 #endif
@@ -252,52 +252,43 @@ __device__ __forceinline__ int ball_classify(const float* p, const float* lo, co
   return box_dist2<D>(p, lo, hi) <= bt.r2 ? 1 : 0;
 }
 
-// Answers of an `inside` callback (RopeWalk::step).
+// Answers of an `inside` callback (RangedWalk::step).
 constexpr int kStop = 0, kTaken = 1, kWalk = 2;
 
-// A short traversal stack held in registers: K entries shifted on push / pop
-// (static indices only, so nothing goes to local memory). A push onto a full
-// stack drops the OLDEST entry and marks the stack `lost`; the walk then
-// recovers the dropped subtrees through ropes (RopeWalk).
+// Traversal stack whose K newest entries live in registers (shifted on push /
+// pop: static indices only) and whose older entries, when a query's pending
+// set outgrows K, spill to a per-thread local array. Most queries never touch
+// the local part, so the walk issues no local-memory traffic in the common
+// case; deep ones stay exact (no entry is ever dropped).
 template <int K>
-struct RegStack {
+struct ShortStack {
   int32_t e[K];
-  int32_t n = 0;  // live entries; bit 30 = an entry was dropped
-  static constexpr int32_t kLost = 1 << 30;
+  int32_t n = 0;  // total entries
+  int32_t spill[kStackDepth];
   __device__ __forceinline__ void push(int32_t v) {
+    if (n >= K) spill[n - K] = e[K - 1];
 #pragma unroll
     for (int k = K - 1; k > 0; --k) e[k] = e[k - 1];
     e[0] = v;
-    if ((n & ~kLost) == K)
-      n |= kLost;
-    else
-      ++n;
+    ++n;
   }
   __device__ __forceinline__ bool pop(int32_t& v) {
-    if ((n & ~kLost) == 0) return false;
+    if (n == 0) return false;
     v = e[0];
 #pragma unroll
     for (int k = 0; k < K - 1; ++k) e[k] = e[k + 1];
     --n;
+    if (n >= K) e[K - 1] = spill[n - K];
     return true;
   }
-  __device__ __forceinline__ bool lost() const { return (n & kLost) != 0; }
 };
 
-// Left-first depth-first walk of the eps-ball query with subtree
-// containment, a K-entry register stack and rope restarts. State per query:
-//   node      the node to process next
-//   min_rank  leaves below it are hidden (query_sphere_masked's mask,
-//             bvh.hpp:45-72; raised past the finished prefix on a restart)
-//   end       the last leaf rank under the walk's start node
-// Left-first order visits leaf ranks in increasing order, so when the stack
-// runs empty after having dropped entries, everything up to the current
-// node's last rank h is finished, and the rest of the start node's range is
-// exactly the chain of right subtrees reached by ropes: the node with split
-// h (the lowest common ancestor of leaves h and h + 1, found from the split
-// numbering without any stored link) has [h + 1, aux_r] as its right child;
-// the walk resumes there with min_rank = h + 1 (which hides the finished left
-// child), and so on until h == end. Callbacks:
+// Depth-first walk of the eps-ball query with subtree containment. State per
+// query: the node to process next, the rank mask (leaves below min_rank are
+// hidden, query_sphere_masked bvh.hpp:45-72) and the pending left
+// subtrees on a ShortStack. Child ranges come from the record (aux = outer
+// range end) and the node's split (its index), so an entry is one node link.
+// Callbacks:
 //     bool visit(int32_t rank, int32_t aux, bool contained)
 //                                               leaf `rank` is within eps
 //                                               (its whole box when contained;
@@ -310,11 +301,11 @@ struct RegStack {
 // internal, masked or not) so the lanes of a warp only diverge on the rare
 // visit / inside actions. The order in which leaves are reported is not the
 // reference's DFS order (callers depend only on the set, or, for early exit,
-// on min(count, minpts) — see CoreQuery).
+// on min(count, minpts) — see k_fd_core).
 template <int D, int K>
-struct RopeWalk {
-  int32_t node, min_rank, end;
-  RegStack<K> stack;
+struct RangedWalk {
+  int32_t node, min_rank, end;  // end: last leaf rank under the start node
+  ShortStack<K> stack;
 
   template <typename Visit, typename Inside, int kFast = -1>
   __device__ __forceinline__ bool step(const TreeView& tv, const float* p, const BallTest& bt,
@@ -356,16 +347,14 @@ struct RopeWalk {
     }
     const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
     if (go_l && go_r) {
-      stack.push(right);
-      node = left;
+      stack.push(left);
+      node = right;
     } else if (go_l) {
       node = left;
     } else if (go_r) {
       node = right;
     } else if (!stack.pop(node)) {
-      if (!stack.lost() || max_r >= end) return false;
-      min_rank = max_r + 1;  // rope: the right subtree after leaf max_r
-      node = split_node(tv, max_r);
+      return false;
     }
     return true;
   }

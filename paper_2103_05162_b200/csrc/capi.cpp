@@ -88,10 +88,16 @@ class HostPool {
     }
     cudaFreeHost(p);
   }
+  void trim() {
+    std::lock_guard<std::mutex> lock(mu_);
+    for (auto& kv : free_) cudaFreeHost(kv.second);
+    free_.clear();
+    cached_ = 0;
+  }
 
  private:
   static constexpr size_t kPinMin = size_t{1} << 20;
-  static constexpr size_t kCacheCap = size_t{16} << 30;
+  static constexpr size_t kCacheCap = size_t{4} << 30;  // pinned bytes kept for reuse
   static size_t round(size_t b) { return (b + (size_t{2} << 20) - 1) & ~((size_t{2} << 20) - 1); }
   std::mutex mu_;
   std::multimap<size_t, void*> free_;
@@ -196,8 +202,7 @@ struct DeviceCall {
   }
   template <typename T>
   T* alloc(int64_t count) {
-    void* p = nullptr;
-    TCB_CUDA(cudaMallocAsync(&p, static_cast<size_t>(std::max<int64_t>(count, 1)) * sizeof(T), st));
+    void* p = tcb::pool_alloc(static_cast<size_t>(std::max<int64_t>(count, 1)) * sizeof(T), st);
     bufs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -578,4 +583,16 @@ TC_EXPORT tc_status tcg_first_bad_border_device(const float* d_coords, int64_t n
                                 static_cast<cudaStream_t>(stream));
     return TC_OK;
   });
+}
+
+TC_EXPORT tc_status tcg_set_pool_release_threshold(uint64_t bytes) {
+  return guarded([&]() -> tc_status {
+    tcb::set_pool_release_threshold(bytes);
+    return TC_OK;
+  });
+}
+
+TC_EXPORT void tcg_release_cached_memory(void) {
+  HostPool::get().trim();
+  tcb::trim_pools();
 }

@@ -80,7 +80,7 @@ k_fd_core(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTes
     int32_t id;
     load_query<D>(leaf_pt, r, p, &id);
   }
-  RopeWalk<D, kStackRegs> walk;
+  RangedWalk<D, kStackRegs> walk;
   walk.min_rank = 0;
   warp_start_node<D>(tv, p, valid, bt, 0, walk.node, walk.end);
   int count = 0;
@@ -135,7 +135,7 @@ k_fd_main(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTes
     load_query<D>(leaf_pt, r, p, &id);
     rank = static_cast<int32_t>(r);
   }
-  RopeWalk<D, kStackRegs> walk;
+  RangedWalk<D, kStackRegs> walk;
   walk.min_rank = rank + 1;
   warp_start_node<D>(tv, p, valid, bt, rank + 1, walk.node, walk.end);
   if (valid) {
@@ -202,7 +202,7 @@ k_fd_main_fof(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, Bal
     load_query<D>(leaf_pt, r, p, &id);
     rank = static_cast<int32_t>(r);
   }
-  RopeWalk<D, kStackRegs> walk;
+  RangedWalk<D, kStackRegs> walk;
   walk.min_rank = rank + 1;
   warp_start_node<D>(tv, p, valid, bt, rank + 1, walk.node, walk.end);
   if (valid) {
@@ -221,9 +221,9 @@ k_fd_main_fof(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, Bal
       return kTaken;
     };
     while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
-      TCB_PROBE_ONLY(++pr[0]; pr[3] += walk.stack.lost();)
+      TCB_PROBE_ONLY(++pr[0]; pr[3] += walk.stack.n > kStackRegs;)
     }
-    TCB_PROBE_ONLY(++pr[0]; pr[5] += walk.stack.lost(); pr[6] = pr[0];)
+    TCB_PROBE_ONLY(++pr[0]; pr[6] = pr[0];)
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
@@ -248,6 +248,15 @@ __global__ void k_gather_keys(const int32_t* __restrict__ keys, const int32_t* _
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < n;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[s] = keys[order[s]];
+}
+
+__global__ void k_key_min(const int32_t* __restrict__ keys, int64_t n, int32_t* out) {
+  int32_t m = INT32_MAX;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = min(m, __ldg(keys + i));
+  m = __reduce_min_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m < 0) atomicMin(out, m);
 }
 
 __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
@@ -335,7 +344,7 @@ constexpr int kFinWindow = 32768;
 
 __global__ void __launch_bounds__(kFinThreads)
 k_fin_window(const uint2* __restrict__ entries, int64_t n, int shift, int b0,
-             int32_t* __restrict__ labels, uint8_t* __restrict__ core_out) {
+             int32_t* __restrict__ labels, uint8_t* __restrict__ core_out, bool vec16) {
   extern __shared__ __align__(16) unsigned char fin_smem[];
   int32_t* s_lab = reinterpret_cast<int32_t*>(fin_smem);
   uint8_t* s_core = fin_smem + sizeof(int32_t) * kFinWindow;
@@ -349,7 +358,7 @@ k_fin_window(const uint2* __restrict__ entries, int64_t n, int shift, int b0,
     s_core[w] = static_cast<uint8_t>(v.x >> 31);
   }
   __syncthreads();
-  if (cnt == (1 << shift)) {  // full window: 16-byte stores (base is 16-aligned)
+  if (vec16 && cnt == (1 << shift)) {  // full window: 16-byte stores (16-aligned outputs)
     int4* dl = reinterpret_cast<int4*>(labels + base);
     const int4* sl = reinterpret_cast<const int4*>(s_lab);
     for (int k = threadIdx.x; k < cnt / 4; k += kFinThreads) __stcs(dl + k, sl[k]);
@@ -429,6 +438,19 @@ void gather_rank_keys(const int32_t* keys, const int32_t* order, int64_t n, int3
   TCB_CUDA(cudaGetLastError());
 }
 
+void check_keys_nonnegative(const int32_t* keys, int64_t n, Scratch& scratch) {
+  cudaStream_t s = scratch.stream();
+  int32_t* d_min = scratch.alloc_n<int32_t>(1);
+  TCB_CUDA(cudaMemsetAsync(d_min, 0, sizeof(int32_t), s));
+  note_launch(), k_key_min<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(keys, n, d_min);
+  TCB_CUDA(cudaGetLastError());
+  auto* h = static_cast<int32_t*>(pinned_staging(sizeof(int32_t)));
+  TCB_CUDA(cudaMemcpyAsync(h, d_min, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  TCB_CUDA(cudaStreamSynchronize(s));
+  // a negative key could label a cluster -1, the noise sentinel
+  if (*h < 0) throw InvalidArgument{"keys must be non-negative"};
+}
+
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s) {
   note_launch(), k_init_uf<<<grid_for(n, 256), 256, 0, s>>>(parent, n);
   TCB_CUDA(cudaMemsetAsync(flags, 0, static_cast<size_t>(n), s));
@@ -452,6 +474,9 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
   uint2* entries = scratch.alloc_n<uint2>(n);
   TCB_CUDA(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * nb, s));
   const int64_t tile = int64_t{kFinThreads} * kFinItems;
+  // caller buffers (e.g. a torch slice) need not be 16-byte aligned: the
+  // window pass then writes element by element
+  const bool vec16 = (reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(core_out)) % 16 == 0;
   note_launch(), k_fin_bucket<<<static_cast<unsigned>((n + tile - 1) / tile), kFinThreads, 0, s>>>(
       parent, flags, key, order, n, shift, nb, cursor, entries, d_ctr, force_core);
   TCB_CUDA(cudaGetLastError());
@@ -468,7 +493,7 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
                                     static_cast<int>(smem)));
       const int blocks = std::min(per, nb - b0);
       note_launch(), k_fin_window<<<blocks, kFinThreads, smem, s>>>(entries, n, shift, b0, labels,
-                                                                   core_out);
+                                                                   core_out, vec16);
     } else {  // wide windows: stores straight to global (L2 still merges a window)
       note_launch(), k_fin_scatter<<<grid_for(e1 - e0, 256), 256, 0, s>>>(entries, e0, e1, labels,
                                                                          core_out);

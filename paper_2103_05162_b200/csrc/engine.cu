@@ -20,19 +20,30 @@ namespace tcb {
 // ---------------------------------------------------------------------------
 namespace {
 
-void raise_pool_threshold() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
-  static std::mutex mu;
-  static bool done[64] = {};
-  std::lock_guard<std::mutex> lock(mu);
-  if (dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = std::numeric_limits<uint64_t>::max();
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+// The library's own stream-ordered memory pool per device (the device's
+// default pool, which other users of the process share, is never touched).
+// Scratch is reused across calls up to the release threshold; above it the
+// pool returns memory to the driver at the next synchronization, so a huge
+// run (C5: ~80 GB) does not stay reserved afterwards.
+constexpr int kMaxDevices = 64;
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[kMaxDevices] = {};
+uint64_t g_pool_threshold = uint64_t{24} << 30;
+
+cudaMemPool_t library_pool(int dev) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    TCB_CUDA(cudaMemPoolCreate(&pool, &props));
+    TCB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &g_pool_threshold));
+    g_pool[dev] = pool;
   }
-  done[dev] = true;
+  return g_pool[dev];
 }
 
 thread_local double t_last_stage_ms[kNumStages] = {};
@@ -45,13 +56,33 @@ Scratch::~Scratch() {
 }
 
 void* Scratch::alloc(size_t bytes) {
-  if (ptrs_.empty()) raise_pool_threshold();
-  void* p = nullptr;
-  bytes = (bytes + 255) & ~size_t{255};
-  cudaError_t e = cudaMallocAsync(&p, bytes, stream_);
-  if (e != cudaSuccess) throw CudaFailure{e, __FILE__, __LINE__};
+  void* p = pool_alloc(bytes, stream_);
   ptrs_.push_back(p);
   return p;
+}
+
+void* pool_alloc(size_t bytes, cudaStream_t stream) {
+  int dev = 0;
+  TCB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw CudaFailure{cudaErrorInvalidDevice, __FILE__, __LINE__};
+  void* p = nullptr;
+  bytes = (bytes + 255) & ~size_t{255};
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes > 0 ? bytes : 256, library_pool(dev), stream);
+  if (e != cudaSuccess) throw CudaFailure{e, __FILE__, __LINE__};
+  return p;
+}
+
+void set_pool_release_threshold(uint64_t bytes) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  g_pool_threshold = bytes;
+  for (cudaMemPool_t pool : g_pool)
+    if (pool) TCB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &bytes));
+}
+
+void trim_pools() {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  for (cudaMemPool_t pool : g_pool)
+    if (pool) cudaMemPoolTrimTo(pool, 0);
 }
 
 void* pinned_staging(size_t bytes) {
@@ -140,6 +171,7 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
   const int32_t* key = b.tree.leaf_order;  // rank -> original index
   if (d_keys) {
+    check_keys_nonnegative(d_keys, n, scratch);
     int32_t* k = scratch.alloc_n<int32_t>(n);
     gather_rank_keys(d_keys, b.tree.leaf_order, n, k, st);
     key = k;

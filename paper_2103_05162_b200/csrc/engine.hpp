@@ -52,6 +52,14 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
                 const std::function<void(cudaStream_t)>& tail = nullptr,
                 const int32_t* d_keys = nullptr, const ChunkSink* sink = nullptr);
 
+// Stream-ordered allocation from the library's private per-device pool (the
+// process's default pool is left alone); release with cudaFreeAsync.
+void* pool_alloc(size_t bytes, cudaStream_t stream);
+// Bytes the private pools keep reserved across calls (default 24 GiB), and an
+// immediate release of everything unused.
+void set_pool_release_threshold(uint64_t bytes);
+void trim_pools();
+
 // Kernel-launch accounting (thread-local; reset at the start of run_device).
 void note_launch();
 void reset_launch_count();

@@ -481,7 +481,7 @@ k_db_main_ranged(DeviceBvh tree, const float4* __restrict__ qpt,
     p[1] = qp.y;
     p[2] = qp.z;
   }
-  RopeWalk<D, kStackRegs> walk;
+  RangedWalk<D, kStackRegs> walk;
   walk.min_rank = own + 1;
   warp_start_node<D>(tv, p, valid, bt, own + 1, walk.node, walk.end);
   if (valid) {

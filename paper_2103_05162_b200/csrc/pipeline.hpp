@@ -34,9 +34,9 @@ struct DevCounters {
 #define TCB_PROBE_ONLY(...)
 #endif
 
-// Stream-ordered scratch allocations released at scope exit (cudaMallocAsync
-// on the default pool; the pool's release threshold is raised once so repeat
-// calls reuse HBM instead of re-mapping it).
+// Stream-ordered scratch allocations released at scope exit (pool_alloc: the
+// library's private per-device pool, so repeat calls reuse HBM instead of
+// re-mapping it).
 class Scratch {
  public:
   explicit Scratch(cudaStream_t s) : stream_(s) {}
@@ -127,6 +127,8 @@ void gather_rank_keys(const int32_t* keys, const int32_t* order, int64_t n, int3
 void permute_flags(const uint8_t* src, const int32_t* order, int64_t n, uint8_t* dst,
                    bool to_rank, cudaStream_t s);
 void init_union_find(int32_t* parent, uint8_t* flags, int64_t n, cudaStream_t s);
+// Throws InvalidArgument when any of the n caller keys is negative (syncs).
+void check_keys_nonnegative(const int32_t* keys, int64_t n, Scratch& scratch);
 // FDBSCAN finalize in rank space: labels[order[rank]] = key of the rank's
 // root (or -1), core flags likewise, through destination buckets
 // (k_fin_bucket, then k_fin_window / k_fin_scatter, dbscan.cu): whole-sector

@@ -168,6 +168,7 @@ struct LocalCtx {
 
 template <int D>
 void local_build(LocalCtx& c, const float* d_coords, const int32_t* d_keys) {
+  check_keys_nonnegative(d_keys, c.n, c.scratch);
   c.ctr = c.scratch.alloc_n<DevCounters>(1);
   TCB_CUDA(cudaMemsetAsync(c.ctr, 0, sizeof(DevCounters), c.st));
   PrimSource src;

@@ -389,17 +389,22 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
 
     marks.mark("5")
     lgid = torch.cat([own_gid, ghost_gid])
-    if minpts == 2 and hasattr(engine, "cluster_keyed") and \
-            (lgid.shape[0] == 0 or int(lgid.max().item()) < 2**31):
+    # The path below must be the same on every rank (each issues a different
+    # sequence of collectives): decide it from all-reduced facts only.
+    gmax = torch.tensor([int(lgid.max().item()) if lgid.numel() else -1], dtype=torch.int64,
+                        device=dev)
+    fits = int(_all_reduce(gmax, dist.ReduceOp.MAX, group).item()) < 2**31
+    e64 = torch.empty(0, dtype=torch.int64, device=dev)
+    no_edges = torch.empty((0, 2), dtype=torch.int64, device=dev)
+    if minpts == 2 and hasattr(engine, "cluster_keyed") and fits:
         # minpts == 2 (friends-of-friends): every within-eps pair is a
         # core-core union and core == "has a neighbour", exact for own points
         # (complete neighbourhoods); no flag exchange is needed. One local run
         # keyed by global id labels the own + ghost set in global ids.
         lx = torch.cat([own_x, ghost_x]).contiguous()
         if lx.shape[0] == 0:
-            e = torch.empty(0, dtype=torch.int64, device=dev)
-            _all_gather_var(torch.empty((0, 2), dtype=torch.int64, device=dev), group)
-            return e, e.to(torch.int32), e.to(torch.uint8)
+            _merge_edges(no_edges, e64, engine, group)
+            return e64, e64.to(torch.int32), e64.to(torch.uint8)
         lab, lcore = engine.cluster_keyed(lx, lgid.to(torch.int32), eps, 2)
         lab = lab.to(torch.int64)
         marks.mark("7")
@@ -414,16 +419,16 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
         marks.report(rank)
         return own_gid, root_gid, own_core
 
-    if hasattr(engine, "local") and (lgid.shape[0] == 0 or int(lgid.max().item()) < 2**31):
+    if hasattr(engine, "local") and fits:
         # 5. one local context (own + ghost points, keyed by global id): exact
         #    own flags, owners' flags for the ghosts, then the main pass on the
         #    same tree; labels come out as global ids
         lx = torch.cat([own_x, ghost_x]).contiguous()
         nl = lx.shape[0]
-        if nl == 0:
-            e = torch.empty(0, dtype=torch.int64, device=dev)
-            _all_gather_var(torch.empty((0, 2), dtype=torch.int64, device=dev), group)
-            return e, e.to(torch.int32), e.to(torch.uint8)
+        if nl == 0:  # still part of the ghost-flag exchange and the merge
+            _all_to_all(torch.empty((0, 1), dtype=torch.uint8, device=dev), [0] * world, group)
+            _merge_edges(no_edges, e64, engine, group)
+            return e64, e64.to(torch.int32), e64.to(torch.uint8)
         ctx = engine.local(lx, lgid.to(torch.int32), eps)
         local_core = ctx.core_flags(minpts)
         own_core = local_core[:n_own]
@@ -448,6 +453,11 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
 
     # 5. local set ordered by global id; exact own flags; owners' ghost flags
     lx = torch.cat([own_x, ghost_x])
+    nl = lx.shape[0]
+    if nl == 0:  # still part of the ghost-flag exchange and the merge
+        _all_to_all(torch.empty((0, 1), dtype=torch.uint8, device=dev), [0] * world, group)
+        _merge_edges(no_edges, e64, engine, group)
+        return e64, e64.to(torch.int32), e64.to(torch.uint8)
     lorder = torch.argsort(lgid)
     lx = lx[lorder].contiguous()
     lgid = lgid[lorder]
@@ -455,11 +465,6 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     inv[lorder] = torch.arange(lorder.shape[0], device=dev)
     own_pos = inv[:n_own]
     ghost_pos = inv[n_own:]
-    nl = lx.shape[0]
-    if nl == 0:
-        e = torch.empty(0, dtype=torch.int64, device=dev)
-        _all_gather_var(torch.empty((0, 2), dtype=torch.int64, device=dev), group)
-        return e, e.to(torch.int32), e.to(torch.uint8)
     local_core = engine.core_flags(lx, eps, minpts)
     own_core = local_core[own_pos]
     ghost_core, _ = _all_to_all(own_core[send_idx].view(-1, 1), send_counts, group)

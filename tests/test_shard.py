@@ -246,3 +246,23 @@ def test_sharded_device_engine_world1(minpts):
     coords = blob_mix(44, 8000, 3)
     labels, core = run_sharded(coords, 0.3, minpts, world=1, use_gpu=True)
     check_against_oracle(coords, 0.3, minpts, labels, core)
+
+
+@pytest.mark.parametrize("minpts", [2, 3, 5])
+def test_sharded_rank_without_points(minpts):
+    """All points at one coordinate: every Morton code is equal, the splitters
+    coincide and one rank owns nothing. That rank must still take part in every
+    collective of the chosen path (divergent collectives would
+    hang), and the result must equal the single-process one."""
+    coords = np.tile(np.array([[1.5, -2.0, 0.25]], np.float32), (40, 1))
+    labels, core = run_sharded(coords, 0.1, minpts, world=2)
+    check_against_oracle(coords, 0.1, minpts, labels, core)
+
+
+def test_sharded_world3_two_clumps_one_empty_rank():
+    """Two coincident clumps and world 3: at least one rank owns no points."""
+    a = np.tile(np.array([[0.0, 0.0, 0.0]], np.float32), (30, 1))
+    b = np.tile(np.array([[5.0, 5.0, 5.0]], np.float32), (30, 1))
+    coords = np.concatenate([a, b])
+    labels, core = run_sharded(coords, 0.2, 4, world=3)
+    check_against_oracle(coords, 0.2, 4, labels, core)
