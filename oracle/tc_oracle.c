@@ -733,6 +733,14 @@ static int64_t bad_border(const float* coords, int64_t n, int dim, double eps2,
   return -1;
 }
 
+static const int32_t* g_sort_labels; /* qsort context (single-threaded oracle) */
+static int cmp_label_index(const void* x, const void* y) {
+  const int64_t i = *(const int64_t*)x, j = *(const int64_t*)y;
+  const int32_t a = g_sort_labels[i], b = g_sort_labels[j];
+  if (a != b) return a < b ? -1 : 1;
+  return i < j ? -1 : (i > j);
+}
+
 int oracle_check_equivalence(const float* coords, int64_t n, int dim, float eps,
                              const int32_t* la, const uint8_t* ca, const int32_t* lb,
                              const uint8_t* cb, char* msg, int64_t msg_len) {
@@ -744,25 +752,33 @@ int oracle_check_equivalence(const float* coords, int64_t n, int dim, float eps,
     if (ca[i] != cb[i]) what = "core flags differ", at = i;
   for (int64_t i = 0; i < n && !what; ++i)
     if ((la[i] == -1) != (lb[i] == -1)) what = "noise sets differ", at = i;
-  if (!what) { /* bijection via two maps label -> label (arrays indexed by label) */
-    int32_t* a2b = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
-    int32_t* b2a = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
-    for (int64_t i = 0; i < n; ++i) a2b[i] = b2a[i] = -2;
-    for (int64_t i = 0; i < n && !what; ++i) {
-      if (!ca[i]) continue;
-      if (la[i] < 0 || la[i] >= n || lb[i] < 0 || lb[i] >= n) {
-        what = "core partitions differ", at = i;
-        break;
-      }
-      if (a2b[la[i]] == -2) a2b[la[i]] = lb[i];
-      else if (a2b[la[i]] != lb[i]) what = "core partitions differ", at = i;
-      if (!what) {
-        if (b2a[lb[i]] == -2) b2a[lb[i]] = la[i];
-        else if (b2a[lb[i]] != la[i]) what = "core partitions differ", at = i;
-      }
+  if (!what) { /* bijection (REF oracle.cpp:144-152): the sequential emplace keeps,
+                 per label, the FIRST core carrying it, and fails at the first core
+                 whose other label differs from that core's; labels are arbitrary
+                 int32, so the first core per label comes from a sort */
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) m += ca[i] != 0;
+    int64_t* ia = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m ? m : 1));
+    int64_t* ib = (int64_t*)malloc(sizeof(int64_t) * (size_t)(m ? m : 1));
+    int64_t* fa = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    int64_t* fb = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
+    int64_t k = 0;
+    for (int64_t i = 0; i < n; ++i)
+      if (ca[i]) ia[k] = ib[k] = i, ++k;
+    g_sort_labels = la;
+    qsort(ia, (size_t)m, sizeof(int64_t), cmp_label_index);
+    g_sort_labels = lb;
+    qsort(ib, (size_t)m, sizeof(int64_t), cmp_label_index);
+    for (int64_t t = 0; t < m; ++t) { /* fa[i] = first core with i's a-label */
+      fa[ia[t]] = (t > 0 && la[ia[t - 1]] == la[ia[t]]) ? fa[ia[t - 1]] : ia[t];
+      fb[ib[t]] = (t > 0 && lb[ib[t - 1]] == lb[ib[t]]) ? fb[ib[t - 1]] : ib[t];
     }
-    free(a2b);
-    free(b2a);
+    for (int64_t i = 0; i < n && !what; ++i)
+      if (ca[i] && (lb[fa[i]] != lb[i] || la[fb[i]] != la[i])) what = "core partitions differ", at = i;
+    free(ia);
+    free(ib);
+    free(fa);
+    free(fb);
   }
   const double eps2 = (double)eps * eps;
   if (!what && (at = bad_border(coords, n, dim, eps2, la, ca)) >= 0)

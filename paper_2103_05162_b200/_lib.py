@@ -112,6 +112,8 @@ def _load() -> C.CDLL:
             "g.build()'` (there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("TCB_LIB_PATH") and not hasattr(lib, name):
+            continue  # A/B of an older build (tools/ab_libs.sh): newer entry points absent
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -41,10 +41,10 @@ struct NodeTraits {
 };
 
 constexpr int kStackDepth = 128;
-// Register-stack entries of the clustering traversals (RangedWalk); deeper
-// pending subtrees spill to local memory.
+// Register-held entries of the clustering traversals' stack (RangedWalk,
+// ShortStack); the rest lives in local memory.
 #ifndef TCB_STACK_REGS
-#define TCB_STACK_REGS 6
+#define TCB_STACK_REGS 0
 #endif
 constexpr int kStackRegs = TCB_STACK_REGS;
 
@@ -279,6 +279,22 @@ struct ShortStack {
     for (int k = 0; k < K - 1; ++k) e[k] = e[k + 1];
     --n;
     if (n >= K) e[K - 1] = spill[n - K];
+    return true;
+  }
+};
+
+// K = 0: the whole stack in local memory (one store / load per push / pop;
+// measured faster than any register part on the issue-bound C2 main pass:
+// K = 6 +19%, K = 2 +67%, the shifts cost more issue slots than the local
+// accesses they save).
+template <>
+struct ShortStack<0> {
+  int32_t n = 0;
+  int32_t e[kStackDepth];
+  __device__ __forceinline__ void push(int32_t v) { e[n++] = v; }
+  __device__ __forceinline__ bool pop(int32_t& v) {
+    if (n == 0) return false;
+    v = e[--n];
     return true;
   }
 };

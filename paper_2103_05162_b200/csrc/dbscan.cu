@@ -38,13 +38,13 @@ constexpr int kQueryBlock = 128;  // 64 / 256 measured equal or slower
 // registers at 36): 14 x 4 warps instead of 12 at its natural 40 registers,
 // main pass 19.2 -> 18.5 ms on C2 despite a few spilled bytes.
 #ifndef TCB_FOF_MIN_BLOCKS
-#define TCB_FOF_MIN_BLOCKS 12
+#define TCB_FOF_MIN_BLOCKS 14
 #endif
 constexpr int kFofMinBlocks = TCB_FOF_MIN_BLOCKS;
 // the same for the minpts > 2 main pass (12: main 22.2 -> 21.2 ms on C3);
 // the core pass is faster uncapped
 #ifndef TCB_MAIN_MIN_BLOCKS
-#define TCB_MAIN_MIN_BLOCKS 10
+#define TCB_MAIN_MIN_BLOCKS 12
 #endif
 constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
 

@@ -290,3 +290,28 @@ def test_write_bin_loads_in_reference(tmp_path):
     got = np.ctypeslib.as_array(L.tc_dataset_coords(ds), shape=(3000,)).reshape(1000, 3).copy()
     L.tc_dataset_free(ds)
     assert np.array_equal(got, a)
+
+
+def test_check_equivalence_arbitrary_label_values():
+    """Labels are arbitrary int32 values in check_equivalence (REF
+    oracle.cpp:144-152 maps them through hash maps): a bijective relabeling to
+    large / negative values passes; merging two clusters fails at the first
+    core of the second one; same verdict as the compiled reference."""
+    rng = np.random.default_rng(3)
+    c = rng.uniform(0, 10, (400, 2)).astype(np.float32)
+    r = oracle.dbscan(c, 0.6, 4, 0)
+    la, ca = r["labels"], r["core"]
+    ids = [v for v in np.unique(la) if v >= 0]
+    assert len(ids) >= 2
+    m = {v: (2**31 - 1 - 5 * k if k % 2 else -1000 - k) for k, v in enumerate(ids)}
+    m[-1] = -1
+    lb = np.array([m[v] for v in la], np.int32)
+    cases = [(lb, True)]
+    merged = la.copy()
+    merged[merged == ids[1]] = ids[0]
+    cases.append((merged, False))
+    for other, ok_want in cases:
+        ok, msg = oracle.check_equivalence(c, 0.6, la, ca, other, ca)
+        assert ok == ok_want, msg
+        if ref.available():
+            assert ref.check_equivalence(c, 0.6, 4, la, ca, other, ca) == (ok, msg)
