@@ -257,7 +257,7 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
         const int32_t slink = s_link[u];
         rec[T::kIntOff + 0] = __int_as_float(link);
         rec[T::kIntOff + 1] = __int_as_float(slink);
-        rec[T::kIntOff + 2] = __int_as_float(link >= 0 ? l : aux);  // a left child's first rank
+        rec[T::kIntOff + 2] = __int_as_float(aux);
         rec[T::kIntOff + 3] = __int_as_float(s_aux[u]);
         float4* dst = nodes + static_cast<int64_t>(p) * T::kVec;
 #pragma unroll
@@ -303,8 +303,7 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
       }
       int32_t* ip = reinterpret_cast<int32_t*>(pf + T::kIntOff);
       __stcg(ip + (left ? 0 : 1), link);
-      // an internal child's aux is the outer end of its range (bvh.cuh)
-      __stcg(ip + (left ? 2 : 3), link >= 0 ? (left ? l : r) : aux);
+      __stcg(ip + (left ? 2 : 3), aux);
       if (link == 0) state->zero_parent = p | (left ? kUpLeftBit : 0);
     }
     if (active) {
@@ -436,13 +435,11 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   TCB_CUDA(cudaMemcpyAsync(scene, &d_ctr->bounds_ord[0], 6 * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, st));
   out.scene_ord = scene;
-  auto* state = scratch.alloc_n<ClimbState>(1);
-  out.tree.root_split = &state->root;
   if (m == 1) {
-    TCB_CUDA(cudaMemsetAsync(state, 0, sizeof(ClimbState), st));
     note_launch(), k_single_leaf<D><<<1, 1, 0, st>>>(boxes, src.aux, out.tree.nodes, leaf_pt);
   } else {
     int32_t* other = scratch.alloc_n<int32_t>(m - 1);
+    auto* state = scratch.alloc_n<ClimbState>(1);
     TCB_CUDA(cudaMemsetAsync(other, 0xff, sizeof(int32_t) * (m - 1), st));
     note_launch(), k_climb<D><<<grid_for(m, kClimbBlock, INT32_MAX), kClimbBlock, 0, st>>>(
         boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, state);

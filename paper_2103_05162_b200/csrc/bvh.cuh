@@ -8,17 +8,11 @@
 //     2D: 64 B = 4 x float4   [L.lo xy,  L.hi xy,  R.lo xy,  R.hi xy  | l, r, auxL, auxR | pad]
 // so one node fetch (two 32 B sectors) decides both children with no second
 // dependent load. Child links: >= 0 internal node index, < 0 = ~leaf_rank
-// (bvh.hpp:91). Internal nodes are numbered by their split (the last leaf rank
-// of the left child), except that the root is moved to node 0 and node 0's
-// record to the spare slot num_leaves - 1 (node_split / split_node below), so
-// a node's index gives its split. aux of an internal child = the outer end of
-// its Karras range: the FIRST leaf rank of a left child, the LAST of a right
-// child (bvh.cpp:88-124 propagates the max rank; together with the split this
-// gives both children's full ranges [aux_l, split] and [split + 1, aux_r]);
-// for a leaf child aux = the primitive's payload (point index for a
-// SinglePoint, or ~cell for a DenseBox in the mixed tree). Because a leaf
-// child's box lives in its parent, a leaf visit never touches the leaf
-// arrays.
+// (bvh.hpp:91). aux for an internal child = its max leaf rank (the right end
+// of its Karras range, bvh.cpp:88-124 computes the same by propagation); for a
+// leaf child = the primitive's payload (point index for a SinglePoint, or
+// ~cell for a DenseBox in the mixed tree). Because a leaf child's box lives in
+// its parent, a leaf visit never touches the leaf arrays.
 //
 // A 1-leaf tree (the reference special case bvh.hpp:49-53) is stored as one
 // pseudo node whose right child is an empty (+inf/-inf) box that no ball hits.
@@ -41,12 +35,6 @@ struct NodeTraits {
 };
 
 constexpr int kStackDepth = 128;
-// Register-held entries of the clustering traversals' stack (RangedWalk,
-// ShortStack); the rest lives in local memory.
-#ifndef TCB_STACK_REGS
-#define TCB_STACK_REGS 0
-#endif
-constexpr int kStackRegs = TCB_STACK_REGS;
 
 // One node record into registers: two 256-bit loads (sm_100 LDG.256; 64 B
 // records are 32-byte aligned): half the load requests of float4 loads on
@@ -152,43 +140,19 @@ __device__ __forceinline__ bool box_inside_ball(const float* p, const float* lo,
   return s <= bt.r2;
 }
 
-// Tree view of a kernel: the node records plus the root's split (read once
-// from the build's device word), to map split <-> node index.
-struct TreeView {
-  const float4* __restrict__ nodes;
-  int32_t root_split;  // split of the root (stored at node 0)
-  int32_t spare;       // num_leaves - 1: where node 0's own record lives
-};
-
-__device__ __forceinline__ TreeView tree_view(const float4* nodes, const int32_t* root_split,
-                                              int32_t num_leaves) {
-  TreeView tv;
-  tv.nodes = nodes;
-  tv.root_split = __ldg(root_split);
-  tv.spare = num_leaves - 1;
-  return tv;
-}
-// split of the internal node stored at index i, and the index of the node
-// whose split is s (the lowest common ancestor of leaves s and s + 1)
-__device__ __forceinline__ int32_t node_split(const TreeView& tv, int32_t i) {
-  return i == 0 ? tv.root_split : (i == tv.spare ? 0 : i);
-}
-__device__ __forceinline__ int32_t split_node(const TreeView& tv, int32_t s) {
-  return s == tv.root_split ? 0 : (s == 0 ? tv.spare : s);
-}
-
-// One traversal step of the closed-ball query (p, sqrt(r2)) over the whole
-// tree (query_sphere, bvh.hpp:38-72, unmasked): processes ONE node, calling
+// One traversal step of the closed-ball query (p, sqrt(r2)) that hides every
+// leaf with rank < min_rank (query_sphere_masked, bvh.hpp:45-72): processes
+// ONE node, calling
 //     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
 // for each leaf child whose box is within the ball (false = stop the query),
 // and advances `node` / the stack. Returns false when the query is finished.
 // The visit order is exactly the reference's (left before right for leaf
 // children; right subtree before left subtree for internal children — its LIFO
-// stack order). Used by the checkers (not on the clustering path).
+// stack order), so early-exit counters match bit for bit.
 template <int D, typename Visit>
 __device__ __forceinline__ bool bvh_step(const float4* __restrict__ nodes, const float* p,
-                                         const BallTest& bt, int32_t& node, int& top,
-                                         int32_t* stack, Visit& visit) {
+                                         const BallTest& bt, int32_t min_rank, int32_t& node,
+                                         int& top, int32_t* stack, Visit& visit) {
   using T = NodeTraits<D>;
   float f[T::kFloats];
   load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
@@ -198,16 +162,16 @@ __device__ __forceinline__ bool bvh_step(const float4* __restrict__ nodes, const
   const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
   bool go_l = false, go_r = false;
   if (left < 0) {
-    if (ball_hits<D>(p, f, f + D, bt))
+    if (~left >= min_rank && ball_hits<D>(p, f, f + D, bt))
       if (!visit(~left, aux_l, f, f + D)) return false;
-  } else {
-    go_l = ball_hits<D>(p, f, f + D, bt);
+  } else if (aux_l >= min_rank && ball_hits<D>(p, f, f + D, bt)) {
+    go_l = true;
   }
   if (right < 0) {
-    if (ball_hits<D>(p, f + 2 * D, f + 3 * D, bt))
+    if (~right >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt))
       if (!visit(~right, aux_r, f + 2 * D, f + 3 * D)) return false;
-  } else {
-    go_r = ball_hits<D>(p, f + 2 * D, f + 3 * D, bt);
+  } else if (aux_r >= min_rank && ball_hits<D>(p, f + 2 * D, f + 3 * D, bt)) {
+    go_r = true;
   }
   if (go_l && go_r) {
     stack[top++] = left;
@@ -252,59 +216,14 @@ __device__ __forceinline__ int ball_classify(const float* p, const float* lo, co
   return box_dist2<D>(p, lo, hi) <= bt.r2 ? 1 : 0;
 }
 
-// Answers of an `inside` callback (RangedWalk::step).
+// Answers of an `inside` callback (bvh_step_ranged).
 constexpr int kStop = 0, kTaken = 1, kWalk = 2;
 
-// Traversal stack whose K newest entries live in registers (shifted on push /
-// pop: static indices only) and whose older entries, when a query's pending
-// set outgrows K, spill to a per-thread local array. Most queries never touch
-// the local part, so the walk issues no local-memory traffic in the common
-// case; deep ones stay exact (no entry is ever dropped).
-template <int K>
-struct ShortStack {
-  int32_t e[K];
-  int32_t n = 0;  // total entries
-  int32_t spill[kStackDepth];
-  __device__ __forceinline__ void push(int32_t v) {
-    if (n >= K) spill[n - K] = e[K - 1];
-#pragma unroll
-    for (int k = K - 1; k > 0; --k) e[k] = e[k - 1];
-    e[0] = v;
-    ++n;
-  }
-  __device__ __forceinline__ bool pop(int32_t& v) {
-    if (n == 0) return false;
-    v = e[0];
-#pragma unroll
-    for (int k = 0; k < K - 1; ++k) e[k] = e[k + 1];
-    --n;
-    if (n >= K) e[K - 1] = spill[n - K];
-    return true;
-  }
-};
-
-// K = 0: the whole stack in local memory (one store / load per push / pop;
-// measured faster than any register part on the issue-bound C2 main pass:
-// K = 6 +19%, K = 2 +67%, the shifts cost more issue slots than the local
-// accesses they save).
-template <>
-struct ShortStack<0> {
-  int32_t n = 0;
-  int32_t e[kStackDepth];
-  __device__ __forceinline__ void push(int32_t v) { e[n++] = v; }
-  __device__ __forceinline__ bool pop(int32_t& v) {
-    if (n == 0) return false;
-    v = e[--n];
-    return true;
-  }
-};
-
-// Depth-first walk of the eps-ball query with subtree containment. State per
-// query: the node to process next, the rank mask (leaves below min_rank are
-// hidden, query_sphere_masked bvh.hpp:45-72) and the pending left
-// subtrees on a ShortStack. Child ranges come from the record (aux = outer
-// range end) and the node's split (its index), so an entry is one node link.
-// Callbacks:
+// Traversal step with subtree containment. Also tracks `nlo`, the first leaf
+// rank of the current node (Karras ranges: a node's left child covers
+// [lo, split], its right child [split + 1, hi]; the root covers [0, n-1]), so
+// that a contained internal child is reported as its unmasked leaf-rank range
+// instead of being walked:
 //     bool visit(int32_t rank, int32_t aux, bool contained)
 //                                               leaf `rank` is within eps
 //                                               (its whole box when contained;
@@ -313,68 +232,71 @@ struct ShortStack<0> {
 //                                               (first >= min_rank) is a hit:
 //                                               kStop, kTaken, or kWalk (not
 //                                               taken as a run: descend)
-// Both children are classified with the same straight-line code (leaf or
-// internal, masked or not) so the lanes of a warp only diverge on the rare
-// visit / inside actions. The order in which leaves are reported is not the
-// reference's DFS order (callers depend only on the set, or, for early exit,
-// on min(count, minpts) — see k_fd_core).
-template <int D, int K>
-struct RangedWalk {
-  int32_t node, min_rank, end;  // end: last leaf rank under the start node
-  ShortStack<K> stack;
+// Pending subtrees go on `stack` (LocalStack below; a shared-memory ring
+// measured slower: it costs occupancy). Both children are classified with the
+// same straight-line code (leaf or internal, masked or not) so the lanes of a
+// warp only diverge on the rare visit / inside actions. Children are masked at
+// min_rank like query_sphere_masked (bvh.hpp:45-72); the order in which
+// leaves are reported is not the reference's DFS order (callers only depend
+// on the set, or, for early exit, on the count — see CoreQuery).
 
-  template <typename Visit, typename Inside, int kFast = -1>
-  __device__ __forceinline__ bool step(const TreeView& tv, const float* p, const BallTest& bt,
-                                       Visit& visit, Inside& inside) {
-    using T = NodeTraits<D>;
-    float f[T::kFloats];
-    load_node<D>(tv.nodes + static_cast<int64_t>(node) * T::kVec, f);
-    const int32_t left = __float_as_int(f[T::kIntOff + 0]);
-    const int32_t right = __float_as_int(f[T::kIntOff + 1]);
-    const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
-    const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
-    const bool leaf_l = left < 0, leaf_r = right < 0;
-    const int32_t split = node_split(tv, node);   // last rank of the left child
-    const int32_t max_r = leaf_r ? ~right : aux_r;  // last rank of the node
-    const int32_t first_l = leaf_l ? ~left : aux_l;
-    const int32_t lo_l = first_l > min_rank ? first_l : min_rank;
-    const int32_t lo_r = split + 1 > min_rank ? split + 1 : min_rank;
-    int cl = ball_classify<D, kFast>(p, f, f + D, bt);
-    int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
-    if (split < min_rank) cl = 0;
-    if (max_r < min_rank) cr = 0;
-    if (cl > 0 && (leaf_l || cl == 2)) {
-      if (leaf_l) {
-        if (!visit(~left, aux_l, cl == 2)) return false;
-      } else {
-        const int a = inside(lo_l, split);
-        if (a == kStop) return false;
-        if (a == kWalk) cl = 1;
-      }
+template <int D, typename Stack, typename Visit, typename Inside, int kFast = -1>
+__device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes, const float* p,
+                                                const BallTest& bt, int32_t min_rank,
+                                                int32_t& node, int32_t& nlo, Stack& stack,
+                                                Visit& visit, Inside& inside) {
+  using T = NodeTraits<D>;
+  float f[T::kFloats];
+  load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
+  const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+  const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+  const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+  const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+  const bool leaf_l = left < 0, leaf_r = right < 0;
+  const int32_t split = leaf_l ? ~left : aux_l;  // last rank of the left child
+  const int32_t max_r = leaf_r ? ~right : aux_r;
+  const int32_t lo_l = nlo > min_rank ? nlo : min_rank;
+  const int32_t lo_r = split + 1 > min_rank ? split + 1 : min_rank;
+  int cl = ball_classify<D, kFast>(p, f, f + D, bt);
+  int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
+  if (split < min_rank) cl = 0;
+  if (max_r < min_rank) cr = 0;
+  if (cl > 0 && (leaf_l || cl == 2)) {
+    if (leaf_l) {
+      if (!visit(~left, aux_l, cl == 2)) return false;
+    } else {
+      const int a = inside(lo_l, aux_l);
+      if (a == kStop) return false;
+      if (a == kWalk) cl = 1;
     }
-    if (cr > 0 && (leaf_r || cr == 2)) {
-      if (leaf_r) {
-        if (!visit(~right, aux_r, cr == 2)) return false;
-      } else {
-        const int a = inside(lo_r, aux_r);
-        if (a == kStop) return false;
-        if (a == kWalk) cr = 1;
-      }
-    }
-    const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
-    if (go_l && go_r) {
-      stack.push(left);
-      node = right;
-    } else if (go_l) {
-      node = left;
-    } else if (go_r) {
-      node = right;
-    } else if (!stack.pop(node)) {
-      return false;
-    }
-    return true;
   }
-};
+  if (cr > 0 && (leaf_r || cr == 2)) {
+    if (leaf_r) {
+      if (!visit(~right, aux_r, cr == 2)) return false;
+    } else {
+      const int a = inside(lo_r, aux_r);
+      if (a == kStop) return false;
+      if (a == kWalk) cr = 1;
+    }
+  }
+  const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
+  if (go_l && go_r) {
+    stack.push(make_int2(left, nlo));
+    node = right;
+    nlo = split + 1;
+  } else if (go_l) {
+    node = left;
+  } else if (go_r) {
+    node = right;
+    nlo = split + 1;
+  } else {
+    int2 e;
+    if (!stack.pop(e)) return false;
+    node = e.x;
+    nlo = e.y;
+  }
+  return true;
+}
 
 // bvh_step in the reference's exact visit order (leaf children at once, left
 // then right; internal children right subtree first), with contained
@@ -387,19 +309,19 @@ struct RangedWalk {
 //     bool visit(int32_t rank, int32_t aux, const float* lo, const float* hi)
 //     bool inside(int32_t first, int32_t last)    (false = stop the query)
 template <int D, typename Stack, typename Visit, typename Inside, int kFast = -1>
-__device__ __forceinline__ bool bvh_step_ordered(const TreeView& tv, const float* p,
+__device__ __forceinline__ bool bvh_step_ordered(const float4* __restrict__ nodes, const float* p,
                                                  const BallTest& bt, int32_t min_rank,
-                                                 int32_t& node, Stack& stack, Visit& visit,
-                                                 Inside& inside) {
+                                                 int32_t& node, int32_t& nlo, Stack& stack,
+                                                 Visit& visit, Inside& inside) {
   using T = NodeTraits<D>;
   float f[T::kFloats];
-  load_node<D>(tv.nodes + static_cast<int64_t>(node) * T::kVec, f);
+  load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
   const int32_t left = __float_as_int(f[T::kIntOff + 0]);
   const int32_t right = __float_as_int(f[T::kIntOff + 1]);
   const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
   const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
   const bool leaf_l = left < 0, leaf_r = right < 0;
-  const int32_t split = node_split(tv, node);
+  const int32_t split = leaf_l ? ~left : aux_l;
   const int32_t max_r = leaf_r ? ~right : aux_r;
   int cl = ball_classify<D, kFast>(p, f, f + D, bt);
   int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
@@ -408,21 +330,22 @@ __device__ __forceinline__ bool bvh_step_ordered(const TreeView& tv, const float
   if (leaf_l && cl > 0 && !visit(~left, aux_l, f, f + D)) return false;
   if (leaf_r && cr > 0 && !visit(~right, aux_r, f + 2 * D, f + 3 * D)) return false;
   const bool go_l = !leaf_l && cl > 0, go_r = !leaf_r && cr > 0;
-  const int32_t lo_l = aux_l > min_rank ? aux_l : min_rank;
+  const int32_t lo_l = nlo > min_rank ? nlo : min_rank;
   const int32_t lo_r = split + 1 > min_rank ? split + 1 : min_rank;
   // the next subtree in DFS order: right first, the left one waits
   bool have_next = false;
   if (go_r) {
-    if (go_l) stack.push(cl == 2 ? make_int2(~lo_l, split) : make_int2(left, 0));
+    if (go_l) stack.push(cl == 2 ? make_int2(~lo_l, aux_l) : make_int2(left, nlo));
     if (cr == 2) {
       if (!inside(lo_r, aux_r)) return false;
     } else {
       node = right;
+      nlo = split + 1;
       have_next = true;
     }
   } else if (go_l) {
     if (cl == 2) {
-      if (!inside(lo_l, split)) return false;
+      if (!inside(lo_l, aux_l)) return false;
     } else {
       node = left;
       have_next = true;
@@ -435,17 +358,23 @@ __device__ __forceinline__ bool bvh_step_ordered(const TreeView& tv, const float
       if (!inside(~e.x, e.y)) return false;
     } else {
       node = e.x;
+      nlo = e.y;
       have_next = true;
     }
   }
   return true;
 }
 
-// Full-depth traversal stack in local memory for bvh_step_ordered (whose run
-// entries keep the reference's DFS order for an order-dependent early exit).
-struct LocalStack {  // per-thread local memory
-  int2 e[kStackDepth];
+// Traversal stacks of (node, first leaf rank) entries for bvh_step_ranged.
+// (caching the top entry in registers measured slower: +14% on the C2 main pass)
+// Traversal stack handle: the entries in a per-thread local array owned by the
+// kernel, the top index a plain member that stays in a register (a struct
+// holding both the array and the top keeps the top in local memory too: one
+// more local load and store per push and pop).
+struct LocalStack {
+  int2* e;
   int top = 0;
+  __device__ __forceinline__ explicit LocalStack(int2* buf) : e(buf) {}
   __device__ __forceinline__ void push(int2 v) { e[top++] = v; }
   __device__ __forceinline__ bool pop(int2& v) {
     if (top == 0) return false;
@@ -465,15 +394,14 @@ struct LocalStack {  // per-thread local memory
 // the root, while exactly one child of the node can matter (its box meets U
 // and its max rank >= the warp's min_rank) and that child is internal, step
 // into it. Nothing outside the stop node can be a hit for any lane, so each
-// lane's own traversal starts there (node; its last leaf rank in `end`)
-// instead of at the root.
+// lane's own traversal starts there (node, nlo) instead of at the root.
 // Every lane must call it (valid = false for lanes without a query).
 template <int D>
-__device__ __forceinline__ void warp_start_node(const TreeView& tv, const float* p, bool valid,
-                                                const BallTest& bt, int32_t min_rank,
-                                                int32_t& node, int32_t& end) {
+__device__ __forceinline__ void warp_start_node(const float4* __restrict__ nodes, const float* p,
+                                                bool valid, const BallTest& bt,
+                                                int32_t min_rank, int32_t& node, int32_t& nlo) {
   node = 0;
-  end = tv.spare;  // num_leaves - 1
+  nlo = 0;
   float ulo[3], uhi[3];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -487,9 +415,10 @@ __device__ __forceinline__ void warp_start_node(const TreeView& tv, const float*
   using T = NodeTraits<D>;
   while (true) {
     float f[T::kFloats];
-    load_node<D>(tv.nodes + static_cast<int64_t>(node) * T::kVec, f);
+    load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
     const int32_t left = __float_as_int(f[T::kIntOff + 0]);
     const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+    const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
     const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
     auto meets = [&](const float* lo, const float* hi) {
       bool ok = true;
@@ -497,14 +426,13 @@ __device__ __forceinline__ void warp_start_node(const TreeView& tv, const float*
       for (int k = 0; k < D; ++k) ok = ok && lo[k] <= uhi[k] && hi[k] >= ulo[k];
       return ok;
     };
-    const int32_t split = node_split(tv, node);
-    const int32_t max_r = right < 0 ? ~right : aux_r;
-    const bool live_l = split >= min_rank && meets(f, f + D);
+    const int32_t max_l = left < 0 ? ~left : aux_l, max_r = right < 0 ? ~right : aux_r;
+    const bool live_l = max_l >= min_rank && meets(f, f + D);
     const bool live_r = max_r >= min_rank && meets(f + 2 * D, f + 3 * D);
     if (live_l && !live_r && left >= 0) {
       node = left;
-      end = split;
     } else if (live_r && !live_l && right >= 0) {
+      nlo = max_l + 1;
       node = right;
     } else {
       return;
@@ -513,19 +441,21 @@ __device__ __forceinline__ void warp_start_node(const TreeView& tv, const float*
 }
 
 // One query per thread, started at the warp's common start node. Q provides
-// begin(q) (false: no query), step(), end(), p[3], node and mask_rank (the
-// query's min_rank). Starting below the root skips only nodes with a single
-// live child, so the order of the query's visit calls is the same as from the
-// root (the DenseBox core pass depends on that order).
+// begin(q) (false: no query), step(), end(), p[3], node, nlo and mask_rank
+// (the query's min_rank). Starting below the root skips only nodes with a
+// single live child, so the order of the query's visit calls is the same as
+// from the root (the DenseBox core pass depends on that order).
 template <int D, class Q>
-__device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp, const TreeView& tv,
+__device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp,
+                                                    const float4* __restrict__ nodes,
                                                     const BallTest& bt) {
   const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = q < m && qp.begin(q);
-  int32_t node, end;
-  warp_start_node<D>(tv, qp.p, valid, bt, valid ? qp.mask_rank : 0, node, end);
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, qp.p, valid, bt, valid ? qp.mask_rank : 0, node, nlo);
   if (valid) {
     qp.node = node;
+    qp.nlo = nlo;
     while (qp.step()) {
     }
     qp.end();
@@ -535,11 +465,11 @@ __device__ __forceinline__ void run_query_warpstart(int64_t m, Q& qp, const Tree
 // The whole query on one thread.
 template <int D, typename Visit>
 __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, const float* p,
-                                          const BallTest& bt, Visit& visit) {
+                                          const BallTest& bt, int32_t min_rank, Visit& visit) {
   int32_t stack[kStackDepth];
   int top = 0;
   int32_t node = 0;
-  while (bvh_step<D>(nodes, p, bt, node, top, stack, visit)) {
+  while (bvh_step<D>(nodes, p, bt, min_rank, node, top, stack, visit)) {
   }
 }
 
@@ -547,7 +477,6 @@ __device__ __forceinline__ void bvh_query(const float4* __restrict__ nodes, cons
 // Device view of a built tree.
 struct DeviceBvh {
   int32_t num_leaves = 0;
-  const int32_t* root_split = nullptr;  // device word: split of the root
   float4* nodes = nullptr;        // num_leaves - 1 nodes (root at 0) + 1 spare slot,
                                   // NodeTraits<D>::kVec float4 each
   int32_t* leaf_order = nullptr;  // leaf rank -> primitive index (sorted values)

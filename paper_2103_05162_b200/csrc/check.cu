@@ -46,7 +46,7 @@ k_border_check(const float4* __restrict__ nodes, const float4* __restrict__ leaf
     }
     return true;
   };
-  bvh_query<D>(nodes, p, bt, visit);
+  bvh_query<D>(nodes, p, bt, 0, visit);
   if (!ok) atomicMin(bad, static_cast<unsigned long long>(i));
 }
 

@@ -33,18 +33,18 @@ namespace tcb {
 namespace {
 
 constexpr int kQueryBlock = 128;  // 64 / 256 measured equal or slower
-
 // Resident blocks per SM the FoF main pass is compiled for (ptxas caps its
-// registers at 36): 14 x 4 warps instead of 12 at its natural 40 registers,
-// main pass 19.2 -> 18.5 ms on C2 despite a few spilled bytes.
+// registers at 40): 12 x 4 warps. With the warp-batched union actions 12 is
+// faster than 14 (32 registers, more spills) and 10 (C2 main 17.9 vs 19.8 /
+// 18.7 ms); the per-query form measured best at 14 (18.5 ms).
 #ifndef TCB_FOF_MIN_BLOCKS
-#define TCB_FOF_MIN_BLOCKS 14
+#define TCB_FOF_MIN_BLOCKS 12
 #endif
 constexpr int kFofMinBlocks = TCB_FOF_MIN_BLOCKS;
-// the same for the minpts > 2 main pass (12: main 22.2 -> 21.2 ms on C3);
+// the same for the minpts > 2 main pass (10: main 21.7 -> 21.3 ms on C3);
 // the core pass is faster uncapped
 #ifndef TCB_MAIN_MIN_BLOCKS
-#define TCB_MAIN_MIN_BLOCKS 12
+#define TCB_MAIN_MIN_BLOCKS 10
 #endif
 constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
 
@@ -64,44 +64,73 @@ __device__ __forceinline__ void flush_counter(unsigned long long* dst, unsigned 
 }
 
 // fdbscan_mark_cores query (dbscan.cpp:36-58): unmasked, early exit once
-// minpts neighbours (self included) are seen. Every hit counts one distance
-// evaluation until the stop, so the reference's counter is min(|N|, minpts)
-// whatever the visit order: a subtree whose box lies inside the ball adds its
-// leaf count at once, capped at the stop.
+// minpts neighbours (self included) are seen. A subtree whose box lies inside
+// the ball adds its leaf count at once; when that crosses minpts the
+// reference would have stopped inside it after exactly minpts - count more
+// leaf hits, so the distance counter (one per hit, dists == count) is still
+// the reference's.
 template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
-k_fd_core(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTest bt, int minpts,
-          uint8_t* __restrict__ flags, DevCounters* ctr) {
-  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
-  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const bool valid = r < m;
-  float p[3] = {0.f, 0.f, 0.f};
-  if (valid) {
-    int32_t id;
+struct CoreQuery {
+  const float4* __restrict__ nodes;
+  const float4* __restrict__ leaf_pt;
+  BallTest bt;
+  int minpts;
+  uint8_t* __restrict__ flags;
+  LocalStack stack;  // handle of the kernel's per-thread stack array
+  unsigned long long dists = 0;
+  float p[3];
+  int32_t id, node, nlo;
+  int count;
+  __device__ bool begin(int64_t r) {
     load_query<D>(leaf_pt, r, p, &id);
+    id = static_cast<int32_t>(r);  // flags are kept in rank space
+    count = 0;
+    node = 0;
+    nlo = 0;
+    stack.reset();
+    return true;
   }
-  RangedWalk<D, kStackRegs> walk;
-  walk.min_rank = 0;
-  warp_start_node<D>(tv, p, valid, bt, 0, walk.node, walk.end);
-  int count = 0;
-  if (valid) {
+  __device__ bool step() {
     auto visit = [&](int32_t, int32_t, bool) -> bool {
+      ++dists;
       return ++count < minpts;  // early exit (dbscan.cpp:48-53)
     };
     auto inside = [&](int32_t first, int32_t last) -> int {
       const int64_t k = static_cast<int64_t>(last) - first + 1;
       if (count + k >= minpts) {
+        dists += static_cast<unsigned long long>(minpts - count);
         count = minpts;
         return kStop;
       }
+      dists += static_cast<unsigned long long>(k);
       count += static_cast<int>(k);
       return kTaken;
     };
-    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
-    }
-    if (count >= minpts) flags[r] = 1;  // flags are kept in rank space
+    return bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, 0, node, nlo, stack, visit, inside);
   }
-  flush_counter(&ctr->dists, static_cast<unsigned long long>(count));
+  __device__ void end() {
+    if (count >= minpts) flags[id] = 1;
+  }
+};
+
+template <int D, int kFast>
+__global__ void __launch_bounds__(kQueryBlock)
+k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
+  int2 stack_buf[kStackDepth];
+  CoreQuery<D, kFast> q{nodes, leaf_pt, bt, minpts, flags, LocalStack(stack_buf)};
+  // one query per thread, started at the warp's common start node
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
+  if (valid) q.begin(r);
+  warp_start_node<D>(nodes, q.p, valid, bt, 0, q.node, q.nlo);
+  if (valid) {
+    while (q.step()) {
+    }
+    q.end();
+  }
+  flush_counter(&ctr->dists, q.dists);
 }
 
 // fdbscan_main_phase (dbscan.cpp:60-88): one thread per leaf rank r (Morton
@@ -120,11 +149,10 @@ k_fd_core(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTes
 //   otherwise the subtree is walked leaf by leaf (per-pair rule).
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kMainMinBlocks)
-k_fd_main(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTest bt,
-          const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+          BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
           const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
           int32_t* __restrict__ reach, DevCounters* ctr) {
-  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -135,9 +163,8 @@ k_fd_main(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTes
     load_query<D>(leaf_pt, r, p, &id);
     rank = static_cast<int32_t>(r);
   }
-  RangedWalk<D, kStackRegs> walk;
-  walk.min_rank = rank + 1;
-  warp_start_node<D>(tv, p, valid, bt, rank + 1, walk.node, walk.end);
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
   if (valid) {
     const bool core_r = flags[rank] != 0;
     int32_t hint = rank;
@@ -162,7 +189,10 @@ k_fd_main(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTes
       pairs += static_cast<unsigned long long>(size);
       return kTaken;
     };
-    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
+    int2 stack_buf[kStackDepth];
+    LocalStack stack(stack_buf);
+    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
     }
   }
   flush_counter(&ctr->pairs, pairs);
@@ -187,10 +217,9 @@ __global__ void k_noncore_ind(const uint8_t* __restrict__ flags, int64_t n,
 // stay exact.
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kFofMinBlocks)
-k_fd_main_fof(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, BallTest bt,
-              int32_t* __restrict__ parent, const int32_t* __restrict__ key,
+k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+              BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
               int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {
-  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -202,9 +231,8 @@ k_fd_main_fof(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, Bal
     load_query<D>(leaf_pt, r, p, &id);
     rank = static_cast<int32_t>(r);
   }
-  RangedWalk<D, kStackRegs> walk;
-  walk.min_rank = rank + 1;
-  warp_start_node<D>(tv, p, valid, bt, rank + 1, walk.node, walk.end);
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
   if (valid) {
     int32_t hint = rank;
     auto visit = [&](int32_t s, int32_t, bool) -> bool {
@@ -220,16 +248,149 @@ k_fd_main_fof(DeviceBvh tree, const float4* __restrict__ leaf_pt, int64_t m, Bal
       record_run(reach, first, last);
       return kTaken;
     };
-    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
-      TCB_PROBE_ONLY(++pr[0]; pr[3] += walk.stack.n > kStackRegs;)
+    int2 stack_buf[kStackDepth];
+    LocalStack stack(stack_buf);
+    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, rank + 1, node, nlo, stack, visit, inside)) {
+      TCB_PROBE_ONLY(++pr[0];)
     }
-    TCB_PROBE_ONLY(++pr[0]; pr[6] = pr[0];)
+    TCB_PROBE_ONLY(++pr[0]; pr[5] += pairs == 0; pr[6] = pr[0]; if (pairs == 0) pr[3] = pr[0];)
   }
   flush_counter(&ctr->pairs, pairs);
   flush_counter(&ctr->dists, pairs);
   TCB_PROBE_ONLY(for (int k = 0; k < 6; ++k) flush_counter(&ctr->probe[k], pr[k]);
                  const unsigned wmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(pr[6]));
                  if ((threadIdx.x & 31) == 0) atomicAdd(&ctr->probe[6], wmax);)
+}
+
+// k_fd_main_fof with warp-batched union actions. In the per-query form a leaf
+// hit or a contained run sends its lane into the union-find code on its own
+// (2-3 active lanes per instruction there: a halo query meets a neighbour on
+// one step in ten), so the warp pays the whole union path for each of them.
+// Here a step only classifies the node's two children and appends the
+// actions it found — (query rank, first, last), a leaf being first == last —
+// to a per-warp queue in shared memory (ballot + popc offsets); whenever the
+// queue holds 32 actions the warp resolves 32 of them at once, one per lane,
+// with the query's root hint kept per query in shared memory (any value a
+// hint ever held is an ancestor of the query's set, so a hint updated by
+// another lane is still a valid hint). Same unions, same run records, same
+// pair counts: the partition and counters are unchanged.
+#ifndef TCB_FOF_BATCH
+#define TCB_FOF_BATCH 1
+#endif
+constexpr int kActCap = 96;  // < 32 queued + up to 2 per lane per step
+
+__device__ __forceinline__ void fof_resolve(int3 e, int32_t* hints, int32_t warp_base,
+                                            int32_t* __restrict__ parent,
+                                            const int32_t* __restrict__ key,
+                                            int32_t* __restrict__ reach, uint8_t* mark) {
+  int32_t* hp = hints + (e.x - warp_base);
+  int32_t hint = *hp;
+  const int32_t old = hint;
+  uf_unite_hinted_keyed(parent, key, e.x, e.y, hint, mark);
+  if (hint != old) *hp = hint;
+  record_run(reach, e.y, e.z);
+}
+
+template <int D, int kFast>
+__global__ void __launch_bounds__(kQueryBlock, kFofMinBlocks)
+k_fd_main_fof_q(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+                BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
+                int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {
+  __shared__ int3 s_act[kQueryBlock / 32][kActCap];
+  __shared__ int32_t s_hint[kQueryBlock];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
+  const int32_t rank = static_cast<int32_t>(r);
+  const int32_t warp_base = rank - lane;
+  int3* act = s_act[w];
+  int32_t* hints = s_hint + (w << 5);
+  unsigned long long pairs = 0;
+  float p[3] = {0.f, 0.f, 0.f};
+  if (valid) {
+    int32_t id;
+    load_query<D>(leaf_pt, r, p, &id);
+  }
+  hints[lane] = rank;
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
+  const int32_t min_rank = rank + 1;
+  // the stack top stays a register: a LocalStack member would live in local
+  // memory next to its array (an extra load / store per push and pop)
+  int2 stack[kStackDepth];
+  int top = 0;
+  bool active = valid;
+  int qn = 0;  // warp-uniform queue length
+  using T = NodeTraits<D>;
+  while (true) {
+    int na = 0;
+    int32_t f0 = 0, l0 = 0, f1 = 0, l1 = 0;
+    if (active) {
+      float f[T::kFloats];
+      load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
+      const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+      const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+      const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+      const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+      const bool leaf_l = left < 0, leaf_r = right < 0;
+      const int32_t split = leaf_l ? ~left : aux_l;  // last rank of the left child
+      const int32_t max_r = leaf_r ? ~right : aux_r;
+      int cl = ball_classify<D, kFast>(p, f, f + D, bt);
+      int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
+      if (split < min_rank) cl = 0;
+      if (max_r < min_rank) cr = 0;
+      const bool act_l = cl > 0 && (leaf_l || cl == 2);
+      const bool act_r = cr > 0 && (leaf_r || cr == 2);
+      // a leaf is the run [rank, rank]; a contained child its unmasked range
+      const int32_t fl = leaf_l ? ~left : (nlo > min_rank ? nlo : min_rank);
+      const int32_t fr = leaf_r ? ~right : (split + 1 > min_rank ? split + 1 : min_rank);
+      if (act_l) pairs += static_cast<unsigned>(split - fl + 1);
+      if (act_r) pairs += static_cast<unsigned>(max_r - fr + 1);
+      na = static_cast<int>(act_l) + static_cast<int>(act_r);
+      f0 = act_l ? fl : fr;
+      l0 = act_l ? split : max_r;
+      f1 = fr;
+      l1 = max_r;
+      const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
+      if (go_l && go_r) {
+        stack[top++] = make_int2(left, nlo);
+        node = right;
+        nlo = split + 1;
+      } else if (go_l) {
+        node = left;
+      } else if (go_r) {
+        node = right;
+        nlo = split + 1;
+      } else if (top > 0) {
+        const int2 e = stack[--top];
+        node = e.x;
+        nlo = e.y;
+      } else {
+        active = false;
+      }
+    }
+    const unsigned m1 = __ballot_sync(0xffffffffu, na >= 1);
+    const unsigned m2 = __ballot_sync(0xffffffffu, na == 2);
+    if (m1) {
+      const unsigned lt = (1u << lane) - 1u;
+      const int off = qn + __popc(m1 & lt) + __popc(m2 & lt);
+      if (na >= 1) act[off] = make_int3(rank, f0, l0);
+      if (na == 2) act[off + 1] = make_int3(rank, f1, l1);
+      qn += __popc(m1) + __popc(m2);
+      if (qn >= 32) {
+        __syncwarp();
+        qn -= 32;
+        fof_resolve(act[qn + lane], hints, warp_base, parent, key, reach, mark);
+        __syncwarp();
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+  }
+  __syncwarp();
+  if (lane < qn) fof_resolve(act[lane], hints, warp_base, parent, key, reach, mark);
+  flush_counter(&ctr->pairs, pairs);
+  flush_counter(&ctr->dists, pairs);
 }
 
 __global__ void k_permute(const uint8_t* __restrict__ src, const int32_t* __restrict__ order,
@@ -393,7 +554,7 @@ void fdbscan_core_pass(const BuiltBvh& b, int64_t n, double eps2, int minpts,
   const BallTest bt = BallTest::make(eps2);
   auto core = bt.fast ? k_fd_core<D, 1> : k_fd_core<D, 0>;
   note_launch(), core<<<grid_for(n, kQueryBlock, INT32_MAX), kQueryBlock, 0, s>>>(
-      b.tree, b.leaf_pt, n, bt, minpts, flags, d_ctr);
+      b.tree.nodes, b.leaf_pt, n, bt, minpts, flags, d_ctr);
   TCB_CUDA(cudaGetLastError());
 }
 
@@ -408,8 +569,9 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
   int32_t* tile_max = scratch.alloc_n<int32_t>(cover_tiles(n));
   TCB_CUDA(cudaMemsetAsync(reach, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
   if (force_core) {
-    auto fof = bt.fast ? k_fd_main_fof<D, 1> : k_fd_main_fof<D, 0>;
-    note_launch(), fof<<<grid, kQueryBlock, 0, s>>>(b.tree, b.leaf_pt, n, bt, parent, key,
+    auto fof = TCB_FOF_BATCH ? (bt.fast ? k_fd_main_fof_q<D, 1> : k_fd_main_fof_q<D, 0>)
+                             : (bt.fast ? k_fd_main_fof<D, 1> : k_fd_main_fof<D, 0>);
+    note_launch(), fof<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, parent, key,
                                                    reach, flags, d_ctr);
   } else {
     int32_t* ind = scratch.alloc_n<int32_t>(n + 1);
@@ -418,7 +580,7 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
     note_launch(), k_noncore_ind<<<grid_for(n + 1, 256), 256, 0, s>>>(flags, n, ind);
     exclusive_scan_i32(ind, noncore_before, n + 1, nullptr, scan_tmp, s);
     auto main = bt.fast ? k_fd_main<D, 1> : k_fd_main<D, 0>;
-    note_launch(), main<<<grid, kQueryBlock, 0, s>>>(b.tree, b.leaf_pt, n, bt, flags, parent,
+    note_launch(), main<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags, parent,
                                                     key, noncore_before, reach, d_ctr);
   }
   // covered runs (all-core): join each covered rank to its predecessor

@@ -40,15 +40,13 @@ __global__ void k_flatten(int32_t* parent, int64_t n) {
 
 template <int D>
 void point_bvh(const float* d_coords, int64_t n, Scratch& scratch, std::vector<float4>& nodes,
-               std::vector<int32_t>& order, int32_t* root) {
+               std::vector<int32_t>& order) {
   DevCounters* ctr = scratch.alloc_n<DevCounters>(1);
   TCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), scratch.stream()));
   PrimSource src;
   src.coords = d_coords;
   src.count = n;
   BuiltBvh b = build_bvh<D>(src, true, ctr, scratch, nullptr);
-  TCB_CUDA(cudaMemcpyAsync(root, b.tree.root_split, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                           scratch.stream()));
   const int64_t nn = n > 1 ? n : 1;  // n - 1 internal nodes + the spare slot
   nodes.resize(static_cast<size_t>(nn * NodeTraits<D>::kVec));
   order.resize(static_cast<size_t>(n));
@@ -93,15 +91,14 @@ TC_EXPORT tc_status tcg_debug_point_bvh(const float* coords, int64_t n, int dim,
     Stream st;
     std::vector<float4> nodes;
     std::vector<int32_t> order;
-    int32_t root_split = 0;
     {
       Scratch scratch(st.s);
       float* d = scratch.alloc_n<float>(n * dim);
       TCB_CUDA(cudaMemcpyAsync(d, coords, sizeof(float) * n * dim, cudaMemcpyHostToDevice, st.s));
       if (dim == 2)
-        point_bvh<2>(d, n, scratch, nodes, order, &root_split);
+        point_bvh<2>(d, n, scratch, nodes, order);
       else
-        point_bvh<3>(d, n, scratch, nodes, order, &root_split);
+        point_bvh<3>(d, n, scratch, nodes, order);
     }
     std::memcpy(leaf_ids, order.data(), sizeof(int32_t) * n);
     if (n == 1) return TC_OK;
@@ -118,9 +115,7 @@ TC_EXPORT tc_status tcg_debug_point_bvh(const float* coords, int64_t n, int dim,
       todo.pop_back();
       const float* f = reinterpret_cast<const float*>(nodes.data() + static_cast<int64_t>(it.ours) * kv);
       const int32_t* ii = reinterpret_cast<const int32_t*>(f + 4 * dim);
-      // our index -> split (bvh.cuh node_split): root at 0, node 0 at the spare slot
-      const int32_t split = it.ours == 0 ? root_split
-                            : (it.ours == static_cast<int32_t>(n - 1) ? 0 : it.ours);
+      const int32_t split = ii[0] < 0 ? ~ii[0] : ii[2];  // last rank of the left child
       const int32_t i = it.karras;
       left[i] = ii[0] < 0 ? ii[0] : split;
       right[i] = ii[1] < 0 ? ii[1] : split + 1;

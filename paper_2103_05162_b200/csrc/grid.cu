@@ -285,7 +285,7 @@ constexpr int kDbMinBlocks = 10;
 
 template <int D, int kFast>
 struct DbCoreQuery {
-  TreeView tv;
+  const float4* __restrict__ nodes;
   const float4* __restrict__ qpt;
   const float4* __restrict__ sorted_pt;
   const int32_t* __restrict__ cell_begin;
@@ -293,7 +293,7 @@ struct DbCoreQuery {
   BallTest bt;
   int minpts;
   uint8_t* __restrict__ flags;
-  LocalStack* stack;  // per-thread traversal stack, kept outside the struct
+  LocalStack stack;  // handle of the kernel's per-thread stack array
   const MemberTree* mt;   // members in member order
   const MemberTree* smt;  // the same cells' members in spatial order
   const int32_t* __restrict__ qoff;  // rank -> points before it (exclusive prefix)
@@ -302,7 +302,7 @@ struct DbCoreQuery {
   const int32_t* __restrict__ list;  // query slots to run (the SinglePoint ones)
   unsigned long long dists = 0;
   float p[3];
-  int32_t id, slot, node, mask_rank = 0;
+  int32_t id, slot, node, nlo, mask_rank = 0;
   int count;
   // the stopping scan of a long cut DenseBox, left to the warp (k_db_core)
   int32_t pend_kb = -1, pend_ke = 0, pend_rem = 0;
@@ -316,8 +316,9 @@ struct DbCoreQuery {
     p[2] = qp.z;
     count = 0;
     node = 0;
+    nlo = 0;
     pend_kb = -1;
-    stack->reset();
+    stack.reset();
     return true;
   }
   __device__ bool step() {
@@ -379,7 +380,7 @@ struct DbCoreQuery {
       return true;
     };
     return bvh_step_ordered<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        tv, p, bt, 0, node, *stack, visit, inside);
+        nodes, p, bt, 0, node, nlo, stack, visit, inside);
   }
   __device__ void end() {
     if (count >= minpts) flags[slot] = 1;
@@ -388,17 +389,16 @@ struct DbCoreQuery {
 
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
-k_db_core(DeviceBvh tree, const float4* __restrict__ qpt, int64_t n,
+k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
           uint8_t* __restrict__ flags, DevCounters* ctr, MemberTree mt,
           MemberTree smt, const int32_t* __restrict__ qoff, int32_t num_prims,
           const int32_t* __restrict__ list, int64_t m) {
-  LocalStack stack;
-  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
-  DbCoreQuery<D, kFast> q{tv, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, &stack, &mt,
+  int2 stack_buf[kStackDepth];
+  DbCoreQuery<D, kFast> q{nodes, qpt, sorted_pt, cell_begin, cell_end, bt, minpts, flags, LocalStack(stack_buf), &mt,
                    &smt, qoff, n, num_prims, list};
-  run_query_warpstart<D>(m, q, tv, bt);
+  run_query_warpstart<D>(m, q, nodes, bt);
   // The stopping scans: position of the rem-th member within eps of p in
   // member order, 32 members per step across the warp (same predicate as the
   // per-member loop; the members of a cell are in random spatial order, so a
@@ -460,14 +460,13 @@ k_db_core(DeviceBvh tree, const float4* __restrict__ qpt, int64_t n,
 // are walked. minpts == 2: every run is taken (all pairs are unions).
 template <int D, bool kForceCore, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
-k_db_main_ranged(DeviceBvh tree, const float4* __restrict__ qpt,
+k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
                  const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
                  const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
                  BallTest bt, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
                  const int32_t* __restrict__ key, const int32_t* __restrict__ qoff,
                  const int32_t* __restrict__ noncore_before, int32_t* __restrict__ reach,
                  DevCounters* ctr, MemberTree mt) {
-  const TreeView tv = tree_view(tree.nodes, tree.root_split, tree.num_leaves);
   const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = q < n;
   unsigned long long pairs = 0, dists = 0;
@@ -481,9 +480,8 @@ k_db_main_ranged(DeviceBvh tree, const float4* __restrict__ qpt,
     p[1] = qp.y;
     p[2] = qp.z;
   }
-  RangedWalk<D, kStackRegs> walk;
-  walk.min_rank = own + 1;
-  warp_start_node<D>(tv, p, valid, bt, own + 1, walk.node, walk.end);
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, own + 1, node, nlo);
   if (valid) {
     const bool core_i = kForceCore ? true : flags[i] != 0;
     int32_t hint = i;
@@ -546,7 +544,10 @@ k_db_main_ranged(DeviceBvh tree, const float4* __restrict__ qpt,
       dists += static_cast<unsigned long long>(cnt);
       return kTaken;
     };
-    while (walk.template step<decltype(visit), decltype(inside), kFast>(tv, p, bt, visit, inside)) {
+    int2 stack_buf[kStackDepth];
+    LocalStack stack(stack_buf);
+    while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+        nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
     }
   }
   unsigned long long v = warp_sum(dists);
@@ -860,7 +861,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
                                                                             num_prims, list);
     auto core = bt.fast ? k_db_core<D, 1> : k_db_core<D, 0>;
     note_launch(), core<<<grid_for(sparse_points, kQueryBlock, INT32_MAX), kQueryBlock, 0, st>>>(
-        b.tree, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr, mt, smt,
+        b.tree.nodes, qpt, n, sorted_pt, cell_begin, cell_end, bt, minpts, flags, ctr, mt, smt,
         qoff, num_prims, list, sparse_points);
   }
   // ---- main pass ----
@@ -879,7 +880,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
   auto main = minpts == 2 ? (bt.fast ? k_db_main_ranged<D, true, 1> : k_db_main_ranged<D, true, 0>)
                           : (bt.fast ? k_db_main_ranged<D, false, 1> : k_db_main_ranged<D, false, 0>);
-  note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree, qpt, qrank, n, sorted_pt, cell_begin,
+  note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin,
                                                 cell_end, bt, flags, parent, qkey, qoff,
                                                 noncore_before, reach, ctr, mt);
   launch_cover_joins(reach, num_prims, tile_max,

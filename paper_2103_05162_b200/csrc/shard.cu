@@ -75,7 +75,7 @@ k_near(const float4* __restrict__ nodes, const float* __restrict__ coords, int64
     hit = true;
     return false;
   };
-  bvh_query<D>(nodes, p, bt, visit);
+  bvh_query<D>(nodes, p, bt, 0, visit);
   mask[i] = hit ? 1 : 0;
 }
 
