@@ -118,15 +118,18 @@ class ClockSampler:
 
 
 def load_traffic():
-    """dram bytes (read + write) per launch of the main-pass kernel from the
-    committed `ncu --set full` summary, if present."""
+    """(dram bytes read + write per launch, limiter evidence) of the main-pass
+    kernel from the committed `ncu --set full` summary (profiles/traffic.json)."""
     path = os.path.join(HERE, "profiles", "traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
-        return t.get("k_fd_main_dram_bytes_per_launch")
+        lim = dict(t.get("limiter") or {})
+        if lim:
+            lim["source"] = t.get("source")
+        return t.get("k_fd_main_dram_bytes_per_launch"), lim or None
     except Exception:
-        return None
+        return None, None
 
 
 def reference_input(n):
@@ -428,7 +431,7 @@ def main():
     main_ms = stage_sum.get("main", 0.0) / steps_n
     peak, peak_kind = peaks()
     achieved = (B_ALG_MAIN * n) / (main_ms * 1e-3) / 1e9 if main_ms > 0 else None
-    traffic = load_traffic()
+    traffic, limiter = load_traffic()
     total_gbs = B_ALG_TOTAL * n / (ms_per_step * 1e-3) / 1e9
 
     if rank == 0:
@@ -446,14 +449,17 @@ def main():
             "stage_ms": {k: round(v / steps_n, 3) for k, v in stage_sum.items()},
             "hbm_gbs_end_to_end": round(total_gbs, 1),
             "roofline": {"bound": "hbm",
-                         "kernel": "main stage: k_fd_main_fof (fused traversal + union-find) "
-                                   "+ k_cover_* run unions, timed by stage events",
+                         "kernel": "main stage: k_fd_main_fof_q (fused traversal + warp-batched "
+                                   "union-find) + k_cover_* run unions, timed by stage events",
                          "achieved": round(achieved, 1) if achieved else None, "peak": peak,
                          "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
                          "traffic": traffic,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                         "alg_bytes_per_point": B_ALG_MAIN},
+                         "alg_bytes_per_point": B_ALG_MAIN,
+                         # what actually bounds the traversal (ncu): the L1 data
+                         # pipe and the issue slots, not HBM
+                         "limiter": limiter},
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                     "h2d_bytes_per_step": n * 3 * 4, "d2h_bytes_per_step": n * 5,
                     "ms_per_step": round(e2e_s * 1e3, 3), "api": "tc_cluster (C ABI)"},

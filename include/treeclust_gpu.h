@@ -190,6 +190,22 @@ tc_status tcg_debug_sort_pairs(const uint64_t* keys, int64_t n, uint64_t* keys_o
 /* Concurrent device unite() over m edges (2*m ints) on n elements, then
  * flatten; parent_out[n] = representative (minimum index of the component). */
 tc_status tcg_debug_union_find(const int32_t* edges, int64_t m, int32_t n, int32_t* parent_out);
+/* Device build_grid (REF dense_grid.cpp:23-77, ref accessor DenseGrid): perm[n]
+ * (sorted position -> point), cell_of_point[n]; when the cell count is <= cap,
+ * cell_id / cell_begin / cell_end / cell_dense[cells]. *num_cells = count. */
+tc_status tcg_debug_grid(const float* coords, int64_t n, int dim, float eps, int minpts,
+                         int32_t* perm, int32_t* cell_of_point, uint64_t* cell_id,
+                         int32_t* cell_begin, int32_t* cell_end, uint8_t* cell_dense,
+                         int64_t cap, int64_t* num_cells);
+/* The DenseBox tree over make_mixed_primitives (REF dense_grid.cpp:79-98,
+ * bvh.cpp:10-124) in the reference's node view: per leaf rank the kind
+ * (1 = DenseBox) and id (point or dense-cell index); left/right/max_rank and
+ * boxes per internal node as tcg_debug_point_bvh. Filled when the leaf count
+ * is <= cap; *num_leaves = leaf count. */
+tc_status tcg_debug_mixed_bvh(const float* coords, int64_t n, int dim, float eps, int minpts,
+                              uint8_t* leaf_kind, int32_t* leaf_id, int32_t* left,
+                              int32_t* right, int32_t* max_rank, float* boxes, int64_t cap,
+                              int64_t* num_leaves);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -109,6 +109,25 @@ def build_grid(coords, eps, minpts) -> dict:
             "end": ce[:m], "dense": cd[:m].astype(bool)}
 
 
+def mixed_bvh(coords, eps, minpts) -> dict:
+    """The DenseBox tree over make_mixed_primitives (dense_grid.cpp:79-98): leaf
+    kinds (1 = DenseBox) / ids per rank and the Bvh node accessors."""
+    a, p = _f32(coords)
+    n, d = a.shape
+    kind = np.empty(n, np.uint8)
+    lid = np.empty(n, np.int32)
+    m1 = max(n - 1, 1)
+    left, right, mr = (np.zeros(m1, np.int32) for _ in range(3))
+    boxes = np.zeros((m1, 6), np.float32)
+    m = lib().ref_mixed_bvh(p, n, d, C.c_float(eps), int(minpts), _ptr(kind, C.c_uint8),
+                            _ptr(lid, C.c_int32), _ptr(left, C.c_int32), _ptr(right, C.c_int32),
+                            _ptr(mr, C.c_int32), _ptr(boxes, C.c_float), n)
+    if m < 0:
+        raise ValueError("reference mixed BVH build failed")
+    return {"leaf_kind": kind[:m], "leaf_id": lid[:m], "left": left[:m - 1],
+            "right": right[:m - 1], "max_rank": mr[:m - 1], "boxes": boxes[:m - 1]}
+
+
 def dbscan(coords, eps, minpts, algo: int, threads: int = 1) -> dict:
     """dbscan_run (algo 0 FDBSCAN, 1 DenseBox) or dbscan_bruteforce (algo 2)."""
     a, p = _f32(coords)

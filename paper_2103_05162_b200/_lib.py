@@ -95,6 +95,16 @@ SIGNATURES = {
                                        C.POINTER(C.c_int32)]),
     "tcg_debug_union_find": (C.c_int, [C.POINTER(C.c_int32), C.c_int64, C.c_int32,
                                        C.POINTER(C.c_int32)]),
+    "tcg_debug_grid": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int, C.c_float, C.c_int,
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_uint8), C.c_int64,
+                                 C.POINTER(C.c_int64)]),
+    "tcg_debug_mixed_bvh": (C.c_int, [C.POINTER(C.c_float), C.c_int64, C.c_int, C.c_float,
+                                      C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int64,
+                                      C.POINTER(C.c_int64)]),
     "tcg_check_equivalence_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P, _P,
                                                _P, C.POINTER(C.c_int), C.POINTER(C.c_int64)]),
     "tcg_first_bad_border_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P,

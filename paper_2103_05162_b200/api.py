@@ -345,3 +345,44 @@ def debug_union_find(edges, n: int) -> np.ndarray:
                                     out.ctypes.data_as(C.POINTER(C.c_int32))),
            "tcg_debug_union_find")
     return out
+
+
+def debug_grid(coords, eps: float, minpts: int) -> dict:
+    """tcg_debug_grid: the device build_grid in the reference's DenseGrid view."""
+    a = np.ascontiguousarray(coords, np.float32)
+    n, d = a.shape
+    perm = np.empty(n, np.int32)
+    cop = np.empty(n, np.int32)
+    cid = np.empty(n, np.uint64)
+    cb, ce = np.empty(n, np.int32), np.empty(n, np.int32)
+    cd = np.empty(n, np.uint8)
+    m = C.c_int64(0)
+    p = lambda v, t: v.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    _check(lib.tcg_debug_grid(p(a, C.c_float), n, d, C.c_float(eps), int(minpts),
+                              p(perm, C.c_int32), p(cop, C.c_int32), p(cid, C.c_uint64),
+                              p(cb, C.c_int32), p(ce, C.c_int32), p(cd, C.c_uint8), n,
+                              C.byref(m)), "tcg_debug_grid")
+    k = m.value
+    return {"perm": perm, "cell_of_point": cop, "cell_id": cid[:k], "begin": cb[:k],
+            "end": ce[:k], "dense": cd[:k].astype(bool)}
+
+
+def debug_mixed_bvh(coords, eps: float, minpts: int) -> dict:
+    """tcg_debug_mixed_bvh: the DenseBox tree in the reference's node view."""
+    a = np.ascontiguousarray(coords, np.float32)
+    n, d = a.shape
+    cap = n
+    kind = np.empty(cap, np.uint8)
+    lid = np.empty(cap, np.int32)
+    m1 = max(cap - 1, 1)
+    left, right, mr = (np.zeros(m1, np.int32) for _ in range(3))
+    boxes = np.zeros((m1, 6), np.float32)
+    m = C.c_int64(0)
+    p = lambda v, t: v.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    _check(lib.tcg_debug_mixed_bvh(p(a, C.c_float), n, d, C.c_float(eps), int(minpts),
+                                   p(kind, C.c_uint8), p(lid, C.c_int32), p(left, C.c_int32),
+                                   p(right, C.c_int32), p(mr, C.c_int32), p(boxes, C.c_float),
+                                   cap, C.byref(m)), "tcg_debug_mixed_bvh")
+    k = m.value
+    return {"leaf_kind": kind[:k], "leaf_id": lid[:k], "left": left[:k - 1],
+            "right": right[:k - 1], "max_rank": mr[:k - 1], "boxes": boxes[:k - 1]}

@@ -29,16 +29,17 @@
 
 namespace tcb {
 
-namespace {
-
-constexpr int kQueryBlock = 128;
-
 struct GridParams {
   double h;
   float origin[3];
   int64_t extent[3];
   int32_t overflow;
 };
+
+namespace {
+
+constexpr int kQueryBlock = 128;
+
 
 template <int D>
 __global__ void k_grid_setup(const DevCounters* ctr, double h, GridParams* gp) {
@@ -701,17 +702,17 @@ MemberTree build_member_tree(const float4* pts, int64_t n, Scratch& scratch) {
   return t;
 }
 
+// The grid and mixed primitives of DenseBox (build_grid + make_mixed_primitives,
+// dense_grid.cpp:23-98), shared by run_densebox and the stage-level debug
+// entry points (tcg_debug_grid / tcg_debug_mixed_bvh).
 template <int D>
-void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
-                  uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
-                  double* dense_fraction) {
+DeviceGrid build_device_grid(const float* d_coords, int64_t n, float eps, int minpts,
+                             DevCounters* ctr, Scratch& scratch) {
   cudaStream_t st = scratch.stream();
-  const BallTest bt = BallTest::make(static_cast<double>(eps) * static_cast<double>(eps));
-  clock.mark(kStGrid);
-
-  // ---- grid ----
+  DeviceGrid g;
   launch_point_bounds<D>(d_coords, n, ctr, st);
   GridParams* gp = scratch.alloc_n<GridParams>(1);
+  g.params = gp;
   const double h = static_cast<double>(eps) / std::sqrt(static_cast<double>(D));
   note_launch(), k_grid_setup<D><<<1, 1, 0, st>>>(ctr, h, gp);
   uint64_t* keys = scratch.alloc_n<uint64_t>(n);
@@ -734,42 +735,93 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
 
   uint64_t* keys_alt = scratch.alloc_n<uint64_t>(n);
   int32_t* vals_alt = scratch.alloc_n<int32_t>(n);
-  void* sort_tmp = scratch.alloc(radix_sort_scratch_bytes(n));
-  bool in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, n, key_and, key_or, sort_tmp, st);
-  const uint64_t* ids = in_alt ? keys_alt : keys;
-  const int32_t* perm = in_alt ? vals_alt : vals;
+  g.sort_tmp = scratch.alloc(radix_sort_scratch_bytes(n));
+  bool in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, n, key_and, key_or, g.sort_tmp, st);
+  g.ids = in_alt ? keys_alt : keys;
+  g.perm = in_alt ? vals_alt : vals;
+  g.spare_keys = in_alt ? keys : keys_alt;
+  g.spare_vals = in_alt ? vals : vals_alt;
 
   int32_t* head = scratch.alloc_n<int32_t>(n);
   int32_t* head_excl = scratch.alloc_n<int32_t>(n);
   int32_t* d_tot = scratch.alloc_n<int32_t>(4);
-  void* scan_tmp = scratch.alloc(scan_scratch_bytes(n));
-  note_launch(), k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(ids, n, head);
-  exclusive_scan_i32(head, head_excl, n, d_tot, scan_tmp, st);
-  int32_t* cell_of_sorted = scratch.alloc_n<int32_t>(n);
-  int32_t* cell_begin = scratch.alloc_n<int32_t>(n);
-  float4* sorted_pt = scratch.alloc_n<float4>(n);
-  note_launch(), k_cell_fill<D><<<grid_for(n, 256), 256, 0, st>>>(head, head_excl, perm, d_coords, n,
-                                                   cell_of_sorted, cell_begin, sorted_pt);
+  g.scan_tmp = scratch.alloc(scan_scratch_bytes(n));
+  note_launch(), k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(g.ids, n, head);
+  exclusive_scan_i32(head, head_excl, n, d_tot, g.scan_tmp, st);
+  g.cell_of_sorted = scratch.alloc_n<int32_t>(n);
+  g.cell_begin = scratch.alloc_n<int32_t>(n);
+  g.sorted_pt = scratch.alloc_n<float4>(n);
+  note_launch(), k_cell_fill<D><<<grid_for(n, 256), 256, 0, st>>>(head, head_excl, g.perm, d_coords, n,
+                                                   g.cell_of_sorted, g.cell_begin, g.sorted_pt);
   TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot, 4, cudaMemcpyDeviceToHost, st));
   TCB_CUDA(cudaStreamSynchronize(st));
-  int32_t num_cells;
-  std::memcpy(&num_cells, h_stage, 4);
+  std::memcpy(&g.num_cells, h_stage, 4);
 
-  // ---- mixed primitives ----
-  int32_t* cell_end = scratch.alloc_n<int32_t>(num_cells);
-  uint8_t* cell_dense = scratch.alloc_n<uint8_t>(num_cells);
-  int32_t* prim_count = scratch.alloc_n<int32_t>(num_cells);
-  int32_t* prim_off = scratch.alloc_n<int32_t>(num_cells);
+  // ---- mixed primitives: counts and offsets ----
+  g.cell_end = scratch.alloc_n<int32_t>(g.num_cells);
+  g.cell_dense = scratch.alloc_n<uint8_t>(g.num_cells);
+  int32_t* prim_count = scratch.alloc_n<int32_t>(g.num_cells);
+  g.prim_off = scratch.alloc_n<int32_t>(g.num_cells);
   note_launch(), k_reset_keys<<<1, 1, 0, st>>>(ctr);
-  note_launch(), k_cell_prims<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_begin, num_cells, n, minpts,
-                                                         cell_end, cell_dense, prim_count, ctr);
-  exclusive_scan_i32(prim_count, prim_off, num_cells, d_tot + 1, scan_tmp, st);
+  note_launch(), k_cell_prims<<<grid_for(g.num_cells, 256), 256, 0, st>>>(
+      g.cell_begin, g.num_cells, n, minpts, g.cell_end, g.cell_dense, prim_count, ctr);
+  exclusive_scan_i32(prim_count, g.prim_off, g.num_cells, d_tot + 1, g.scan_tmp, st);
   TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot + 1, 4, cudaMemcpyDeviceToHost, st));
   TCB_CUDA(cudaMemcpyAsync(h_stage + 4, &ctr->count_a, 4, cudaMemcpyDeviceToHost, st));
   TCB_CUDA(cudaStreamSynchronize(st));
-  int32_t num_prims, num_dense;
-  std::memcpy(&num_prims, h_stage, 4);
-  std::memcpy(&num_dense, h_stage + 4, 4);
+  std::memcpy(&g.num_prims, h_stage, 4);
+  std::memcpy(&g.num_dense, h_stage + 4, 4);
+  return g;
+}
+
+// One DenseBox (tight member box) per dense cell and one SinglePoint per member
+// of every other cell, in cell order (make_mixed_primitives, dense_grid.cpp:79-98).
+template <int D>
+void build_mixed_prims(const DeviceGrid& g, int64_t n, Scratch& scratch, float4** lo,
+                       float4** hi, int32_t** aux) {
+  cudaStream_t st = scratch.stream();
+  float4* prim_lo = scratch.alloc_n<float4>(g.num_prims);
+  float4* prim_hi = scratch.alloc_n<float4>(g.num_prims);
+  int32_t* prim_aux = scratch.alloc_n<int32_t>(g.num_prims);
+  if (g.num_dense > 0)
+    note_launch(), k_prim_init<<<grid_for(g.num_cells, 256), 256, 0, st>>>(
+        g.cell_dense, g.prim_off, g.num_cells, reinterpret_cast<uint4*>(prim_lo),
+        reinterpret_cast<uint4*>(prim_hi), prim_aux);
+  note_launch(), k_prim_fill<D><<<grid_for(n, 256), 256, 0, st>>>(
+      g.sorted_pt, g.cell_of_sorted, g.cell_begin, g.cell_dense, g.prim_off, n, prim_lo, prim_hi,
+      prim_aux);
+  if (g.num_dense > 0)
+    note_launch(), k_prim_decode<<<grid_for(g.num_cells, 256), 256, 0, st>>>(
+        g.cell_dense, g.prim_off, g.num_cells, prim_lo, prim_hi);
+  TCB_CUDA(cudaGetLastError());
+  *lo = prim_lo;
+  *hi = prim_hi;
+  *aux = prim_aux;
+}
+
+template <int D>
+void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32_t* d_labels,
+                  uint8_t* d_core, DevCounters* ctr, Scratch& scratch, StageClock& clock,
+                  double* dense_fraction) {
+  cudaStream_t st = scratch.stream();
+  const BallTest bt = BallTest::make(static_cast<double>(eps) * static_cast<double>(eps));
+  clock.mark(kStGrid);
+
+  // ---- grid ----
+  const DeviceGrid grid = build_device_grid<D>(d_coords, n, eps, minpts, ctr, scratch);
+  const GridParams* gp = grid.params;
+  uint64_t* keys = grid.spare_keys;
+  int32_t* vals = grid.spare_vals;
+  void* sort_tmp = grid.sort_tmp;
+  void* scan_tmp = grid.scan_tmp;
+  const int32_t* cell_of_sorted = grid.cell_of_sorted;
+  const int32_t* cell_begin = grid.cell_begin;
+  const float4* sorted_pt = grid.sorted_pt;
+  const int32_t num_cells = grid.num_cells;
+  const int32_t* cell_end = grid.cell_end;
+  const uint8_t* cell_dense = grid.cell_dense;
+  const int32_t* prim_off = grid.prim_off;
+  const int32_t num_prims = grid.num_prims, num_dense = grid.num_dense;
   const int64_t sparse_points = num_prims - num_dense;
   *dense_fraction = static_cast<double>(n - sparse_points) / static_cast<double>(n);
   if (num_dense == 0) {
@@ -783,21 +835,9 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
     run_fdbscan<D>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock);
     return;
   }
-
-  float4* prim_lo = scratch.alloc_n<float4>(num_prims);
-  float4* prim_hi = scratch.alloc_n<float4>(num_prims);
-  int32_t* prim_aux = scratch.alloc_n<int32_t>(num_prims);
-  if (num_dense > 0)
-    note_launch(), k_prim_init<<<grid_for(num_cells, 256), 256, 0, st>>>(
-        cell_dense, prim_off, num_cells, reinterpret_cast<uint4*>(prim_lo),
-        reinterpret_cast<uint4*>(prim_hi), prim_aux);
-  note_launch(), k_prim_fill<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
-                                                   cell_dense, prim_off, n, prim_lo, prim_hi,
-                                                   prim_aux);
-  if (num_dense > 0)
-    note_launch(), k_prim_decode<<<grid_for(num_cells, 256), 256, 0, st>>>(cell_dense, prim_off, num_cells,
-                                                            prim_lo, prim_hi);
-  TCB_CUDA(cudaGetLastError());
+  float4 *prim_lo, *prim_hi;
+  int32_t* prim_aux;
+  build_mixed_prims<D>(grid, n, scratch, &prim_lo, &prim_hi, &prim_aux);
 
   // ---- BVH over the mixed primitives ----
   PrimSource src;
@@ -892,6 +932,10 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   clock.finish();
 }
 
+template DeviceGrid build_device_grid<2>(const float*, int64_t, float, int, DevCounters*, Scratch&);
+template DeviceGrid build_device_grid<3>(const float*, int64_t, float, int, DevCounters*, Scratch&);
+template void build_mixed_prims<2>(const DeviceGrid&, int64_t, Scratch&, float4**, float4**, int32_t**);
+template void build_mixed_prims<3>(const DeviceGrid&, int64_t, Scratch&, float4**, float4**, int32_t**);
 template void run_densebox<2>(const float*, int64_t, float, int, int32_t*, uint8_t*,
                               DevCounters*, Scratch&, StageClock&, double*);
 template void run_densebox<3>(const float*, int64_t, float, int, int32_t*, uint8_t*,

@@ -148,6 +148,34 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
                  const int32_t* d_keys = nullptr, const ChunkSink* sink = nullptr);
 
 // ---- DenseBox (grid.cu) ----
+struct GridParams;  // cell side, origin, extents (grid.cu)
+// build_grid (dense_grid.cpp:23-77) on the device plus the primitive counts of
+// make_mixed_primitives (dense_grid.cpp:79-98). Cells are in cell-id order,
+// members of a cell in index order (perm), exactly the reference's grid.
+struct DeviceGrid {
+  const GridParams* params = nullptr;
+  const uint64_t* ids = nullptr;    // sorted cell id per sorted position
+  const int32_t* perm = nullptr;    // sorted position -> point index
+  uint64_t* spare_keys = nullptr;   // n-entry sort buffers free for reuse
+  int32_t* spare_vals = nullptr;
+  void* sort_tmp = nullptr;
+  void* scan_tmp = nullptr;
+  int32_t* cell_of_sorted = nullptr;  // sorted position -> cell
+  int32_t* cell_begin = nullptr;      // num_cells (first sorted position)
+  float4* sorted_pt = nullptr;        // (x, y, z, point index bits) in sorted order
+  int32_t num_cells = 0;
+  int32_t* cell_end = nullptr;
+  uint8_t* cell_dense = nullptr;
+  int32_t* prim_off = nullptr;        // first primitive of each cell
+  int32_t num_prims = 0, num_dense = 0;
+};
+template <int D>
+DeviceGrid build_device_grid(const float* d_coords, int64_t n, float eps, int minpts,
+                             DevCounters* ctr, Scratch& scratch);
+// Primitive boxes and payloads (point index, or ~cell for a DenseBox).
+template <int D>
+void build_mixed_prims(const DeviceGrid& g, int64_t n, Scratch& scratch, float4** lo,
+                       float4** hi, int32_t** aux);
 template <int D>
 void run_densebox(const float* d_coords, int64_t n, float eps, int minpts,
                   int32_t* d_labels, uint8_t* d_core, DevCounters* d_ctr,

@@ -86,6 +86,45 @@ def test_device_bvh_is_the_reference_tree():
             assert np.array_equal(t[k], w[k]), (d, k)
 
 
+def test_device_grid_golden():
+    """Device build_grid (REF dense_grid.cpp:23-77) == the reference's grid.npz:
+    perm, cell of every point, cell ids, ranges and dense flags."""
+    g = npz("grid.npz")
+    for s in (3, 8):
+        _, coords, eps, mp = instance(s)
+        got = tb.api.debug_grid(coords, eps, mp)
+        for k in ("perm", "cell_of_point", "cell_id", "begin", "end", "dense"):
+            assert np.array_equal(got[k], g[f"s{s}_{k}"]), (s, k)
+
+
+def _stage_inputs():
+    rng = np.random.default_rng(12)
+    lattice = np.stack(np.meshgrid(np.arange(150), np.arange(150)), -1).reshape(-1, 2)
+    yield "taxi2d", Dataset.taxi_like(200_000, seed=3).coords(), 0.001, 40
+    yield "blobs3d", Dataset.blobs(20, 8000, 3, 1.0, 0.15, 9).coords(), 0.2, 30
+    yield "lattice2d", (lattice * 0.01 + rng.uniform(-0.004, 0.004, lattice.shape)).astype(
+        np.float32), 0.1, 20
+    yield "sparse3d", Dataset.hacc_like(150_000, seed=4).coords(), 0.042, 5
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_device_grid_and_mixed_tree_are_the_reference():
+    """Stage by stage against the compiled reference (not only end to end):
+    the device grid equals build_grid and the DenseBox tree over the mixed
+    primitives equals the reference's Bvh (leaf kinds / ids per rank, node
+    links, max ranks and boxes), node for node."""
+    for name, c, eps, mp in _stage_inputs():
+        got = tb.api.debug_grid(c, eps, mp)
+        want = ref.build_grid(c, eps, mp)
+        for k in ("perm", "cell_of_point", "cell_id", "begin", "end", "dense"):
+            assert np.array_equal(got[k], want[k]), (name, k)
+        t = tb.api.debug_mixed_bvh(c, eps, mp)
+        w = ref.mixed_bvh(c, eps, mp)
+        assert want["dense"].any() or name == "sparse3d", name
+        for k in ("leaf_kind", "leaf_id", "left", "right", "max_rank", "boxes"):
+            assert np.array_equal(t[k], w[k]), (name, k)
+
+
 @pytest.mark.parametrize("d", [2, 3])
 def test_morton_prefix_sort_fixup_and_fallback(d):
     """The build sorts Morton codes on their top bits and fixes equal-prefix

@@ -44,6 +44,9 @@ METRICS = [
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("launch__registers_per_thread", "registers / thread"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+     "L1 LSU data-pipe wavefronts % of peak"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue slots busy %"),
 ]
 
 
@@ -83,6 +86,7 @@ def main():
         lines.append(f"| `{k}` | {c} | {v / c / 1e3:.1f} | {v / tot * 100:.1f}% |")
     lines += ["", "## `--set full` captures", ""]
     traffic = None
+    bound = {}
     recs = [r for fp in fpaths.split(",") for r in full(fp)]
     for rec in recs:
         lines.append(f"### `{rec['kernel']}`")
@@ -92,12 +96,17 @@ def main():
         lines.append("")
         if kfilter in rec["kernel"] and traffic is None and "DRAM read" in rec:
             traffic = to_bytes(*rec["DRAM read"]) + to_bytes(*rec["DRAM write"])
+            for key, label in (("l1_lsu_wavefront_pct", "L1 LSU data-pipe wavefronts % of peak"),
+                               ("issue_active_pct", "issue slots busy %"),
+                               ("dram_pct", "DRAM % of peak")):
+                if label in rec:
+                    bound[key] = round(float(rec[label][0].replace(",", "")), 1)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if traffic is not None and write_traffic:
         with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
             json.dump({"k_fd_main_dram_bytes_per_launch": traffic, "source": f"{tag} ncu --set full",
-                       "kernel": kfilter}, f, indent=1)
+                       "kernel": kfilter, "limiter": bound}, f, indent=1)
     print("\n".join(lines))
 
 
