@@ -20,6 +20,9 @@ shard.py: redistribution, eps halo, local passes, cross-shard merge) — weak
 scaling; `--replicas` instead runs N independent 37M clouds. Timed as the max
 over ranks. (TCB_BENCH_BACKEND=gloo TCB_BENCH_SAME_DEVICE=1 lets a 1-GPU box
 smoke-test the N>1 protocol with every rank on cuda:0.)
+`--sweep NAME` writes a parameter sweep (the reference's `treeclust bench`
+CSV plus device / tc_cluster times and, per row, the reference CPU path on the
+same points with a parity verdict) instead of the bench line.
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref = /root/reference/proj compiled unmodified) through its public C
 ABI on the host cores, on the same 37M-point workload: input from the oracle's
@@ -212,6 +215,111 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# Parameter sweeps (the reference's `treeclust bench`,
+# REF tools/treeclust_cli.cpp:146-198, and the paper's minpts / eps / n
+# sweeps): one row per (n, eps, minpts, algorithm) with the
+# reference's CSV columns, the device-resident and tc_cluster times, and the
+# reference CPU path timed on the same points (this script's reference leg:
+# oracle/_ref through dbscan_run, threads = 0) with a parity verdict.
+SWEEPS = {
+    # name: (generator, n list, eps list, minpts list, algorithms, reference algorithms)
+    "hacc-n": ("hacc", [1_000_000, 4_000_000, 16_000_000, 37_000_000], [0.042], [2], [0, 1],
+               [0, 1]),
+    "hacc-minpts": ("hacc", [4_000_000], [0.042], [2, 5, 10, 50, 100], [0, 1], [0, 1]),
+    "hacc-eps": ("hacc", [4_000_000], [0.02, 0.042, 0.084, 0.16], [5], [0, 1], [0, 1]),
+    # FDBSCAN on road data resolves ~1e11 pairs at 8M points: the CPU
+    # reference is timed for DenseBox only there
+    "taxi-minpts": ("taxi", [8_000_000], [0.001], [100, 300, 1000, 3000], [0, 1], [1]),
+    "tiny": ("hacc", [20_000, 60_000], [0.042, 0.3], [2, 5], [0, 1], [0, 1]),
+}
+SWEEP_COLUMNS = ["algorithm", "n", "eps", "minpts", "build_s", "preprocess_s", "main_s",
+                 "finalize_s", "total_s", "clusters", "cores", "noise", "dense_fraction",
+                 "device_ms", "mpts_per_s", "tc_cluster_ms", "pair_resolutions",
+                 "distance_evaluations", "ref_s", "ref_threads", "speedup_vs_ref", "parity"]
+
+
+def sweep_points(kind, n):
+    """The sweep input from the oracle's generators (byte-identical to the
+    product's tcg_generate_*): hacc_like keeps C2's density at every n."""
+    from oracle import oracle
+    return oracle.hacc_like(n) if kind == "hacc" else oracle.taxi_like(n)
+
+
+def run_sweep(args):
+    import csv
+    import io
+
+    import numpy as np
+    import torch
+    import paper_2103_05162_b200 as tb
+    from oracle import ref
+
+    kind, n_list, eps_list, minpts_list, algos, ref_algos = SWEEPS[args.sweep]
+    names = {0: "fdbscan", 1: "densebox"}
+    rows = []
+    for n in n_list:
+        coords = sweep_points(kind, n)
+        ds = tb.Dataset.from_array(coords)
+        x = torch.from_numpy(coords).cuda()
+        for eps in eps_list:
+            for minpts in minpts_list:
+                for algo in algos:
+                    a = tb.Algorithm(algo)
+                    t_abi = float("inf")
+                    for _ in range(2):  # the first call also grows the memory pools
+                        t0 = time.perf_counter()
+                        res = tb.cluster(ds, eps, minpts, a)
+                        t_abi = min(t_abi, time.perf_counter() - t0)
+                    best = float("inf")
+                    for _ in range(3):
+                        torch.cuda.synchronize()
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                        tb.cluster_device(x, eps, minpts, a)
+                        e1.record()
+                        torch.cuda.synchronize()
+                        best = min(best, e0.elapsed_time(e1))
+                    s = res.stats
+                    total = (s["build_seconds"] + s["preprocess_seconds"] + s["main_seconds"]
+                             + s["finalize_seconds"])
+                    ref_s, parity = None, None
+                    if not args.no_ref and algo in ref_algos:
+                        t0 = time.perf_counter()
+                        want = ref.dbscan(coords, eps, minpts, algo, threads=0)
+                        ref_s = time.perf_counter() - t0
+                        cm = want["core"] == 1
+                        parity = bool(
+                            np.array_equal(res.core_flags, want["core"])
+                            and np.array_equal(res.labels == -1, want["labels"] == -1)
+                            and np.array_equal(res.labels[cm], want["labels"][cm])
+                            and all(s[k] == want["stats"][k] for k in (
+                                "pair_resolutions", "cluster_count", "core_count",
+                                "noise_count")))
+                    rows.append([names[algo], n, eps, minpts, s["build_seconds"],
+                                 s["preprocess_seconds"], s["main_seconds"], s["finalize_seconds"],
+                                 total, s["cluster_count"], s["core_count"], s["noise_count"],
+                                 s["dense_point_fraction"], round(best, 3),
+                                 round(n / best / 1e3, 2), round(t_abi * 1e3, 3),
+                                 s["pair_resolutions"], s["distance_evaluations"],
+                                 None if ref_s is None else round(ref_s, 3),
+                                 None if ref_s is None else os.cpu_count(),
+                                 None if ref_s is None else round(ref_s / t_abi, 1), parity])
+                    print(",".join(str(v) for v in rows[-1]), file=sys.stderr, flush=True)
+        del ds, x
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(SWEEP_COLUMNS)
+    w.writerows(rows)
+    if args.sweep_out:
+        with open(args.sweep_out, "w") as f:
+            f.write(buf.getvalue())
+    else:
+        sys.stdout.write(buf.getvalue())
+    return 0 if all(r[-1] is not False for r in rows) else 1
+
+
 def run_sharded(args, rank, world, dev, n):
     """N>1: one global HACC-like cloud of world*n points (rank r generates the
     slab x in [r*L, (r+1)*L) with its own seed, same density as C2), clustered
@@ -313,7 +421,14 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="run the Morton-range sharded path even at N=1 (its overhead vs the "
                          "direct path)")
+    ap.add_argument("--sweep", choices=sorted(SWEEPS),
+                    help="parameter sweep (CSV) with the reference CPU path timed per row")
+    ap.add_argument("--sweep-out", help="CSV path for --sweep (default: stdout)")
+    ap.add_argument("--no-ref", action="store_true", help="--sweep without the reference column")
     args = ap.parse_args()
+
+    if args.sweep:
+        return run_sweep(args)
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)

@@ -97,6 +97,21 @@ tc_status tcg_generate_hacc_like(int64_t n, double box_len, double halo_frac,
                                  uint64_t seed, tc_dataset** out);
 /* 2D taxi-trajectory-like points in the unit square. */
 tc_status tcg_generate_taxi_like(int64_t n, uint64_t seed, tc_dataset** out);
+/* The same generators writing straight into device memory (SURVEY §8f row
+ * f4): d_out holds n*dim floats (lattice: side^dim*dim), work enqueued on
+ * `stream` (a cudaStream_t; the HACC-like / taxi-like host passes synchronize
+ * it). Output equals the host generators' above (tc_generate_blobs /
+ * _uniform / _lattice: REF datagen.cpp:10-88) for the same arguments, up to
+ * last-bit libm differences (see gen.cu); errors as the host generators. */
+tc_status tcg_generate_blobs_device(int k, int64_t per_blob, int dim, float separation,
+                                    float sigma, uint64_t seed, float* d_out, void* stream);
+tc_status tcg_generate_uniform_device(int64_t n, int dim, const float* lo, const float* hi,
+                                      uint64_t seed, float* d_out, void* stream);
+tc_status tcg_generate_lattice_device(int64_t side, int dim, float spacing, float* d_out,
+                                      void* stream);
+tc_status tcg_generate_hacc_like_device(int64_t n, double box_len, double halo_frac,
+                                        uint64_t seed, float* d_out, void* stream);
+tc_status tcg_generate_taxi_like_device(int64_t n, uint64_t seed, float* d_out, void* stream);
 /* testutil::random_instance (REF tests/test_util.hpp:27-60): returns the
  * instance's dataset and writes its eps / minpts. */
 tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n,

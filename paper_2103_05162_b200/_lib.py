@@ -69,6 +69,14 @@ SIGNATURES = {
     "tcg_last_launch_count": (C.c_int64, []),
     "tcg_generate_hacc_like": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_uint64, _PP]),
     "tcg_generate_taxi_like": (C.c_int, [C.c_int64, C.c_uint64, _PP]),
+    "tcg_generate_blobs_device": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_float, C.c_float,
+                                            C.c_uint64, _P, _P]),
+    "tcg_generate_uniform_device": (C.c_int, [C.c_int64, C.c_int, C.POINTER(C.c_float),
+                                              C.POINTER(C.c_float), C.c_uint64, _P, _P]),
+    "tcg_generate_lattice_device": (C.c_int, [C.c_int64, C.c_int, C.c_float, _P, _P]),
+    "tcg_generate_hacc_like_device": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_uint64,
+                                                _P, _P]),
+    "tcg_generate_taxi_like_device": (C.c_int, [C.c_int64, C.c_uint64, _P, _P]),
     "tcg_random_instance": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_float),
                                       C.POINTER(C.c_int), _PP]),
     "tcg_morton_codes_device": (C.c_int, [_P, C.c_int64, C.c_int, C.POINTER(C.c_float),

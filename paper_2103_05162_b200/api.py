@@ -386,3 +386,50 @@ def debug_mixed_bvh(coords, eps: float, minpts: int) -> dict:
     k = m.value
     return {"leaf_kind": kind[:k], "leaf_id": lid[:k], "left": left[:k - 1],
             "right": right[:k - 1], "max_rank": mr[:k - 1], "boxes": boxes[:k - 1]}
+
+
+def generate_device(kind: str, *args, device=None, stream=None):
+    """Device-side generators (tcg_generate_*_device): a
+    float32 [n, dim] CUDA tensor equal to the host generator's output.
+
+      generate_device("blobs", k, per_blob, dim, separation, sigma, seed)
+      generate_device("uniform", n, dim, lo, hi, seed)
+      generate_device("lattice", side, dim, spacing)
+      generate_device("hacc_like", n, box_len=None, halo_frac=0.23, seed=11)
+      generate_device("taxi_like", n, seed=5)
+    """
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    if kind == "blobs":
+        k, per_blob, dim, sep, sigma, seed = args
+        shape = (k * per_blob, dim)
+        call = lambda o, s: lib.tcg_generate_blobs_device(k, per_blob, dim, sep, sigma, seed, o, s)  # noqa: E731
+    elif kind == "uniform":
+        n, dim, lo, hi, seed = args
+        lo_a = (C.c_float * 3)(*([float(v) for v in lo] + [0.0] * (3 - len(lo))))
+        hi_a = (C.c_float * 3)(*([float(v) for v in hi] + [0.0] * (3 - len(hi))))
+        shape = (n, dim)
+        call = lambda o, s: lib.tcg_generate_uniform_device(n, dim, lo_a, hi_a, seed, o, s)  # noqa: E731
+    elif kind == "lattice":
+        side, dim, spacing = args
+        shape = (side ** dim, dim)
+        call = lambda o, s: lib.tcg_generate_lattice_device(side, dim, spacing, o, s)  # noqa: E731
+    elif kind == "hacc_like":
+        n = args[0]
+        box_len = args[1] if len(args) > 1 and args[1] is not None else 36.8 * (n / 37e6) ** (1 / 3)
+        halo_frac = args[2] if len(args) > 2 else 0.23
+        seed = args[3] if len(args) > 3 else 11
+        shape = (n, 3)
+        call = lambda o, s: lib.tcg_generate_hacc_like_device(n, box_len, halo_frac, seed, o, s)  # noqa: E731
+    elif kind == "taxi_like":
+        n = args[0]
+        seed = args[1] if len(args) > 1 else 5
+        shape = (n, 2)
+        call = lambda o, s: lib.tcg_generate_taxi_like_device(n, seed, o, s)  # noqa: E731
+    else:
+        raise ValueError(kind)
+    out = torch.empty(shape, dtype=torch.float32, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(call(C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)), f"tcg_generate_{kind}_device")
+    return out

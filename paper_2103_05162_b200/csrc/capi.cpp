@@ -539,6 +539,60 @@ TC_EXPORT tc_status tcg_generate_taxi_like(int64_t n, uint64_t seed, tc_dataset*
   return guarded([&] { return publish(tcb::gen_taxi_like(n, seed), out); });
 }
 
+TC_EXPORT tc_status tcg_generate_blobs_device(int k, int64_t per_blob, int dim,
+                                              float separation, float sigma, uint64_t seed,
+                                              float* d_out, void* stream) {
+  if (!d_out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    tcb::reset_launch_count();
+    tcb::gen_blobs_device(k, per_blob, dim, separation, sigma, seed, d_out,
+                          static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tcg_generate_uniform_device(int64_t n, int dim, const float* lo,
+                                                const float* hi, uint64_t seed, float* d_out,
+                                                void* stream) {
+  if (!d_out || !lo || !hi) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    tcb::reset_launch_count();
+    tcb::gen_uniform_device(n, dim, lo, hi, seed, d_out, static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tcg_generate_lattice_device(int64_t side, int dim, float spacing,
+                                                float* d_out, void* stream) {
+  if (!d_out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    tcb::reset_launch_count();
+    tcb::gen_lattice_device(side, dim, spacing, d_out, static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tcg_generate_hacc_like_device(int64_t n, double box_len, double halo_frac,
+                                                  uint64_t seed, float* d_out, void* stream) {
+  if (!d_out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    tcb::reset_launch_count();
+    tcb::gen_hacc_like_device(n, box_len, halo_frac, seed, d_out,
+                              static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
+}
+
+TC_EXPORT tc_status tcg_generate_taxi_like_device(int64_t n, uint64_t seed, float* d_out,
+                                                  void* stream) {
+  if (!d_out) return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&] {
+    tcb::reset_launch_count();
+    tcb::gen_taxi_like_device(n, seed, d_out, static_cast<cudaStream_t>(stream));
+    return TC_OK;
+  });
+}
+
 TC_EXPORT tc_status tcg_random_instance(uint64_t seed, int64_t min_n, int64_t max_n, float* eps,
                                         int* minpts, tc_dataset** out) {
   if (!out || !eps || !minpts || min_n < 1 || max_n < min_n) return TC_ERR_INVALID_ARGUMENT;

@@ -50,3 +50,27 @@ def test_reference_arm_other_ranks_exit_quietly():
                           "--steps", "1", "--warmup", "1"], cwd=ROOT, capture_output=True,
                          text=True, timeout=120, env={**os.environ, "RANK": "1", "WORLD_SIZE": "2"})
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_sweep_rows_match_the_reference(tmp_path):
+    """bench.py --sweep (REF treeclust_cli.cpp:146-198):
+    the reference's CSV columns plus device / tc_cluster times, and per row the
+    reference CPU path on the same points with a parity verdict — every row
+    of the small sweep must be parity-exact."""
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    import csv
+
+    out = tmp_path / "tiny.csv"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--sweep", "tiny",
+                        "--sweep-out", str(out)], capture_output=True, text=True, cwd=ROOT,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = list(csv.DictReader(open(out)))
+    assert len(rows) == 2 * 2 * 2 * 2
+    assert rows[0].keys() >= {"algorithm", "n", "eps", "minpts", "build_s", "total_s",
+                              "clusters", "cores", "noise", "dense_fraction", "device_ms",
+                              "ref_s", "parity"}
+    assert all(row["parity"] == "True" for row in rows)
+    assert all(float(row["ref_s"]) > 0 and float(row["device_ms"]) > 0 for row in rows)
