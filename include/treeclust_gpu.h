@@ -36,15 +36,38 @@ const char* tcg_version(void);
  *   stats    : may be NULL. When non-NULL the call synchronizes the stream at
  *              the end to read counters and stage times back.
  * The call is stream-ordered: with stats == NULL it returns once the work is
- * enqueued, except for the few small device->host reads that size later
- * launches (DenseBox cell/primitive counts). Scratch comes from the stream-
- * ordered memory pool (tcg_set_pool_release_threshold) and is released before
- * return. */
+ * enqueued, except for the few small device->host reads that validate the
+ * input or size later launches, each a stream synchronization:
+ *   - after the Morton pass (both algorithms): the non-finite-coordinate flag
+ *     (TC_ERR_INVALID_ARGUMENT) and the AND / OR of the keys, which select
+ *     the radix-sort passes;
+ *   - after the Morton prefix sort's fix-up pass: whether an equal-prefix group
+ *     longer than 256 points (many coincident points) needs the full sort;
+ *   - DenseBox: the grid's finiteness / overflow check (TC_ERR_INVALID_ARGUMENT)
+ *     and the cell and primitive counts.
+ * It is therefore not capturable into a CUDA graph. Scratch comes from the
+ * library's stream-ordered memory pool (tcg_set_pool_release_threshold) and
+ * is released before return. */
 tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
                              float eps, int minpts, tc_algorithm algorithm,
                              int64_t oracle_cap, int32_t* d_labels,
                              uint8_t* d_core, void* stream,
                              tc_cluster_stats* stats);
+
+/* Multi-GPU clustering of a host dataset: the points are
+ * sharded by Morton range over num_devices shards, shard s on CUDA device
+ * devices[s] (a device may be listed more than once); each shard receives
+ * the eps halo of its neighbours (peer copies over NVLink), clusters its own
+ * + ghost points, and the cross-shard unions are merged with min-id hooking.
+ * Same output contract as tc_cluster (REF treeclust.h:82-92): core flags,
+ * noise and core labels (minimum core index of the cluster) equal
+ * tc_cluster's, every border label a valid adjacent cluster. FDBSCAN and
+ * DenseBox give the same clustering (the shards run the point pipeline);
+ * brute force is not sharded (TC_ERR_INVALID_ARGUMENT). Stats: counts and
+ * wall-clock phases (build = partition + halo, main = local runs, finalize =
+ * merge + relabel); pair_resolutions / distance_evaluations are 0. */
+tc_status tcg_cluster_multi(const tc_dataset* ds, float eps, int minpts, tc_algorithm algorithm,
+                            const int* devices, int num_devices, tc_result** out);
 
 /* FDBSCAN with caller keys: d_keys[i] is a unique non-negative int32 key of
  * point i (e.g. its global id across shards; a negative key could collide

@@ -180,6 +180,25 @@ def cluster(ds: Dataset, eps: float, minpts: int, algorithm: Algorithm = Algorit
         lib.tc_result_free(res)
 
 
+def cluster_multi(ds: Dataset, eps: float, minpts: int, devices,
+                  algorithm: Algorithm = Algorithm.FDBSCAN) -> Result:
+    """``tcg_cluster_multi``: the Morton-range sharded path over the listed CUDA
+    devices (one shard per entry; entries may repeat), host in / host out."""
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    res = C.c_void_p()
+    _check(lib.tcg_cluster_multi(ds.handle, C.c_float(eps), int(minpts), int(algorithm), devs,
+                                 len(devices), C.byref(res)), "tcg_cluster_multi")
+    try:
+        n = int(lib.tc_result_size(res))
+        labels = np.ctypeslib.as_array(lib.tc_result_labels(res), shape=(n,)).copy()
+        core = np.ctypeslib.as_array(lib.tc_result_core_flags(res), shape=(n,)).copy()
+        st = TcClusterStats()
+        _check(lib.tc_result_stats(res, C.byref(st)), "tc_result_stats")
+        return Result(labels, core, st.to_dict())
+    finally:
+        lib.tc_result_free(res)
+
+
 def cluster_raw(ds: Dataset, eps: float, minpts: int, algorithm: Algorithm = Algorithm.FDBSCAN,
                 threads: int = 0, oracle_cap: int = 0) -> int:
     """``tc_cluster`` then ``tc_result_free``; returns the status (for timing the ABI)."""

@@ -386,6 +386,32 @@ TC_EXPORT tc_status tc_cluster(const tc_dataset* ds, float eps, int minpts, tc_a
   });
 }
 
+TC_EXPORT tc_status tcg_cluster_multi(const tc_dataset* ds, float eps, int minpts,
+                                      tc_algorithm algorithm, const int* devices,
+                                      int num_devices, tc_result** out) {
+  if (!ds || !out || !devices || num_devices < 1 || num_devices > 64)
+    return TC_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> tc_status {
+    if (algorithm != TC_ALGO_FDBSCAN && algorithm != TC_ALGO_DENSEBOX)
+      return TC_ERR_INVALID_ARGUMENT;
+    if (!(eps > 0.f) || !std::isfinite(eps) || minpts < 2) return TC_ERR_INVALID_ARGUMENT;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+    for (int s = 0; s < num_devices; ++s)
+      if (devices[s] < 0 || devices[s] >= count) return count ? TC_ERR_INVALID_ARGUMENT
+                                                              : TC_ERR_INTERNAL;
+    auto res = std::make_unique<tc_result>(ds->n);
+    if (ds->dim == 2)
+      tcb::cluster_multi<2>(ds->coords.ptr, ds->n, eps, minpts, devices, num_devices,
+                            res->labels.ptr, res->core.ptr, &res->stats);
+    else
+      tcb::cluster_multi<3>(ds->coords.ptr, ds->n, eps, minpts, devices, num_devices,
+                            res->labels.ptr, res->core.ptr, &res->stats);
+    *out = res.release();
+    return TC_OK;
+  });
+}
+
 TC_EXPORT int64_t tc_result_size(const tc_result* res) { return res ? res->n : 0; }
 TC_EXPORT const int32_t* tc_result_labels(const tc_result* res) { return res ? res->labels.ptr : nullptr; }
 TC_EXPORT const uint8_t* tc_result_core_flags(const tc_result* res) { return res ? res->core.ptr : nullptr; }

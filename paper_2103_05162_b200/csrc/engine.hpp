@@ -69,4 +69,11 @@ int64_t launch_count();
 void set_last_stage_ms(const double* ms);
 int get_last_stage_ms(double* out, int cap);
 
+// ---- Morton-range sharded path behind the C ABI (multi.cu) ----
+// num shards, shard s on CUDA device devices[s] (devices may repeat); host
+// coords in, host labels / core flags out in input order.
+template <int D>
+void cluster_multi(const float* h_coords, int64_t n, float eps, int minpts, const int* devices,
+                   int num, int32_t* h_labels, uint8_t* h_core, tc_cluster_stats* stats);
+
 }  // namespace tcb

@@ -266,3 +266,53 @@ def test_sharded_world3_two_clumps_one_empty_rank():
     coords = np.concatenate([a, b])
     labels, core = run_sharded(coords, 0.2, 4, world=3)
     check_against_oracle(coords, 0.2, 4, labels, core)
+
+
+# ---------------- tcg_cluster_multi: the sharded path behind the C ABI ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("shards", [1, 2, 3, 5])
+@pytest.mark.parametrize("case", ["blobs3d-2", "blobs3d-5", "blobs2d-4", "hacc-2", "hacc-20"])
+def test_cluster_multi_matches_single_gpu(shards, case):
+    """tcg_cluster_multi with `shards` shards on cuda:0 (the
+    same device listed repeatedly: the full partition / halo / merge protocol
+    through peer copies) equals tc_cluster: core flags, noise, core labels,
+    counts; every border label valid (device border check)."""
+    import torch
+
+    import paper_2103_05162_b200 as tb
+    from paper_2103_05162_b200 import Algorithm, Dataset
+
+    if case.startswith("blobs3d"):
+        ds, eps = Dataset.blobs(12, 4000, 3, 1.0, 0.12, 17), 0.09
+    elif case.startswith("blobs2d"):
+        ds, eps = Dataset.blobs(10, 5000, 2, 1.0, 0.1, 5), 0.03
+    else:
+        ds, eps = Dataset.hacc_like(400_000, seed=7), 0.042
+    minpts = int(case.split("-")[1])
+    want = tb.cluster(ds, eps, minpts, Algorithm.FDBSCAN)
+    got = tb.cluster_multi(ds, eps, minpts, [0] * shards)
+    assert np.array_equal(got.core_flags, want.core_flags)
+    assert np.array_equal(got.labels == -1, want.labels == -1)
+    cm = want.core_flags == 1
+    assert np.array_equal(got.labels[cm], want.labels[cm])
+    for k in ("cluster_count", "core_count", "noise_count"):
+        assert got.stats[k] == want.stats[k], k
+    x = torch.from_numpy(ds.coords()).cuda()
+    bad = tb.api.first_bad_border(x, eps, torch.from_numpy(got.labels).cuda(),
+                                  torch.from_numpy(got.core_flags).cuda())
+    assert bad < 0
+
+
+@pytest.mark.gpu
+def test_cluster_multi_argument_errors():
+    import paper_2103_05162_b200 as tb
+    from paper_2103_05162_b200 import Algorithm, Dataset, Status, TreeclustError
+
+    ds = Dataset.blobs(2, 100, 2, 1.0, 0.1, 1)
+    for args in ((0.0, 5, [0]), (0.1, 1, [0]), (0.1, 5, [99]), (0.1, 5, [])):
+        with pytest.raises(TreeclustError) as e:
+            tb.cluster_multi(ds, *args)
+        assert e.value.status == Status.INVALID_ARGUMENT, args
+    with pytest.raises(TreeclustError) as e:
+        tb.cluster_multi(ds, 0.1, 5, [0], Algorithm.BRUTEFORCE)
+    assert e.value.status == Status.INVALID_ARGUMENT
