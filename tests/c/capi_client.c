@@ -11,7 +11,8 @@
  *   capi_client device   REF test_capi.cpp:103-150: the three algorithms give
  *                        identical labels and 3 clusters on
  *                        blobs(3, 80, 2, 20, 0.5, 21); the brute-force cap;
- *                        tc_verify PASS
+ *                        tc_verify PASS; tcg_cluster_multi (two shards) equal
+ *                        to tc_cluster
  * Exit status 0 = every check passed. */
 #include <stddef.h>
 #include <stdio.h>
@@ -19,6 +20,7 @@
 #include <string.h>
 
 #include "treeclust.h"
+#include "treeclust_gpu.h"
 
 static int failures = 0;
 #define CHECK(cond)                                                   \
@@ -123,6 +125,30 @@ static void device_checks(void) {
   CHECK(tc_cluster(one, 1.f, 5, TC_ALGO_BRUTEFORCE, 1, 100, &res) == TC_OK);
   tc_result_free(res);
   tc_dataset_free(one);
+
+  /* the multi-GPU entry (treeclust_gpu.h) from C: two shards on device 0
+   * give tc_cluster's labels on blobs(3, 80, 2, 20, 0.5, 21) */
+  tc_dataset* m = NULL;
+  CHECK(tc_generate_blobs(3, 80, 2, 20.f, 0.5f, 21, &m) == TC_OK);
+  tc_result* single = NULL;
+  tc_result* multi = NULL;
+  const int devs[2] = {0, 0};
+  CHECK(tc_cluster(m, 1.5f, 5, TC_ALGO_FDBSCAN, 0, 0, &single) == TC_OK);
+  CHECK(tcg_cluster_multi(m, 1.5f, 5, TC_ALGO_FDBSCAN, devs, 2, &multi) == TC_OK);
+  if (single && multi) {
+    const int32_t* a = tc_result_labels(single);
+    const int32_t* b = tc_result_labels(multi);
+    const uint8_t* ca = tc_result_core_flags(single);
+    const uint8_t* cb = tc_result_core_flags(multi);
+    for (int i = 0; i < 240; ++i) {
+      CHECK(ca[i] == cb[i]);
+      CHECK((a[i] == -1) == (b[i] == -1));
+      if (ca[i]) CHECK(a[i] == b[i]);
+    }
+  }
+  tc_result_free(single);
+  tc_result_free(multi);
+  tc_dataset_free(m);
 
   tc_dataset* v = NULL; /* REF test_capi.cpp:142-150 */
   CHECK(tc_generate_blobs(3, 100, 2, 10.f, 0.6f, 31, &v) == TC_OK);
