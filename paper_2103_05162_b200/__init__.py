@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     cluster_multi,
     cluster_raw,
     device_count,
+    generate_device,
     last_launch_count,
     last_stage_ms,
     load_device,
