@@ -36,15 +36,40 @@ __global__ void k_reset_build(DevCounters* ctr) {
 // Primitive box accessors. Points: degenerate box at the point.
 template <int D>
 struct PointBoxes {
+  static constexpr bool kQuad = true;
   const float* coords;
   __device__ __forceinline__ void box(int64_t i, float* lo, float* hi) const {
 #pragma unroll
     for (int k = 0; k < D; ++k) lo[k] = hi[k] = coords[i * D + k];
   }
+  // the streaming kernels read four points (D float4) per load group when
+  // the coordinates are 16-byte aligned
+  __device__ __forceinline__ bool quad_ok() const {
+    return (reinterpret_cast<uintptr_t>(coords) & 15u) == 0;
+  }
+  __device__ __forceinline__ void quad(int64_t q, float (&c)[4][3]) const {
+    const float4* v = reinterpret_cast<const float4*>(coords) + q * D;
+    float f[4 * D];
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const float4 a = __ldcs(v + u);
+      f[4 * u] = a.x;
+      f[4 * u + 1] = a.y;
+      f[4 * u + 2] = a.z;
+      f[4 * u + 3] = a.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < D; ++k) c[i][k] = f[i * D + k];
+  }
 };
 
 template <int D>
 struct ExplicitBoxes {
+  static constexpr bool kQuad = false;
+  __device__ __forceinline__ bool quad_ok() const { return false; }
+  __device__ __forceinline__ void quad(int64_t, float (&)[4][3]) const {}
   const float4* lo4;
   const float4* hi4;
   __device__ __forceinline__ void box(int64_t i, float* lo, float* hi) const {
@@ -72,8 +97,33 @@ __global__ void __launch_bounds__(256)
 k_centroid_bounds(Src src, int64_t m, bool check_finite, DevCounters* ctr) {
   float mn[3] = {FLT_MAX, FLT_MAX, FLT_MAX}, mx[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
   bool bad = false;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t first = tid;
+  if (Src::kQuad && src.quad_ok()) {  // points: a point's box is its centroid
+    for (int64_t q = tid; q < m / 4; q += stride) {
+      float c[4][3];
+      src.quad(q, c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float lo[3], cc[3];
+#pragma unroll
+        for (int k = 0; k < D; ++k) lo[k] = c[i][k];
+        if (check_finite) {
+#pragma unroll
+          for (int k = 0; k < D; ++k) bad |= !isfinite(lo[k]);
+        }
+        centroid<D>(lo, lo, cc);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          mn[k] = fminf(mn[k], cc[k]);
+          mx[k] = fmaxf(mx[k], cc[k]);
+        }
+      }
+    }
+    first = m / 4 * 4 + tid;
+  }
+  for (int64_t i = first; i < m; i += stride) {
     float lo[3], hi[3], c[3];
     src.box(i, lo, hi);
     if (check_finite) {
@@ -107,11 +157,7 @@ k_morton(Src src, int64_t m, DevCounters* ctr, uint64_t* __restrict__ keys,
     w_lo[k] = lo_s[k];
   }
   uint64_t acc_and = ~0ull, acc_or = 0;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float lo[3], hi[3], c[3];
-    src.box(i, lo, hi);
-    centroid<D>(lo, hi, c);
+  auto encode = [&](const float* c) {
     uint64_t code;
     if (D == 2) {
       uint64_t x = quantize(c[0], w_lo[0], w[0], cells_d, cells);
@@ -123,10 +169,41 @@ k_morton(Src src, int64_t m, DevCounters* ctr, uint64_t* __restrict__ keys,
       uint64_t z = quantize(c[2], w_lo[2], w[2], cells_d, cells);
       code = spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
     }
-    keys[i] = code;
-    vals[i] = static_cast<int32_t>(i);
     acc_and &= code;
     acc_or |= code;
+    return code;
+  };
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t first = tid;
+  if (Src::kQuad && src.quad_ok()) {  // four points per thread, 16-byte loads and stores
+    for (int64_t q = tid; q < m / 4; q += stride) {
+      float c[4][3];
+      src.quad(q, c);
+      uint64_t code[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float lo[3], cc[3];
+#pragma unroll
+        for (int k = 0; k < D; ++k) lo[k] = c[i][k];
+        centroid<D>(lo, lo, cc);
+        code[i] = encode(cc);
+      }
+      ulonglong2* k2 = reinterpret_cast<ulonglong2*>(keys + 4 * q);
+      k2[0] = make_ulonglong2(code[0], code[1]);
+      k2[1] = make_ulonglong2(code[2], code[3]);
+      const int32_t i0 = static_cast<int32_t>(4 * q);
+      reinterpret_cast<int4*>(vals)[q] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+    }
+    first = m / 4 * 4 + tid;
+  }
+  for (int64_t i = first; i < m; i += stride) {
+    float lo[3], hi[3], c[3];
+    src.box(i, lo, hi);
+    centroid<D>(lo, hi, c);
+    const uint64_t code = encode(c);
+    keys[i] = code;
+    vals[i] = static_cast<int32_t>(i);
   }
   publish_and_or(acc_and, acc_or, ctr);
 }
