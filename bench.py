@@ -362,9 +362,14 @@ def run_sharded(args, rank, world, dev, n):
     value = n * world / (ms * 1e-3) / 1e6
 
     # e2e: the rank's points from pinned host memory -> sharded clustering ->
-    # labels + core flags of its own points back to the host, every step.
+    # global ids, labels and core flags of its own points back into pinned
+    # host buffers (ids and labels as int32: global ids < 2^31), every step.
     host_x = c.pin_memory()
     host_gid = (torch.arange(n, dtype=torch.int64) + rank * n).pin_memory()
+    cap = 2 * n
+    out_g = torch.empty(cap, dtype=torch.int32).pin_memory()
+    out_l = torch.empty(cap, dtype=torch.int32).pin_memory()
+    out_c = torch.empty(cap, dtype=torch.uint8).pin_memory()
     e2e_ms, h2d, d2h = [], 0, 0
     for it in range(1 + args.steps):
         dist.barrier()
@@ -375,13 +380,39 @@ def run_sharded(args, rank, world, dev, n):
         xd = host_x.to(dev, non_blocking=True)
         gd = host_gid.to(dev, non_blocking=True)
         og, lab, cor = cluster_sharded(xd, gd, EPS, MINPTS, engine)
-        out = (og.cpu(), lab.cpu(), cor.cpu())
+        k = og.shape[0]
+        if k > cap:  # (a rank owning more than twice its input)
+            cap = k
+            out_g = torch.empty(cap, dtype=torch.int32).pin_memory()
+            out_l = torch.empty(cap, dtype=torch.int32).pin_memory()
+            out_c = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        out_g[:k].copy_(og.to(torch.int32), non_blocking=True)
+        out_l[:k].copy_(lab.to(torch.int32), non_blocking=True)
+        out_c[:k].copy_(cor, non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
         if it >= 1:
             e2e_ms.append(e0.elapsed_time(e1))
         h2d = host_x.numel() * 4 + host_gid.numel() * 8
-        d2h = sum(o.numel() * o.element_size() for o in out)
+        d2h = k * (4 + 4 + 1)
+    # roofline of the local main pass (the last keyed run's stage events on
+    # this rank, over its own + ghost points)
+    engine.record_stages = True  # one more (untimed) run for the stage events
+    cluster_sharded(x, gid, EPS, MINPTS, engine)
+    engine.record_stages = False
+    stages = engine.last_stages or {}
+    main_ms = float(stages.get("main", 0.0))
+    n_local = getattr(engine, "last_local_n", n)
+    peak, peak_kind = peaks()
+    roofline = None
+    if main_ms > 0:
+        achieved = B_ALG_MAIN * n_local / (main_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "rank 0's local main stage (k_fd_main_fof_q + "
+                                              "k_cover_*) of the keyed run",
+                    "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": load_traffic()[0],
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                    "alg_bytes_per_point": B_ALG_MAIN, "main_ms": round(main_ms, 3)}
     te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device=dev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = n * world / (float(te.item()) * 1e-3) / 1e6
@@ -400,7 +431,8 @@ def run_sharded(args, rank, world, dev, n):
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": round(float(te.item()), 3),
                     "api": "paper_2103_05162_b200.shard.cluster_sharded (host tensors in/out)"},
-            "cpu_baseline": None, "roofline": None,
+            # the CPU baseline is a rank-0, N=1 figure (bench contract)
+            "cpu_baseline": None, "roofline": roofline,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
@@ -433,6 +465,9 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="run the Morton-range sharded path even at N=1 (its overhead vs the "
                          "direct path)")
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="sharded path: run the multi-rank protocol (redistribution, halo, merge "
+                         "collectives) even on one rank (TCB_SHARD_FORCE_EXCHANGE=1)")
     ap.add_argument("--sweep", choices=sorted(SWEEPS),
                     help="parameter sweep (CSV) with the reference CPU path timed per row")
     ap.add_argument("--sweep-out", help="CSV path for --sweep (default: stdout)")
@@ -441,6 +476,8 @@ def main():
 
     if args.sweep:
         return run_sweep(args)
+    if args.force_exchange:
+        os.environ["TCB_SHARD_FORCE_EXCHANGE"] = "1"
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)

@@ -162,6 +162,32 @@ tc_status tcg_morton_codes_device(const float* d_coords, int64_t n, int dim, con
 tc_status tcg_near_boxes_device(const float* d_coords, int64_t n, int dim, float eps,
                                 const float* d_box_lo, const float* d_box_hi, int64_t num_boxes,
                                 uint8_t* d_mask, void* stream);
+/* Redistribution by Morton range: point i goes to owner o = the number of the
+ * (ascending) num_splitters splitters <= d_codes[i] (o in [0, num_splitters]).
+ * d_rows receives n rows of dim + 4 int32 words — the coordinates' bits, the
+ * int64 global id, the int64 code — grouped by owner (owner 0 first; order
+ * inside a group unspecified); d_counts[o] (num_splitters + 1 int64, device)
+ * the rows per owner. num_splitters < 1024. One pass over the points replaces
+ * the bucketize + stable sort + gathers of the all-to-all payload. */
+tc_status tcg_shard_route_device(const float* d_coords, const int64_t* d_gid,
+                                 const int64_t* d_codes, int64_t n, int dim,
+                                 const int64_t* d_splitters, int num_splitters, int32_t* d_rows,
+                                 int64_t* d_counts, void* stream);
+/* Region boxes of a shard for the eps-halo: the tight boxes of the occupied
+ * Morton-prefix cells of its points (the prefix length chosen so the shard's
+ * code range spans at most 65536 cells). d_box_lo / d_box_hi need room for
+ * 65536*dim floats; *d_num_boxes (device int64) receives the count. Every
+ * point lies in one of the boxes. */
+tc_status tcg_shard_region_boxes_device(const float* d_coords, const int64_t* d_codes, int64_t n,
+                                        int dim, float* d_box_lo, float* d_box_hi,
+                                        int64_t* d_num_boxes, void* stream);
+/* d_mask[i] bit j = point i lies within eps of a box owned by peer j
+ * (d_box_owner[b] in [0, 64)), from one traversal of an LBVH over all the
+ * peers' boxes: every rank's halo sends in one pass. */
+tc_status tcg_near_peers_device(const float* d_coords, int64_t n, int dim, float eps,
+                                const float* d_box_lo, const float* d_box_hi,
+                                const int32_t* d_box_owner, int64_t num_boxes, uint64_t* d_mask,
+                                void* stream);
 /* Exact core flags (|N_eps(i)| >= minpts, i itself included) of n points. */
 tc_status tcg_core_flags_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
                                 uint8_t* d_core, void* stream);

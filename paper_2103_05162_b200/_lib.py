@@ -83,6 +83,11 @@ SIGNATURES = {
                                           C.POINTER(C.c_float), _P, _P]),
     "tcg_near_boxes_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, C.c_int64,
                                         _P, _P]),
+    "tcg_shard_route_device": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int, _P, C.c_int, _P, _P,
+                                         _P]),
+    "tcg_shard_region_boxes_device": (C.c_int, [_P, _P, C.c_int64, C.c_int, _P, _P, _P, _P]),
+    "tcg_near_peers_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P, C.c_int64,
+                                        _P, _P]),
     "tcg_core_flags_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, C.c_int, _P, _P]),
     "tcg_binary_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "tcg_load_binary_device": (C.c_int, [C.c_char_p, _P, C.c_int64, C.c_int, _P]),

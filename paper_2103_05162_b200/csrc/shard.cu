@@ -216,6 +216,206 @@ __global__ void k_flatten_all(int32_t* parent, int64_t n) {
   }
 }
 
+// ---- redistribution: owner by Morton range + packed rows in owner order ----
+// owner = number of splitters <= code (torch.bucketize(right=True)); a row is
+// dim coordinate words, the global id (2 words) and the code (2 words).
+constexpr int kRouteThreads = 256;
+constexpr int kMaxRanks = 1024;
+
+__device__ __forceinline__ int route_owner(const int64_t* s_split, int nsplit, int64_t code) {
+  int lo = 0, hi = nsplit;  // first splitter > code
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s_split[mid] <= code) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kRouteThreads)
+k_route_count(const int64_t* __restrict__ codes, int64_t n, const int64_t* __restrict__ split,
+              int nsplit, unsigned long long* __restrict__ counts) {
+  __shared__ int64_t s_split[kMaxRanks];
+  __shared__ unsigned int s_cnt[kMaxRanks];
+  for (int i = threadIdx.x; i < nsplit; i += blockDim.x) s_split[i] = split[i];
+  for (int i = threadIdx.x; i <= nsplit; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&s_cnt[route_owner(s_split, nsplit, codes[i])], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= nsplit; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(counts + i, static_cast<unsigned long long>(s_cnt[i]));
+}
+
+// cursor[o] = exclusive prefix of counts (one block)
+__global__ void k_route_offsets(const unsigned long long* __restrict__ counts, int world,
+                                unsigned long long* __restrict__ cursor) {
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (int o = 0; o < world; ++o) {
+      cursor[o] = acc;
+      acc += counts[o];
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRouteThreads)
+k_route_scatter(const float* __restrict__ coords, const int64_t* __restrict__ gid,
+                const int64_t* __restrict__ codes, int64_t n, const int64_t* __restrict__ split,
+                int nsplit, unsigned long long* __restrict__ cursor, int32_t* __restrict__ rows) {
+  __shared__ int64_t s_split[kMaxRanks];
+  __shared__ unsigned int s_cnt[kMaxRanks];
+  __shared__ unsigned long long s_base[kMaxRanks];
+  for (int i = threadIdx.x; i < nsplit; i += blockDim.x) s_split[i] = split[i];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t b0 = blockIdx.x * static_cast<int64_t>(blockDim.x); b0 < n; b0 += stride) {
+    for (int i = threadIdx.x; i <= nsplit; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    const int64_t i = b0 + threadIdx.x;
+    int o = 0;
+    unsigned loc = 0;
+    int64_t code = 0;
+    if (i < n) {
+      code = codes[i];
+      o = route_owner(s_split, nsplit, code);
+      loc = atomicAdd(&s_cnt[o], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k <= nsplit; k += blockDim.x)
+      if (s_cnt[k]) s_base[k] = atomicAdd(cursor + k, static_cast<unsigned long long>(s_cnt[k]));
+    __syncthreads();
+    if (i < n) {
+      int32_t* row = rows + static_cast<int64_t>(s_base[o] + loc) * (D + 4);
+#pragma unroll
+      for (int k = 0; k < D; ++k) row[k] = __float_as_int(coords[i * D + k]);
+      const int64_t g = gid[i];
+      row[D] = static_cast<int32_t>(g & 0xffffffff);
+      row[D + 1] = static_cast<int32_t>(g >> 32);
+      row[D + 2] = static_cast<int32_t>(code & 0xffffffff);
+      row[D + 3] = static_cast<int32_t>(code >> 32);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- region boxes: tight boxes of Morton-prefix cells of a shard's points --
+// The cell of a point is code >> shift, with the shift chosen on the device so
+// that the shard's code range spans at most 2^kCellBits cells; each occupied
+// cell's box is reduced with order-preserving atomics, then the occupied ones
+// are compacted. Every point lies in the box of its cell: the boxes cover the
+// shard, which is all the eps-halo selection needs (tcg_near_peers_device).
+constexpr int kCellBits = 16;
+
+__global__ void k_code_range(const int64_t* __restrict__ codes, int64_t n,
+                             unsigned long long* range) {
+  unsigned long long mn = ~0ull, mx = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long c = static_cast<unsigned long long>(codes[i]);
+    mn = c < mn ? c : mn;
+    mx = c > mx ? c : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(range, mn);
+    atomicMax(range + 1, mx);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_cell_boxes(const float* __restrict__ coords, const int64_t* __restrict__ codes, int64_t n,
+             const unsigned long long* __restrict__ range, uint32_t* __restrict__ cell_ord) {
+  const unsigned long long lo = range[0], hi = range[1];
+  int shift = 0;
+  while (((hi >> shift) - (lo >> shift)) >= (1ull << kCellBits)) ++shift;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t c = (static_cast<unsigned long long>(codes[i]) >> shift) - (lo >> shift);
+    uint32_t* b = cell_ord + c * (2 * D);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const uint32_t v = f2ord(coords[i * D + k]);
+      atomicMin(b + k, v);
+      atomicMax(b + D + k, v);
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_cell_compact(const uint32_t* __restrict__ cell_ord, float* __restrict__ box_lo,
+               float* __restrict__ box_hi, unsigned long long* __restrict__ count) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       c < (int64_t{1} << kCellBits); c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t* b = cell_ord + c * (2 * D);
+    if (b[0] > b[D]) continue;  // no point in this cell
+    const unsigned long long k = atomicAdd(count, 1ull);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      box_lo[k * D + j] = ord2f(b[j]);
+      box_hi[k * D + j] = ord2f(b[D + j]);
+    }
+  }
+}
+
+__global__ void k_fill_u32(uint32_t* p, int64_t n, uint32_t a, uint32_t b, int period, int half) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = (i % period) < half ? a : b;
+}
+
+// ---- halo: the set of peers (bit j = peer j) whose region boxes lie within
+// eps of each point, from one traversal of an LBVH over all peers' boxes ----
+template <int D>
+__global__ void __launch_bounds__(128)
+k_near_peers(const float4* __restrict__ nodes, const float* __restrict__ coords, int64_t n,
+             BallTest bt, unsigned long long* __restrict__ mask) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  float p[3] = {coords[i * D], coords[i * D + 1], D == 3 ? coords[i * D + 2] : 0.f};
+  unsigned long long m = 0;
+  auto visit = [&](int32_t, int32_t owner, const float*, const float*) -> bool {
+    m |= 1ull << owner;
+    return true;
+  };
+  bvh_query<D>(nodes, p, bt, 0, visit);
+  mask[i] = m;
+}
+
+template <int D>
+void near_peers(const float* d_coords, int64_t n, float eps, const float* d_lo, const float* d_hi,
+                const int32_t* d_owner, int64_t nb, unsigned long long* d_mask, cudaStream_t st) {
+  Scratch scratch(st);
+  if (nb == 0) {
+    TCB_CUDA(cudaMemsetAsync(d_mask, 0, static_cast<size_t>(n) * 8, st));
+    return;
+  }
+  DevCounters* ctr = scratch.alloc_n<DevCounters>(1);
+  TCB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), st));
+  float4* lo4 = scratch.alloc_n<float4>(nb);
+  float4* hi4 = scratch.alloc_n<float4>(nb);
+  note_launch(), k_pack_boxes<D><<<grid_for(nb, 256), 256, 0, st>>>(d_lo, d_hi, nb, lo4, hi4);
+  PrimSource src;
+  src.lo = lo4;
+  src.hi = hi4;
+  src.aux = d_owner;
+  src.count = nb;
+  BuiltBvh b = build_bvh<D>(src, false, ctr, scratch, nullptr);
+  const BallTest bt = BallTest::make(static_cast<double>(eps) * static_cast<double>(eps));
+  note_launch(), k_near_peers<D><<<grid_for(n, 128, INT32_MAX), 128, 0, st>>>(b.tree.nodes,
+                                                                              d_coords, n, bt,
+                                                                              d_mask);
+  TCB_CUDA(cudaGetLastError());
+}
+
 template <typename Fn>
 tc_status run_guarded(Fn&& fn) {
   try {
@@ -355,6 +555,91 @@ TC_EXPORT tc_status tcg_local_cluster(tcg_local* ctx, const uint8_t* d_core_in, 
 }
 
 TC_EXPORT void tcg_local_free(tcg_local* ctx) { delete ctx; }
+
+TC_EXPORT tc_status tcg_shard_route_device(const float* d_coords, const int64_t* d_gid,
+                                           const int64_t* d_codes, int64_t n, int dim,
+                                           const int64_t* d_splitters, int num_splitters,
+                                           int32_t* d_rows, int64_t* d_counts, void* stream) {
+  if ((n > 0 && (!d_coords || !d_gid || !d_codes || !d_rows)) || n < 0 ||
+      n > std::numeric_limits<int32_t>::max() || (dim != 2 && dim != 3) || !d_counts ||
+      num_splitters < 0 || num_splitters >= kMaxRanks || (num_splitters > 0 && !d_splitters))
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    reset_launch_count();
+    auto st = static_cast<cudaStream_t>(stream);
+    auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+    const int world = num_splitters + 1;
+    TCB_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * world, st));
+    if (n == 0) return;
+    Scratch scratch(st);
+    auto* cursor = scratch.alloc_n<unsigned long long>(world);
+    const unsigned g = grid_for(n, kRouteThreads, 148 * 8);
+    note_launch(), k_route_count<<<g, kRouteThreads, 0, st>>>(d_codes, n, d_splitters,
+                                                             num_splitters, counts);
+    note_launch(), k_route_offsets<<<1, 32, 0, st>>>(counts, world, cursor);
+    if (dim == 2)
+      note_launch(), k_route_scatter<2><<<g, kRouteThreads, 0, st>>>(
+          d_coords, d_gid, d_codes, n, d_splitters, num_splitters, cursor, d_rows);
+    else
+      note_launch(), k_route_scatter<3><<<g, kRouteThreads, 0, st>>>(
+          d_coords, d_gid, d_codes, n, d_splitters, num_splitters, cursor, d_rows);
+    TCB_CUDA(cudaGetLastError());
+  });
+}
+
+TC_EXPORT tc_status tcg_shard_region_boxes_device(const float* d_coords, const int64_t* d_codes,
+                                                  int64_t n, int dim, float* d_box_lo,
+                                                  float* d_box_hi, int64_t* d_num_boxes,
+                                                  void* stream) {
+  if ((n > 0 && (!d_coords || !d_codes)) || n < 0 || (dim != 2 && dim != 3) || !d_box_lo ||
+      !d_box_hi || !d_num_boxes)
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    reset_launch_count();
+    auto st = static_cast<cudaStream_t>(stream);
+    auto* count = reinterpret_cast<unsigned long long*>(d_num_boxes);
+    TCB_CUDA(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+    if (n == 0) return;
+    Scratch scratch(st);
+    auto* range = scratch.alloc_n<unsigned long long>(2);
+    note_launch(), k_fill_u32<<<1, 32, 0, st>>>(reinterpret_cast<uint32_t*>(range), 4,
+                                                 0xffffffffu, 0u, 4, 2);
+    const int64_t words = (int64_t{1} << kCellBits) * 2 * dim;
+    auto* cell_ord = scratch.alloc_n<uint32_t>(words);
+    note_launch(), k_fill_u32<<<grid_for(words, 256), 256, 0, st>>>(cell_ord, words, 0xffffffffu,
+                                                                     0u, 2 * dim, dim);
+    note_launch(), k_code_range<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(d_codes, n, range);
+    const unsigned g = grid_for(n, 256, 148 * 16);
+    const unsigned gc = grid_for(int64_t{1} << kCellBits, 256);
+    if (dim == 2) {
+      note_launch(), k_cell_boxes<2><<<g, 256, 0, st>>>(d_coords, d_codes, n, range, cell_ord);
+      note_launch(), k_cell_compact<2><<<gc, 256, 0, st>>>(cell_ord, d_box_lo, d_box_hi, count);
+    } else {
+      note_launch(), k_cell_boxes<3><<<g, 256, 0, st>>>(d_coords, d_codes, n, range, cell_ord);
+      note_launch(), k_cell_compact<3><<<gc, 256, 0, st>>>(cell_ord, d_box_lo, d_box_hi, count);
+    }
+    TCB_CUDA(cudaGetLastError());
+  });
+}
+
+TC_EXPORT tc_status tcg_near_peers_device(const float* d_coords, int64_t n, int dim, float eps,
+                                          const float* d_box_lo, const float* d_box_hi,
+                                          const int32_t* d_box_owner, int64_t num_boxes,
+                                          uint64_t* d_mask, void* stream) {
+  if (bad_shape(d_coords, n, dim) || !d_mask || num_boxes < 0 || !(eps > 0.f) ||
+      (num_boxes > 0 && (!d_box_lo || !d_box_hi || !d_box_owner)))
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    reset_launch_count();
+    if (n == 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    auto* mask = reinterpret_cast<unsigned long long*>(d_mask);
+    if (dim == 2)
+      near_peers<2>(d_coords, n, eps, d_box_lo, d_box_hi, d_box_owner, num_boxes, mask, st);
+    else
+      near_peers<3>(d_coords, n, eps, d_box_lo, d_box_hi, d_box_owner, num_boxes, mask, st);
+  });
+}
 
 TC_EXPORT tc_status tcg_union_edges_device(const int32_t* d_edges, int64_t m, int32_t n,
                                            int32_t* d_root, void* stream) {

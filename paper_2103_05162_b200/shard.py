@@ -58,6 +58,9 @@ class DeviceEngine:
     def __init__(self, device):
         self.device = torch.device(device)
         self.launches = 0  # kernels of this library launched through the engine
+        self.record_stages = False  # keep the local run's stage times (last_stages)
+        self.last_stages = None
+        self.last_local_n = 0
 
     def _s(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -119,17 +122,72 @@ class DeviceEngine:
         labels = torch.empty(n, dtype=torch.int32, device=x.device)
         core = torch.empty(n, dtype=torch.uint8, device=x.device)
         keys = keys.contiguous()
+        st = TcClusterStats() if self.record_stages else None  # stats: stage events kept
         _check(lib.tcg_cluster_keyed_device(C.c_void_p(x.data_ptr()), C.c_void_p(keys.data_ptr()),
                                             n, d, C.c_float(eps), int(minpts),
                                             C.c_void_p(labels.data_ptr()),
-                                            C.c_void_p(core.data_ptr()), self._s(), None),
+                                            C.c_void_p(core.data_ptr()), self._s(),
+                                            C.byref(st) if st is not None else None),
                "tcg_cluster_keyed_device")
         self._count()
+        if self.record_stages:  # (reading the stage events waits for the run)
+            from .api import last_stage_ms
+            self.last_stages = last_stage_ms()
+            self.last_local_n = n
         return labels, core
 
     def local(self, x, keys, eps):
         """A LocalContext over (x, keys): one tree for the core and main passes."""
         return LocalContext(self, x, keys, eps)
+
+    def route(self, x, gid, codes, splitters):
+        """Rows (dim + 4 int32 words: coords, gid, code) grouped by owner, and
+        the per-owner counts (host list)."""
+        n, d = x.shape
+        world = splitters.shape[0] + 1
+        rows = torch.empty((n, d + 4), dtype=torch.int32, device=x.device)
+        counts = torch.empty(world, dtype=torch.int64, device=x.device)
+        sp = splitters.contiguous()
+        _check(lib.tcg_shard_route_device(C.c_void_p(x.data_ptr()), C.c_void_p(gid.data_ptr()),
+                                          C.c_void_p(codes.data_ptr()), n, d,
+                                          C.c_void_p(sp.data_ptr()), sp.shape[0],
+                                          C.c_void_p(rows.data_ptr()),
+                                          C.c_void_p(counts.data_ptr()), self._s()),
+               "tcg_shard_route_device")
+        self._count()
+        return rows, counts.tolist()
+
+    def region_boxes(self, x, codes):
+        """(k, 2*dim) float32 boxes covering the points (Morton-prefix cells)."""
+        n, d = x.shape
+        cap = 1 << 16
+        lo = torch.empty((cap, d), dtype=torch.float32, device=x.device)
+        hi = torch.empty((cap, d), dtype=torch.float32, device=x.device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
+        _check(lib.tcg_shard_region_boxes_device(C.c_void_p(x.data_ptr()),
+                                                 C.c_void_p(codes.data_ptr()), n, d,
+                                                 C.c_void_p(lo.data_ptr()), C.c_void_p(hi.data_ptr()),
+                                                 C.c_void_p(cnt.data_ptr()), self._s()),
+               "tcg_shard_region_boxes_device")
+        self._count()
+        k = int(cnt.item())
+        return torch.cat([lo[:k], hi[:k]], 1)
+
+    def near_peers(self, x, eps, blo, bhi, owner):
+        """Bit j of mask[i]: point i lies within eps of a box of peer j."""
+        n, d = x.shape
+        mask = torch.zeros(n, dtype=torch.int64, device=x.device)
+        if n == 0:
+            return mask
+        blo, bhi = blo.contiguous(), bhi.contiguous()
+        owner = owner.to(device=x.device, dtype=torch.int32).contiguous()
+        _check(lib.tcg_near_peers_device(C.c_void_p(x.data_ptr()), n, d, C.c_float(eps),
+                                         C.c_void_p(blo.data_ptr()), C.c_void_p(bhi.data_ptr()),
+                                         C.c_void_p(owner.data_ptr()), blo.shape[0],
+                                         C.c_void_p(mask.data_ptr()), self._s()),
+               "tcg_near_peers_device")
+        self._count()
+        return mask
 
     def union_edges(self, edges, n):
         root = torch.empty(n, dtype=torch.int32, device=self.device)
@@ -287,7 +345,8 @@ class _StageMarks:
 
 
 # ---------------------------------------------------------------------------
-def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples=4096):
+def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples=4096,
+                    force_exchange=None):
     """Clusters the union of every rank's (x, gid) points.
 
     x: (n_local, dim) float32 tensor on the engine's device; gid: (n_local,)
@@ -295,7 +354,15 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     for the points this rank owns after the Morton-range redistribution;
     labels are global ids of the cluster representative (minimum core id), -1
     for noise. Identical to the single-GPU result on the concatenated input.
+
+    force_exchange (default: TCB_SHARD_FORCE_EXCHANGE=1): run the
+    multi-rank protocol even on a single rank (sampling, the all-to-all
+    redistribution to itself, the halo exchange with no peers), so that one
+    GPU exercises the backend's collectives exactly as N ranks issue them.
     """
+    if force_exchange is None:
+        import os
+        force_exchange = os.environ.get("TCB_SHARD_FORCE_EXCHANGE") == "1"
     if not (eps > 0) or minpts < 2:
         raise TreeclustError(Status.INVALID_ARGUMENT, "cluster_sharded")
     world = dist.get_world_size(group)
@@ -303,6 +370,7 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     dev = x.device
     n, dim = x.shape
     marks = _StageMarks(dev)
+    single = world == 1 and not force_exchange  # no exchange at all
 
     # 1. global scene box
     if n:
@@ -318,7 +386,7 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     # 2. codes and splitters
     codes = engine.morton(x, lo, hi) if n else torch.empty(0, dtype=torch.int64, device=dev)
     k = min(n, samples)
-    if k and world > 1:
+    if k and not single:
         # a pseudo-random subsample (fixed seed) stands in for the local
         # distribution; only load balance depends on it, never correctness
         g = torch.Generator(device=dev)
@@ -328,23 +396,27 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
         sample = codes[:0]
     allsamp = torch.sort(torch.cat(_all_gather_var(sample, group))).values
     m = allsamp.shape[0]
-    if world > 1 and m:
-        q = torch.tensor([(j * m) // world for j in range(1, world)], device=dev)
+    if not single and m:
+        q = torch.tensor([(j * m) // world for j in range(1, world)], dtype=torch.int64, device=dev)
         splitters = allsamp[q.clamp(max=m - 1)]
     else:
         splitters = torch.empty(0, dtype=torch.int64, device=dev)
-    owner = torch.bucketize(codes, splitters, right=True)
+    owner = None if hasattr(engine, "route") else torch.bucketize(codes, splitters, right=True)
 
     marks.mark("3")
     # 3. redistribution by Morton range (the codes travel along: step 4
     #    orders the own points by them)
-    if world == 1:
+    if single:
         own_x, own_gid, own_codes = x.contiguous(), gid, codes
     else:
-        order = torch.argsort(owner, stable=True)
-        counts = torch.bincount(owner, minlength=world).tolist() if n else [0] * world
-        payload = torch.cat([x[order].view(torch.int32), gid[order].view(torch.int32).view(-1, 2),
-                             codes[order].view(torch.int32).view(-1, 2)], 1)
+        if hasattr(engine, "route"):  # one device pass: owners + packed rows in owner order
+            payload, counts = engine.route(x.contiguous(), gid.contiguous(), codes, splitters)
+        else:
+            order = torch.argsort(owner, stable=True)
+            counts = torch.bincount(owner, minlength=world).tolist() if n else [0] * world
+            payload = torch.cat([x[order].view(torch.int32),
+                                 gid[order].view(torch.int32).view(-1, 2),
+                                 codes[order].view(torch.int32).view(-1, 2)], 1)
         recv, _ = _all_to_all(payload, counts, group)
         own_x, own_gid = _unpack(recv[:, :dim + 2], dim)
         own_codes = recv[:, dim + 2:].clone(memory_format=torch.contiguous_format).view(
@@ -353,11 +425,13 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
 
     marks.mark("4")
     # 4. region boxes and the eps halo (a single rank has no peers)
-    if world == 1:
+    if single:
         ghost_x = own_x[:0]
         ghost_gid = own_gid[:0]
         send_idx = torch.empty(0, dtype=torch.int64, device=dev)
         send_counts = [0]
+    elif n_own and hasattr(engine, "region_boxes"):  # Morton-prefix cell boxes, no sort
+        boxes = engine.region_boxes(own_x, own_codes)
     elif n_own:
         perm = torch.argsort(own_codes)
         xs = own_x[perm]
@@ -369,18 +443,34 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
         boxes = torch.cat([blo, bhi], 1)
     else:
         boxes = torch.empty((0, 2 * dim), dtype=torch.float32, device=dev)
-    if world > 1:
+    if not single:
         peer_boxes = _all_gather_var(boxes, group)
         send_idx, send_counts = [], []
-        for j in range(world):
-            if j == rank or n_own == 0 or peer_boxes[j].shape[0] == 0:
-                send_counts.append(0)
-                continue
-            pb = peer_boxes[j]
-            mask = engine.near_boxes(own_x, eps, pb[:, :dim], pb[:, dim:])
-            idx = torch.nonzero(mask, as_tuple=False).view(-1)
-            send_idx.append(idx)
-            send_counts.append(int(idx.shape[0]))
+        if hasattr(engine, "near_peers") and world <= 64:
+            # one traversal per own point over every peer's boxes (bit j = peer j)
+            others = [j for j in range(world) if j != rank and peer_boxes[j].shape[0]]
+            if n_own and others:
+                ball = torch.cat([peer_boxes[j] for j in others])
+                bown = torch.cat([torch.full((peer_boxes[j].shape[0],), j, dtype=torch.int32,
+                                             device=dev) for j in others])
+                pmask = engine.near_peers(own_x, eps, ball[:, :dim], ball[:, dim:], bown)
+            for j in range(world):
+                if j not in others or n_own == 0:
+                    send_counts.append(0)
+                    continue
+                idx = torch.nonzero((pmask >> j) & 1, as_tuple=False).view(-1)
+                send_idx.append(idx)
+                send_counts.append(int(idx.shape[0]))
+        else:
+            for j in range(world):
+                if j == rank or n_own == 0 or peer_boxes[j].shape[0] == 0:
+                    send_counts.append(0)
+                    continue
+                pb = peer_boxes[j]
+                mask = engine.near_boxes(own_x, eps, pb[:, :dim], pb[:, dim:])
+                idx = torch.nonzero(mask, as_tuple=False).view(-1)
+                send_idx.append(idx)
+                send_counts.append(int(idx.shape[0]))
         send_idx = torch.cat(send_idx) if send_idx else torch.empty(0, dtype=torch.int64, device=dev)
         halo_payload = torch.cat([own_x[send_idx].view(torch.int32),
                                   own_gid[send_idx].view(torch.int32).view(-1, 2)], 1)

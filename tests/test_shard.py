@@ -136,6 +136,48 @@ class OracleEngine:
         return torch.from_numpy(np.array([find(i) for i in range(n)], np.int32))
 
 
+class OracleEngineFused(OracleEngine):
+    """OracleEngine plus numpy doubles of the fused device stages
+    (tcg_shard_route_device, tcg_shard_region_boxes_device,
+    tcg_near_peers_device), so the CPU tests drive the same protocol branch
+    as the DeviceEngine."""
+
+    def route(self, x, gid, codes, splitters):
+        c = codes.numpy()
+        owner = np.searchsorted(splitters.numpy(), c, side="right")
+        order = np.argsort(owner, kind="stable")
+        d = x.shape[1]
+        rows = np.concatenate([x.numpy()[order].view(np.int32),
+                               gid.numpy()[order].view(np.int32).reshape(-1, 2),
+                               c[order].view(np.int32).reshape(-1, 2)], 1).reshape(-1, d + 4)
+        counts = np.bincount(owner, minlength=splitters.shape[0] + 1)
+        return torch.from_numpy(np.ascontiguousarray(rows)), [int(v) for v in counts]
+
+    def region_boxes(self, x, codes):
+        c = codes.numpy().astype(np.uint64)
+        lo, hi = int(c.min()), int(c.max())
+        shift = 0
+        while (hi >> shift) - (lo >> shift) >= (1 << 16):
+            shift += 1
+        cell = (c >> np.uint64(shift)) - np.uint64(lo >> shift)
+        uniq, inv = np.unique(cell, return_inverse=True)
+        p = x.numpy()
+        blo = np.full((len(uniq), p.shape[1]), np.inf, np.float32)
+        bhi = np.full((len(uniq), p.shape[1]), -np.inf, np.float32)
+        np.minimum.at(blo, inv, p)
+        np.maximum.at(bhi, inv, p)
+        return torch.from_numpy(np.concatenate([blo, bhi], 1))
+
+    def near_peers(self, x, eps, blo, bhi, owner):
+        mask = np.zeros(x.shape[0], np.int64)
+        own = owner.numpy()
+        for j in np.unique(own):
+            sel = own == j
+            m = self.near_boxes(x, eps, blo[torch.from_numpy(sel)], bhi[torch.from_numpy(sel)])
+            mask |= m.numpy().astype(np.int64) << int(j)
+        return torch.from_numpy(mask)
+
+
 def free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -144,10 +186,17 @@ def free_port():
     return p
 
 
-def _worker(rank, world, port, coords, eps, minpts, use_gpu, out_q):
+def _worker(rank, world, port, coords, eps, minpts, use_gpu, out_q, backend="gloo",
+            force_exchange=False, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        import torch as _t
+        _t.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=_t.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2103_05162_b200.shard import DeviceEngine, cluster_sharded
 
     n = coords.shape[0]
@@ -160,22 +209,34 @@ def _worker(rank, world, port, coords, eps, minpts, use_gpu, out_q):
         x = x.cuda()
         gid = gid.cuda()
     else:
-        engine = OracleEngine()
-    g, lab, core = cluster_sharded(x, gid, eps, minpts, engine, block=64, samples=256)
+        engine = OracleEngineFused() if fused else OracleEngine()
+    g, lab, core = cluster_sharded(x, gid, eps, minpts, engine, block=64, samples=256,
+                                   force_exchange=force_exchange)
     out_q.put((rank, g.cpu().numpy(), lab.cpu().numpy(), core.cpu().numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def run_sharded(coords, eps, minpts, world=2, use_gpu=False):
+def run_sharded(coords, eps, minpts, world=2, use_gpu=False, backend="gloo",
+                force_exchange=False, fused=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, coords, eps, minpts, use_gpu, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, coords, eps, minpts, use_gpu, q,
+                                               backend, force_exchange, fused))
              for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(world)]
+    import queue
+    import time
+    res, deadline = [], time.time() + 600
+    while len(res) < world:  # fail fast when a rank dies instead of waiting out the timeout
+        try:
+            res.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"a rank exited with {dead}"
+            assert time.time() < deadline, "sharded run timed out"
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -218,6 +279,15 @@ def test_sharded_world2_matches_single_process(dim, eps, minpts):
     check_against_oracle(coords, eps, minpts, labels, core)
 
 
+@pytest.mark.parametrize("world,minpts", [(2, 2), (3, 5)])
+def test_sharded_fused_stages(world, minpts):
+    """The protocol branch of the fused device stages (route, region boxes,
+    one-pass peer halo), with their numpy doubles."""
+    coords = blob_mix(31 + world, 1500, 3)
+    labels, core = run_sharded(coords, 0.4, minpts, world=world, fused=True)
+    check_against_oracle(coords, 0.4, minpts, labels, core)
+
+
 def test_sharded_world3_uneven():
     coords = blob_mix(5, 1500, 3)[:1237]
     labels, core = run_sharded(coords, 0.4, 4, world=3)
@@ -245,6 +315,28 @@ def test_sharded_world1(minpts):
 def test_sharded_device_engine_world1(minpts):
     coords = blob_mix(44, 8000, 3)
     labels, core = run_sharded(coords, 0.3, minpts, world=1, use_gpu=True)
+    check_against_oracle(coords, 0.3, minpts, labels, core)
+
+
+@pytest.mark.parametrize("minpts", [2, 4])
+def test_sharded_world1_forced_exchange(minpts):
+    """One rank running the whole multi-rank protocol (redistribution to
+    itself, halo exchange with no peers, edge merge)."""
+    coords = blob_mix(23, 1200, 3)
+    labels, core = run_sharded(coords, 0.35, minpts, world=1, force_exchange=True)
+    check_against_oracle(coords, 0.35, minpts, labels, core)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("minpts", [2, 6])
+def test_sharded_nccl_world1_forced_exchange(minpts):
+    """The NCCL branch of every collective (device tensors in all_reduce,
+    padded all_gather, variable all_to_all_single incl. empty sends) on the
+    one GPU of the box: the multi-rank protocol forced on a single rank, with
+    the product engine, against the oracle."""
+    coords = blob_mix(45, 8000, 3)
+    labels, core = run_sharded(coords, 0.3, minpts, world=1, use_gpu=True, backend="nccl",
+                               force_exchange=True)
     check_against_oracle(coords, 0.3, minpts, labels, core)
 
 
