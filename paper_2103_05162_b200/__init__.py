@@ -23,6 +23,8 @@ from .api import (  # noqa: F401
     last_launch_count,
     last_stage_ms,
     load_device,
+    release_cached_memory,
+    set_pool_release_threshold,
     status_string,
     verify,
 )

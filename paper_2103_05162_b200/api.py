@@ -318,6 +318,18 @@ def last_stage_ms() -> dict:
     return {STAGES[i]: arr[i] for i in range(k)}
 
 
+def set_pool_release_threshold(nbytes: int) -> None:
+    """Scratch bytes the library's device memory pool keeps across calls
+    (tcg_set_pool_release_threshold; default 24 GiB). Raise it for repeated
+    runs larger than that (the 497M-point case needs ~80 GB of scratch)."""
+    _check(lib.tcg_set_pool_release_threshold(int(nbytes)), "tcg_set_pool_release_threshold")
+
+
+def release_cached_memory() -> None:
+    """Frees the library's cached device scratch and pinned host staging now."""
+    lib.tcg_release_cached_memory()
+
+
 def last_launch_count() -> int:
     return int(lib.tcg_last_launch_count())
 
