@@ -408,3 +408,82 @@ def test_cluster_multi_argument_errors():
     with pytest.raises(TreeclustError) as e:
         tb.cluster_multi(ds, 0.1, 5, [0], Algorithm.BRUTEFORCE)
     assert e.value.status == Status.INVALID_ARGUMENT
+
+
+# ---------------- the fused shard stages, directly ----------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim", [2, 3])
+def test_route_rows_and_counts(dim):
+    """tcg_shard_route_device: every point lands in its owner's group exactly
+    once (owner = bucketize(code, splitters, right=True)), rows carry the
+    coordinates' bits, the global id and the code."""
+    from paper_2103_05162_b200.shard import DeviceEngine
+
+    rng = np.random.default_rng(dim)
+    n = 50_000
+    x = torch.from_numpy(rng.uniform(-3, 3, (n, dim)).astype(np.float32)).cuda()
+    gid = torch.from_numpy(rng.permutation(n).astype(np.int64) + 10**9).cuda()
+    eng = DeviceEngine("cuda:0")
+    codes = eng.morton(x, x.min(0).values, x.max(0).values)
+    splitters = torch.sort(codes[torch.randint(0, n, (5,), device="cuda")]).values
+    rows, counts = eng.route(x, gid, codes, splitters)
+    owner = torch.bucketize(codes, splitters, right=True)
+    assert counts == torch.bincount(owner, minlength=6).tolist()
+    rows = rows.cpu()
+    start = 0
+    for o, c in enumerate(counts):
+        grp = rows[start:start + c]
+        start += c
+        g = grp[:, dim:dim + 2].contiguous().view(torch.int64).view(-1)
+        sel = (owner == o).cpu()
+        assert torch.equal(torch.sort(g).values, torch.sort(gid.cpu()[sel]).values)
+        want = dict(zip(gid.cpu()[sel].tolist(), codes.cpu()[sel].tolist()))
+        got_codes = grp[:, dim + 2:].contiguous().view(torch.int64).view(-1).tolist()
+        assert all(want[a] == b for a, b in zip(g.tolist(), got_codes))
+        pos = {v: i for i, v in enumerate(gid.cpu().tolist())}
+        xs = x.cpu()[[pos[v] for v in g.tolist()]]
+        assert torch.equal(grp[:, :dim].contiguous().view(torch.float32), xs)
+
+
+@pytest.mark.gpu
+def test_region_boxes_cover_and_near_peers():
+    """tcg_shard_region_boxes_device covers every point with tight cell boxes;
+    tcg_near_peers_device flags exactly the points within eps of a peer's
+    boxes (against a brute-force fp64 check)."""
+    from paper_2103_05162_b200.shard import DeviceEngine
+
+    rng = np.random.default_rng(7)
+    pts = np.concatenate([rng.normal(0, 0.3, (20_000, 3)), rng.uniform(-2, 2, (20_000, 3))])
+    x = torch.from_numpy(pts.astype(np.float32)).cuda()
+    eng = DeviceEngine("cuda:0")
+    codes = eng.morton(x, x.min(0).values, x.max(0).values)
+    boxes = eng.region_boxes(x, codes).cpu().numpy()
+    assert 0 < len(boxes) <= 1 << 16
+    p = x.cpu().numpy()
+    inside = np.zeros(len(p), bool)
+    for b in boxes:
+        inside |= np.all((p >= b[:3]) & (p <= b[3:]), axis=1)
+    assert inside.all()
+    # two "peers": the boxes of two halves of another cloud
+    q = rng.uniform(-2.5, 2.5, (3000, 3)).astype(np.float32)
+    qx = torch.from_numpy(q).cuda()
+    qc = eng.morton(qx, qx.min(0).values, qx.max(0).values)
+    half = len(q) // 2
+    b0 = eng.region_boxes(qx[:half].contiguous(), qc[:half].contiguous())
+    b1 = eng.region_boxes(qx[half:].contiguous(), qc[half:].contiguous())
+    ball = torch.cat([b0, b1])
+    own = torch.cat([torch.full((b0.shape[0],), 2, dtype=torch.int32),
+                     torch.full((b1.shape[0],), 5, dtype=torch.int32)]).cuda()
+    eps = 0.05
+    mask = eng.near_peers(x, eps, ball[:, :3], ball[:, 3:], own).cpu().numpy()
+    e2 = np.float64(np.float32(eps)) ** 2
+    pd = p.astype(np.float64)
+    for bit, bx in ((2, b0.cpu().numpy()), (5, b1.cpu().numpy())):
+        lo, hi = bx[None, :, :3].astype(np.float64), bx[None, :, 3:].astype(np.float64)
+        want = np.zeros(len(p), bool)
+        for c0 in range(0, len(p), 1000):
+            pc = pd[c0:c0 + 1000, None, :]
+            d = np.maximum(np.maximum(lo - pc, pc - hi), 0)
+            want[c0:c0 + 1000] = ((d * d).sum(2) <= e2).any(1)
+        assert np.array_equal(((mask >> bit) & 1).astype(bool), want)
+    assert ((mask & ~((1 << 2) | (1 << 5))) == 0).all()
