@@ -173,6 +173,11 @@ tc_status tcg_shard_route_device(const float* d_coords, const int64_t* d_gid,
                                  const int64_t* d_codes, int64_t n, int dim,
                                  const int64_t* d_splitters, int num_splitters, int32_t* d_rows,
                                  int64_t* d_counts, void* stream);
+/* The inverse of the row packing (after the all-to-all): n rows of dim + 4
+ * int32 words -> d_coords (n*dim floats), d_gid (n int64) and, if not NULL,
+ * d_codes (n int64), in one pass. */
+tc_status tcg_shard_unpack_rows_device(const int32_t* d_rows, int64_t n, int dim, float* d_coords,
+                                       int64_t* d_gid, int64_t* d_codes, void* stream);
 /* Region boxes of a shard for the eps-halo: the tight boxes of the occupied
  * Morton-prefix cells of its points (the prefix length chosen so the shard's
  * code range spans at most 65536 cells). d_box_lo / d_box_hi need room for

@@ -85,6 +85,7 @@ SIGNATURES = {
                                         _P, _P]),
     "tcg_shard_route_device": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int, _P, C.c_int, _P, _P,
                                          _P]),
+    "tcg_shard_unpack_rows_device": (C.c_int, [_P, C.c_int64, C.c_int, _P, _P, _P, _P]),
     "tcg_shard_region_boxes_device": (C.c_int, [_P, _P, C.c_int64, C.c_int, _P, _P, _P, _P]),
     "tcg_near_peers_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P, C.c_int64,
                                         _P, _P]),

@@ -300,6 +300,25 @@ k_route_scatter(const float* __restrict__ coords, const int64_t* __restrict__ gi
   }
 }
 
+// rows (dim coordinate words, gid, code) -> contiguous coordinates, global
+// ids and codes (codes optional): the inverse of k_route_scatter's packing
+template <int D>
+__global__ void __launch_bounds__(256)
+k_unpack_rows(const int32_t* __restrict__ rows, int64_t n, float* __restrict__ coords,
+              int64_t* __restrict__ gid, int64_t* __restrict__ codes) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t* row = rows + i * (D + 4);
+#pragma unroll
+    for (int k = 0; k < D; ++k) coords[i * D + k] = __int_as_float(row[k]);
+    gid[i] = static_cast<int64_t>(static_cast<uint32_t>(row[D])) |
+             (static_cast<int64_t>(row[D + 1]) << 32);
+    if (codes)
+      codes[i] = static_cast<int64_t>(static_cast<uint32_t>(row[D + 2])) |
+                 (static_cast<int64_t>(row[D + 3]) << 32);
+  }
+}
+
 // ---- region boxes: tight boxes of Morton-prefix cells of a shard's points --
 // The cell of a point is code >> shift, with the shift chosen on the device so
 // that the shard's code range spans at most 2^kCellBits cells; each occupied
@@ -583,6 +602,24 @@ TC_EXPORT tc_status tcg_shard_route_device(const float* d_coords, const int64_t*
     else
       note_launch(), k_route_scatter<3><<<g, kRouteThreads, 0, st>>>(
           d_coords, d_gid, d_codes, n, d_splitters, num_splitters, cursor, d_rows);
+    TCB_CUDA(cudaGetLastError());
+  });
+}
+
+TC_EXPORT tc_status tcg_shard_unpack_rows_device(const int32_t* d_rows, int64_t n, int dim,
+                                                 float* d_coords, int64_t* d_gid,
+                                                 int64_t* d_codes, void* stream) {
+  if ((n > 0 && (!d_rows || !d_coords || !d_gid)) || n < 0 || (dim != 2 && dim != 3))
+    return TC_ERR_INVALID_ARGUMENT;
+  return run_guarded([&] {
+    reset_launch_count();
+    if (n == 0) return;
+    auto st = static_cast<cudaStream_t>(stream);
+    const unsigned g = grid_for(n, 256, 148 * 16);
+    if (dim == 2)
+      note_launch(), k_unpack_rows<2><<<g, 256, 0, st>>>(d_rows, n, d_coords, d_gid, d_codes);
+    else
+      note_launch(), k_unpack_rows<3><<<g, 256, 0, st>>>(d_rows, n, d_coords, d_gid, d_codes);
     TCB_CUDA(cudaGetLastError());
   });
 }

@@ -157,6 +157,21 @@ class DeviceEngine:
         self._count()
         return rows, counts.tolist()
 
+    def unpack(self, rows, dim, with_codes):
+        """(coords [n, dim] f32, gid [n] i64, codes [n] i64 or None) from rows."""
+        n = rows.shape[0]
+        x = torch.empty((n, dim), dtype=torch.float32, device=rows.device)
+        g = torch.empty(n, dtype=torch.int64, device=rows.device)
+        c = torch.empty(n, dtype=torch.int64, device=rows.device) if with_codes else None
+        rows = rows.contiguous()
+        _check(lib.tcg_shard_unpack_rows_device(C.c_void_p(rows.data_ptr()), n, dim,
+                                                C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()),
+                                                C.c_void_p(c.data_ptr()) if c is not None else None,
+                                                self._s()),
+               "tcg_shard_unpack_rows_device")
+        self._count()
+        return x, g, c
+
     def region_boxes(self, x, codes):
         """(k, 2*dim) float32 boxes covering the points (Morton-prefix cells)."""
         n, d = x.shape
@@ -418,9 +433,12 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
                                  gid[order].view(torch.int32).view(-1, 2),
                                  codes[order].view(torch.int32).view(-1, 2)], 1)
         recv, _ = _all_to_all(payload, counts, group)
-        own_x, own_gid = _unpack(recv[:, :dim + 2], dim)
-        own_codes = recv[:, dim + 2:].clone(memory_format=torch.contiguous_format).view(
-            torch.int64).view(-1)
+        if hasattr(engine, "unpack"):
+            own_x, own_gid, own_codes = engine.unpack(recv, dim, True)
+        else:
+            own_x, own_gid = _unpack(recv[:, :dim + 2], dim)
+            own_codes = recv[:, dim + 2:].clone(memory_format=torch.contiguous_format).view(
+                torch.int64).view(-1)
     n_own = own_x.shape[0]
 
     marks.mark("4")
