@@ -402,7 +402,7 @@ k_near_peers(const float4* __restrict__ nodes, const float* __restrict__ coords,
   float p[3] = {coords[i * D], coords[i * D + 1], D == 3 ? coords[i * D + 2] : 0.f};
   unsigned long long m = 0;
   auto visit = [&](int32_t, int32_t owner, const float*, const float*) -> bool {
-    m |= 1ull << owner;
+    if (static_cast<uint32_t>(owner) < 64u) m |= 1ull << owner;  // (owners >= 64 unsupported)
     return true;
   };
   bvh_query<D>(nodes, p, bt, 0, visit);
