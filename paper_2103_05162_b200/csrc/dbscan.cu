@@ -444,6 +444,9 @@ __global__ void k_init_uf(int32_t* __restrict__ parent, int64_t n) {
 constexpr int kFinThreads = 1024;
 constexpr int kFinItems = 8;
 constexpr int kFinMaxBuckets = 4096;
+// large inputs: up to this many buckets (dynamic shared counters) so that the
+// windows still fit pass 2's shared memory (497M points: 15168 windows of 32K)
+constexpr int kFinMaxBucketsLarge = 16384;
 
 // 2 resident blocks (32 registers, a few entries spilled to L1): 0.69 -> 0.60 ms on C2
 __global__ void __launch_bounds__(kFinThreads, 2)
@@ -451,7 +454,7 @@ k_fin_bucket(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
              const int32_t* __restrict__ key, const int32_t* __restrict__ order, int64_t n,
              int shift, int nb, uint32_t* __restrict__ cursor, uint2* __restrict__ entries,
              DevCounters* ctr, bool derive_core) {
-  __shared__ uint32_t s_cnt[kFinMaxBuckets];
+  extern __shared__ uint32_t s_cnt[];  // nb counters
   for (int b = threadIdx.x; b < nb; b += kFinThreads) s_cnt[b] = 0;
   __syncthreads();
   long long noise = 0, clusters = 0, cores = 0;
@@ -629,8 +632,8 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
   // 4096 when that keeps the windows within shared memory (pass 2)
   int shift = 12;
   while (((n + (int64_t{1} << shift) - 1) >> shift) > kFinMaxBuckets / 2) ++shift;
-  if (shift > 15 && ((n + (int64_t{1} << 15) - 1) >> 15) <= kFinMaxBuckets) shift = 15;
-  while (((n + (int64_t{1} << shift) - 1) >> shift) > kFinMaxBuckets) ++shift;
+  if (shift > 15 && ((n + (int64_t{1} << 15) - 1) >> 15) <= kFinMaxBucketsLarge) shift = 15;
+  while (((n + (int64_t{1} << shift) - 1) >> shift) > kFinMaxBucketsLarge) ++shift;
   const int nb = static_cast<int>((n + (int64_t{1} << shift) - 1) >> shift);
   uint32_t* cursor = scratch.alloc_n<uint32_t>(nb);
   uint2* entries = scratch.alloc_n<uint2>(n);
@@ -639,8 +642,13 @@ void finalize_labels_bucketed(int32_t* parent, uint8_t* flags, const int32_t* ke
   // caller buffers (e.g. a torch slice) need not be 16-byte aligned: the
   // window pass then writes element by element
   const bool vec16 = (reinterpret_cast<uintptr_t>(labels) | reinterpret_cast<uintptr_t>(core_out)) % 16 == 0;
-  note_launch(), k_fin_bucket<<<static_cast<unsigned>((n + tile - 1) / tile), kFinThreads, 0, s>>>(
-      parent, flags, key, order, n, shift, nb, cursor, entries, d_ctr, force_core);
+  const size_t cnt_bytes = sizeof(uint32_t) * static_cast<size_t>(nb);
+  if (cnt_bytes > 48 * 1024)
+    TCB_CUDA(cudaFuncSetAttribute(k_fin_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(cnt_bytes)));
+  note_launch(), k_fin_bucket<<<static_cast<unsigned>((n + tile - 1) / tile), kFinThreads,
+                                 cnt_bytes, s>>>(parent, flags, key, order, n, shift, nb, cursor,
+                                                 entries, d_ctr, force_core);
   TCB_CUDA(cudaGetLastError());
   // pass 2, in chunks of whole buckets when a sink copies finished output
   // ranges to the host while the next chunk is written
