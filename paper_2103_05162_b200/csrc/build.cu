@@ -148,25 +148,26 @@ k_morton(Src src, int64_t m, DevCounters* ctr, uint64_t* __restrict__ keys,
   constexpr uint64_t cells = 1ull << bits;
   const double cells_d = static_cast<double>(cells);
   float lo_s[3], w_lo[3];
-  double w[3];
+  double w[3], rw[3];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     lo_s[k] = ord2f(ctr->bounds_ord[k]);
     float hi_s = ord2f(ctr->bounds_ord[3 + k]);
     w[k] = __dsub_rn(static_cast<double>(hi_s), static_cast<double>(lo_s[k]));
+    rw[k] = w[k] > 0.0 ? __drcp_rn(w[k]) : 0.0;
     w_lo[k] = lo_s[k];
   }
   uint64_t acc_and = ~0ull, acc_or = 0;
   auto encode = [&](const float* c) {
     uint64_t code;
     if (D == 2) {
-      uint64_t x = quantize(c[0], w_lo[0], w[0], cells_d, cells);
-      uint64_t y = quantize(c[1], w_lo[1], w[1], cells_d, cells);
+      uint64_t x = quantize_rcp(c[0], w_lo[0], w[0], rw[0], cells_d, cells);
+      uint64_t y = quantize_rcp(c[1], w_lo[1], w[1], rw[1], cells_d, cells);
       code = spread2(x) | (spread2(y) << 1);
     } else {
-      uint64_t x = quantize(c[0], w_lo[0], w[0], cells_d, cells);
-      uint64_t y = quantize(c[1], w_lo[1], w[1], cells_d, cells);
-      uint64_t z = quantize(c[2], w_lo[2], w[2], cells_d, cells);
+      uint64_t x = quantize_rcp(c[0], w_lo[0], w[0], rw[0], cells_d, cells);
+      uint64_t y = quantize_rcp(c[1], w_lo[1], w[1], rw[1], cells_d, cells);
+      uint64_t z = quantize_rcp(c[2], w_lo[2], w[2], rw[2], cells_d, cells);
       code = spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
     }
     acc_and &= code;

@@ -93,6 +93,27 @@ __device__ __forceinline__ uint64_t quantize(float v, float lo, double w, double
   return quantize_d(static_cast<double>(v), lo, w, cells_d, cells);
 }
 
+// quantize() with the division replaced by a multiplication with rw =
+// RN(1/w): t' = RN(d * rw) is within 3 * 2^-53 (relative, t <= 1) of
+// RN(d / w), and cells_d is a power of two (exact scaling), so t' * cells_d
+// has the same integer part as the exact chain unless it lies within
+// 3 * 2^-53 * cells_d of an integer; a margin of cells_d * 2^-48 (10x that)
+// sends those rare cases to the exact chain. Bit-identical to quantize().
+__device__ __forceinline__ uint64_t quantize_rcp(float v, float lo, double w, double rw,
+                                                 double cells_d, uint64_t cells) {
+  if (w <= 0.0) return 0;
+  const double d = __dsub_rn(static_cast<double>(v), static_cast<double>(lo));
+  const double x = __dmul_rn(__dmul_rn(d, rw), cells_d);  // (scaling by 2^k is exact)
+  const double fl = floor(x);
+  const double frac = x - fl;
+  const double margin = cells_d * 0x1.0p-48;
+  if (d < 0.0 || frac < margin || frac > 1.0 - margin)
+    return quantize_d(static_cast<double>(v), lo, w, cells_d, cells);
+  uint64_t q = static_cast<uint64_t>(fl);
+  if (q >= cells) q = cells - 1;
+  return q;
+}
+
 // ---------------------------------------------------------------------------
 // Order-preserving float <-> uint32 mapping for atomicMin/atomicMax bounds.
 // ---------------------------------------------------------------------------
