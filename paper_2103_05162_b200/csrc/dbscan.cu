@@ -447,6 +447,9 @@ constexpr int kFinMaxBuckets = 4096;
 // large inputs: up to this many buckets (dynamic shared counters) so that the
 // windows still fit pass 2's shared memory (497M points: 15168 windows of 32K)
 constexpr int kFinMaxBucketsLarge = 16384;
+#ifndef TCB_FIN_BATCHED
+#define TCB_FIN_BATCHED 1
+#endif
 
 // 2 resident blocks (32 registers, a few entries spilled to L1): 0.69 -> 0.60 ms on C2
 __global__ void __launch_bounds__(kFinThreads, 2)
@@ -461,15 +464,38 @@ k_fin_bucket(int32_t* __restrict__ parent, const uint8_t* __restrict__ flags,
   const int64_t base = static_cast<int64_t>(blockIdx.x) * (kFinThreads * kFinItems);
   uint2 e[kFinItems];
   uint32_t loc[kFinItems];
+#if TCB_FIN_BATCHED
+  // The union-find is final here; the only writes are path compressions to
+  // roots, and a root's own entry never changes, so plain (batchable) loads
+  // are safe: any value an entry held is an ancestor and every chase ends at
+  // the true root. The first two levels of all items are loaded together.
+  int32_t pr[kFinItems], qr[kFinItems];
+#pragma unroll
+  for (int j = 0; j < kFinItems; ++j) {
+    const int64_t s = base + j * kFinThreads + threadIdx.x;
+    pr[j] = s < n ? parent[s] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kFinItems; ++j) qr[j] = parent[pr[j]];
+#endif
 #pragma unroll
   for (int j = 0; j < kFinItems; ++j) {
     const int64_t s = base + j * kFinThreads + threadIdx.x;
     e[j].x = 0xffffffffu;
     if (s < n) {
+#if TCB_FIN_BATCHED
+      int32_t p = pr[j], q = qr[j];
+      while (p != q) {
+        p = q;
+        q = parent[p];
+      }
+      if (p != pr[j]) parent[s] = p;
+#else
       int32_t p = ld_relaxed(parent + s);
       int32_t q;
       while (p != (q = ld_relaxed(parent + p))) p = q;
       st_relaxed(parent + s, p);
+#endif
       const bool core = flags[s] != 0 || (derive_core && p != s);
       const int32_t lab = (core || p != s) ? __ldg(key + p) : -1;  // dbscan.cpp:215
       noise += lab == -1;
