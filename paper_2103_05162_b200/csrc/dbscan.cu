@@ -378,7 +378,9 @@ k_fd_main_fof_q(const float4* __restrict__ nodes, const float4* __restrict__ lea
       if (na >= 1) act[off] = make_int3(rank, f0, l0);
       if (na == 2) act[off + 1] = make_int3(rank, f1, l1);
       qn += __popc(m1) + __popc(m2);
-      if (qn >= 32) {
+      // resolve down to fewer than 32 queued: a step adds up to 64, so the
+      // queue (kActCap = 96) never overflows
+      while (qn >= 32) {
         __syncwarp();
         qn -= 32;
         fof_resolve(act[qn + lane], hints, warp_base, parent, key, reach, mark);

@@ -616,3 +616,19 @@ def test_device_morton_codes_golden():
         assert st == 0
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint64), g[f"codes{d}"]), d
+
+
+def test_fof_action_queue_never_overflows():
+    """Regression: with eps near the cloud's extent nearly every child is a
+    contained run, lanes queue two union actions per step, and the per-warp
+    action queue must be drained below 32 after every step (it overflowed
+    into the next warp's queue before; intermittent illegal address). Many
+    repetitions, each against the oracle's labels."""
+    c = oracle.hacc_like(20_000)
+    ds = Dataset.from_array(c)
+    want = oracle.dbscan(c, 0.3, 2, 0)
+    for _ in range(40):
+        got = tb.cluster(ds, 0.3, 2, Algorithm.FDBSCAN)
+        assert np.array_equal(got.labels, want["labels"])
+        assert np.array_equal(got.core_flags, want["core"])
+        assert got.stats["pair_resolutions"] == want["stats"]["pair_resolutions"]
