@@ -280,16 +280,32 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
 #endif
 constexpr int kActCap = 96;  // < 32 queued + up to 2 per lane per step
 
+// The hint slots are read and written by the lanes resolving actions of the
+// same query concurrently: shared-memory atomics (whichever value wins is a
+// valid hint), so the accesses are race-free by the memory model.
+__device__ __forceinline__ int32_t ld_shared_relaxed(int32_t* p) { return atomicAdd(p, 0); }
+__device__ __forceinline__ void st_shared_relaxed(int32_t* p, int32_t v) { atomicExch(p, v); }
+
 __device__ __forceinline__ void fof_resolve(int3 e, int32_t* hints, int32_t warp_base,
                                             int32_t* __restrict__ parent,
                                             const int32_t* __restrict__ key,
                                             int32_t* __restrict__ reach, uint8_t* mark) {
   int32_t* hp = hints + (e.x - warp_base);
-  int32_t hint = *hp;
+  int32_t hint = ld_shared_relaxed(hp);
   const int32_t old = hint;
   uf_unite_hinted_keyed(parent, key, e.x, e.y, hint, mark);
-  if (hint != old) *hp = hint;
+  if (hint != old) st_shared_relaxed(hp, hint);
   record_run(reach, e.y, e.z);
+}
+
+__device__ __noinline__ int fof_drain_batch(const int3* act, int qn, int lane, int32_t* hints,
+                                            int32_t warp_base, int32_t* __restrict__ parent,
+                                            const int32_t* __restrict__ key,
+                                            int32_t* __restrict__ reach, uint8_t* mark) {
+  qn -= 32;
+  fof_resolve(act[qn + lane], hints, warp_base, parent, key, reach, mark);
+  __syncwarp();
+  return qn;
 }
 
 template <int D, int kFast>
@@ -380,11 +396,14 @@ k_fd_main_fof_q(const float4* __restrict__ nodes, const float4* __restrict__ lea
       qn += __popc(m1) + __popc(m2);
       // resolve down to fewer than 32 queued: a step adds up to 64, so the
       // queue (kActCap = 96) never overflows
-      while (qn >= 32) {
+      if (qn >= 32) {
         __syncwarp();
         qn -= 32;
         fof_resolve(act[qn + lane], hints, warp_base, parent, key, reach, mark);
         __syncwarp();
+        // (rare) still 32 or more queued: one more batch, out of line so the
+        // common path keeps its registers
+        if (qn >= 32) qn = fof_drain_batch(act, qn, lane, hints, warp_base, parent, key, reach, mark);
       }
     }
     if (!__any_sync(0xffffffffu, active)) break;

@@ -47,6 +47,34 @@ print("keyed", int((lab >= 0).sum()), int((lab2 >= 0).sum()))
 ds.save("/tmp/san.bin")
 y = tb.load_device("/tmp/san.bin")
 print("load", bool(torch.equal(y, x)))
+# eps near the extent (every child a contained run: full action queues) and tiny eps
+from oracle import oracle
+h = oracle.hacc_like(20000)
+hd = tb.Dataset.from_array(h)
+for eps in (0.3, 1.0, 1e-4):
+    for algo, mp in ((0, 2), (0, 5), (1, 2), (1, 50)):
+        r = tb.cluster(hd, eps, mp, tb.Algorithm(algo))
+        print("eps", eps, algo, mp, r.stats["cluster_count"])
+# the fused shard stages
+hx = torch.from_numpy(h).cuda()
+gid = torch.arange(h.shape[0], dtype=torch.int64, device="cuda")
+codes = eng.morton(hx, hx.min(0).values, hx.max(0).values)
+spl = torch.sort(codes[torch.randint(0, h.shape[0], (3,), device="cuda")]).values
+rows, counts = eng.route(hx, gid, codes, spl)
+ux, ug, uc = eng.unpack(rows, 3, True)
+bx = eng.region_boxes(ux, uc)
+own = torch.zeros(bx.shape[0], dtype=torch.int32, device="cuda") + 3
+pm = eng.near_peers(hx, 0.05, bx[:, :3], bx[:, 3:], own)
+torch.cuda.synchronize()
+print("shard", counts, int(bx.shape[0]), int((pm != 0).sum()))
+# device generators and the device checker
+gz = tb.generate_device("hacc_like", 5000)
+gt = tb.generate_device("taxi_like", 5000)
+a = tb.cluster(hd, 0.042, 5, tb.Algorithm.FDBSCAN)
+b = tb.cluster(hd, 0.042, 5, tb.Algorithm.DENSEBOX)
+chk = tb.api.check_equivalence_device(hx, 0.042, *(torch.from_numpy(np.ascontiguousarray(v)).cuda()
+                                       for v in (a.labels, a.core_flags, b.labels, b.core_flags)))
+print("check", chk[0], int(gz.shape[0]), int(gt.shape[0]))
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 900 $CS --tool $tool --error-exitcode 9 python /tmp/san_run.py > gpurun_out/sanitize_$tool.log 2>&1
