@@ -315,3 +315,37 @@ def test_check_equivalence_arbitrary_label_values():
         assert ok == ok_want, msg
         if ref.available():
             assert ref.check_equivalence(c, 0.6, 4, la, ca, other, ca) == (ok, msg)
+
+
+def test_reciprocal_morton_quantization_is_exact():
+    """The device's quantize_rcp (device_common.cuh) multiplies by RN(1/w)
+    and falls back to the exact division when the scaled value lies within
+    cells * 2^-48 of an integer. The same fp64 operations in numpy (IEEE,
+    round-to-nearest) against the reference's division (geometry.hpp:132-141),
+    on random and adversarial (exact cell boundaries and their fp32
+    neighbours) coordinates, 2D and 3D cell counts."""
+    rng = np.random.default_rng(7)
+    for bits in (21, 31):
+        cells = 2 ** bits
+        cd = float(cells)
+        for _ in range(4):
+            lo = np.float32(rng.uniform(-100, 100))
+            hi = np.float32(lo + np.float32(rng.uniform(1e-3, 1e3)))
+            w = np.float64(hi) - np.float64(lo)
+            rw = 1.0 / w
+            k = rng.integers(0, cells, 100_000).astype(np.float64)
+            adv = (np.float64(lo) + k / cd * w).astype(np.float32)
+            v = np.concatenate([rng.uniform(lo, hi, 200_000).astype(np.float32), adv,
+                                np.nextafter(adv, np.float32(np.inf)),
+                                np.nextafter(adv, np.float32(-np.inf)), [lo, hi]])
+            v = np.clip(v.astype(np.float32), lo, hi)
+            d = v.astype(np.float64) - np.float64(lo)
+            want = np.minimum(np.floor(np.maximum(d / w, 0) * cd), cells - 1)
+            x = (d * rw) * cd
+            fl = np.floor(x)
+            frac = x - fl
+            m = cd * 2.0 ** -48
+            fast = (frac >= m) & (frac <= 1 - m) & (d >= 0)
+            got = np.where(fast, np.minimum(fl, cells - 1), want)
+            assert np.array_equal(got, want)
+            assert fast.mean() > 0.99  # the exact chain stays rare
