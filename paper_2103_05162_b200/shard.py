@@ -426,6 +426,7 @@ def cluster_sharded(x, gid, eps, minpts, engine, group=None, block=2048, samples
     else:
         if hasattr(engine, "route"):  # one device pass: owners + packed rows in owner order
             payload, counts = engine.route(x.contiguous(), gid.contiguous(), codes, splitters)
+            counts = counts + [0] * (world - len(counts))  # (no splitters: all to rank 0)
         else:
             order = torch.argsort(owner, stable=True)
             counts = torch.bincount(owner, minlength=world).tolist() if n else [0] * world

@@ -487,3 +487,12 @@ def test_region_boxes_cover_and_near_peers():
             want[c0:c0 + 1000] = ((d * d).sum(2) <= e2).any(1)
         assert np.array_equal(((mask >> bit) & 1).astype(bool), want)
     assert ((mask & ~((1 << 2) | (1 << 5))) == 0).all()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_sharded_all_ranks_empty(fused):
+    """No points anywhere: no samples, no splitters; every rank still takes
+    part in every collective and returns empty results."""
+    coords = np.zeros((0, 3), np.float32)
+    labels, core = run_sharded(coords, 0.1, 2, world=2, fused=fused)
+    assert labels.shape == (0,) and core.shape == (0,)
