@@ -98,10 +98,16 @@ __global__ void k_reset_keys(DevCounters* ctr) {
 
 // head[k] = 1 where a new cell starts in sorted order.
 __global__ void __launch_bounds__(256)
-k_cell_heads(const uint64_t* __restrict__ ids, int64_t n, int32_t* __restrict__ head) {
+k_cell_heads(const uint64_t* __restrict__ ids, int64_t n, int minpts, int32_t* __restrict__ head,
+             int32_t* __restrict__ any_dense) {
+  bool dense = false;  // a run of >= minpts equal sorted ids starts here
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
-       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    head[k] = (k == 0 || ids[k] != ids[k - 1]) ? 1 : 0;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t id = ids[k];
+    head[k] = (k == 0 || id != ids[k - 1]) ? 1 : 0;
+    dense |= k + minpts - 1 < n && ids[k + minpts - 1] == id;
+  }
+  if (__any_sync(0xffffffffu, dense) && (threadIdx.x & 31) == 0) atomicOr(any_dense, 1);
 }
 
 // From the exclusive scan of heads: cell index per sorted position, cell
@@ -707,7 +713,7 @@ MemberTree build_member_tree(const float4* pts, int64_t n, Scratch& scratch) {
 // entry points (tcg_debug_grid / tcg_debug_mixed_bvh).
 template <int D>
 DeviceGrid build_device_grid(const float* d_coords, int64_t n, float eps, int minpts,
-                             DevCounters* ctr, Scratch& scratch) {
+                             DevCounters* ctr, Scratch& scratch, bool stop_if_no_dense) {
   cudaStream_t st = scratch.stream();
   DeviceGrid g;
   launch_point_bounds<D>(d_coords, n, ctr, st);
@@ -741,21 +747,31 @@ DeviceGrid build_device_grid(const float* d_coords, int64_t n, float eps, int mi
   g.perm = in_alt ? vals_alt : vals;
   g.spare_keys = in_alt ? keys : keys_alt;
   g.spare_vals = in_alt ? vals : vals_alt;
-
   int32_t* head = scratch.alloc_n<int32_t>(n);
   int32_t* head_excl = scratch.alloc_n<int32_t>(n);
-  int32_t* d_tot = scratch.alloc_n<int32_t>(4);
+  int32_t* d_tot = scratch.alloc_n<int32_t>(4);  // [0] cells, [1] prims, [2] any dense
   g.scan_tmp = scratch.alloc(scan_scratch_bytes(n));
-  note_launch(), k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(g.ids, n, head);
+  TCB_CUDA(cudaMemsetAsync(d_tot + 2, 0, sizeof(int32_t), st));
+  // heads of the sorted cell runs, and whether any run holds >= minpts points
+  note_launch(), k_cell_heads<<<grid_for(n, 256), 256, 0, st>>>(g.ids, n, minpts, head, d_tot + 2);
   exclusive_scan_i32(head, head_excl, n, d_tot, g.scan_tmp, st);
+  TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot, 12, cudaMemcpyDeviceToHost, st));
+  TCB_CUDA(cudaStreamSynchronize(st));
+  int32_t any_dense;
+  std::memcpy(&g.num_cells, h_stage, 4);
+  std::memcpy(&any_dense, h_stage + 8, 4);
+  if (stop_if_no_dense && !any_dense) {
+    // no dense cell: DenseBox is the point pipeline (run_densebox), the rest
+    // of the grid is not needed
+    g.num_prims = static_cast<int32_t>(n);
+    g.num_dense = 0;
+    return g;
+  }
   g.cell_of_sorted = scratch.alloc_n<int32_t>(n);
   g.cell_begin = scratch.alloc_n<int32_t>(n);
   g.sorted_pt = scratch.alloc_n<float4>(n);
   note_launch(), k_cell_fill<D><<<grid_for(n, 256), 256, 0, st>>>(head, head_excl, g.perm, d_coords, n,
                                                    g.cell_of_sorted, g.cell_begin, g.sorted_pt);
-  TCB_CUDA(cudaMemcpyAsync(h_stage, d_tot, 4, cudaMemcpyDeviceToHost, st));
-  TCB_CUDA(cudaStreamSynchronize(st));
-  std::memcpy(&g.num_cells, h_stage, 4);
 
   // ---- mixed primitives: counts and offsets ----
   g.cell_end = scratch.alloc_n<int32_t>(g.num_cells);
@@ -808,7 +824,8 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   clock.mark(kStGrid);
 
   // ---- grid ----
-  const DeviceGrid grid = build_device_grid<D>(d_coords, n, eps, minpts, ctr, scratch);
+  const DeviceGrid grid = build_device_grid<D>(d_coords, n, eps, minpts, ctr, scratch,
+                                               /*stop_if_no_dense=*/true);
   const GridParams* gp = grid.params;
   uint64_t* keys = grid.spare_keys;
   int32_t* vals = grid.spare_vals;
@@ -932,8 +949,10 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   clock.finish();
 }
 
-template DeviceGrid build_device_grid<2>(const float*, int64_t, float, int, DevCounters*, Scratch&);
-template DeviceGrid build_device_grid<3>(const float*, int64_t, float, int, DevCounters*, Scratch&);
+template DeviceGrid build_device_grid<2>(const float*, int64_t, float, int, DevCounters*, Scratch&,
+                                         bool);
+template DeviceGrid build_device_grid<3>(const float*, int64_t, float, int, DevCounters*, Scratch&,
+                                         bool);
 template void build_mixed_prims<2>(const DeviceGrid&, int64_t, Scratch&, float4**, float4**, int32_t**);
 template void build_mixed_prims<3>(const DeviceGrid&, int64_t, Scratch&, float4**, float4**, int32_t**);
 template void run_densebox<2>(const float*, int64_t, float, int, int32_t*, uint8_t*,

@@ -169,9 +169,11 @@ struct DeviceGrid {
   int32_t* prim_off = nullptr;        // first primitive of each cell
   int32_t num_prims = 0, num_dense = 0;
 };
+// stop_if_no_dense: return right after the cell sort (num_dense = 0, only
+// params / ids / perm / sort buffers set) when no cell holds minpts points.
 template <int D>
 DeviceGrid build_device_grid(const float* d_coords, int64_t n, float eps, int minpts,
-                             DevCounters* ctr, Scratch& scratch);
+                             DevCounters* ctr, Scratch& scratch, bool stop_if_no_dense = false);
 // Primitive boxes and payloads (point index, or ~cell for a DenseBox).
 template <int D>
 void build_mixed_prims(const DeviceGrid& g, int64_t n, Scratch& scratch, float4** lo,
