@@ -47,6 +47,9 @@ constexpr int kFofMinBlocks = TCB_FOF_MIN_BLOCKS;
 #define TCB_MAIN_MIN_BLOCKS 10
 #endif
 constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
+#ifndef TCB_MAIN_BATCH
+#define TCB_MAIN_BATCH 1
+#endif
 
 template <int D>
 __device__ __forceinline__ void load_query(const float4* leaf_pt, int64_t r, float* p,
@@ -414,6 +417,179 @@ k_fd_main_fof_q(const float4* __restrict__ nodes, const float4* __restrict__ lea
   flush_counter(&ctr->dists, pairs);
 }
 
+// k_fd_main (minpts > 2) with warp-batched pair resolution, as
+// k_fd_main_fof_q does for minpts == 2: a step classifies the node's two
+// children for the lane's query (leaf hits, contained runs with their
+// noncore prefix counts, the border query's `settled` state — all decided by
+// the query's own lane, in its traversal), and queues the union-find work it
+// implies — UNITE (core-core pair or all-core run), CLAIM_B (a core query
+// claims a border leaf under its root hint), CLAIM_SELF (a border query
+// joins the cluster of a core) — which the warp resolves 32 at a time, one
+// per lane, with the queries' root hints in shared memory. Same pairs, same
+// core-core unions (the partition); border claims are first-come as in the
+// per-query form (any adjacent cluster, dbscan.hpp:82-99).
+constexpr int kActUnite = 0, kActClaimB = 1, kActClaimSelf = 2;
+
+__device__ __forceinline__ void main_resolve(int4 e, int32_t* hints, int32_t warp_base,
+                                             int32_t* __restrict__ parent,
+                                             const int32_t* __restrict__ key,
+                                             int32_t* __restrict__ reach) {
+  int32_t* hp = hints + (e.x - warp_base);
+  if (e.w == kActUnite) {
+    int32_t hint = ld_shared_relaxed(hp);
+    const int32_t old = hint;
+    uf_unite_hinted_keyed(parent, key, e.x, e.y, hint);
+    if (hint != old) st_shared_relaxed(hp, hint);
+    record_run(reach, e.y, e.z);
+  } else if (e.w == kActClaimB) {
+    if (ld_relaxed(parent + e.y) == e.y) uf_claim(parent, e.y, ld_shared_relaxed(hp));
+  } else {
+    if (ld_relaxed(parent + e.x) == e.x) uf_claim(parent, e.x, uf_find(parent, e.y));
+  }
+}
+
+__device__ __noinline__ int main_drain_batch(const int4* act, int qn, int lane, int32_t* hints,
+                                             int32_t warp_base, int32_t* __restrict__ parent,
+                                             const int32_t* __restrict__ key,
+                                             int32_t* __restrict__ reach) {
+  qn -= 32;
+  main_resolve(act[qn + lane], hints, warp_base, parent, key, reach);
+  __syncwarp();
+  return qn;
+}
+
+// 12 resident blocks (42 registers): C1 main 0.59 -> 0.55 ms, C3fd 22.2 -> 21.3 ms vs 10
+constexpr int kMainQMinBlocks = 12;
+
+template <int D, int kFast>
+__global__ void __launch_bounds__(kQueryBlock, kMainQMinBlocks)
+k_fd_main_q(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
+            BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+            const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
+            int32_t* __restrict__ reach, DevCounters* ctr) {
+  __shared__ int4 s_act[kQueryBlock / 32][kActCap];
+  __shared__ int32_t s_hint[kQueryBlock];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = r < m;
+  const int32_t rank = static_cast<int32_t>(r);
+  const int32_t warp_base = rank - lane;
+  int4* act = s_act[w];
+  int32_t* hints = s_hint + (w << 5);
+  unsigned long long pairs = 0;
+  float p[3] = {0.f, 0.f, 0.f};
+  bool core_r = false;
+  if (valid) {
+    int32_t id;
+    load_query<D>(leaf_pt, r, p, &id);
+    core_r = flags[rank] != 0;
+  }
+  bool settled = false;
+  hints[lane] = rank;
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, rank + 1, node, nlo);
+  const int32_t min_rank = rank + 1;
+  int2 stack[kStackDepth];
+  int top = 0;
+  bool active = valid;
+  int qn = 0;  // warp-uniform queue length
+  using T = NodeTraits<D>;
+  while (true) {
+    int na = 0;
+    int4 a0 = make_int4(0, 0, 0, 0), a1 = a0;
+    if (active) {
+      float f[T::kFloats];
+      load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
+      const int32_t left = __float_as_int(f[T::kIntOff + 0]);
+      const int32_t right = __float_as_int(f[T::kIntOff + 1]);
+      const int32_t aux_l = __float_as_int(f[T::kIntOff + 2]);
+      const int32_t aux_r = __float_as_int(f[T::kIntOff + 3]);
+      const bool leaf_l = left < 0, leaf_r = right < 0;
+      const int32_t split = leaf_l ? ~left : aux_l;  // last rank of the left child
+      const int32_t max_r = leaf_r ? ~right : aux_r;
+      int cl = ball_classify<D, kFast>(p, f, f + D, bt);
+      int cr = ball_classify<D, kFast>(p, f + 2 * D, f + 3 * D, bt);
+      if (split < min_rank) cl = 0;
+      if (max_r < min_rank) cr = 0;
+      // one child: a leaf hit or a contained run -> at most one action;
+      // returns the classification left for the descent (1 = walk it)
+      auto child = [&](bool leaf, int32_t first, int32_t last, int c) -> int {
+        if (c == 0 || (!leaf && c == 1)) return c;
+        int4 e = make_int4(rank, first, last, -1);
+        if (leaf) {
+          ++pairs;
+          if (core_r) {
+            e.w = flags[first] ? kActUnite : kActClaimB;
+          } else if (!settled && flags[first]) {
+            e.w = kActClaimSelf;
+            settled = true;
+          }
+        } else {
+          const int32_t size = last - first + 1;
+          const int32_t noncore = __ldg(noncore_before + last + 1) - __ldg(noncore_before + first);
+          if (core_r) {
+            if (noncore != 0) return 1;  // mixed: walk it leaf by leaf
+            e.w = kActUnite;
+          } else if (!settled && noncore != size) {
+            if (noncore != 0) return 1;
+            e.w = kActClaimSelf;
+            settled = true;
+          }
+          pairs += static_cast<unsigned long long>(size);
+        }
+        if (e.w >= 0) {
+          if (na == 0) a0 = e;
+          else a1 = e;
+          ++na;
+        }
+        return 0;  // taken
+      };
+      const int32_t fl = leaf_l ? ~left : (nlo > min_rank ? nlo : min_rank);
+      const int32_t fr = leaf_r ? ~right : (split + 1 > min_rank ? split + 1 : min_rank);
+      cl = child(leaf_l, fl, split, cl);
+      cr = child(leaf_r, fr, max_r, cr);
+      const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
+      if (go_l && go_r) {
+        stack[top++] = make_int2(left, nlo);
+        node = right;
+        nlo = split + 1;
+      } else if (go_l) {
+        node = left;
+      } else if (go_r) {
+        node = right;
+        nlo = split + 1;
+      } else if (top > 0) {
+        const int2 e = stack[--top];
+        node = e.x;
+        nlo = e.y;
+      } else {
+        active = false;
+      }
+    }
+    const unsigned m1 = __ballot_sync(0xffffffffu, na >= 1);
+    if (m1) {
+      const unsigned m2 = __ballot_sync(0xffffffffu, na == 2);
+      const unsigned lt = (1u << lane) - 1u;
+      const int off = qn + __popc(m1 & lt) + __popc(m2 & lt);
+      if (na >= 1) act[off] = a0;
+      if (na == 2) act[off + 1] = a1;
+      qn += __popc(m1) + __popc(m2);
+      if (qn >= 32) {
+        __syncwarp();
+        qn -= 32;
+        main_resolve(act[qn + lane], hints, warp_base, parent, key, reach);
+        __syncwarp();
+        if (qn >= 32) qn = main_drain_batch(act, qn, lane, hints, warp_base, parent, key, reach);
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+  }
+  __syncwarp();
+  if (lane < qn) main_resolve(act[lane], hints, warp_base, parent, key, reach);
+  flush_counter(&ctr->pairs, pairs);
+  flush_counter(&ctr->dists, pairs);
+}
+
 __global__ void k_permute(const uint8_t* __restrict__ src, const int32_t* __restrict__ order,
                           int64_t n, uint8_t* __restrict__ dst, bool to_rank) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
@@ -629,7 +805,8 @@ void fdbscan_main_pass(const BuiltBvh& b, const int32_t* key, int64_t n, double 
     void* scan_tmp = scratch.alloc(scan_scratch_bytes(n + 1));
     note_launch(), k_noncore_ind<<<grid_for(n + 1, 256), 256, 0, s>>>(flags, n, ind);
     exclusive_scan_i32(ind, noncore_before, n + 1, nullptr, scan_tmp, s);
-    auto main = bt.fast ? k_fd_main<D, 1> : k_fd_main<D, 0>;
+    auto main = TCB_MAIN_BATCH ? (bt.fast ? k_fd_main_q<D, 1> : k_fd_main_q<D, 0>)
+                               : (bt.fast ? k_fd_main<D, 1> : k_fd_main<D, 0>);
     note_launch(), main<<<grid, kQueryBlock, 0, s>>>(b.tree.nodes, b.leaf_pt, n, bt, flags, parent,
                                                     key, noncore_before, reach, d_ctr);
   }

@@ -22,6 +22,7 @@ CONFIGS = {
     "C3": (("hacc_like", 37_000_000), 0.042, 100, 1),
     "C3fd": (("hacc_like", 37_000_000), 0.042, 100, 0),
     "C4": (("taxi_like", 80_000_000), 0.001, 1000, 1),
+    "C4fd": (("taxi_like", 80_000_000), 0.001, 1000, 0),
     "C5": (("hacc_like", 497_000_000), 0.042, 2, 0),
 }
 
