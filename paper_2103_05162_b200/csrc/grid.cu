@@ -289,6 +289,9 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
 // Resident 128-thread blocks per SM the DenseBox traversals are compiled
 // for (register cap; C4 main pass 63.7 -> 62.8 ms).
 constexpr int kDbMinBlocks = 10;
+#ifndef TCB_DB_MAIN_Q
+#define TCB_DB_MAIN_Q 1
+#endif
 
 template <int D, int kFast>
 struct DbCoreQuery {
@@ -557,6 +560,177 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
         nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
     }
   }
+  unsigned long long v = warp_sum(dists);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
+  v = warp_sum(pairs);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->pairs, v);
+}
+
+// k_db_main_ranged with warp-batched union-find work (as k_fd_main_q): the
+// query's own lane walks the mixed tree and runs the member scans; the
+// unions and claims its pairs imply are queued per warp and resolved 32 at
+// a time with the root hints in shared memory (shared atomics). Action
+// (x = query slot, y = target slot, z, w): z >= 0 a union, recording the
+// primitive-rank run [z, w] when w > z; z == -1 a core query claiming border
+// y under its hint; z == -2 a border query joining core y's cluster.
+constexpr int kDbActCap = 96;
+
+template <bool kForceCore>
+__device__ __forceinline__ void db_resolve(int4 e, int32_t* hints, int32_t warp_base,
+                                           int32_t* __restrict__ parent,
+                                           const int32_t* __restrict__ key,
+                                           int32_t* __restrict__ reach, uint8_t* flags) {
+  int32_t* hp = hints + (e.x - warp_base);
+  if (e.z >= 0) {
+    int32_t hint = atomicAdd(hp, 0);
+    const int32_t old = hint;
+    uf_unite_hinted_keyed(parent, key, e.x, e.y, hint, kForceCore ? flags : nullptr);
+    if (hint != old) atomicExch(hp, hint);
+    record_run(reach, e.z, e.w);
+  } else if (e.z == -1) {
+    if (ld_relaxed(parent + e.y) == e.y) uf_claim(parent, e.y, atomicAdd(hp, 0));
+  } else {
+    if (ld_relaxed(parent + e.x) == e.x) uf_claim(parent, e.x, uf_find(parent, e.y));
+  }
+}
+
+template <bool kForceCore>
+__device__ __noinline__ int db_drain_batch(const int4* act, int qn, int lane, int32_t* hints,
+                                           int32_t warp_base, int32_t* __restrict__ parent,
+                                           const int32_t* __restrict__ key,
+                                           int32_t* __restrict__ reach, uint8_t* flags) {
+  qn -= 32;
+  db_resolve<kForceCore>(act[qn + lane], hints, warp_base, parent, key, reach, flags);
+  __syncwarp();
+  return qn;
+}
+
+template <int D, bool kForceCore, int kFast>
+__global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
+k_db_main_q(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
+            const int32_t* __restrict__ qrank, int64_t n,
+            const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
+            BallTest bt, uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
+            const int32_t* __restrict__ key, const int32_t* __restrict__ qoff,
+            const int32_t* __restrict__ noncore_before, int32_t* __restrict__ reach,
+            DevCounters* ctr, MemberTree mt) {
+  __shared__ int4 s_act[kQueryBlock / 32][kDbActCap];
+  __shared__ int32_t s_hint[kQueryBlock];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = q < n;
+  const int32_t i = static_cast<int32_t>(q);  // this query's slot
+  const int32_t warp_base = i - lane;
+  int4* act = s_act[w];
+  int32_t* hints = s_hint + (w << 5);
+  unsigned long long pairs = 0, dists = 0;
+  float p[3] = {0.f, 0.f, 0.f};
+  int32_t own = 0;
+  if (valid) {
+    const float4 qp = qpt[q];
+    own = qrank[q];
+    p[0] = qp.x;
+    p[1] = qp.y;
+    p[2] = qp.z;
+  }
+  hints[lane] = i;
+  int32_t node, nlo;
+  warp_start_node<D>(nodes, p, valid, bt, own + 1, node, nlo);
+  const bool core_i = kForceCore ? true : (valid && flags[i] != 0);
+  bool settled = false;
+  int na = 0;
+  int4 a0 = make_int4(0, 0, 0, 0), a1 = a0;
+  auto push = [&](int4 e) {
+    if (na == 0) a0 = e;
+    else a1 = e;
+    ++na;
+  };
+  // the pair (i, slot j), dbscan.hpp:82-99, as a queued action
+  auto pair = [&](int32_t j) {
+    ++pairs;
+    if (kForceCore || (core_i && flags[j])) {
+      push(make_int4(i, j, 0, 0));
+    } else if (core_i) {
+      push(make_int4(i, j, -1, -1));
+    } else if (!settled && flags[j]) {
+      push(make_int4(i, j, -2, -2));
+      settled = true;
+    }
+  };
+  auto visit = [&](int32_t s, int32_t aux, bool contained) -> bool {
+    const int32_t base = __ldg(qoff + s);
+    if (aux >= 0) {
+      ++dists;
+      pair(base);
+    } else {
+      const int32_t c = ~aux;
+      const int32_t kb = cell_begin[c], ke = cell_end[c];
+      if (contained) {
+        ++dists;
+        pair(base);
+      } else {
+        int hits;
+        const int64_t pos = member_scan<D>(mt, kb, ke, p, bt, 1, hits);
+        if (pos >= 0) {
+          dists += static_cast<unsigned long long>(pos - kb + 1);
+          pair(base + static_cast<int32_t>(pos - kb));
+        } else {
+          dists += static_cast<unsigned long long>(ke - kb);
+        }
+      }
+    }
+    return true;
+  };
+  auto inside = [&](int32_t first, int32_t last) -> int {
+    const int32_t cnt = last - first + 1;
+    bool run = kForceCore;
+    if (!kForceCore) {
+      const int32_t nc = __ldg(noncore_before + last + 1) - __ldg(noncore_before + first);
+      if (core_i) {
+        if (nc != 0) return kWalk;
+        run = true;
+      } else if (!settled && nc != cnt) {
+        if (nc != 0) return kWalk;
+        push(make_int4(i, __ldg(qoff + first), -2, -2));
+        settled = true;
+      }
+    }
+    if (run) push(make_int4(i, __ldg(qoff + first), first, last));
+    pairs += static_cast<unsigned long long>(cnt);
+    dists += static_cast<unsigned long long>(cnt);
+    return kTaken;
+  };
+  int2 stack_buf[kStackDepth];
+  LocalStack stack(stack_buf);
+  bool active = valid;
+  int qn = 0;  // warp-uniform queue length
+  while (true) {
+    na = 0;
+    if (active)
+      active = bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
+          nodes, p, bt, own + 1, node, nlo, stack, visit, inside);
+    const unsigned m1 = __ballot_sync(0xffffffffu, na >= 1);
+    if (m1) {
+      const unsigned m2 = __ballot_sync(0xffffffffu, na == 2);
+      const unsigned lt = (1u << lane) - 1u;
+      const int off = qn + __popc(m1 & lt) + __popc(m2 & lt);
+      if (na >= 1) act[off] = a0;
+      if (na == 2) act[off + 1] = a1;
+      qn += __popc(m1) + __popc(m2);
+      if (qn >= 32) {
+        __syncwarp();
+        qn -= 32;
+        db_resolve<kForceCore>(act[qn + lane], hints, warp_base, parent, key, reach, flags);
+        __syncwarp();
+        if (qn >= 32)
+          qn = db_drain_batch<kForceCore>(act, qn, lane, hints, warp_base, parent, key, reach,
+                                          flags);
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+  }
+  __syncwarp();
+  if (lane < qn) db_resolve<kForceCore>(act[lane], hints, warp_base, parent, key, reach, flags);
   unsigned long long v = warp_sum(dists);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctr->dists, v);
   v = warp_sum(pairs);
@@ -935,11 +1109,20 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
     exclusive_scan_i32(ind, noncore_before, num_prims + 1, nullptr, scan_tmp, st);
   }
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
-  auto main = minpts == 2 ? (bt.fast ? k_db_main_ranged<D, true, 1> : k_db_main_ranged<D, true, 0>)
-                          : (bt.fast ? k_db_main_ranged<D, false, 1> : k_db_main_ranged<D, false, 0>);
-  note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt, cell_begin,
-                                                cell_end, bt, flags, parent, qkey, qoff,
-                                                noncore_before, reach, ctr, mt);
+  // minpts > 2: unions and border claims batched per warp (C4 main 62.8 ->
+  // 59.2 ms); minpts == 2 keeps the per-query form (26.3 vs 26.7 ms on C2)
+  if (TCB_DB_MAIN_Q && minpts > 2) {
+    auto main = bt.fast ? k_db_main_q<D, false, 1> : k_db_main_q<D, false, 0>;
+    note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, cell_begin,
+                                                  cell_end, bt, flags, parent, qkey, qoff,
+                                                  noncore_before, reach, ctr, mt);
+  } else {
+    auto main = minpts == 2 ? (bt.fast ? k_db_main_ranged<D, true, 1> : k_db_main_ranged<D, true, 0>)
+                            : (bt.fast ? k_db_main_ranged<D, false, 1> : k_db_main_ranged<D, false, 0>);
+    note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, sorted_pt,
+                                                  cell_begin, cell_end, bt, flags, parent, qkey,
+                                                  qoff, noncore_before, reach, ctr, mt);
+  }
   launch_cover_joins(reach, num_prims, tile_max,
                      SlotJoin{parent, qkey, qoff, minpts == 2 ? flags : nullptr}, st);
   TCB_CUDA(cudaGetLastError());
