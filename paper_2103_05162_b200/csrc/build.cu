@@ -218,6 +218,16 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
   return 64 + __clz(static_cast<int>(static_cast<uint32_t>(i) ^ static_cast<uint32_t>(j)));
 }
 
+// delta(s, s+1) of every boundary as one byte (<= 96; -1 past the end as
+// 0xff), so the climb's global phase reads 1-byte values from an L2-resident
+// array instead of two 8-byte codes per boundary.
+__global__ void __launch_bounds__(256)
+k_boundary_deltas(const uint64_t* __restrict__ codes, int64_t m, int8_t* __restrict__ delta) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    delta[s] = static_cast<int8_t>(key_delta(codes, m, s, s + 1));
+}
+
 // ---------------------------------------------------------------------------
 // Single-pass bottom-up build (Apetrei 2014) of the Karras radix tree
 // (bvh.cpp:49-124): topology, boxes and leaf gather in one kernel.
@@ -240,6 +250,9 @@ __device__ __forceinline__ int key_delta(const uint64_t* __restrict__ codes, int
 // The tree is the reference's tree node for node; only the numbering of the
 // internal nodes differs (tcg_debug_point_bvh renumbers to Karras indices).
 // ---------------------------------------------------------------------------
+#ifndef TCB_CLIMB_DELTAS
+#define TCB_CLIMB_DELTAS 1
+#endif
 constexpr int kClimbBlock = 128;  // 256: topology 3.04 vs 2.90 ms on C2; 64: 3.06; 512 slower still
 
 struct ClimbState {
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(kClimbBlock)
 k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__ order,
         const int32_t* __restrict__ prim_aux, int64_t m, float4* nodes,
         int32_t* __restrict__ other, float4* __restrict__ leaf_pt,
-        ClimbState* state) {
+        ClimbState* state, const int8_t* __restrict__ deltas) {
   using T = NodeTraits<D>;
   const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   bool active = s < m;
@@ -292,8 +305,14 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
     const int64_t b0 = s - t;
     const int64_t b1 = min(b0 + kClimbBlock - 1, m - 1);
     // every boundary delta a subtree inside the block can ask for, computed once
-    s_delta[t + 1] = key_delta(codes, m, b0 + t, b0 + t + 1);
-    if (t == 0) s_delta[0] = b0 > 0 ? key_delta(codes, m, b0 - 1, b0) : -1;
+    if (deltas) {
+      if (b0 + t < m) s_delta[t + 1] = deltas[b0 + t];
+      else s_delta[t + 1] = -1;
+      if (t == 0) s_delta[0] = b0 > 0 ? deltas[b0 - 1] : -1;
+    } else {
+      s_delta[t + 1] = key_delta(codes, m, b0 + t, b0 + t + 1);
+      if (t == 0) s_delta[0] = b0 > 0 ? key_delta(codes, m, b0 - 1, b0) : -1;
+    }
     __syncthreads();
     auto publish = [&] {
 #pragma unroll
@@ -370,7 +389,9 @@ k_climb(Src src, const uint64_t* __restrict__ codes, const int32_t* __restrict__
     int32_t p = 0;
     bool left = false;
     if (active) {
-      left = l == 0 || (r != m - 1 && key_delta(codes, m, r, r + 1) > key_delta(codes, m, l - 1, l));
+      left = l == 0 ||
+             (r != m - 1 && (deltas ? deltas[r] > deltas[l - 1]
+                                    : key_delta(codes, m, r, r + 1) > key_delta(codes, m, l - 1, l)));
       p = left ? r : l - 1;
       float* pf = reinterpret_cast<float*>(nodes + static_cast<int64_t>(p) * T::kVec);
       float* slot = pf + (left ? 0 : 2 * D);
@@ -519,8 +540,13 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     int32_t* other = scratch.alloc_n<int32_t>(m - 1);
     auto* state = scratch.alloc_n<ClimbState>(1);
     TCB_CUDA(cudaMemsetAsync(other, 0xff, sizeof(int32_t) * (m - 1), st));
+    int8_t* deltas = nullptr;
+    if (TCB_CLIMB_DELTAS) {
+      deltas = scratch.alloc_n<int8_t>(m);
+      note_launch(), k_boundary_deltas<<<grid_for(m, 256, 148 * 16), 256, 0, st>>>(codes, m, deltas);
+    }
     note_launch(), k_climb<D><<<grid_for(m, kClimbBlock, INT32_MAX), kClimbBlock, 0, st>>>(
-        boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, state);
+        boxes, codes, order, src.aux, m, out.tree.nodes, other, leaf_pt, state, deltas);
     note_launch(), k_root_to_zero<D><<<1, NodeTraits<D>::kVec, 0, st>>>(out.tree.nodes, m, state);
   }
   TCB_CUDA(cudaGetLastError());
