@@ -180,8 +180,8 @@ tc_status tcg_shard_unpack_rows_device(const int32_t* d_rows, int64_t n, int dim
                                        int64_t* d_gid, int64_t* d_codes, void* stream);
 /* Region boxes of a shard for the eps-halo: the tight boxes of the occupied
  * Morton-prefix cells of its points (the prefix length chosen so the shard's
- * code range spans at most 65536 cells). d_box_lo / d_box_hi need room for
- * 65536*dim floats; *d_num_boxes (device int64) receives the count. Every
+ * code range spans at most 4096 cells). d_box_lo / d_box_hi need room for
+ * 4096*dim floats; *d_num_boxes (device int64) receives the count. Every
  * point lies in one of the boxes. */
 tc_status tcg_shard_region_boxes_device(const float* d_coords, const int64_t* d_codes, int64_t n,
                                         int dim, float* d_box_lo, float* d_box_hi,

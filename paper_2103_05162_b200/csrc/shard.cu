@@ -325,7 +325,13 @@ k_unpack_rows(const int32_t* __restrict__ rows, int64_t n, float* __restrict__ c
 // cell's box is reduced with order-preserving atomics, then the occupied ones
 // are compacted. Every point lies in the box of its cell: the boxes cover the
 // shard, which is all the eps-halo selection needs (tcg_near_peers_device).
-constexpr int kCellBits = 16;
+// 4096 cells: a block reduces its points' boxes in shared memory (96 KB in
+// 3D) and merges each touched cell into the global boxes once — 37M global
+// atomics per pass become a few million (a 65536-cell table took 2.1 ms on
+// 37M points, almost all of it in contended global atomics). The cells are
+// Morton-prefix blocks of the shard's own range, so a coarse cell's tight
+// box stays inside the shard's region and the halo is as thin as before.
+constexpr int kCellBits = 12;
 
 __global__ void k_code_range(const int64_t* __restrict__ codes, int64_t n,
                              unsigned long long* range) {
@@ -349,21 +355,38 @@ __global__ void k_code_range(const int64_t* __restrict__ codes, int64_t n,
 }
 
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 k_cell_boxes(const float* __restrict__ coords, const int64_t* __restrict__ codes, int64_t n,
              const unsigned long long* __restrict__ range, uint32_t* __restrict__ cell_ord) {
   const unsigned long long lo = range[0], hi = range[1];
   int shift = 0;
   while (((hi >> shift) - (lo >> shift)) >= (1ull << kCellBits)) ++shift;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  extern __shared__ uint32_t s_box[];  // [cell][lo D | hi D]
+  constexpr int kWords = (1 << kCellBits) * 2 * D;
+  for (int w = threadIdx.x; w < kWords; w += blockDim.x) s_box[w] = (w % (2 * D)) < D ? ~0u : 0u;
+  __syncthreads();
+  // a contiguous chunk per block (consecutive points share cells more often)
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
     const uint64_t c = (static_cast<unsigned long long>(codes[i]) >> shift) - (lo >> shift);
-    uint32_t* b = cell_ord + c * (2 * D);
+    uint32_t* b = s_box + c * (2 * D);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const uint32_t v = f2ord(coords[i * D + k]);
       atomicMin(b + k, v);
       atomicMax(b + D + k, v);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < (1 << kCellBits); c += blockDim.x) {
+    const uint32_t* b = s_box + c * (2 * D);
+    if (b[0] > b[D]) continue;  // untouched here
+    uint32_t* g = cell_ord + static_cast<int64_t>(c) * (2 * D);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      atomicMin(g + k, b[k]);
+      atomicMax(g + D + k, b[D + k]);
     }
   }
 }
@@ -646,13 +669,18 @@ TC_EXPORT tc_status tcg_shard_region_boxes_device(const float* d_coords, const i
     note_launch(), k_fill_u32<<<grid_for(words, 256), 256, 0, st>>>(cell_ord, words, 0xffffffffu,
                                                                      0u, 2 * dim, dim);
     note_launch(), k_code_range<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(d_codes, n, range);
-    const unsigned g = grid_for(n, 256, 148 * 16);
+    const unsigned g = grid_for(n, 1024, 148 * 2);
     const unsigned gc = grid_for(int64_t{1} << kCellBits, 256);
+    const size_t smem = sizeof(uint32_t) * (size_t{1} << kCellBits) * 2 * dim;
     if (dim == 2) {
-      note_launch(), k_cell_boxes<2><<<g, 256, 0, st>>>(d_coords, d_codes, n, range, cell_ord);
+      TCB_CUDA(cudaFuncSetAttribute(k_cell_boxes<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      note_launch(), k_cell_boxes<2><<<g, 1024, smem, st>>>(d_coords, d_codes, n, range, cell_ord);
       note_launch(), k_cell_compact<2><<<gc, 256, 0, st>>>(cell_ord, d_box_lo, d_box_hi, count);
     } else {
-      note_launch(), k_cell_boxes<3><<<g, 256, 0, st>>>(d_coords, d_codes, n, range, cell_ord);
+      TCB_CUDA(cudaFuncSetAttribute(k_cell_boxes<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      note_launch(), k_cell_boxes<3><<<g, 1024, smem, st>>>(d_coords, d_codes, n, range, cell_ord);
       note_launch(), k_cell_compact<3><<<gc, 256, 0, st>>>(cell_ord, d_box_lo, d_box_hi, count);
     }
     TCB_CUDA(cudaGetLastError());

@@ -175,7 +175,7 @@ class DeviceEngine:
     def region_boxes(self, x, codes):
         """(k, 2*dim) float32 boxes covering the points (Morton-prefix cells)."""
         n, d = x.shape
-        cap = 1 << 16
+        cap = 1 << 12
         lo = torch.empty((cap, d), dtype=torch.float32, device=x.device)
         hi = torch.empty((cap, d), dtype=torch.float32, device=x.device)
         cnt = torch.zeros(1, dtype=torch.int64, device=x.device)

@@ -157,7 +157,7 @@ class OracleEngineFused(OracleEngine):
         c = codes.numpy().astype(np.uint64)
         lo, hi = int(c.min()), int(c.max())
         shift = 0
-        while (hi >> shift) - (lo >> shift) >= (1 << 16):
+        while (hi >> shift) - (lo >> shift) >= (1 << 12):
             shift += 1
         cell = (c >> np.uint64(shift)) - np.uint64(lo >> shift)
         uniq, inv = np.unique(cell, return_inverse=True)
@@ -458,7 +458,7 @@ def test_region_boxes_cover_and_near_peers():
     eng = DeviceEngine("cuda:0")
     codes = eng.morton(x, x.min(0).values, x.max(0).values)
     boxes = eng.region_boxes(x, codes).cpu().numpy()
-    assert 0 < len(boxes) <= 1 << 16
+    assert 0 < len(boxes) <= 1 << 12
     p = x.cpu().numpy()
     inside = np.zeros(len(p), bool)
     for b in boxes:
