@@ -240,11 +240,15 @@ constexpr int kStop = 0, kTaken = 1, kWalk = 2;
 // leaves are reported is not the reference's DFS order (callers only depend
 // on the set, or, for early exit, on the count — see CoreQuery).
 
+// self >= 0 (an order-free query of the leaf at rank `self`, e.g. an
+// early-exit count): of two children to walk, the one holding `self` goes
+// first — its Morton neighbours, the likeliest hits, are counted soonest.
 template <int D, typename Stack, typename Visit, typename Inside, int kFast = -1>
 __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes, const float* p,
                                                 const BallTest& bt, int32_t min_rank,
                                                 int32_t& node, int32_t& nlo, Stack& stack,
-                                                Visit& visit, Inside& inside) {
+                                                Visit& visit, Inside& inside,
+                                                int32_t self = -1) {
   using T = NodeTraits<D>;
   float f[T::kFloats];
   load_node<D>(nodes + static_cast<int64_t>(node) * T::kVec, f);
@@ -281,9 +285,14 @@ __device__ __forceinline__ bool bvh_step_ranged(const float4* __restrict__ nodes
   }
   const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
   if (go_l && go_r) {
-    stack.push(make_int2(left, nlo));
-    node = right;
-    nlo = split + 1;
+    if (self >= 0 && self <= split) {  // (nlo <= self: the walk never leaves self's side first)
+      stack.push(make_int2(right, split + 1));
+      node = left;
+    } else {
+      stack.push(make_int2(left, nlo));
+      node = right;
+      nlo = split + 1;
+    }
   } else if (go_l) {
     node = left;
   } else if (go_r) {

@@ -47,6 +47,9 @@ constexpr int kFofMinBlocks = TCB_FOF_MIN_BLOCKS;
 #define TCB_MAIN_MIN_BLOCKS 10
 #endif
 constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
+#ifndef TCB_CORE_NEAR_FIRST
+#define TCB_CORE_NEAR_FIRST 1
+#endif
 #ifndef TCB_MAIN_BATCH
 #define TCB_MAIN_BATCH 1
 #endif
@@ -110,7 +113,7 @@ struct CoreQuery {
       return kTaken;
     };
     return bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, 0, node, nlo, stack, visit, inside);
+        nodes, p, bt, 0, node, nlo, stack, visit, inside, TCB_CORE_NEAR_FIRST ? id : -1);
   }
   __device__ void end() {
     if (count >= minpts) flags[id] = 1;
