@@ -285,6 +285,15 @@ k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_
 #define TCB_FOF_BATCH 1
 #endif
 constexpr int kActCap = 96;  // < 32 queued + up to 2 per lane per step
+// The FoF pass walks, of two children, the one holding the nearest unmasked
+// ranks (min_rank) first — the query's Morton neighbours are met (and
+// united) first, which keeps its root hint current and the warp's lanes in
+// the same subtrees: C2 main 16.4 -> 16.0 ms, C5 221 -> 214 ms (DenseBox
+// minpts 2 likewise, main 26.2 -> 23.9 ms; the minpts > 2 passes measured
+// slower with it and keep right-first).
+#ifndef TCB_FOF_SELF_FIRST
+#define TCB_FOF_SELF_FIRST 1
+#endif
 
 // The hint slots are read and written by the lanes resolving actions of the
 // same query concurrently: shared-memory atomics (whichever value wins is a
@@ -376,9 +385,17 @@ k_fd_main_fof_q(const float4* __restrict__ nodes, const float4* __restrict__ lea
       l1 = max_r;
       const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
       if (go_l && go_r) {
-        stack[top++] = make_int2(left, nlo);
-        node = right;
-        nlo = split + 1;
+#if TCB_FOF_SELF_FIRST
+        if (split >= min_rank) {  // the left child holds the nearest unmasked ranks
+          stack[top++] = make_int2(right, split + 1);
+          node = left;
+        } else
+#endif
+        {
+          stack[top++] = make_int2(left, nlo);
+          node = right;
+          nlo = split + 1;
+        }
       } else if (go_l) {
         node = left;
       } else if (go_r) {
@@ -553,9 +570,11 @@ k_fd_main_q(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt
       cr = child(leaf_r, fr, max_r, cr);
       const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
       if (go_l && go_r) {
-        stack[top++] = make_int2(left, nlo);
-        node = right;
-        nlo = split + 1;
+        {  // (self-first measured slower here: C3 main 21.2 -> 21.6 ms)
+          stack[top++] = make_int2(left, nlo);
+          node = right;
+          nlo = split + 1;
+        }
       } else if (go_l) {
         node = left;
       } else if (go_r) {

@@ -557,7 +557,7 @@ k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qp
     int2 stack_buf[kStackDepth];
     LocalStack stack(stack_buf);
     while (bvh_step_ranged<D, LocalStack, decltype(visit), decltype(inside), kFast>(
-        nodes, p, bt, own + 1, node, nlo, stack, visit, inside)) {
+        nodes, p, bt, own + 1, node, nlo, stack, visit, inside, own + 1)) {
     }
   }
   unsigned long long v = warp_sum(dists);
