@@ -8,5 +8,6 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   make -s -j16 EXTRA="$flags" OBJDIR=build_ab_$name OUT=../ab/libtreeclust_b200_$name.so >/dev/null 2>&1 \
     || { echo "build $name failed"; exit 1; }
+  rm -rf build_ab_$name  # objects are not needed once linked (keeps the gpurun snapshot small)
   echo "built ab/libtreeclust_b200_$name.so ($flags)"
 done
