@@ -53,6 +53,9 @@ constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
 #ifndef TCB_MAIN_BATCH
 #define TCB_MAIN_BATCH 1
 #endif
+#ifndef TCB_MAIN_CORE_LEFT_FIRST
+#define TCB_MAIN_CORE_LEFT_FIRST 1
+#endif
 
 template <int D>
 __device__ __forceinline__ void load_query(const float4* leaf_pt, int64_t r, float* p,
@@ -570,7 +573,13 @@ k_fd_main_q(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt
       cr = child(leaf_r, fr, max_r, cr);
       const bool go_l = cl == 1 && !leaf_l, go_r = cr == 1 && !leaf_r;
       if (go_l && go_r) {
-        {  // (self-first measured slower here: C3 main 21.2 -> 21.6 ms)
+#if TCB_MAIN_CORE_LEFT_FIRST
+        if (core_r) {  // core queries: ascending ranks first
+          stack[top++] = make_int2(right, split + 1);
+          node = left;
+        } else
+#endif
+        {  // (left-first for every query measured slower: C3 main 21.2 -> 21.6 ms)
           stack[top++] = make_int2(left, nlo);
           node = right;
           nlo = split + 1;
