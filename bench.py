@@ -460,6 +460,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--points", type=int, default=N_POINTS, help="points per rank (default: 37M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay leg")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the Morton-range sharded path")
     ap.add_argument("--sharded", action="store_true",
@@ -557,6 +558,40 @@ def main():
     ms_per_step = elapsed_ms / args.steps
     value = n * world / (ms_per_step * 1e-3) / 1e6
 
+    # ---- the same step captured once in a CUDA graph and replayed (FDBSCAN
+    # never synchronizes the host, so tcg_cluster_device_async captures) ----
+    graph = None
+    if not args.no_graph:
+        try:
+            gl = torch.empty_like(labels)
+            gc = torch.empty_like(core)
+            gs = torch.empty(1, dtype=torch.int32, device=dev)
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs, capture_error_mode="relaxed"):
+                tb.cluster_device_async(x, EPS, MINPTS, tb.Algorithm.FDBSCAN, gl, gc, gs, cs)
+            for _ in range(2):
+                g.replay()
+            torch.cuda.synchronize()
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(cs)
+            for _ in range(args.steps):
+                g.replay()
+            g1.record(cs)
+            torch.cuda.synchronize()
+            gms = g0.elapsed_time(g1) / args.steps
+            cm = core == 1
+            graph = {"ms_per_step": round(gms, 3), "value": round(n / (gms * 1e-3) / 1e6, 3),
+                     "unit": UNIT, "status": int(gs.item()),
+                     "labels_equal": bool(torch.equal(gc, core) and torch.equal(gl[cm], labels[cm])
+                                          and torch.equal(gl == -1, labels == -1)),
+                     "api": "tcg_cluster_device_async captured once in a CUDA graph, replayed"}
+            del g
+        except Exception as e:  # reported, never fatal for the bench line
+            graph = {"error": str(e)[:200]}
+
     # ---- e2e through the C ABI with host buffers (H2D + D2H inside) ----
     e2e_times = []
     for it in range(2 + args.steps):
@@ -632,6 +667,7 @@ def main():
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
                     "h2d_bytes_per_step": n * 3 * 4, "d2h_bytes_per_step": n * 5,
                     "ms_per_step": round(e2e_s * 1e3, 3), "api": "tc_cluster (C ABI)"},
+            "graph": graph,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches,

@@ -35,24 +35,36 @@ const char* tcg_version(void);
  *   stream   : cudaStream_t to launch on (NULL = legacy default stream)
  *   stats    : may be NULL. When non-NULL the call synchronizes the stream at
  *              the end to read counters and stage times back.
- * The call is stream-ordered: with stats == NULL it returns once the work is
- * enqueued, except for the few small device->host reads that validate the
- * input or size later launches, each a stream synchronization:
- *   - after the Morton pass (both algorithms): the non-finite-coordinate flag
- *     (TC_ERR_INVALID_ARGUMENT) and the AND / OR of the keys, which select
- *     the radix-sort passes;
- *   - after the Morton prefix sort's fix-up pass: whether an equal-prefix group
- *     longer than 256 points (many coincident points) needs the full sort;
- *   - DenseBox: the grid's finiteness / overflow check (TC_ERR_INVALID_ARGUMENT)
- *     and the cell and primitive counts.
- * It is therefore not capturable into a CUDA graph. Scratch comes from the
- * library's stream-ordered memory pool (tcg_set_pool_release_threshold) and
- * is released before return. */
+ * The call is stream-ordered. FDBSCAN with stats == NULL never synchronizes
+ * the host: the radix-sort passes are planned on the device from the AND / OR
+ * of the Morton keys, the rare fallback sort (an equal-prefix group longer
+ * than 256 points) is launched guarded and runs only when the device asks
+ * for it, and a non-finite coordinate is detected on the device — the run
+ * then does no traversal work and writes every label -1 / core flag 0 (with
+ * stats != NULL, or through tcg_cluster_device_async's status word, the call
+ * reports TC_ERR_INVALID_ARGUMENT). Such a call can be captured into a CUDA
+ * graph (capture mode relaxed or thread-local) and replayed. DenseBox still
+ * reads back the grid's finiteness / overflow check (TC_ERR_INVALID_ARGUMENT)
+ * and the cell and primitive counts (stream synchronizations), and brute
+ * force its non-finite flag. Scratch comes from the library's stream-ordered
+ * memory pool (tcg_set_pool_release_threshold) and is released before return
+ * (inside a captured graph: by the graph's own free nodes). */
 tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
                              float eps, int minpts, tc_algorithm algorithm,
                              int64_t oracle_cap, int32_t* d_labels,
                              uint8_t* d_core, void* stream,
                              tc_cluster_stats* stats);
+
+/* tcg_cluster_device with stats == NULL and the run's status written on the
+ * device: *d_status (device int32, may be NULL) becomes TC_OK, or
+ * TC_ERR_INVALID_ARGUMENT when a coordinate is non-finite (FDBSCAN; the
+ * outputs are then all noise). Argument errors known on the host are still
+ * returned directly. For FDBSCAN the call never synchronizes the host and is
+ * capturable into a CUDA graph. */
+tc_status tcg_cluster_device_async(const float* d_coords, int64_t n, int dim, float eps,
+                                   int minpts, tc_algorithm algorithm, int64_t oracle_cap,
+                                   int32_t* d_labels, uint8_t* d_core, void* stream,
+                                   int32_t* d_status);
 
 /* Multi-GPU clustering of a host dataset: the points are
  * sharded by Morton range over num_devices shards, shard s on CUDA device

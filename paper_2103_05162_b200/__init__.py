@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     TreeclustError,
     cluster,
     cluster_device,
+    cluster_device_async,
     cluster_multi,
     cluster_raw,
     device_count,

@@ -98,6 +98,8 @@ SIGNATURES = {
     "tcg_local_free": (None, [_P]),
     "tcg_cluster_multi": (C.c_int, [_P, C.c_float, C.c_int, C.c_int, C.POINTER(C.c_int), C.c_int,
                                     _PP]),
+    "tcg_cluster_device_async": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, C.c_int, C.c_int,
+                                         C.c_int64, _P, _P, _P, _P]),
     "tcg_cluster_keyed_device": (C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_float, C.c_int, _P, _P,
                                          _P, C.POINTER(TcClusterStats)]),
     "tcg_cluster_given_core_device": (C.c_int, [_P, C.c_int64, C.c_int, C.c_float, _P, _P, _P,

@@ -239,6 +239,36 @@ def cluster_device(coords, eps: float, minpts: int, algorithm: Algorithm = Algor
     return labels, core, (st.to_dict() if st is not None else None)
 
 
+def cluster_device_async(coords, eps: float, minpts: int,
+                         algorithm: Algorithm = Algorithm.FDBSCAN, labels=None, core=None,
+                         status=None, stream=None, oracle_cap: int = 0):
+    """``tcg_cluster_device_async``: ``cluster_device`` without stats, the run's
+    status written to ``status`` (an int32 CUDA tensor of one element; the
+    non-finite-coordinate error of FDBSCAN is found on the device). For FDBSCAN
+    the call never synchronizes the host, so it can be captured in a CUDA graph.
+    Returns ``(labels, core, status)``."""
+    import torch
+
+    if not (coords.is_cuda and coords.dtype == torch.float32 and coords.dim() == 2
+            and coords.is_contiguous()):
+        raise TreeclustError(Status.INVALID_ARGUMENT, "tcg_cluster_device_async")
+    n, d = coords.shape
+    if labels is None:
+        labels = torch.empty(n, dtype=torch.int32, device=coords.device)
+    if core is None:
+        core = torch.empty(n, dtype=torch.uint8, device=coords.device)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=coords.device)
+    s = stream if stream is not None else torch.cuda.current_stream(coords.device)
+    _check(lib.tcg_cluster_device_async(C.c_void_p(coords.data_ptr()), n, d, C.c_float(eps),
+                                        int(minpts), int(algorithm), int(oracle_cap),
+                                        C.c_void_p(labels.data_ptr()),
+                                        C.c_void_p(core.data_ptr()), C.c_void_p(s.cuda_stream),
+                                        C.c_void_p(status.data_ptr())),
+           "tcg_cluster_device_async")
+    return labels, core, status
+
+
 def load_device(path: str, device=None):
     """``tcg_binary_info`` + ``tcg_load_binary_device``: a .bin point file to a
     (n, dim) float32 CUDA tensor, file reads overlapped with the copies."""

@@ -477,7 +477,7 @@ __global__ void k_single_leaf(Src src, const int32_t* __restrict__ prim_aux, flo
 template <int D, class Src>
 BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finite,
                     bool points_mode, DevCounters* d_ctr, Scratch& scratch,
-                    StageClock* clock) {
+                    StageClock* clock, bool stream_ordered) {
   cudaStream_t st = scratch.stream();
   const int64_t m = src.count;
   BuiltBvh out;
@@ -496,35 +496,53 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
   TCB_CUDA(cudaGetLastError());
 
-  // One small read-back: finiteness + key AND/OR decide the sort passes.
-  auto* h = static_cast<unsigned char*>(pinned_staging(64));
-  TCB_CUDA(cudaMemcpyAsync(h, &d_ctr->key_and, 16, cudaMemcpyDeviceToHost, st));
-  TCB_CUDA(cudaMemcpyAsync(h + 16, &d_ctr->nonfinite, 4, cudaMemcpyDeviceToHost, st));
-  TCB_CUDA(cudaStreamSynchronize(st));
-  unsigned long long key_and, key_or;
-  int32_t nonfinite;
-  std::memcpy(&key_and, h, 8);
-  std::memcpy(&key_or, h + 8, 8);
-  std::memcpy(&nonfinite, h + 16, 4);
-  if (validate_finite && nonfinite) throw InvalidArgument{"PointSet: non-finite coordinate"};
+  const uint64_t* codes;
+  int32_t* order;
+  if (stream_ordered) {
+    // No read-back: the device plans the sort passes from the key AND/OR and
+    // the non-finite flag stays on the device (run_device reports it).
+    if (clock) clock->mark(kStSort);
+    uint64_t* keys_alt = scratch.alloc_n<uint64_t>(m);
+    int32_t* vals_alt = scratch.alloc_n<int32_t>(m);
+    uint64_t* keys_out = scratch.alloc_n<uint64_t>(m);
+    int32_t* vals_out = scratch.alloc_n<int32_t>(m);
+    void* sort_tmp = scratch.alloc(radix_sort_async_scratch_bytes(m));
+    radix_sort_pairs_prefix_async(keys, vals, keys_alt, vals_alt, keys_out, vals_out, m,
+                                  &d_ctr->key_and, sort_tmp, st);
+    codes = keys_out;
+    order = vals_out;
+    out.sort_passes = -1;  // decided on the device
+  } else {
+    // One small read-back: finiteness + key AND/OR decide the sort passes.
+    auto* h = static_cast<unsigned char*>(pinned_staging(64));
+    TCB_CUDA(cudaMemcpyAsync(h, &d_ctr->key_and, 16, cudaMemcpyDeviceToHost, st));
+    TCB_CUDA(cudaMemcpyAsync(h + 16, &d_ctr->nonfinite, 4, cudaMemcpyDeviceToHost, st));
+    TCB_CUDA(cudaStreamSynchronize(st));
+    unsigned long long key_and, key_or;
+    int32_t nonfinite;
+    std::memcpy(&key_and, h, 8);
+    std::memcpy(&key_or, h + 8, 8);
+    std::memcpy(&nonfinite, h + 16, 4);
+    if (validate_finite && nonfinite) throw InvalidArgument{"PointSet: non-finite coordinate"};
 
-  if (clock) clock->mark(kStSort);
-  uint64_t* keys_alt = scratch.alloc_n<uint64_t>(m);
-  int32_t* vals_alt = scratch.alloc_n<int32_t>(m);
-  void* sort_tmp = scratch.alloc(radix_sort_scratch_bytes(m));
-  // Morton codes are nearly unique at their top 40 bits (C2: groups of <= 6
-  // points), so the LSD passes skip the low 24 bits and one fix-up pass
-  // orders the small groups; a long group (many coincident points) falls
-  // back to the full sort of freshly computed codes. Same order either way.
-  bool in_alt = false;
-  if (!radix_sort_pairs_prefix(keys, vals, keys_alt, vals_alt, m, key_and, key_or, sort_tmp, st,
-                               &in_alt, &out.sort_passes)) {
-    note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
-    in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, m, key_and, key_or, sort_tmp, st,
-                              &out.sort_passes);
+    if (clock) clock->mark(kStSort);
+    uint64_t* keys_alt = scratch.alloc_n<uint64_t>(m);
+    int32_t* vals_alt = scratch.alloc_n<int32_t>(m);
+    void* sort_tmp = scratch.alloc(radix_sort_scratch_bytes(m));
+    // Morton codes are nearly unique at their top 40 bits (C2: groups of <= 6
+    // points), so the LSD passes skip the low 24 bits and one fix-up pass
+    // orders the small groups; a long group (many coincident points) falls
+    // back to the full sort of freshly computed codes. Same order either way.
+    bool in_alt = false;
+    if (!radix_sort_pairs_prefix(keys, vals, keys_alt, vals_alt, m, key_and, key_or, sort_tmp, st,
+                                 &in_alt, &out.sort_passes)) {
+      note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
+      in_alt = radix_sort_pairs(keys, vals, keys_alt, vals_alt, m, key_and, key_or, sort_tmp, st,
+                                &out.sort_passes);
+    }
+    codes = in_alt ? keys_alt : keys;
+    order = in_alt ? vals_alt : vals;
   }
-  const uint64_t* codes = in_alt ? keys_alt : keys;
-  int32_t* order = in_alt ? vals_alt : vals;
   out.tree.leaf_order = order;
 
   if (clock) clock->mark(kStTopo);
@@ -591,16 +609,16 @@ template void launch_point_bounds<3>(const float*, int64_t, DevCounters*, cudaSt
 
 template <int D>
 BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
-                   Scratch& scratch, StageClock* clock) {
+                   Scratch& scratch, StageClock* clock, bool stream_ordered) {
   if (src.coords) {
     PointBoxes<D> b{src.coords};
-    return build_impl<D>(b, src, validate_finite, true, d_ctr, scratch, clock);
+    return build_impl<D>(b, src, validate_finite, true, d_ctr, scratch, clock, stream_ordered);
   }
   ExplicitBoxes<D> b{src.lo, src.hi};
-  return build_impl<D>(b, src, validate_finite, false, d_ctr, scratch, clock);
+  return build_impl<D>(b, src, validate_finite, false, d_ctr, scratch, clock, stream_ordered);
 }
 
-template BuiltBvh build_bvh<2>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*);
-template BuiltBvh build_bvh<3>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*);
+template BuiltBvh build_bvh<2>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*, bool);
+template BuiltBvh build_bvh<3>(const PrimSource&, bool, DevCounters*, Scratch&, StageClock*, bool);
 
 }  // namespace tcb

@@ -515,6 +515,18 @@ TC_EXPORT tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim
   });
 }
 
+TC_EXPORT tc_status tcg_cluster_device_async(const float* d_coords, int64_t n, int dim, float eps,
+                                             int minpts, tc_algorithm algorithm,
+                                             int64_t oracle_cap, int32_t* d_labels,
+                                             uint8_t* d_core, void* stream, int32_t* d_status) {
+  return guarded([&]() -> tc_status {
+    tcb::run_device(d_coords, n, dim, eps, minpts, algorithm, oracle_cap, d_labels, d_core,
+                    static_cast<cudaStream_t>(stream), false, nullptr, nullptr, nullptr, nullptr,
+                    d_status);
+    return TC_OK;
+  });
+}
+
 TC_EXPORT tc_status tcg_cluster_keyed_device(const float* d_coords, const int32_t* d_keys,
                                              int64_t n, int dim, float eps, int minpts,
                                              int32_t* d_labels, uint8_t* d_core, void* stream,

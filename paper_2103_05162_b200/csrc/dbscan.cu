@@ -127,6 +127,7 @@ template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
+  if (ctr->nonfinite) return;  // stream-ordered run over bad input: no work
   int2 stack_buf[kStackDepth];
   CoreQuery<D, kFast> q{nodes, leaf_pt, bt, minpts, flags, LocalStack(stack_buf)};
   // one query per thread, started at the warp's common start node
@@ -162,6 +163,7 @@ k_fd_main(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, 
           BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
           const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
           int32_t* __restrict__ reach, DevCounters* ctr) {
+  if (ctr->nonfinite) return;  // stream-ordered run over bad input: no work
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kQueryBlock, kFofMinBlocks)
 k_fd_main_fof(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
               BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
               int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {
+  if (ctr->nonfinite) return;  // stream-ordered run over bad input: no work
   const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool valid = r < m;
   unsigned long long pairs = 0;
@@ -331,6 +334,7 @@ __global__ void __launch_bounds__(kQueryBlock, kFofMinBlocks)
 k_fd_main_fof_q(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
                 BallTest bt, int32_t* __restrict__ parent, const int32_t* __restrict__ key,
                 int32_t* __restrict__ reach, uint8_t* __restrict__ mark, DevCounters* ctr) {
+  if (ctr->nonfinite) return;  // stream-ordered run over bad input: no work
   __shared__ int3 s_act[kQueryBlock / 32][kActCap];
   __shared__ int32_t s_hint[kQueryBlock];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -490,6 +494,7 @@ k_fd_main_q(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt
             BallTest bt, const uint8_t* __restrict__ flags, int32_t* __restrict__ parent,
             const int32_t* __restrict__ key, const int32_t* __restrict__ noncore_before,
             int32_t* __restrict__ reach, DevCounters* ctr) {
+  if (ctr->nonfinite) return;  // stream-ordered run over bad input: no work
   __shared__ int4 s_act[kQueryBlock / 32][kActCap];
   __shared__ int32_t s_hint[kQueryBlock];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

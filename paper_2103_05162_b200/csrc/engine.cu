@@ -165,7 +165,10 @@ void run_fdbscan(const float* d_coords, int64_t n, float eps, int minpts, int32_
   src.coords = d_coords;
   src.count = n;
   clock.mark(kStBounds);
-  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock);
+  // stream-ordered: no host read-back; a non-finite coordinate is reported
+  // by run_device from ctr->nonfinite
+  BuiltBvh b = build_bvh<D>(src, /*validate_finite=*/true, ctr, scratch, &clock,
+                            /*stream_ordered=*/true);
 
   int32_t* parent = scratch.alloc_n<int32_t>(n);
   uint8_t* flags = scratch.alloc_n<uint8_t>(n);
@@ -195,6 +198,26 @@ template void run_fdbscan<2>(const float*, int64_t, float, int, int32_t*, uint8_
 template void run_fdbscan<3>(const float*, int64_t, float, int, int32_t*, uint8_t*, DevCounters*,
                              Scratch&, StageClock&, const int32_t*, const ChunkSink*);
 
+namespace {
+
+// A stream-ordered FDBSCAN run over a non-finite coordinate did no traversal
+// work: its outputs become all noise and the device status says why.
+__global__ void k_nonfinite_outputs(const DevCounters* __restrict__ ctr, int64_t n,
+                                    int32_t* __restrict__ labels, uint8_t* __restrict__ core,
+                                    int32_t* __restrict__ d_status) {
+  const bool bad = ctr->nonfinite != 0;
+  if (d_status && blockIdx.x == 0 && threadIdx.x == 0)
+    *d_status = bad ? TC_ERR_INVALID_ARGUMENT : TC_OK;
+  if (!bad) return;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    labels[i] = -1;
+    core[i] = 0;
+  }
+}
+
+}  // namespace
+
 // ---------------------------------------------------------------------------
 // Entry
 // ---------------------------------------------------------------------------
@@ -202,7 +225,7 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
                 tc_algorithm algo, int64_t oracle_cap, int32_t* d_labels, uint8_t* d_core,
                 cudaStream_t stream, bool want_stats, RunOutput* out,
                 const std::function<void(cudaStream_t)>& tail, const int32_t* d_keys,
-                const ChunkSink* sink) {
+                const ChunkSink* sink, int32_t* d_status) {
   if (dim != 2 && dim != 3) throw InvalidArgument{"PointSet: dimension must be 2 or 3"};
   if (n < 1) throw InvalidArgument{"PointSet: empty"};
   if (!(eps > 0.f) || !std::isfinite(eps))
@@ -228,6 +251,10 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
       else
         run_fdbscan<3>(d_coords, n, eps, minpts, d_labels, d_core, ctr, scratch, clock, d_keys,
                        sink);
+      note_launch(), k_nonfinite_outputs<<<grid_for(n, 256, 148 * 4), 256, 0, stream>>>(
+          ctr, n, d_labels, d_core, d_status);
+      TCB_CUDA(cudaGetLastError());
+      d_status = nullptr;  // written
       break;
     case TC_ALGO_DENSEBOX:
       if (dim == 2)
@@ -252,11 +279,13 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
       throw InvalidArgument{"unknown algorithm"};
   }
 
+  if (d_status) TCB_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int32_t), stream));  // TC_OK
   if (tail) tail(stream);
   if (want_stats || out) {
     DevCounters h;
     TCB_CUDA(cudaMemcpyAsync(&h, ctr, sizeof h, cudaMemcpyDeviceToHost, stream));
     TCB_CUDA(cudaStreamSynchronize(stream));
+    if (h.nonfinite) throw InvalidArgument{"PointSet: non-finite coordinate"};
     RunOutput ro;
     clock.collect(ro.stage_ms);
     set_last_stage_ms(ro.stage_ms);

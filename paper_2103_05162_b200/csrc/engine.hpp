@@ -43,6 +43,10 @@ using ChunkSink = std::function<void(int64_t i0, int64_t i1, cudaStream_t)>;
 
 // Full device pipeline. d_coords/d_labels/d_core are device pointers.
 // want_stats: synchronize at the end and fill `out`.
+// FDBSCAN never synchronizes the host before that end (the build's sort is
+// planned on the device); a non-finite coordinate turns the outputs into
+// all noise, sets *d_status (device int, optional) to TC_ERR_INVALID_ARGUMENT
+// and, with want_stats / out, throws InvalidArgument after the final sync.
 // `tail` (optional) is invoked after the last kernel is enqueued and before
 // the final synchronization, e.g. to enqueue the device->host result copies.
 void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts,
@@ -50,7 +54,8 @@ void run_device(const float* d_coords, int64_t n, int dim, float eps, int minpts
                 uint8_t* d_core, cudaStream_t stream, bool want_stats,
                 RunOutput* out,
                 const std::function<void(cudaStream_t)>& tail = nullptr,
-                const int32_t* d_keys = nullptr, const ChunkSink* sink = nullptr);
+                const int32_t* d_keys = nullptr, const ChunkSink* sink = nullptr,
+                int32_t* d_status = nullptr);
 
 // Stream-ordered allocation from the library's private per-device pool (the
 // process's default pool is left alone); release with cudaFreeAsync.

@@ -99,9 +99,13 @@ struct BuiltBvh {
 // Builds the LBVH of bvh.cpp:10-124 (scene bounds over centroids, Morton,
 // stable (code, index) sort, Karras topology, refit). Checks the points for
 // non-finite coordinates when validate_finite (throws InvalidArgument).
+// stream_ordered: no host synchronization (the sort passes are planned on the
+// device, see radix_sort_pairs_prefix_async); a non-finite coordinate only
+// sets d_ctr->nonfinite, which the traversal kernels honour by doing nothing
+// and the caller must check or report.
 template <int D>
 BuiltBvh build_bvh(const PrimSource& src, bool validate_finite, DevCounters* d_ctr,
-                   Scratch& scratch, StageClock* clock);
+                   Scratch& scratch, StageClock* clock, bool stream_ordered = false);
 
 // Raw point bounds into d_ctr->bounds_ord + finiteness flag (resets both).
 template <int D>

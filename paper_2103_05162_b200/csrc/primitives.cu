@@ -94,11 +94,28 @@ struct PassShifts {
   int count;
 };
 
+}  // namespace
+
+// Device-side pass plan of the stream-ordered sort (radix_sort_pairs_prefix_async).
+struct SortPlan {
+  int32_t count;               // active passes (slots 0..count-1)
+  int32_t shift[kMaxPasses];
+  int32_t fix;                 // prefix plan: the low bits vary, the fix-up orders groups
+  int32_t src_alt;             // where the last active pass left the pairs
+  int32_t pad[5];
+};
+
+namespace {
+
 // Histogram of the first sorted digit window only; every onesweep pass builds
 // the histogram of the NEXT window from the keys it already holds.
 __global__ void __launch_bounds__(kSortThreads)
 k_sort_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
-            uint32_t* __restrict__ ghist) {
+            uint32_t* __restrict__ ghist, const SortPlan* __restrict__ plan) {
+  if (plan) {  // stream-ordered sort: the first window comes from the device plan
+    if (plan->count == 0) return;
+    shift = plan->shift[0];
+  }
   __shared__ uint32_t h[kRadix];
   for (int i = threadIdx.x; i < kRadix; i += kSortThreads) h[i] = 0;
   __syncthreads();
@@ -130,20 +147,36 @@ __device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// kLoop: a block keeps taking tiles until none is left (the guarded
+// fallback passes run on a one-block-per-SM grid); otherwise one tile each.
+template <bool kLoop>
 __global__ void __launch_bounds__(kSortThreads, TCB_SORT_MINB)
 k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
                 uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, int64_t n,
                 int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
                 uint32_t* __restrict__ tile_counter, int next_shift,
-                uint32_t* __restrict__ ghist_next) {
+                uint32_t* __restrict__ ghist_next, const SortPlan* __restrict__ plan,
+                int slot) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
+  if (plan) {  // stream-ordered sort: inactive slots do nothing
+    const int cnt = plan->count;
+    if (slot >= cnt) return;
+    shift = plan->shift[slot];
+    next_shift = slot + 1 < cnt ? plan->shift[slot + 1] : -1;
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int num_tiles = static_cast<int>((n + kTile - 1) / kTile);
+  // Tiles are taken in counter order, so a block only ever looks back at
+  // tiles already owned by running blocks: a grid smaller than the tile count
+  // (the guarded fallback passes) loops safely.
+  do {
   if (threadIdx.x == 0) S.tile = static_cast<int>(atomicAdd(tile_counter, 1u));
   for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
   S.next_hist[threadIdx.x] = 0;  // kSortThreads == kRadix
   __syncthreads();
   const int tile = S.tile;
+  if (kLoop && tile >= num_tiles) return;
 
   const int64_t tile_base = static_cast<int64_t>(tile) * kTile;
   const int64_t base = tile_base + w * (kIPT * 32);
@@ -250,6 +283,8 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
     keys_out[out] = key;
     vals_out[out] = S.vals[p];
   }
+  if (kLoop) __syncthreads();  // S is reused by the next tile
+  } while (kLoop);
 }
 
 // ---------------------------------------------------------------------------
@@ -335,8 +370,9 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
     uint32_t* ghist = counters + 64;
     TCB_CUDA(cudaMemsetAsync(counters, 0, (64 + kMaxPasses * kRadix) * sizeof(uint32_t), stream));
     note_launch(), k_sort_hist<<<grid_for(n, kSortThreads, 148 * 4), kSortThreads, 0, stream>>>(
-        keys, n, ps.shift[0], ghist);
-    TCB_CUDA(cudaFuncSetAttribute(k_sort_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        keys, n, ps.shift[0], ghist, nullptr);
+    TCB_CUDA(cudaFuncSetAttribute(k_sort_onesweep<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(OnesweepSmem))));
     for (int p = 0; p < ps.count; ++p) {
       const uint64_t* kin = in_alt ? keys_alt : keys;
@@ -344,10 +380,10 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
       uint64_t* kout = in_alt ? keys : keys_alt;
       int32_t* vout = in_alt ? vals : vals_alt;
       TCB_CUDA(cudaMemsetAsync(status, 0, num_tiles * kRadix * sizeof(uint32_t), stream));
-      note_launch(), k_sort_onesweep<<<static_cast<unsigned>(num_tiles), kSortThreads,
+      note_launch(), k_sort_onesweep<false><<<static_cast<unsigned>(num_tiles), kSortThreads,
                                        sizeof(OnesweepSmem), stream>>>(
           kin, vin, kout, vout, n, ps.shift[p], ghist + p * kRadix, status, counters + p,
-          p + 1 < ps.count ? ps.shift[p + 1] : -1, ghist + (p + 1) * kRadix);
+          p + 1 < ps.count ? ps.shift[p + 1] : -1, ghist + (p + 1) * kRadix, nullptr, 0);
       TCB_CUDA(cudaGetLastError());
       in_alt = !in_alt;
     }
@@ -419,6 +455,165 @@ bool radix_sort_pairs_prefix(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
   *in_alt = alt;
   if (passes_run) *passes_run = passes;
   return true;
+}
+
+namespace {
+
+// Plan of a stream-ordered sort from the device-side AND / OR of the keys:
+// the varying 8-bit windows at and above lo_bit. gate (optional): no passes
+// unless *gate != 0 (the fallback sort runs only after a failed fix-up).
+__global__ void k_sort_plan(const unsigned long long* __restrict__ and_or, int lo_bit,
+                            const uint32_t* __restrict__ gate, int64_t n, SortPlan* plan) {
+  if (threadIdx.x != 0) return;
+  const uint64_t varying = and_or[0] ^ and_or[1];
+  int c = 0;
+  if (n > 1 && (gate == nullptr || *gate != 0))
+    for (int shift = lo_bit; shift < 64; shift += kRadixBits)
+      if ((varying >> shift) & (kRadix - 1)) plan->shift[c++] = shift;
+  plan->count = c;
+  plan->src_alt = c & 1;
+  plan->fix = n > 1 && lo_bit > 0 && ((varying & ((uint64_t{1} << lo_bit) - 1)) != 0);
+}
+
+// Zeroes a slot's look-back status words when the slot is active.
+__global__ void k_zero_status(const SortPlan* __restrict__ plan, int slot,
+                              uint32_t* __restrict__ status, int64_t words) {
+  if (slot >= plan->count) return;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < words;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    status[i] = 0;
+}
+
+// Fix-up of the stream-ordered prefix sort: reads the pairs where the plan's
+// passes left them and writes the final order to (kout, vout); without a
+// varying low window it is a copy.
+__global__ void __launch_bounds__(256)
+k_sort_fixup_planned(const SortPlan* __restrict__ plan, const uint64_t* __restrict__ k0,
+                     const int32_t* __restrict__ v0, const uint64_t* __restrict__ k1,
+                     const int32_t* __restrict__ v1, uint64_t* __restrict__ kout,
+                     int32_t* __restrict__ vout, int64_t n, int cut,
+                     uint32_t* __restrict__ too_long) {
+  const bool alt = plan->src_alt != 0;
+  const uint64_t* kin = alt ? k1 : k0;
+  const int32_t* vin = alt ? v1 : v0;
+  const bool fix = plan->fix != 0;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = kin[k];
+    const int32_t v = vin[k];
+    if (!fix) {
+      kout[k] = key;
+      vout[k] = v;
+      continue;
+    }
+    const uint64_t top = key >> cut;
+    int64_t b = k, e = k + 1;
+    while (b > 0 && k - b < kFixMax && (kin[b - 1] >> cut) == top) --b;
+    while (e < n && e - k < kFixMax && (kin[e] >> cut) == top) ++e;
+    if (e - b > kFixMax) {
+      *too_long = 1;
+      continue;
+    }
+    int64_t r = b;
+    for (int64_t j = b; j < e; ++j) {
+      const uint64_t kj = kin[j];
+      r += kj < key || (kj == key && vin[j] < v);
+    }
+    kout[r] = key;
+    vout[r] = v;
+  }
+}
+
+// Fallback of the stream-ordered prefix sort (a fix-up group was too long):
+// mode 0 moves the prefix-sorted pairs into (k0, v0) when the passes left
+// them in (k1, v1); mode 1 copies the fallback sort's result into the output.
+// Both do nothing unless the fallback plan has passes.
+__global__ void k_sort_fallback_copy(const SortPlan* __restrict__ first,
+                                     const SortPlan* __restrict__ fb, int mode,
+                                     uint64_t* __restrict__ k0, int32_t* __restrict__ v0,
+                                     uint64_t* __restrict__ k1, int32_t* __restrict__ v1,
+                                     uint64_t* __restrict__ kout, int32_t* __restrict__ vout,
+                                     int64_t n) {
+  if (fb->count == 0) return;
+  const uint64_t* ks;
+  const int32_t* vs;
+  uint64_t* kd;
+  int32_t* vd;
+  if (mode == 0) {
+    if (!first->src_alt) return;
+    ks = k1, vs = v1, kd = k0, vd = v0;
+  } else {
+    ks = fb->src_alt ? k1 : k0, vs = fb->src_alt ? v1 : v0, kd = kout, vd = vout;
+  }
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    kd[i] = ks[i];
+    vd[i] = vs[i];
+  }
+}
+
+// The planned LSD passes: slot p reads (keys, vals) when p is even.
+void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* vals_alt,
+                    int64_t n, const SortPlan* plan, int slots, unsigned grid, uint32_t* status,
+                    uint32_t* counters, uint32_t* ghist, cudaStream_t stream) {
+  const int64_t num_tiles = num_sort_tiles(n);
+  const bool loop = grid < num_tiles;
+  TCB_CUDA(cudaMemsetAsync(counters, 0, (64 + kMaxPasses * kRadix) * sizeof(uint32_t), stream));
+  note_launch(), k_sort_hist<<<std::min<unsigned>(grid, 148 * 4), kSortThreads, 0, stream>>>(
+      keys, n, 0, ghist, plan);
+  auto kern = loop ? k_sort_onesweep<true> : k_sort_onesweep<false>;
+  TCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(OnesweepSmem))));
+  for (int p = 0; p < slots; ++p) {
+    const bool in_alt = p & 1;
+    note_launch(), k_zero_status<<<std::min<unsigned>(grid, 148 * 4), 256, 0, stream>>>(
+        plan, p, status, num_tiles * kRadix);
+    note_launch(), kern<<<grid, kSortThreads, sizeof(OnesweepSmem), stream>>>(
+        in_alt ? keys_alt : keys, in_alt ? vals_alt : vals, in_alt ? keys : keys_alt,
+        in_alt ? vals : vals_alt, n, 0, ghist + p * kRadix, status, counters + p, -1,
+        ghist + (p + 1) * kRadix, plan, p);
+    TCB_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace
+
+size_t radix_sort_async_scratch_bytes(int64_t n) {
+  return radix_sort_scratch_bytes(n) + 2 * sizeof(SortPlan) + 256;
+}
+
+void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
+                                   int32_t* vals_alt, uint64_t* keys_out, int32_t* vals_out,
+                                   int64_t n, const unsigned long long* d_and_or, void* scratch,
+                                   cudaStream_t stream) {
+  const int64_t num_tiles = num_sort_tiles(std::max<int64_t>(n, 1));
+  uint32_t* status = static_cast<uint32_t*>(scratch);
+  uint32_t* counters = status + num_tiles * kRadix;
+  uint32_t* ghist = counters + 64;
+  char* tail = static_cast<char*>(scratch) + radix_sort_scratch_bytes(n);
+  uint32_t* too_long = reinterpret_cast<uint32_t*>(tail - 64);
+  SortPlan* plan = reinterpret_cast<SortPlan*>(tail);
+  SortPlan* fb = plan + 1;
+  TCB_CUDA(cudaMemsetAsync(too_long, 0, sizeof(uint32_t), stream));
+  note_launch(), k_sort_plan<<<1, 32, 0, stream>>>(d_and_or, kFixBits, nullptr, n, plan);
+  // the windows above kFixBits: at most (64 - kFixBits) / 8 passes
+  constexpr int kPrefixSlots = (64 - kFixBits + kRadixBits - 1) / kRadixBits;
+  planned_passes(keys, vals, keys_alt, vals_alt, n, plan, kPrefixSlots,
+                 static_cast<unsigned>(num_tiles), status, counters, ghist, stream);
+  note_launch(), k_sort_fixup_planned<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(
+      plan, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, kFixBits, too_long);
+  // Fallback, all guarded on the device (no work unless a group was too
+  // long): the full sort of the prefix-sorted pairs (stable, so ties keep
+  // their index order) into (keys_out, vals_out).
+  note_launch(), k_sort_plan<<<1, 32, 0, stream>>>(d_and_or, 0, too_long, n, fb);
+  const unsigned small = static_cast<unsigned>(std::min<int64_t>(num_tiles, 148));
+  note_launch(), k_sort_fallback_copy<<<small, 256, 0, stream>>>(
+      plan, fb, 0, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n);
+  planned_passes(keys, vals, keys_alt, vals_alt, n, fb, kMaxPasses, small, status, counters, ghist,
+                 stream);
+  note_launch(), k_sort_fallback_copy<<<small, 256, 0, stream>>>(
+      plan, fb, 1, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n);
+  TCB_CUDA(cudaGetLastError());
 }
 
 size_t scan_scratch_bytes(int64_t n) {

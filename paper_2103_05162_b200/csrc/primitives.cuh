@@ -39,6 +39,19 @@ bool radix_sort_pairs_prefix(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
                              void* scratch, cudaStream_t stream, bool* in_alt,
                              int* passes_run = nullptr);
 
+// Stream-ordered radix_sort_pairs_prefix: no host synchronization, so it can
+// be captured in a CUDA graph. The digit windows come from the device-side
+// AND / OR of the keys (d_and_or[0], d_and_or[1]), every pass is launched and
+// the inactive ones return at once; the result always lands in (keys_out,
+// vals_out). A fix-up group longer than kFixMax triggers, on the device, a
+// full LSD sort of the prefix-sorted pairs (launched guarded, idle otherwise).
+// (keys, vals) and the *_alt buffers are clobbered.
+size_t radix_sort_async_scratch_bytes(int64_t n);
+void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
+                                   int32_t* vals_alt, uint64_t* keys_out, int32_t* vals_out,
+                                   int64_t n, const unsigned long long* d_and_or, void* scratch,
+                                   cudaStream_t stream);
+
 // Exclusive scan of n int32 counts into out (may alias in); writes the total
 // to *d_total (device pointer) when non-null.
 size_t scan_scratch_bytes(int64_t n);

@@ -648,3 +648,84 @@ def test_randomized_stress_against_oracle():
 
     runs, bad = stress.run(600.0, max_runs=300, seed=2024, verbose=False)
     assert runs == 300 and not bad, bad[:5]
+
+
+# ---------------- stream-ordered FDBSCAN: CUDA-graph capture ----------------
+@pytest.mark.parametrize("minpts,dup", [(2, 0), (5, 0), (2, 3000), (5, 3000)])
+def test_fdbscan_captured_in_cuda_graph(minpts, dup):
+    """tcg_cluster_device_async (FDBSCAN) never synchronizes the host, so one
+    call captures into a CUDA graph; replays on new coordinates (copied into
+    the captured input buffer) equal eager runs. dup > 256 coincident points
+    make the Morton prefix sort take its device-guarded fallback."""
+    import torch
+
+    rng = np.random.default_rng(minpts + dup)
+
+    def cloud(seed):
+        ds = Dataset.blobs(12, 4000, 3, 4.0, 0.4, seed)
+        c = ds.coords()
+        if dup:
+            c[:dup] = c[dup]  # one point repeated dup + 1 times
+        return torch.from_numpy(c).cuda()
+
+    x = cloud(1)
+    n = x.shape[0]
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    core = torch.empty(n, dtype=torch.uint8, device="cuda")
+    status = torch.full((1,), 77, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):  # warm-up (lazy pool / attribute setup) off the capture
+        tb.cluster_device_async(x, 0.15, minpts, Algorithm.FDBSCAN, labels, core, status, s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+        tb.cluster_device_async(x, 0.15, minpts, Algorithm.FDBSCAN, labels, core, status, s)
+    for seed in (2, 3, 4):
+        new = cloud(seed + int(rng.integers(1000)))
+        x.copy_(new)
+        status.fill_(77)
+        g.replay()
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        want_l, want_c, _ = tb.cluster_device(new, 0.15, minpts, Algorithm.FDBSCAN, stats=True)
+        torch.cuda.synchronize()
+        assert torch.equal(core, want_c)
+        cm = core == 1  # core labels are deterministic (min core index); borders valid
+        assert torch.equal(labels[cm], want_l[cm]), seed
+        assert torch.equal(labels == -1, want_l == -1), seed
+        ref_run = oracle.dbscan(new.cpu().numpy(), 0.15, minpts, 0) if n <= 50000 else None
+        if ref_run is not None:
+            assert_parity(labels.cpu().numpy(), core.cpu().numpy(), ref_run["labels"],
+                          ref_run["core"], f"graph {seed}")
+
+
+def test_async_status_reports_nonfinite_on_device():
+    import torch
+
+    c = np.random.default_rng(3).uniform(0, 10, (5000, 3)).astype(np.float32)
+    for bad in (0, 4321, 4999):
+        x = torch.from_numpy(c.copy()).cuda()
+        x[bad, 1] = float("nan") if bad % 2 == 0 else float("inf")
+        lab, core, st = tb.cluster_device_async(x, 0.5, 3)
+        torch.cuda.synchronize()
+        assert int(st.item()) == int(Status.INVALID_ARGUMENT)
+        assert (lab == -1).all() and (core == 0).all()
+        with pytest.raises(TreeclustError) as e:
+            tb.cluster_device(x, 0.5, 3, stats=True)
+        assert e.value.status == Status.INVALID_ARGUMENT
+    # all points non-finite: still no traversal work, status set
+    x = torch.full((100000, 3), float("nan"), device="cuda")
+    lab, core, st = tb.cluster_device_async(x, 0.5, 2)
+    torch.cuda.synchronize()
+    assert int(st.item()) == int(Status.INVALID_ARGUMENT) and (lab == -1).all()
+    # a clean run afterwards reports OK and matches the host API
+    x = torch.from_numpy(c).cuda()
+    lab, core, st = tb.cluster_device_async(x, 0.5, 3)
+    torch.cuda.synchronize()
+    assert int(st.item()) == int(Status.OK)
+    host = tb.cluster(Dataset.from_array(c), 0.5, 3)
+    assert_parity(lab.cpu().numpy(), core.cpu().numpy(), host.labels, host.core_flags)
+    for algo in (1, 2):  # the other algorithms write the status too
+        lab, core, st = tb.cluster_device_async(x, 0.5, 3, Algorithm(algo))
+        torch.cuda.synchronize()
+        assert int(st.item()) == int(Status.OK)
