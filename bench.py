@@ -576,10 +576,11 @@ def main():
             torch.cuda.synchronize()
             g0 = torch.cuda.Event(enable_timing=True)
             g1 = torch.cuda.Event(enable_timing=True)
-            g0.record(cs)
+            rs = torch.cuda.current_stream(dev)  # replay() launches on the current stream
+            g0.record(rs)
             for _ in range(args.steps):
                 g.replay()
-            g1.record(cs)
+            g1.record(rs)
             torch.cuda.synchronize()
             gms = g0.elapsed_time(g1) / args.steps
             cm = core == 1
