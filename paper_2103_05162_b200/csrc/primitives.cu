@@ -127,16 +127,21 @@ k_sort_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
     if (h[i]) atomicAdd(ghist + i, h[i]);
 }
 
-struct OnesweepSmem {
-  uint64_t keys[kTile];
-  int32_t vals[kTile];
+struct SortShared {
   uint32_t wcnt[kSortWarps][kRadix];
   uint32_t tile_start[kRadix];
   uint32_t global_start[kRadix];
   uint32_t warp_tot[32];
   uint32_t next_hist[kRadix];
-  int tile;
+  int tile[1];
 };
+
+struct OnesweepSmem {
+  uint64_t keys[kTile];
+  int32_t vals[kTile];
+  SortShared c;
+};
+
 
 __device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
   uint32_t v;
@@ -147,50 +152,21 @@ __device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// kLoop: a block keeps taking tiles until none is left (the guarded
-// fallback passes run on a one-block-per-SM grid); otherwise one tile each.
-template <bool kLoop>
-__global__ void __launch_bounds__(kSortThreads, TCB_SORT_MINB)
-k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
-                uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, int64_t n,
-                int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
-                uint32_t* __restrict__ tile_counter, int next_shift,
-                uint32_t* __restrict__ ghist_next, const SortPlan* __restrict__ plan,
-                int slot) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
-  if (plan) {  // stream-ordered sort: inactive slots do nothing
-    const int cnt = plan->count;
-    if (slot >= cnt) return;
-    shift = plan->shift[slot];
-    next_shift = slot + 1 < cnt ? plan->shift[slot + 1] : -1;
-  }
+// One onesweep tile whose keys / values are in registers: stable ranking,
+// digit counts published for the look-back, the next window's histogram,
+// scatter through the staging arrays (tile order by digit), contiguous
+// global writes. S.wcnt and S.next_hist must be zero on entry.
+__device__ __forceinline__ void onesweep_tile(SortShared& S, uint64_t* st_keys, int32_t* st_vals,
+                                              const uint64_t (&k)[kIPT], const int32_t (&v)[kIPT],
+                                              int tile, int64_t n, int shift, int next_shift,
+                                              const uint32_t* __restrict__ ghist,
+                                              uint32_t* __restrict__ status,
+                                              uint64_t* __restrict__ keys_out,
+                                              int32_t* __restrict__ vals_out,
+                                              uint32_t* __restrict__ ghist_next) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int num_tiles = static_cast<int>((n + kTile - 1) / kTile);
-  // Tiles are taken in counter order, so a block only ever looks back at
-  // tiles already owned by running blocks: a grid smaller than the tile count
-  // (the guarded fallback passes) loops safely.
-  do {
-  if (threadIdx.x == 0) S.tile = static_cast<int>(atomicAdd(tile_counter, 1u));
-  for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
-  S.next_hist[threadIdx.x] = 0;  // kSortThreads == kRadix
-  __syncthreads();
-  const int tile = S.tile;
-  if (kLoop && tile >= num_tiles) return;
-
   const int64_t tile_base = static_cast<int64_t>(tile) * kTile;
   const int64_t base = tile_base + w * (kIPT * 32);
-  uint64_t k[kIPT];
-  int32_t v[kIPT];
-#pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
-    const int64_t idx = base + j * 32 + lane;
-    if (idx < n) {
-      k[j] = __ldcs(keys_in + idx);
-      v[j] = __ldcs(vals_in + idx);
-    }
-  }
-
   if (next_shift >= 0) {
 #pragma unroll
     for (int j = 0; j < kIPT; ++j)
@@ -269,23 +245,70 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
     if (idx < n) {
       const uint32_t dd = static_cast<uint32_t>(k[j] >> shift) & (kRadix - 1);
       const uint32_t pos = S.tile_start[dd] + S.wcnt[w][dd] + rank[j];
-      S.keys[pos] = k[j];
-      S.vals[pos] = v[j];
+      st_keys[pos] = k[j];
+      st_vals[pos] = v[j];
     }
   }
   __syncthreads();
 
   const int tile_n = static_cast<int>(n - tile_base < kTile ? n - tile_base : kTile);
   for (int p = threadIdx.x; p < tile_n; p += kSortThreads) {
-    const uint64_t key = S.keys[p];
+    const uint64_t key = st_keys[p];
     const uint32_t dd = static_cast<uint32_t>(key >> shift) & (kRadix - 1);
     const uint32_t out = S.global_start[dd] + (p - S.tile_start[dd]);
     keys_out[out] = key;
-    vals_out[out] = S.vals[p];
+    vals_out[out] = st_vals[p];
   }
-  if (kLoop) __syncthreads();  // S is reused by the next tile
+}
+
+// kLoop: a block keeps taking tiles until none is left (the guarded
+// fallback passes run on a one-block-per-SM grid); otherwise one tile each.
+template <bool kLoop>
+__global__ void __launch_bounds__(kSortThreads, TCB_SORT_MINB)
+k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in,
+                uint64_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, int64_t n,
+                int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
+                uint32_t* __restrict__ tile_counter, int next_shift,
+                uint32_t* __restrict__ ghist_next, const SortPlan* __restrict__ plan,
+                int slot) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OnesweepSmem& B = *reinterpret_cast<OnesweepSmem*>(smem_raw);
+  SortShared& S = B.c;
+  if (plan) {  // stream-ordered sort: inactive slots do nothing
+    const int cnt = plan->count;
+    if (slot >= cnt) return;
+    shift = plan->shift[slot];
+    next_shift = slot + 1 < cnt ? plan->shift[slot + 1] : -1;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int num_tiles = static_cast<int>((n + kTile - 1) / kTile);
+  // Tiles are taken in counter order, so a block only ever looks back at
+  // tiles already owned by running blocks: a grid smaller than the tile count
+  // (the guarded fallback passes) loops safely.
+  do {
+    if (threadIdx.x == 0) S.tile[0] = static_cast<int>(atomicAdd(tile_counter, 1u));
+    for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
+    S.next_hist[threadIdx.x] = 0;  // kSortThreads == kRadix
+    __syncthreads();
+    const int tile = S.tile[0];
+    if (kLoop && tile >= num_tiles) return;
+    const int64_t base = static_cast<int64_t>(tile) * kTile + w * (kIPT * 32);
+    uint64_t k[kIPT];
+    int32_t v[kIPT];
+#pragma unroll
+    for (int j = 0; j < kIPT; ++j) {
+      const int64_t idx = base + j * 32 + lane;
+      if (idx < n) {
+        k[j] = __ldcs(keys_in + idx);
+        v[j] = __ldcs(vals_in + idx);
+      }
+    }
+    onesweep_tile(S, B.keys, B.vals, k, v, tile, n, shift, next_shift, ghist, status, keys_out,
+                  vals_out, ghist_next);
+    if (kLoop) __syncthreads();  // S is reused by the next tile
   } while (kLoop);
 }
+
 
 // ---------------------------------------------------------------------------
 // Exclusive scan (reduce-then-scan, 3 kernels)
@@ -562,13 +585,14 @@ void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* 
   note_launch(), k_sort_hist<<<std::min<unsigned>(grid, 148 * 4), kSortThreads, 0, stream>>>(
       keys, n, 0, ghist, plan);
   auto kern = loop ? k_sort_onesweep<true> : k_sort_onesweep<false>;
+  const size_t smem = sizeof(OnesweepSmem);
   TCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(sizeof(OnesweepSmem))));
+                                static_cast<int>(smem)));
   for (int p = 0; p < slots; ++p) {
     const bool in_alt = p & 1;
     note_launch(), k_zero_status<<<std::min<unsigned>(grid, 148 * 4), 256, 0, stream>>>(
         plan, p, status, num_tiles * kRadix);
-    note_launch(), kern<<<grid, kSortThreads, sizeof(OnesweepSmem), stream>>>(
+    note_launch(), kern<<<grid, kSortThreads, smem, stream>>>(
         in_alt ? keys_alt : keys, in_alt ? vals_alt : vals, in_alt ? keys : keys_alt,
         in_alt ? vals : vals_alt, n, 0, ghist + p * kRadix, status, counters + p, -1,
         ghist + (p + 1) * kRadix, plan, p);
