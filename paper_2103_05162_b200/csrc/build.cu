@@ -194,7 +194,7 @@ k_morton(Src src, int64_t m, DevCounters* ctr, uint64_t* __restrict__ keys,
       k2[0] = make_ulonglong2(code[0], code[1]);
       k2[1] = make_ulonglong2(code[2], code[3]);
       const int32_t i0 = static_cast<int32_t>(4 * q);
-      reinterpret_cast<int4*>(vals)[q] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
+      if (vals) reinterpret_cast<int4*>(vals)[q] = make_int4(i0, i0 + 1, i0 + 2, i0 + 3);
     }
     first = m / 4 * 4 + tid;
   }
@@ -204,7 +204,7 @@ k_morton(Src src, int64_t m, DevCounters* ctr, uint64_t* __restrict__ keys,
     centroid<D>(lo, hi, c);
     const uint64_t code = encode(c);
     keys[i] = code;
-    vals[i] = static_cast<int32_t>(i);
+    if (vals) vals[i] = static_cast<int32_t>(i);
   }
   publish_and_or(acc_and, acc_or, ctr);
 }
@@ -493,7 +493,9 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
   note_launch(), k_centroid_bounds<D><<<g, 256, 0, st>>>(boxes, m, validate_finite, d_ctr);
   uint64_t* keys = scratch.alloc_n<uint64_t>(m);
   int32_t* vals = scratch.alloc_n<int32_t>(m);
-  note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys, vals);
+  // the stream-ordered sort's first pass generates the identity values itself
+  note_launch(), k_morton<D><<<g, 256, 0, st>>>(boxes, m, d_ctr, keys,
+                                               stream_ordered ? nullptr : vals);
   TCB_CUDA(cudaGetLastError());
 
   const uint64_t* codes;
@@ -508,7 +510,7 @@ BuiltBvh build_impl(const Src& boxes, const PrimSource& src, bool validate_finit
     int32_t* vals_out = scratch.alloc_n<int32_t>(m);
     void* sort_tmp = scratch.alloc(radix_sort_async_scratch_bytes(m));
     radix_sort_pairs_prefix_async(keys, vals, keys_alt, vals_alt, keys_out, vals_out, m,
-                                  &d_ctr->key_and, sort_tmp, st);
+                                  &d_ctr->key_and, sort_tmp, st, /*iota_vals=*/true);
     codes = keys_out;
     order = vals_out;
     out.sort_passes = -1;  // decided on the device

@@ -300,7 +300,7 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
       const int64_t idx = base + j * 32 + lane;
       if (idx < n) {
         k[j] = __ldcs(keys_in + idx);
-        v[j] = __ldcs(vals_in + idx);
+        v[j] = vals_in ? __ldcs(vals_in + idx) : static_cast<int32_t>(idx);  // null: identity
       }
     }
     onesweep_tile(S, B.keys, B.vals, k, v, tile, n, shift, next_shift, ghist, status, keys_out,
@@ -515,15 +515,18 @@ k_sort_fixup_planned(const SortPlan* __restrict__ plan, const uint64_t* __restri
                      const int32_t* __restrict__ v0, const uint64_t* __restrict__ k1,
                      const int32_t* __restrict__ v1, uint64_t* __restrict__ kout,
                      int32_t* __restrict__ vout, int64_t n, int cut,
-                     uint32_t* __restrict__ too_long) {
+                     uint32_t* __restrict__ too_long, bool iota) {
   const bool alt = plan->src_alt != 0;
   const uint64_t* kin = alt ? k1 : k0;
   const int32_t* vin = alt ? v1 : v0;
   const bool fix = plan->fix != 0;
+  // iota: the values were never materialized; without a pass they are 0..n-1
+  const bool ident = iota && plan->count == 0;
+  auto val = [&](int64_t i) { return ident ? static_cast<int32_t>(i) : vin[i]; };
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t key = kin[k];
-    const int32_t v = vin[k];
+    const int32_t v = val(k);
     if (!fix) {
       kout[k] = key;
       vout[k] = v;
@@ -540,7 +543,7 @@ k_sort_fixup_planned(const SortPlan* __restrict__ plan, const uint64_t* __restri
     int64_t r = b;
     for (int64_t j = b; j < e; ++j) {
       const uint64_t kj = kin[j];
-      r += kj < key || (kj == key && vin[j] < v);
+      r += kj < key || (kj == key && val(j) < v);
     }
     kout[r] = key;
     vout[r] = v;
@@ -556,14 +559,20 @@ __global__ void k_sort_fallback_copy(const SortPlan* __restrict__ first,
                                      uint64_t* __restrict__ k0, int32_t* __restrict__ v0,
                                      uint64_t* __restrict__ k1, int32_t* __restrict__ v1,
                                      uint64_t* __restrict__ kout, int32_t* __restrict__ vout,
-                                     int64_t n) {
+                                     int64_t n, bool iota) {
   if (fb->count == 0) return;
   const uint64_t* ks;
   const int32_t* vs;
   uint64_t* kd;
   int32_t* vd;
   if (mode == 0) {
-    if (!first->src_alt) return;
+    if (!first->src_alt) {
+      if (iota && first->count == 0)  // no pass ran: materialize the identity values
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+          v0[i] = static_cast<int32_t>(i);
+      return;
+    }
     ks = k1, vs = v1, kd = k0, vd = v0;
   } else {
     ks = fb->src_alt ? k1 : k0, vs = fb->src_alt ? v1 : v0, kd = kout, vd = vout;
@@ -578,7 +587,7 @@ __global__ void k_sort_fallback_copy(const SortPlan* __restrict__ first,
 // The planned LSD passes: slot p reads (keys, vals) when p is even.
 void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* vals_alt,
                     int64_t n, const SortPlan* plan, int slots, unsigned grid, uint32_t* status,
-                    uint32_t* counters, uint32_t* ghist, cudaStream_t stream) {
+                    uint32_t* counters, uint32_t* ghist, cudaStream_t stream, bool iota_vals) {
   const int64_t num_tiles = num_sort_tiles(n);
   const bool loop = grid < num_tiles;
   TCB_CUDA(cudaMemsetAsync(counters, 0, (64 + kMaxPasses * kRadix) * sizeof(uint32_t), stream));
@@ -593,7 +602,8 @@ void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* 
     note_launch(), k_zero_status<<<std::min<unsigned>(grid, 148 * 4), 256, 0, stream>>>(
         plan, p, status, num_tiles * kRadix);
     note_launch(), kern<<<grid, kSortThreads, smem, stream>>>(
-        in_alt ? keys_alt : keys, in_alt ? vals_alt : vals, in_alt ? keys : keys_alt,
+        in_alt ? keys_alt : keys, in_alt ? vals_alt : (p == 0 && iota_vals ? nullptr : vals),
+        in_alt ? keys : keys_alt,
         in_alt ? vals : vals_alt, n, 0, ghist + p * kRadix, status, counters + p, -1,
         ghist + (p + 1) * kRadix, plan, p);
     TCB_CUDA(cudaGetLastError());
@@ -609,7 +619,7 @@ size_t radix_sort_async_scratch_bytes(int64_t n) {
 void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
                                    int32_t* vals_alt, uint64_t* keys_out, int32_t* vals_out,
                                    int64_t n, const unsigned long long* d_and_or, void* scratch,
-                                   cudaStream_t stream) {
+                                   cudaStream_t stream, bool iota_vals) {
   const int64_t num_tiles = num_sort_tiles(std::max<int64_t>(n, 1));
   uint32_t* status = static_cast<uint32_t*>(scratch);
   uint32_t* counters = status + num_tiles * kRadix;
@@ -623,20 +633,21 @@ void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys
   // the windows above kFixBits: at most (64 - kFixBits) / 8 passes
   constexpr int kPrefixSlots = (64 - kFixBits + kRadixBits - 1) / kRadixBits;
   planned_passes(keys, vals, keys_alt, vals_alt, n, plan, kPrefixSlots,
-                 static_cast<unsigned>(num_tiles), status, counters, ghist, stream);
+                 static_cast<unsigned>(num_tiles), status, counters, ghist, stream, iota_vals);
   note_launch(), k_sort_fixup_planned<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(
-      plan, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, kFixBits, too_long);
+      plan, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, kFixBits, too_long,
+      iota_vals);
   // Fallback, all guarded on the device (no work unless a group was too
   // long): the full sort of the prefix-sorted pairs (stable, so ties keep
   // their index order) into (keys_out, vals_out).
   note_launch(), k_sort_plan<<<1, 32, 0, stream>>>(d_and_or, 0, too_long, n, fb);
   const unsigned small = static_cast<unsigned>(std::min<int64_t>(num_tiles, 148));
   note_launch(), k_sort_fallback_copy<<<small, 256, 0, stream>>>(
-      plan, fb, 0, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n);
+      plan, fb, 0, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, iota_vals);
   planned_passes(keys, vals, keys_alt, vals_alt, n, fb, kMaxPasses, small, status, counters, ghist,
-                 stream);
+                 stream, false);
   note_launch(), k_sort_fallback_copy<<<small, 256, 0, stream>>>(
-      plan, fb, 1, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n);
+      plan, fb, 1, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, false);
   TCB_CUDA(cudaGetLastError());
 }
 

@@ -45,12 +45,13 @@ bool radix_sort_pairs_prefix(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
 // the inactive ones return at once; the result always lands in (keys_out,
 // vals_out). A fix-up group longer than kFixMax triggers, on the device, a
 // full LSD sort of the prefix-sorted pairs (launched guarded, idle otherwise).
-// (keys, vals) and the *_alt buffers are clobbered.
+// (keys, vals) and the *_alt buffers are clobbered. iota_vals: vals holds
+// nothing yet and stands for 0..n-1 (the first pass generates them).
 size_t radix_sort_async_scratch_bytes(int64_t n);
 void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
                                    int32_t* vals_alt, uint64_t* keys_out, int32_t* vals_out,
                                    int64_t n, const unsigned long long* d_and_or, void* scratch,
-                                   cudaStream_t stream);
+                                   cudaStream_t stream, bool iota_vals = false);
 
 // Exclusive scan of n int32 counts into out (may alias in); writes the total
 // to *d_total (device pointer) when non-null.

@@ -651,8 +651,9 @@ def test_randomized_stress_against_oracle():
 
 
 # ---------------- stream-ordered FDBSCAN: CUDA-graph capture ----------------
-@pytest.mark.parametrize("minpts,dup", [(2, 0), (5, 0), (2, 3000), (5, 3000)])
-def test_fdbscan_captured_in_cuda_graph(minpts, dup):
+@pytest.mark.parametrize("minpts,dup,dim", [(2, 0, 3), (5, 0, 3), (2, 3000, 3), (5, 3000, 3),
+                                            (2, 0, 2), (5, 3000, 2)])
+def test_fdbscan_captured_in_cuda_graph(minpts, dup, dim):
     """tcg_cluster_device_async (FDBSCAN) never synchronizes the host, so one
     call captures into a CUDA graph; replays on new coordinates (copied into
     the captured input buffer) equal eager runs. dup > 256 coincident points
@@ -662,7 +663,7 @@ def test_fdbscan_captured_in_cuda_graph(minpts, dup):
     rng = np.random.default_rng(minpts + dup)
 
     def cloud(seed):
-        ds = Dataset.blobs(12, 4000, 3, 4.0, 0.4, seed)
+        ds = Dataset.blobs(12, 4000, dim, 4.0, 0.4, seed)
         c = ds.coords()
         if dup:
             c[:dup] = c[dup]  # one point repeated dup + 1 times
