@@ -270,7 +270,7 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
                 int shift, const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
                 uint32_t* __restrict__ tile_counter, int next_shift,
                 uint32_t* __restrict__ ghist_next, const SortPlan* __restrict__ plan,
-                int slot) {
+                int slot, uint32_t* __restrict__ status_next) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem& B = *reinterpret_cast<OnesweepSmem*>(smem_raw);
   SortShared& S = B.c;
@@ -292,6 +292,9 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
     __syncthreads();
     const int tile = S.tile[0];
     if (kLoop && tile >= num_tiles) return;
+    // planned passes alternate two status arrays: each tile clears its row of
+    // the next pass's (idle during this pass) instead of a memset launch
+    if (status_next) status_next[static_cast<int64_t>(tile) * kRadix + threadIdx.x] = 0;
     const int64_t base = static_cast<int64_t>(tile) * kTile + w * (kIPT * 32);
     uint64_t k[kIPT];
     int32_t v[kIPT];
@@ -406,7 +409,8 @@ bool radix_sort_pairs(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
       note_launch(), k_sort_onesweep<false><<<static_cast<unsigned>(num_tiles), kSortThreads,
                                        sizeof(OnesweepSmem), stream>>>(
           kin, vin, kout, vout, n, ps.shift[p], ghist + p * kRadix, status, counters + p,
-          p + 1 < ps.count ? ps.shift[p + 1] : -1, ghist + (p + 1) * kRadix, nullptr, 0);
+          p + 1 < ps.count ? ps.shift[p + 1] : -1, ghist + (p + 1) * kRadix, nullptr, 0,
+          nullptr);
       TCB_CUDA(cudaGetLastError());
       in_alt = !in_alt;
     }
@@ -584,10 +588,12 @@ __global__ void k_sort_fallback_copy(const SortPlan* __restrict__ first,
   }
 }
 
-// The planned LSD passes: slot p reads (keys, vals) when p is even.
+// The planned LSD passes: slot p reads (keys, vals) when p is even and uses
+// status[p & 1]; the active slots are a prefix, each clearing the other array.
 void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* vals_alt,
-                    int64_t n, const SortPlan* plan, int slots, unsigned grid, uint32_t* status,
-                    uint32_t* counters, uint32_t* ghist, cudaStream_t stream, bool iota_vals) {
+                    int64_t n, const SortPlan* plan, int slots, unsigned grid,
+                    uint32_t* const (&status)[2], uint32_t* counters, uint32_t* ghist,
+                    cudaStream_t stream, bool iota_vals) {
   const int64_t num_tiles = num_sort_tiles(n);
   const bool loop = grid < num_tiles;
   TCB_CUDA(cudaMemsetAsync(counters, 0, (64 + kMaxPasses * kRadix) * sizeof(uint32_t), stream));
@@ -597,15 +603,15 @@ void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* 
   const size_t smem = sizeof(OnesweepSmem);
   TCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
+  note_launch(), k_zero_status<<<std::min<unsigned>(grid, 148 * 4), 256, 0, stream>>>(
+      plan, 0, status[0], num_tiles * kRadix);
   for (int p = 0; p < slots; ++p) {
     const bool in_alt = p & 1;
-    note_launch(), k_zero_status<<<std::min<unsigned>(grid, 148 * 4), 256, 0, stream>>>(
-        plan, p, status, num_tiles * kRadix);
     note_launch(), kern<<<grid, kSortThreads, smem, stream>>>(
         in_alt ? keys_alt : keys, in_alt ? vals_alt : (p == 0 && iota_vals ? nullptr : vals),
         in_alt ? keys : keys_alt,
-        in_alt ? vals : vals_alt, n, 0, ghist + p * kRadix, status, counters + p, -1,
-        ghist + (p + 1) * kRadix, plan, p);
+        in_alt ? vals : vals_alt, n, 0, ghist + p * kRadix, status[p & 1], counters + p, -1,
+        ghist + (p + 1) * kRadix, plan, p, status[(p + 1) & 1]);
     TCB_CUDA(cudaGetLastError());
   }
 }
@@ -613,7 +619,9 @@ void planned_passes(uint64_t* keys, int32_t* vals, uint64_t* keys_alt, int32_t* 
 }  // namespace
 
 size_t radix_sort_async_scratch_bytes(int64_t n) {
-  return radix_sort_scratch_bytes(n) + 2 * sizeof(SortPlan) + 256;
+  // + the two plans, + the second look-back status array
+  return radix_sort_scratch_bytes(n) + 256 +
+         static_cast<size_t>(num_sort_tiles(std::max<int64_t>(n, 1))) * kRadix * sizeof(uint32_t);
 }
 
 void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys_alt,
@@ -628,12 +636,14 @@ void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys
   uint32_t* too_long = reinterpret_cast<uint32_t*>(tail - 64);
   SortPlan* plan = reinterpret_cast<SortPlan*>(tail);
   SortPlan* fb = plan + 1;
+  static_assert(2 * sizeof(SortPlan) <= 256, "plans fit their slot");
+  uint32_t* const status2[2] = {status, reinterpret_cast<uint32_t*>(tail + 256)};
   TCB_CUDA(cudaMemsetAsync(too_long, 0, sizeof(uint32_t), stream));
   note_launch(), k_sort_plan<<<1, 32, 0, stream>>>(d_and_or, kFixBits, nullptr, n, plan);
   // the windows above kFixBits: at most (64 - kFixBits) / 8 passes
   constexpr int kPrefixSlots = (64 - kFixBits + kRadixBits - 1) / kRadixBits;
   planned_passes(keys, vals, keys_alt, vals_alt, n, plan, kPrefixSlots,
-                 static_cast<unsigned>(num_tiles), status, counters, ghist, stream, iota_vals);
+                 static_cast<unsigned>(num_tiles), status2, counters, ghist, stream, iota_vals);
   note_launch(), k_sort_fixup_planned<<<grid_for(n, 256, 148 * 16), 256, 0, stream>>>(
       plan, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, kFixBits, too_long,
       iota_vals);
@@ -644,8 +654,8 @@ void radix_sort_pairs_prefix_async(uint64_t* keys, int32_t* vals, uint64_t* keys
   const unsigned small = static_cast<unsigned>(std::min<int64_t>(num_tiles, 148));
   note_launch(), k_sort_fallback_copy<<<small, 256, 0, stream>>>(
       plan, fb, 0, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, iota_vals);
-  planned_passes(keys, vals, keys_alt, vals_alt, n, fb, kMaxPasses, small, status, counters, ghist,
-                 stream, false);
+  planned_passes(keys, vals, keys_alt, vals_alt, n, fb, kMaxPasses, small, status2, counters,
+                 ghist, stream, false);
   note_launch(), k_sort_fallback_copy<<<small, 256, 0, stream>>>(
       plan, fb, 1, keys, vals, keys_alt, vals_alt, keys_out, vals_out, n, false);
   TCB_CUDA(cudaGetLastError());
