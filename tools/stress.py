@@ -26,8 +26,8 @@ def cloud(rng):
         pts = c[rng.integers(0, k, n)] + rng.normal(0, rng.uniform(0.05, 1), (n, d))
     elif kind == "uniform":
         pts = rng.uniform(-1, 1, (n, d)) * rng.uniform(0.1, 100)
-    elif kind == "dups":
-        base = rng.uniform(-1, 1, (max(1, n // 50), d))
+    elif kind == "dups":  # ~50 copies per point, or ~1000 (Morton groups > 256: fallback sort)
+        base = rng.uniform(-1, 1, (max(1, n // int(rng.choice([50, 1000]))), d))
         pts = base[rng.integers(0, len(base), n)]
     else:
         s = int(round(n ** (1 / d))) + 1
@@ -49,6 +49,15 @@ def one(rng):
     got = tb.cluster(tb.Dataset.from_array(pts), eps, minpts, tb.Algorithm(algo))
     _, core, _ = tb.cluster_device(torch.from_numpy(pts).cuda(), eps, minpts, tb.Algorithm(algo),
                                    stats=True)
+    if algo == 0:  # the stream-ordered entry too (device status word)
+        alab, acore, ast = tb.cluster_device_async(torch.from_numpy(pts).cuda(), eps, minpts)
+        torch.cuda.synchronize()
+        wcm = want["core"] == 1
+        alab = alab.cpu().numpy()
+        if (int(ast.item()) != 0 or not np.array_equal(acore.cpu().numpy(), want["core"])
+                or not np.array_equal(alab[wcm], want["labels"][wcm])
+                or not np.array_equal(alab == -1, want["labels"] == -1)):
+            return desc + " (async)", False
     torch.cuda.synchronize()
     cm = want["core"] == 1
     ok = (np.array_equal(got.core_flags, want["core"])
@@ -79,4 +88,5 @@ def run(budget_s, max_runs=None, seed=12345, verbose=True):
 
 
 if __name__ == "__main__":
-    run(float(sys.argv[1]) if len(sys.argv) > 1 else 120.0)
+    run(float(sys.argv[1]) if len(sys.argv) > 1 else 120.0,
+        seed=int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
