@@ -60,7 +60,9 @@ tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim,
  * TC_ERR_INVALID_ARGUMENT when a coordinate is non-finite (FDBSCAN; the
  * outputs are then all noise). Argument errors known on the host are still
  * returned directly. For FDBSCAN the call never synchronizes the host and is
- * capturable into a CUDA graph. */
+ * capturable into a CUDA graph; on a capturing stream any other algorithm
+ * (and tcg_cluster_device with stats) returns TC_ERR_INVALID_ARGUMENT before
+ * enqueuing anything, so the capture stays valid. */
 tc_status tcg_cluster_device_async(const float* d_coords, int64_t n, int dim, float eps,
                                    int minpts, tc_algorithm algorithm, int64_t oracle_cap,
                                    int32_t* d_labels, uint8_t* d_core, void* stream,

@@ -501,10 +501,22 @@ TC_EXPORT int tcg_device_count(void) {
 
 TC_EXPORT const char* tcg_version(void) { return "treeclust-b200 0.1 (sm_100a)"; }
 
+// Only FDBSCAN without stats enqueues a run with no host synchronization; any
+// other call on a capturing stream is refused before it touches the capture.
+static bool capture_refused(void* stream, tc_algorithm algorithm, bool stats) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone && (algorithm != TC_ALGO_FDBSCAN || stats);
+}
+
 TC_EXPORT tc_status tcg_cluster_device(const float* d_coords, int64_t n, int dim, float eps,
                                        int minpts, tc_algorithm algorithm, int64_t oracle_cap,
                                        int32_t* d_labels, uint8_t* d_core, void* stream,
                                        tc_cluster_stats* stats) {
+  if (capture_refused(stream, algorithm, stats != nullptr)) return TC_ERR_INVALID_ARGUMENT;
   return guarded([&]() -> tc_status {
     tcb::RunOutput ro;
     tcb::run_device(d_coords, n, dim, eps, minpts, algorithm, oracle_cap, d_labels, d_core,
@@ -519,6 +531,7 @@ TC_EXPORT tc_status tcg_cluster_device_async(const float* d_coords, int64_t n, i
                                              int minpts, tc_algorithm algorithm,
                                              int64_t oracle_cap, int32_t* d_labels,
                                              uint8_t* d_core, void* stream, int32_t* d_status) {
+  if (capture_refused(stream, algorithm, false)) return TC_ERR_INVALID_ARGUMENT;
   return guarded([&]() -> tc_status {
     tcb::run_device(d_coords, n, dim, eps, minpts, algorithm, oracle_cap, d_labels, d_core,
                     static_cast<cudaStream_t>(stream), false, nullptr, nullptr, nullptr, nullptr,

@@ -730,3 +730,36 @@ def test_async_status_reports_nonfinite_on_device():
         lab, core, st = tb.cluster_device_async(x, 0.5, 3, Algorithm(algo))
         torch.cuda.synchronize()
         assert int(st.item()) == int(Status.OK)
+
+
+def test_capture_of_a_synchronizing_call_is_refused_cleanly():
+    """DenseBox / brute force (and stats read-backs) synchronize the host, so on
+    a capturing stream they return INVALID_ARGUMENT before enqueuing anything:
+    the capture stays valid and the FDBSCAN call captured next replays."""
+    import torch
+
+    c = Dataset.blobs(4, 3000, 3, 4.0, 0.4, 21).coords()
+    x = torch.from_numpy(c).cuda()
+    s = torch.cuda.Stream()
+    lab = torch.empty(len(c), dtype=torch.int32, device="cuda")
+    core = torch.empty(len(c), dtype=torch.uint8, device="cuda")
+    st = torch.empty(1, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(s):
+        tb.cluster_device_async(x, 0.2, 5, Algorithm.FDBSCAN, lab, core, st, s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+        for algo in (Algorithm.DENSEBOX, Algorithm.BRUTEFORCE):
+            with pytest.raises(TreeclustError) as e:
+                tb.cluster_device_async(x, 0.2, 5, algo, lab, core, st, s)
+            assert e.value.status == Status.INVALID_ARGUMENT
+        with pytest.raises(TreeclustError) as e:
+            tb.cluster_device(x, 0.2, 5, Algorithm.FDBSCAN, lab, core, s, stats=True)
+        assert e.value.status == Status.INVALID_ARGUMENT
+        tb.cluster_device_async(x, 0.2, 5, Algorithm.FDBSCAN, lab, core, st, s)
+    lab.fill_(-7)
+    g.replay()
+    torch.cuda.synchronize()
+    host = tb.cluster(Dataset.from_array(c), 0.2, 5)
+    assert int(st.item()) == 0
+    assert_parity(lab.cpu().numpy(), core.cpu().numpy(), host.labels, host.core_flags)
