@@ -288,7 +288,16 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
 // minpts is reached. Dense members are core already and skip (dbscan.cpp:118).
 // Resident 128-thread blocks per SM the DenseBox traversals are compiled
 // for (register cap; C4 main pass 63.7 -> 62.8 ms).
-constexpr int kDbMinBlocks = 10;
+#ifndef TCB_DB_RANGED_MIN_BLOCKS  // k_db_main_ranged (DenseBox minpts == 2 main pass)
+#define TCB_DB_RANGED_MIN_BLOCKS 12  // C2 DenseBox main 23.9 -> 23.3 ms (8: 26.6, 14: 24.0)
+#endif
+constexpr int kDbRangedMinBlocks = TCB_DB_RANGED_MIN_BLOCKS;
+#ifndef TCB_DB_CORE_MIN_BLOCKS  // C4 core 18.5 ms (8: 19.1, 12: 18.7)
+#define TCB_DB_CORE_MIN_BLOCKS 10
+#endif
+#ifndef TCB_DB_Q_MIN_BLOCKS  // C4 main 59.1 ms (8: 63.6, 12: 71.0)
+#define TCB_DB_Q_MIN_BLOCKS 10
+#endif
 #ifndef TCB_DB_MAIN_Q
 #define TCB_DB_MAIN_Q 1
 #endif
@@ -398,7 +407,7 @@ struct DbCoreQuery {
 };
 
 template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
+__global__ void __launch_bounds__(kQueryBlock, TCB_DB_CORE_MIN_BLOCKS)
 k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int64_t n,
           const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell_begin,
           const int32_t* __restrict__ cell_end, BallTest bt, int minpts,
@@ -469,7 +478,7 @@ k_db_core(const float4* __restrict__ nodes, const float4* __restrict__ qpt, int6
 // border query counts coreless runs and every run once claimed; other runs
 // are walked. minpts == 2: every run is taken (all pairs are unions).
 template <int D, bool kForceCore, int kFast>
-__global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
+__global__ void __launch_bounds__(kQueryBlock, kDbRangedMinBlocks)
 k_db_main_ranged(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
                  const int32_t* __restrict__ qrank, int64_t n, const float4* __restrict__ sorted_pt,
                  const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
@@ -606,7 +615,7 @@ __device__ __noinline__ int db_drain_batch(const int4* act, int qn, int lane, in
 }
 
 template <int D, bool kForceCore, int kFast>
-__global__ void __launch_bounds__(kQueryBlock, kDbMinBlocks)
+__global__ void __launch_bounds__(kQueryBlock, TCB_DB_Q_MIN_BLOCKS)
 k_db_main_q(const float4* __restrict__ nodes, const float4* __restrict__ qpt,
             const int32_t* __restrict__ qrank, int64_t n,
             const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
