@@ -42,11 +42,17 @@ constexpr int kQueryBlock = 128;  // 64 / 256 measured equal or slower
 #endif
 constexpr int kFofMinBlocks = TCB_FOF_MIN_BLOCKS;
 // the same for the minpts > 2 main pass (10: main 21.7 -> 21.3 ms on C3);
-// the core pass is faster uncapped
+// the core pass at 16 (the SM's full 64 warps, 32 registers): C3 core 10.25
+// -> 9.84 ms (14: 9.85, uncapped 10.25); the queued main pass at 12 (10:
+// 21.5, 14: 52.7 ms)
 #ifndef TCB_MAIN_MIN_BLOCKS
 #define TCB_MAIN_MIN_BLOCKS 10
 #endif
 constexpr int kMainMinBlocks = TCB_MAIN_MIN_BLOCKS;
+#ifndef TCB_CORE_MIN_BLOCKS  // 0: uncapped
+#define TCB_CORE_MIN_BLOCKS 16
+#endif
+constexpr int kCoreMinBlocks = TCB_CORE_MIN_BLOCKS;
 #ifndef TCB_CORE_NEAR_FIRST
 #define TCB_CORE_NEAR_FIRST 1
 #endif
@@ -124,7 +130,7 @@ struct CoreQuery {
 };
 
 template <int D, int kFast>
-__global__ void __launch_bounds__(kQueryBlock)
+__global__ void __launch_bounds__(kQueryBlock, kCoreMinBlocks)
 k_fd_core(const float4* __restrict__ nodes, const float4* __restrict__ leaf_pt, int64_t m,
           BallTest bt, int minpts, uint8_t* __restrict__ flags, DevCounters* ctr) {
   if (ctr->nonfinite) return;  // stream-ordered run over bad input: no work
@@ -486,7 +492,10 @@ __device__ __noinline__ int main_drain_batch(const int4* act, int qn, int lane, 
 }
 
 // 12 resident blocks (42 registers): C1 main 0.59 -> 0.55 ms, C3fd 22.2 -> 21.3 ms vs 10
-constexpr int kMainQMinBlocks = 12;
+#ifndef TCB_MAIN_Q_MIN_BLOCKS
+#define TCB_MAIN_Q_MIN_BLOCKS 12
+#endif
+constexpr int kMainQMinBlocks = TCB_MAIN_Q_MIN_BLOCKS;
 
 template <int D, int kFast>
 __global__ void __launch_bounds__(kQueryBlock, kMainQMinBlocks)
