@@ -1119,7 +1119,8 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   }
   const unsigned g = grid_for(n, kQueryBlock, INT32_MAX);
   // minpts > 2: unions and border claims batched per warp (C4 main 62.8 ->
-  // 59.2 ms); minpts == 2 keeps the per-query form (26.3 vs 26.7 ms on C2)
+  // 59.2 ms); minpts == 2 keeps the per-query form (re-measured at the final
+  // launch bounds: 23.4 vs 26.7 ms on C2)
   if (TCB_DB_MAIN_Q && minpts > 2) {
     auto main = bt.fast ? k_db_main_q<D, false, 1> : k_db_main_q<D, false, 0>;
     note_launch(), main<<<g, kQueryBlock, 0, st>>>(b.tree.nodes, qpt, qrank, n, cell_begin,
