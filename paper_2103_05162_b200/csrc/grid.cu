@@ -233,7 +233,8 @@ k_prim_decode(const uint8_t* __restrict__ cell_dense, const int32_t* __restrict_
   }
 }
 
-// rank_of_prim[order[s]] = s; per leaf query count (1 or the cell's size).
+// rank_of_prim[order[s]] = s for the DenseBox primitives (the only ones
+// k_queries looks up); per leaf query count (1 or the cell's size).
 __global__ void __launch_bounds__(256)
 k_leaf_counts(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
               const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
@@ -241,8 +242,8 @@ k_leaf_counts(const int32_t* __restrict__ order, const int32_t* __restrict__ pri
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int32_t p = order[s];
-    rank_of_prim[p] = static_cast<int32_t>(s);
     int32_t a = prim_aux[p];
+    if (a < 0) rank_of_prim[p] = static_cast<int32_t>(s);
     qcount[s] = a >= 0 ? 1 : cell_end[~a] - cell_begin[~a];
   }
 }
@@ -264,22 +265,38 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t c = cell_of_sorted[k];
-    const int32_t b = cell_begin[c];
-    const bool dense = cell_dense[c];
-    const int32_t off = static_cast<int32_t>(k - b);
-    const int32_t p = prim_off[c] + (dense ? 0 : off);
-    const int32_t s = rank_of_prim[p];
-    const int32_t dst = qoff[s] + (dense ? off : 0);
+    if (!cell_dense[c]) continue;  // SinglePoints: k_queries_single, in slot order
+    const int32_t off = static_cast<int32_t>(k - cell_begin[c]);
+    const int32_t s = rank_of_prim[prim_off[c]];
+    const int32_t dst = qoff[s] + off;  // a cell's members are contiguous slots
     float4 pt = sorted_pt[k];
     const int32_t i = __float_as_int(pt.w);
     key[dst] = i;
-    if (dense) {
-      pt.w = __int_as_float(i | static_cast<int32_t>(0x80000000u));
-      flags[dst] = 1;
-      parent[dst] = qoff[s];  // the cell's first (minimum-index) member (dbscan.cpp:98-104)
-    }
+    pt.w = __int_as_float(i | static_cast<int32_t>(0x80000000u));
+    flags[dst] = 1;
+    parent[dst] = qoff[s];  // the cell's first (minimum-index) member (dbscan.cpp:98-104)
     qpt[dst] = pt;
     qrank[dst] = s;
+  }
+}
+
+// The SinglePoint queries, one per leaf rank s: slot qoff[s], written in slot
+// order (the per-point form above scattered them from cell order).
+template <int D>
+__global__ void __launch_bounds__(256)
+k_queries_single(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
+                 const float* __restrict__ coords, const int32_t* __restrict__ qoff, int64_t m,
+                 float4* __restrict__ qpt, int32_t* __restrict__ qrank,
+                 int32_t* __restrict__ key) {
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t i = prim_aux[order[s]];
+    if (i < 0) continue;  // a DenseBox: its members come from k_queries
+    const int32_t dst = qoff[s];
+    const float* c = coords + static_cast<int64_t>(i) * D;
+    qpt[dst] = make_float4(c[0], c[1], D == 3 ? c[2] : 0.f, __int_as_float(i));
+    key[dst] = i;
+    qrank[dst] = static_cast<int32_t>(s);
   }
 }
 
@@ -1066,6 +1083,8 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   note_launch(), k_queries<D><<<grid_for(n, 256), 256, 0, st>>>(sorted_pt, cell_of_sorted, cell_begin,
                                                  cell_dense, prim_off, rank_of_prim, qoff, n,
                                                  qpt, qrank, qkey, parent, flags);
+  note_launch(), k_queries_single<D><<<grid_for(num_prims, 256), 256, 0, st>>>(
+      b.tree.leaf_order, prim_aux, d_coords, qoff, num_prims, qpt, qrank, qkey);
   TCB_CUDA(cudaGetLastError());
 
   const MemberTree mt = build_member_tree<D>(sorted_pt, n, scratch);
