@@ -133,7 +133,7 @@ struct SortShared {
   uint32_t global_start[kRadix];
   uint32_t warp_tot[32];
   uint32_t next_hist[kRadix];
-  int tile[1];
+  int tile;
 };
 
 struct OnesweepSmem {
@@ -141,7 +141,6 @@ struct OnesweepSmem {
   int32_t vals[kTile];
   SortShared c;
 };
-
 
 __device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
   uint32_t v;
@@ -286,11 +285,11 @@ k_sort_onesweep(const uint64_t* __restrict__ keys_in, const int32_t* __restrict_
   // tiles already owned by running blocks: a grid smaller than the tile count
   // (the guarded fallback passes) loops safely.
   do {
-    if (threadIdx.x == 0) S.tile[0] = static_cast<int>(atomicAdd(tile_counter, 1u));
+    if (threadIdx.x == 0) S.tile = static_cast<int>(atomicAdd(tile_counter, 1u));
     for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&S.wcnt[0][0])[i] = 0;
     S.next_hist[threadIdx.x] = 0;  // kSortThreads == kRadix
     __syncthreads();
-    const int tile = S.tile[0];
+    const int tile = S.tile;
     if (kLoop && tile >= num_tiles) return;
     // planned passes alternate two status arrays: each tile clears its row of
     // the next pass's (idle during this pass) instead of a memset launch
