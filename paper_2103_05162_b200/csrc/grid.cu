@@ -238,11 +238,13 @@ k_prim_decode(const uint8_t* __restrict__ cell_dense, const int32_t* __restrict_
 __global__ void __launch_bounds__(256)
 k_leaf_counts(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
               const int32_t* __restrict__ cell_begin, const int32_t* __restrict__ cell_end,
-              int64_t m, int32_t* __restrict__ rank_of_prim, int32_t* __restrict__ qcount) {
+              int64_t m, int32_t* __restrict__ rank_of_prim, int32_t* __restrict__ qcount,
+              int32_t* __restrict__ aux_of_rank) {
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int32_t p = order[s];
     int32_t a = prim_aux[p];
+    aux_of_rank[s] = a;  // k_queries_single reads it in rank order
     if (a < 0) rank_of_prim[p] = static_cast<int32_t>(s);
     qcount[s] = a >= 0 ? 1 : cell_end[~a] - cell_begin[~a];
   }
@@ -284,13 +286,12 @@ k_queries(const float4* __restrict__ sorted_pt, const int32_t* __restrict__ cell
 // order (the per-point form above scattered them from cell order).
 template <int D>
 __global__ void __launch_bounds__(256)
-k_queries_single(const int32_t* __restrict__ order, const int32_t* __restrict__ prim_aux,
-                 const float* __restrict__ coords, const int32_t* __restrict__ qoff, int64_t m,
-                 float4* __restrict__ qpt, int32_t* __restrict__ qrank,
-                 int32_t* __restrict__ key) {
+k_queries_single(const int32_t* __restrict__ aux_of_rank, const float* __restrict__ coords,
+                 const int32_t* __restrict__ qoff, int64_t m, float4* __restrict__ qpt,
+                 int32_t* __restrict__ qrank, int32_t* __restrict__ key) {
   for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < m;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t i = prim_aux[order[s]];
+    const int32_t i = aux_of_rank[s];
     if (i < 0) continue;  // a DenseBox: its members come from k_queries
     const int32_t dst = qoff[s];
     const float* c = coords + static_cast<int64_t>(i) * D;
@@ -1070,9 +1071,10 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   int32_t* rank_of_prim = scratch.alloc_n<int32_t>(num_prims);
   int32_t* qcount = scratch.alloc_n<int32_t>(num_prims);
   int32_t* qoff = scratch.alloc_n<int32_t>(num_prims);
+  int32_t* aux_of_rank = scratch.alloc_n<int32_t>(num_prims);
   note_launch(), k_leaf_counts<<<grid_for(num_prims, 256), 256, 0, st>>>(b.tree.leaf_order, prim_aux,
                                                           cell_begin, cell_end, num_prims,
-                                                          rank_of_prim, qcount);
+                                                          rank_of_prim, qcount, aux_of_rank);
   exclusive_scan_i32(qcount, qoff, num_prims, nullptr, scan_tmp, st);
   float4* qpt = scratch.alloc_n<float4>(n);
   int32_t* qrank = scratch.alloc_n<int32_t>(n);
@@ -1084,7 +1086,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
                                                  cell_dense, prim_off, rank_of_prim, qoff, n,
                                                  qpt, qrank, qkey, parent, flags);
   note_launch(), k_queries_single<D><<<grid_for(num_prims, 256), 256, 0, st>>>(
-      b.tree.leaf_order, prim_aux, d_coords, qoff, num_prims, qpt, qrank, qkey);
+      aux_of_rank, d_coords, qoff, num_prims, qpt, qrank, qkey);
   TCB_CUDA(cudaGetLastError());
 
   const MemberTree mt = build_member_tree<D>(sorted_pt, n, scratch);
