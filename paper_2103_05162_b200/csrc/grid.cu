@@ -1064,7 +1064,7 @@ void run_densebox(const float* d_coords, int64_t n, float eps, int minpts, int32
   src.aux = prim_aux;
   src.count = num_prims;
   clock.mark(kStBounds);
-  BuiltBvh b = build_bvh<D>(src, false, ctr, scratch, &clock);
+  BuiltBvh b = build_bvh<D>(src, false, ctr, scratch, &clock, /*stream_ordered=*/true);
 
   // ---- query order + dense unions ----
   clock.mark(kStGrid);
